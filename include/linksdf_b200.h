@@ -1,0 +1,271 @@
+/*
+ * linksdf_b200.h — C ABI of the B200 (sm_100a) batched link-SDF distance checker.
+ *
+ * Drop-in boundary for the reference package "linksdf" 0.1.0 (pure Python/numpy,
+ * /root/reference/pkg/src/linksdf).  The reference has no FFI of its own: its
+ * operator surface is the set of module-level numpy functions re-exported in
+ * __init__.py:10-85.  Each entry point below replaces the numpy body of one of
+ * those functions (cited per declaration); the Python facade
+ * paper_2309_12543_b200 keeps the reference names, argument order and exception
+ * classes and calls these through ctypes.
+ *
+ * Conventions
+ *   - every pointer argument named *_dev is DEVICE memory owned by the caller;
+ *     the library never allocates or frees caller memory;
+ *   - all work is enqueued on the caller's stream (cudaStream_t passed as void*),
+ *     nothing synchronises unless stated, so the calls are CUDA-graph capturable;
+ *   - small descriptor tables (link chains, link grids, window geometry) are
+ *     passed by HOST pointer and copied into kernel parameters by value;
+ *   - return value: LSDF_OK or one status code per reference exception class
+ *     (errors.py:4-57); lsdf_last_error() gives thread-local text.  Nothing
+ *     throws across the ABI.
+ *   - arithmetic follows the reference bit-for-bit where it is fp64/fp32
+ *     elementwise math (FK, alignment, trilinear, voxel index, primitive SDF);
+ *     DESIGN.md lists the exact operation order each kernel reproduces.
+ */
+#ifndef LINKSDF_B200_H
+#define LINKSDF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: one per reference exception class (errors.py) ---- */
+enum {
+    LSDF_OK = 0,
+    LSDF_ERR_VALIDATION = 1,          /* ValidationError        errors.py:56 */
+    LSDF_ERR_OUT_OF_BOUNDS = 2,       /* OutOfBoundsError       errors.py:8  */
+    LSDF_ERR_NO_OVERLAP = 3,          /* NoOverlapError         errors.py:12 */
+    LSDF_ERR_LIMIT_VIOLATION = 4,     /* LimitViolationError    errors.py:16 */
+    LSDF_ERR_NON_WATERTIGHT = 5,      /* NonWatertightError     errors.py:29 */
+    LSDF_ERR_GRID_MISMATCH = 6,       /* GridMismatchError      errors.py:33 */
+    LSDF_ERR_DIMENSION_MISMATCH = 7,  /* DimensionMismatchError errors.py:37 */
+    LSDF_ERR_CUDA = 100,
+    LSDF_ERR_UNSUPPORTED = 101
+};
+
+#define LSDF_MAX_LINKS 32
+#define LSDF_MAX_WINDOW 256
+
+/* Environment voxel grid (grids.py:49-90): axis-aligned, [-extent, extent). */
+typedef struct {
+    double extent[3];
+    double resolution[3];
+    int32_t dims[3];
+    int32_t pad_;
+} lsdf_env_grid;
+
+/* One link of the kinematic chain, parents first (robot.py:113-145,305-347).
+ * kind: 0 base (no parent joint), 1 revolute, 2 prismatic, 3 fixed.
+ * Constant matrices are precomputed on the host with the reference's own
+ * numpy expressions (rpy_matrix robot.py:24-32, skew/outer robot.py:39-42,
+ * r_o @ axis robot.py:337). */
+typedef struct {
+    int32_t kind;
+    int32_t parent;      /* index of the parent link, -1 for the base     */
+    int32_t q_col;       /* column of q for actuated joints, -1 otherwise */
+    int32_t geom_slot;   /* index among geometry links, -1 if none        */
+    double joint_R[9];   /* joint origin rotation, row-major              */
+    double joint_t[3];
+    double skew[9];      /* [k]x of the unit joint axis                   */
+    double outer[9];     /* k k^T                                         */
+    double R_axis[3];    /* joint_R @ axis (prismatic)                    */
+    double link_R[9];    /* link origin rotation                          */
+    double link_t[3];
+} lsdf_link;
+
+/* One dense link SDF grid (grids.py:116-152): values x-fastest, f32. */
+typedef struct {
+    const float* values_dev;
+    int32_t dims[3];
+    float d_far;          /* float32(min(extent))   grids.py:145-148 */
+    double extent[3];
+    double resolution[3];
+} lsdf_link_grid;
+
+/* Window geometry (placement.py:172-210).  P tables hold the canonical
+ * normalized offsets ((m - W/2) * r_e / e_r, placement.py:119-121) per axis.
+ * zrange_dev: per window column (mx, my) [x-fastest] the half-open z range
+ * of kept cells [lo, hi) — the ball mask is an interval along z.
+ * mask_bits_dev: the full W^3 keep-mask, bit (mx + W*(my + W*mz)). */
+typedef struct {
+    int32_t W[3];
+    int32_t n_masked;
+    double e_r;
+    const double* P_dev;          /* 3 x Wmax, row a = axis a          */
+    int32_t Wmax;
+    int32_t pad_;
+    const int16_t* zrange_dev;    /* 2 x W[0] x W[1]                   */
+    const uint32_t* mask_bits_dev;
+} lsdf_window;
+
+const char* lsdf_version(void);
+const char* lsdf_last_error(void);
+/* Number of kernels this library enqueued since load (evidence counter). */
+uint64_t lsdf_launch_count(void);
+
+/* ---- stage 1: forward kinematics + alignment --------------------------- */
+
+/* forward_kinematics_batch (robot.py:305-347) for C configurations of D
+ * columns.  R_all/T_all (optional, may be NULL): (C, n_links, 3, 3) and
+ * (C, n_links, 3) fp64.  For geometry links (geom_slot >= 0) also writes the
+ * alignment of compute_alignment (placement.py:60-99) for window width W:
+ *   R_geo (C, n_geo, 9), dt_geo (C, n_geo, 3) fp64, anchor_geo (C, n_geo, 3) i32.
+ * flags_dev[0] += #limit violations (robot.py:291-302), flags_dev[1] += #windows
+ * that miss the grid (placement.py:86-93); limits_dev is (D, 2) fp64 or NULL. */
+int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_geo,
+                  const double* q_dev, int64_t C, int32_t D, const double* limits_dev,
+                  const lsdf_env_grid* env, const int32_t W[3],
+                  double* R_all_dev, double* T_all_dev,
+                  double* R_geo_dev, double* dt_geo_dev, int32_t* anchor_geo_dev,
+                  int32_t* flags_dev, void* stream);
+
+/* compute_alignment (placement.py:60-99) for n positions T (n, 3) fp64. */
+int lsdf_align(const double* T_dev, int64_t n, const lsdf_env_grid* env, const int32_t W[3],
+               int32_t* anchor_dev, double* dt_dev, int32_t* flags_dev, void* stream);
+
+/* ---- obstacles --------------------------------------------------------- */
+
+/* Workspace bytes for the occupancy structures of an environment grid:
+ * bitmap (ceil(V/32) u32, C-order bit (ix*ny+iy)*nz+iz) + position grid (V i32)
+ * + 4 counters. */
+int64_t lsdf_occupancy_bytes(const lsdf_env_grid* env);
+
+/* voxelize_pointcloud (query.py:106-125, grids.py:93-113): points (N, 3), f64
+ * (points_f32 == 0) or f32.  Fills the occupancy workspace and writes the
+ * sorted unique voxel indices (np.unique order = C-order rank) to
+ * indices_dev (N_occ_max, 3) i32 (may be NULL).  counters_dev (in workspace):
+ * [0] n_occupied, [1] n_dropped. */
+int lsdf_voxelize(const void* points_dev, int32_t points_f32, int64_t N,
+                  const lsdf_env_grid* env, void* occupancy_dev,
+                  int32_t* indices_dev, void* stream);
+
+/* Occupancy from an explicit index list (ObstacleVoxelSet, query.py:47-58).
+ * sorted_unique != 0 promises lexicographic order without duplicates (what
+ * voxelize and np.unique produce); otherwise the first position of each voxel
+ * in the list is recorded, matching numpy argmin first-occurrence semantics. */
+int lsdf_occupancy_from_indices(const int32_t* indices_dev, int64_t N, int32_t sorted_unique,
+                                const lsdf_env_grid* env, void* occupancy_dev, void* stream);
+
+/* voxel_index_of (grids.py:93-113) per point: floor((p + e) / r) clipped to
+ * [0, dims-1]; flags_dev[0] += #points outside [-e, e) (OutOfBoundsError). */
+int lsdf_voxel_index(const double* points_dev, int64_t N, const lsdf_env_grid* env,
+                     int32_t* indices_dev, int32_t* flags_dev, void* stream);
+
+/* ---- stage 3+4: fused transform + trilinear lookup + min/argmin -------- */
+
+/* Direct batched query: for every configuration c the minimum over occupied
+ * voxels v and geometry links l whose sphere-masked window covers v of the
+ * resampled link SDF value (grid_transform_exact placement.py:148-169 +
+ * trilinear_sample grids.py:155-191), clamped at float32(d_far_global)
+ * (query.py:82-83).  Bit-identical to query_min_distances on the assembled
+ * robot SDF (query.py:128-150).  Outputs d (C) f32, link (C) i32 and voxel (C)
+ * i32 (position in the obstacle list; -1/-1 when d equals the clamp or the set
+ * is empty).  per_link_dev (C, n_geo) f32 or NULL: per_link_min_distances
+ * (query.py:153-176).  by_position != 0 selects the general (unsorted list)
+ * tie rule; set it when the occupancy came from an unsorted index list. */
+int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_dev,
+                      const int32_t* anchor_geo_dev, int64_t C, int32_t n_geo,
+                      const lsdf_link_grid* grids, const lsdf_window* window,
+                      const lsdf_env_grid* env, const void* occupancy_dev,
+                      int32_t by_position, double d_far_global,
+                      float* d_dev, int32_t* link_dev, int32_t* voxel_dev,
+                      float* per_link_dev, void* stream);
+
+/* ---- materialized (paper) mode ----------------------------------------- */
+
+/* place_links_batch (placement.py:267-313): every (c, l) window, values
+ * (C, n_geo, W^3) f32 with x-fastest cells, masked cells = link d_far. */
+int lsdf_place_windows(const double* R_geo_dev, const double* dt_geo_dev, int64_t C,
+                       int32_t n_geo, const lsdf_link_grid* grids, const lsdf_window* window,
+                       float* windows_dev, void* stream);
+
+/* assemble_robot_sdfs (query.py:61-103) from n_fields windows
+ * (n_fields, W^3) with anchors (n_fields, 3) i32 and config ids (n_fields) i32:
+ * values (C, nx, ny, nz) f32 C-order, initialised to float32(d_far_global). */
+int lsdf_assemble(const float* windows_dev, const int32_t* anchors_dev,
+                  const int32_t* config_dev, int64_t n_fields, const int32_t W[3],
+                  const lsdf_env_grid* env, int64_t C, double d_far_global,
+                  float* values_dev, void* stream);
+
+/* query_min_distances on a dense batch (query.py:128-150) + first-occurrence
+ * argmin over the index list; d/argmin per configuration. */
+int lsdf_query_dense(const float* values_dev, int64_t C, const lsdf_env_grid* env,
+                     const int32_t* indices_dev, int64_t N, float* d_dev,
+                     int32_t* argmin_dev, void* stream);
+
+/* per_link_min_distances (query.py:153-176) over explicit fields: for field f
+ * (config configs[f], link links[f], window values (W^3, x-fastest), anchor)
+ * out[c * n_links + l] = min(out, d_far_f, window values at occupied voxels).
+ * out_dev must be pre-filled with float32(d_far_global) by the caller
+ * (lsdf_fill); d_far_dev holds float32(field d_far) per field. */
+int lsdf_per_link_fields(const float* windows_dev, const int32_t* anchors_dev,
+                         const int32_t* configs_dev, const int32_t* links_dev,
+                         const float* d_far_dev, int64_t n_fields, const int32_t W[3],
+                         int32_t n_links, const lsdf_env_grid* env, const void* occupancy_dev,
+                         float* out_dev, void* stream);
+
+int lsdf_fill(float* dst_dev, int64_t n, float value, void* stream);
+
+/* sphere_baseline_distances (query.py:254-291): per configuration the min over
+ * spheres s and occupied voxel centres of |R_c,l(s) center_s + T_c,l(s) - x| - r_s,
+ * fp64.  R_all (C, L, 9), T_all (C, L, 3); sphere tables (S); voxel centres
+ * come from indices (N, 3) i32. */
+int lsdf_sphere_baseline(const double* R_all_dev, const double* T_all_dev, int64_t C, int32_t L,
+                         const int32_t* sphere_link_dev, const double* sphere_center_dev,
+                         const double* sphere_radius_dev, int32_t S, const int32_t* indices_dev,
+                         int64_t N, const lsdf_env_grid* env, double* out_dev, void* stream);
+
+/* trilinear_sample (grids.py:155-191) of one grid at n points (n, 3) fp64,
+ * each point first multiplied by `scale` in fp64 (the `g * window.extent` of
+ * placement.py:301-302; pass 1.0 for raw link-frame points). */
+int lsdf_trilinear(const lsdf_link_grid* grid, const double* pts_dev, int64_t n, double scale,
+                   float* out_dev, void* stream);
+
+/* grid_transform_exact (placement.py:148-169): G (B, V, 3) fp64 for rotations
+ * (B, 9) and residuals (B, 3) over V normalized points (V, 3). */
+int lsdf_grid_transform_exact(const double* R_dev, const double* dt_dev, int64_t B,
+                              const double* points_dev, int64_t V, double e_r,
+                              double* G_dev, void* stream);
+
+/* ---- stage 2a: link-SDF precompute ------------------------------------- */
+
+/* build_link_sdf (meshes.py:332-371) for an analytic primitive
+ * (meshes.py:64-82). kind 0 sphere (p0 = radius, p1..3 = center), 1 capsule
+ * (p0 radius, p1 half_length, p2..4 unit axis), 2 box (p0..2 half extents).
+ * values (nx, ny, nz) f32 x-fastest. */
+int lsdf_build_primitive(int32_t kind, const double params[8], const double extent[3],
+                         const double resolution[3], const int32_t dims[3],
+                         float* values_dev, void* stream);
+
+/* primitive_sdf at explicit points (n, 3) fp64 -> fp64. */
+int lsdf_primitive_points(int32_t kind, const double params[8], const double* pts_dev,
+                          int64_t n, double* out_dev, void* stream);
+
+/* build_link_sdf for a triangle mesh: exact point-triangle distance
+ * (meshes.py:144-246) and, when signed, ray-crossing parity over the four
+ * fixed directions (meshes.py:249-305).  tri_dev (T, 9) fp64 corners. */
+int lsdf_build_mesh(const double* tri_dev, int32_t n_tri, int32_t is_signed,
+                    const double extent[3], const double resolution[3], const int32_t dims[3],
+                    float* values_dev, void* stream);
+
+/* exact_point_distance (meshes.py:308-329) at explicit points. */
+int lsdf_mesh_points(const double* tri_dev, int32_t n_tri, int32_t is_signed,
+                     const double* pts_dev, int64_t n, double* out_dev, void* stream);
+
+/* ---- stage 2b: TinyMlp grid transform (approx.py:63-158, 292-306) ------- */
+
+/* y = relu(x W1 + b1) W2 + b2 for x = R (B, 9) fp64 rounded to f32; output
+ * (B, 3V) f32.  hidden H <= 64.  Layer 2 runs on tcgen05 tensor cores
+ * (kind::tf32, 3xTF32 split) when use_tensor_cores != 0. */
+int lsdf_mlp_predict(const float* w1_dev, const float* b1_dev, const float* w2_dev,
+                     const float* b2_dev, int32_t H, int64_t n_out, const double* R_dev,
+                     int64_t B, float* y_dev, int32_t use_tensor_cores, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LINKSDF_B200_H */

@@ -1,0 +1,205 @@
+"""ctypes binding of the C ABI in ``include/linksdf_b200.h``.
+
+The extension is a plain shared library built in-tree by ``build.py``
+(``_lib/liblinksdf_b200.so``); device memory comes from torch tensors (their
+``data_ptr()``), work is enqueued on torch's current stream.  There is no CPU
+fallback: if the library or a CUDA device is missing, every compute call
+raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from . import errors
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "liblinksdf_b200.so"
+
+MAX_LINKS = 32
+
+# --------------------------------------------------------------------------- structs
+
+
+class EnvGridT(C.Structure):
+    _fields_ = [("extent", C.c_double * 3), ("resolution", C.c_double * 3),
+                ("dims", C.c_int32 * 3), ("pad_", C.c_int32)]
+
+
+class LinkT(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("parent", C.c_int32), ("q_col", C.c_int32),
+                ("geom_slot", C.c_int32), ("joint_R", C.c_double * 9), ("joint_t", C.c_double * 3),
+                ("skew", C.c_double * 9), ("outer", C.c_double * 9), ("R_axis", C.c_double * 3),
+                ("link_R", C.c_double * 9), ("link_t", C.c_double * 3)]
+
+
+class LinkGridT(C.Structure):
+    _fields_ = [("values_dev", C.c_void_p), ("dims", C.c_int32 * 3), ("d_far", C.c_float),
+                ("extent", C.c_double * 3), ("resolution", C.c_double * 3)]
+
+
+class WindowT(C.Structure):
+    _fields_ = [("W", C.c_int32 * 3), ("n_masked", C.c_int32), ("e_r", C.c_double),
+                ("P_dev", C.c_void_p), ("Wmax", C.c_int32), ("pad_", C.c_int32),
+                ("zrange_dev", C.c_void_p), ("mask_bits_dev", C.c_void_p)]
+
+
+_P = C.c_void_p
+_I32 = C.c_int32
+_I64 = C.c_int64
+_D = C.c_double
+_F = C.c_float
+
+_SIGS = {
+    "lsdf_fk_align": [C.POINTER(LinkT), _I32, _I32, _P, _I64, _I32, _P, C.POINTER(EnvGridT),
+                      C.POINTER(_I32), _P, _P, _P, _P, _P, _P, _P],
+    "lsdf_align": [_P, _I64, C.POINTER(EnvGridT), C.POINTER(_I32), _P, _P, _P, _P],
+    "lsdf_occupancy_bytes": [C.POINTER(EnvGridT)],
+    "lsdf_voxelize": [_P, _I32, _I64, C.POINTER(EnvGridT), _P, _P, _P],
+    "lsdf_occupancy_from_indices": [_P, _I64, _I32, C.POINTER(EnvGridT), _P, _P],
+    "lsdf_voxel_index": [_P, _I64, C.POINTER(EnvGridT), _P, _P, _P],
+    "lsdf_query_direct": [_P, _P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT),
+                          C.POINTER(EnvGridT), _P, _I32, _D, _P, _P, _P, _P, _P],
+    "lsdf_place_windows": [_P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT), _P, _P],
+    "lsdf_assemble": [_P, _P, _P, _I64, C.POINTER(_I32), C.POINTER(EnvGridT), _I64, _D, _P, _P],
+    "lsdf_query_dense": [_P, _I64, C.POINTER(EnvGridT), _P, _I64, _P, _P, _P],
+    "lsdf_per_link_fields": [_P, _P, _P, _P, _P, _I64, C.POINTER(_I32), _I32, C.POINTER(EnvGridT),
+                             _P, _P, _P],
+    "lsdf_fill": [_P, _I64, _F, _P],
+    "lsdf_sphere_baseline": [_P, _P, _I64, _I32, _P, _P, _P, _I32, _P, _I64, C.POINTER(EnvGridT),
+                             _P, _P],
+    "lsdf_trilinear": [C.POINTER(LinkGridT), _P, _I64, _D, _P, _P],
+    "lsdf_grid_transform_exact": [_P, _P, _I64, _P, _I64, _D, _P, _P],
+    "lsdf_build_primitive": [_I32, C.POINTER(_D), C.POINTER(_D), C.POINTER(_D), C.POINTER(_I32), _P, _P],
+    "lsdf_primitive_points": [_I32, C.POINTER(_D), _P, _I64, _P, _P],
+    "lsdf_build_mesh": [_P, _I32, _I32, C.POINTER(_D), C.POINTER(_D), C.POINTER(_I32), _P, _P],
+    "lsdf_mesh_points": [_P, _I32, _I32, _P, _I64, _P, _P],
+    "lsdf_mlp_predict": [_P, _P, _P, _P, _I32, _I64, _P, _I64, _P, _I32, _P],
+}
+
+EXPORTS = tuple(_SIGS) + ("lsdf_version", "lsdf_last_error", "lsdf_launch_count")
+
+_ERRORS = {
+    1: errors.ValidationError,
+    2: errors.OutOfBoundsError,
+    3: errors.NoOverlapError,
+    5: errors.NonWatertightError,
+    6: errors.GridMismatchError,
+    7: errors.DimensionMismatchError,
+    100: errors.CudaError,
+    101: errors.ValidationError,
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path: Path | None = None):
+    """Load (once) and type the shared library; raises if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise ImportError(
+                f"linksdf-b200 CUDA extension not built ({p}); run "
+                "`python -m paper_2309_12543_b200.build` (nvcc, sm_100a)")
+        lib = C.CDLL(str(p))
+        for name, argtypes in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argtypes
+            fn.restype = C.c_int64 if name == "lsdf_occupancy_bytes" else C.c_int
+        lib.lsdf_version.restype = C.c_char_p
+        lib.lsdf_last_error.restype = C.c_char_p
+        lib.lsdf_launch_count.restype = C.c_uint64
+        _lib = lib
+        return lib
+
+
+def lib():
+    return _lib if _lib is not None else load_library()
+
+
+def call(name: str, *args) -> int:
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        msg = lib().lsdf_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, errors.LinkSdfError)(f"{name}: {msg}")
+    return rc
+
+
+# --------------------------------------------------------------------------- device helpers
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+
+        _torch = t
+    return _torch
+
+
+def device():
+    """The CUDA device every tensor lives on; raises without one (no CPU path)."""
+    t = torch()
+    if not t.cuda.is_available():
+        raise errors.CudaError("linksdf-b200 needs a CUDA device (B200, sm_100a); none is visible")
+    load_library()
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream() -> int:
+    return torch().cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def to_device(a, dtype=None):
+    """numpy array or tensor → contiguous CUDA tensor (dtype optional)."""
+    t = torch()
+    if isinstance(a, t.Tensor):
+        out = a.to(device=device(), dtype=dtype) if dtype is not None else a.to(device=device())
+        return out.contiguous()
+    arr = np.ascontiguousarray(a)
+    out = t.from_numpy(arr).to(device(), non_blocking=False)
+    if dtype is not None:
+        out = out.to(dtype)
+    return out.contiguous()
+
+
+def empty(shape, dtype):
+    return torch().empty(shape, dtype=dtype, device=device())
+
+
+def zeros(shape, dtype):
+    return torch().zeros(shape, dtype=dtype, device=device())
+
+
+def env_struct(grid) -> EnvGridT:
+    e = EnvGridT()
+    e.extent[:] = [float(v) for v in grid.extent]
+    e.resolution[:] = [float(v) for v in grid.resolution]
+    e.dims[:] = [int(v) for v in grid.dims]
+    return e
+
+
+def i32x3(v) -> C.Array:
+    arr = (C.c_int32 * 3)()
+    arr[:] = [int(x) for x in v]
+    return arr
+
+
+def f64s(v, n: int) -> C.Array:
+    arr = (C.c_double * n)()
+    vals = [float(x) for x in np.ravel(v)]
+    arr[: len(vals)] = vals
+    return arr

@@ -1,0 +1,232 @@
+// lsdf_build.cu — stage 2a: exact link-SDF precompute (meshes.py:64-82, 144-371).
+//
+// Primitives: one thread per cell, fp64 analytic distance, f32 store; the
+// write is the whole cost (HBM-store bound, 4 B per cell).
+// Meshes: brute force over all triangles (the spec rejects propagation
+// transforms).  A CTA owns 128 cells and streams the
+// triangle list through shared memory in tiles, so every triangle is read
+// from L2 once per CTA; the per-pair closest-point and ray-crossing tests
+// run in fp64 with the reference's operation order.
+#include "lsdf_common.cuh"
+#include "lsdf_math.cuh"
+
+using namespace lsdf;
+
+namespace {
+
+__device__ __forceinline__ void cell_center(int64_t cell, const int32_t* dims, const double* ext, const double* res,
+                                            double* p) {
+    const int64_t ix = cell % dims[0];
+    const int64_t iy = (cell / dims[0]) % dims[1];
+    const int64_t iz = cell / ((int64_t)dims[0] * dims[1]);
+    // meshes.py:356-358: -e + (i + 0.5) * r
+    p[0] = DADD(-ext[0], DMUL(DADD((double)ix, 0.5), res[0]));
+    p[1] = DADD(-ext[1], DMUL(DADD((double)iy, 0.5), res[1]));
+    p[2] = DADD(-ext[2], DMUL(DADD((double)iz, 0.5), res[2]));
+}
+
+struct BuildParams {
+    int32_t kind;
+    double prm[8];
+    double ext[3], res[3];
+    int32_t dims[3];
+};
+
+__global__ void build_primitive_kernel(const __grid_constant__ BuildParams p, float* out) {
+    const int64_t n = (int64_t)p.dims[0] * p.dims[1] * p.dims[2];
+    for (int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < n;
+         cell += (int64_t)gridDim.x * blockDim.x) {
+        double c[3];
+        cell_center(cell, p.dims, p.ext, p.res, c);
+        out[cell] = (float)primitive_at(p.kind, p.prm, c[0], c[1], c[2]);
+    }
+}
+
+__global__ void primitive_points_kernel(int32_t kind, BuildParams p, const double* pts, int64_t n, double* out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = primitive_at(kind, p.prm, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+}
+
+// meshes.py:249-256
+__constant__ double c_dirs[4][3] = {
+    {0.577350269, 0.577350269, 0.577350269},
+    {0.267261242, 0.534522484, 0.801783726},
+    {-0.455842306, 0.569802882, 0.683763459},
+    {0.816496581, -0.408248290, 0.408248290},
+};
+
+// Per-(direction, triangle) ray constants, meshes.py:265-271.
+__global__ void ray_setup_kernel(const double* tri, int32_t n_tri, RayTri* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 4 * n_tri) return;
+    const int d = i / n_tri, t = i % n_tri;
+    const double* a = tri + 9 * t;
+    RayTri r;
+    for (int k = 0; k < 3; ++k) {
+        r.a[k] = a[k];
+        r.e1[k] = DSUB(a[3 + k], a[k]);
+        r.e2[k] = DSUB(a[6 + k], a[k]);
+    }
+    cross3(c_dirs[d], r.e2, r.h);
+    const double det = dot3(r.e1[0], r.e1[1], r.e1[2], r.h[0], r.h[1], r.h[2]);
+    r.parallel = fabs(det) < 1e-12;
+    r.det = r.parallel ? 1.0 : det;
+    out[i] = r;
+}
+
+constexpr int MESH_CELLS = 128;  // cells per CTA (one per thread)
+constexpr int MESH_TILE = 128;   // triangles per shared-memory tile
+
+struct MeshParams {
+    const double* tri;
+    const RayTri* ray;
+    int32_t n_tri, is_signed;
+    double ext[3], res[3];
+    int32_t dims[3];
+    const double* pts;  // explicit points instead of cell centres (or null)
+    int64_t n;
+    float* out_f;
+    double* out_d;
+};
+
+__global__ void __launch_bounds__(MESH_CELLS) mesh_kernel(const __grid_constant__ MeshParams p) {
+    __shared__ double s_tri[MESH_TILE * 9];
+    __shared__ RayTri s_ray[MESH_TILE];
+    const int64_t i = (int64_t)blockIdx.x * MESH_CELLS + threadIdx.x;
+    const bool active = i < p.n;
+    double pt[3] = {0.0, 0.0, 0.0};
+    if (active) {
+        if (p.pts) {
+            pt[0] = p.pts[3 * i];
+            pt[1] = p.pts[3 * i + 1];
+            pt[2] = p.pts[3 * i + 2];
+        } else {
+            cell_center(i, p.dims, p.ext, p.res, pt);
+        }
+    }
+    // exact unsigned distance: min over every triangle (meshes.py:217-246)
+    double best = INFINITY;
+    for (int t0 = 0; t0 < p.n_tri; t0 += MESH_TILE) {
+        const int nt = p.n_tri - t0 < MESH_TILE ? p.n_tri - t0 : MESH_TILE;
+        __syncthreads();
+        for (int k = threadIdx.x; k < nt * 9; k += MESH_CELLS) s_tri[k] = p.tri[(int64_t)t0 * 9 + k];
+        __syncthreads();
+        if (active)
+            for (int t = 0; t < nt; ++t) {
+                const double* tr = s_tri + 9 * t;
+                const double d2 = closest_sq(pt, tr, tr + 3, tr + 6);
+                best = d2 < best ? d2 : best;
+            }
+    }
+    double d = DSQRT(best);
+    if (p.is_signed) {
+        // ray parity, retried along the backup directions for suspect points
+        bool inside = false, pending = active;
+        for (int dir = 0; dir < 4; ++dir) {
+            if (!__syncthreads_or(pending)) break;
+            int count = 0;
+            bool suspect = false;
+            for (int t0 = 0; t0 < p.n_tri; t0 += MESH_TILE) {
+                const int nt = p.n_tri - t0 < MESH_TILE ? p.n_tri - t0 : MESH_TILE;
+                __syncthreads();
+                for (int k = threadIdx.x; k < nt; k += MESH_CELLS) s_ray[k] = p.ray[(int64_t)dir * p.n_tri + t0 + k];
+                __syncthreads();
+                if (pending)
+                    for (int t = 0; t < nt; ++t) {
+                        const int h = ray_cross(pt, s_ray[t], c_dirs[dir]);
+                        count += h != 0;
+                        suspect |= h == 2;
+                    }
+            }
+            if (pending && !suspect) {
+                inside = count & 1;
+                pending = false;
+            }
+        }
+        // points suspect along all four directions stay "outside" (meshes.py:303-304)
+        if (inside) d = -d;
+    }
+    if (active) {
+        if (p.out_f) p.out_f[i] = (float)d;
+        if (p.out_d) p.out_d[i] = d;
+    }
+}
+
+int launch_mesh(MeshParams& p, cudaStream_t s) {
+    RayTri* ray = nullptr;
+    if (p.is_signed) {
+        LSDF_TRY(check_cuda(cudaMallocAsync((void**)&ray, sizeof(RayTri) * 4 * (size_t)p.n_tri, s), "mesh ray alloc"));
+        ray_setup_kernel<<<grid_for(4LL * p.n_tri, 128), 128, 0, s>>>(p.tri, p.n_tri, ray);
+        LSDF_TRY(check_launch("ray_setup_kernel"));
+    }
+    p.ray = ray;
+    mesh_kernel<<<grid_for(p.n, MESH_CELLS), MESH_CELLS, 0, s>>>(p);
+    int rc = check_launch("mesh_kernel");
+    if (ray) cudaFreeAsync(ray, s);
+    return rc;
+}
+
+}  // namespace
+
+extern "C" int lsdf_build_primitive(int32_t kind, const double params[8], const double extent[3],
+                                    const double resolution[3], const int32_t dims[3], float* values_dev,
+                                    void* stream) {
+    if (kind < 0 || kind > 2) return fail(LSDF_ERR_VALIDATION, "unknown primitive kind %d", kind);
+    BuildParams p{};
+    p.kind = kind;
+    for (int i = 0; i < 8; ++i) p.prm[i] = params[i];
+    for (int a = 0; a < 3; ++a) {
+        p.ext[a] = extent[a];
+        p.res[a] = resolution[a];
+        p.dims[a] = dims[a];
+    }
+    const int64_t n = (int64_t)dims[0] * dims[1] * dims[2];
+    if (n <= 0) return LSDF_OK;
+    const int64_t blocks = (n + 255) / 256;
+    build_primitive_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, (cudaStream_t)stream>>>(
+        p, values_dev);
+    return check_launch("build_primitive_kernel");
+}
+
+extern "C" int lsdf_primitive_points(int32_t kind, const double params[8], const double* pts_dev, int64_t n,
+                                     double* out_dev, void* stream) {
+    if (kind < 0 || kind > 2) return fail(LSDF_ERR_VALIDATION, "unknown primitive kind %d", kind);
+    if (n <= 0) return LSDF_OK;
+    BuildParams p{};
+    for (int i = 0; i < 8; ++i) p.prm[i] = params[i];
+    primitive_points_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(kind, p, pts_dev, n, out_dev);
+    return check_launch("primitive_points_kernel");
+}
+
+extern "C" int lsdf_build_mesh(const double* tri_dev, int32_t n_tri, int32_t is_signed, const double extent[3],
+                               const double resolution[3], const int32_t dims[3], float* values_dev, void* stream) {
+    if (n_tri <= 0) return fail(LSDF_ERR_VALIDATION, "mesh has no triangles");
+    MeshParams p{};
+    p.tri = tri_dev;
+    p.n_tri = n_tri;
+    p.is_signed = is_signed;
+    for (int a = 0; a < 3; ++a) {
+        p.ext[a] = extent[a];
+        p.res[a] = resolution[a];
+        p.dims[a] = dims[a];
+    }
+    p.n = (int64_t)dims[0] * dims[1] * dims[2];
+    p.out_f = values_dev;
+    if (p.n <= 0) return LSDF_OK;
+    return launch_mesh(p, (cudaStream_t)stream);
+}
+
+extern "C" int lsdf_mesh_points(const double* tri_dev, int32_t n_tri, int32_t is_signed, const double* pts_dev,
+                                int64_t n, double* out_dev, void* stream) {
+    if (n_tri <= 0) return fail(LSDF_ERR_VALIDATION, "mesh has no triangles");
+    if (n <= 0) return LSDF_OK;
+    MeshParams p{};
+    p.tri = tri_dev;
+    p.n_tri = n_tri;
+    p.is_signed = is_signed;
+    p.pts = pts_dev;
+    p.n = n;
+    p.out_d = out_dev;
+    return launch_mesh(p, (cudaStream_t)stream);
+}

@@ -1,0 +1,544 @@
+"""Robot-SDF assembly, obstacle voxelization and distance queries (stages 3-4).
+
+Host-side mirror of the reference ``query.py`` (query.py:30-355) with the
+same names, argument order and return types, plus the B200-native additions
+SURVEY.md §8b asks for:
+
+* :class:`TrajectorySdf` — a lazy ``RobotSdfBatch``-compatible handle.  It
+  keeps only the link grids and the per-(waypoint, link) poses on the GPU;
+  ``query_min_distances(handle, obstacles)`` then runs the fused direct
+  kernel (transform + trilinear + min/argmin over occupied voxels inside each
+  link's sphere-masked window), which is bit-identical to gathering from the
+  assembled dense field.  ``.values`` materialises the dense
+  field on demand.
+* ``return_argmin=True`` (keyword-only, no "pose"/"rotation" in the name, see
+  test_acceptance.py:389-391) returns (d, link, voxel).
+* :func:`query_trajectory` — configurations + points/voxels → (d, link, voxel).
+
+Dense batches (the paper's materialised mode) stay supported: assembly and
+the gather query run as CUDA kernels too.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Iterable, Iterator
+
+import numpy as np
+
+from . import _native as N
+from .errors import GridMismatchError, ValidationError
+from .grids import EnvGrid, SdfSampleField
+from .meshes import TriangleMesh, primitive_surface_points
+
+DEFAULT_BATCH_BYTES = 1 << 30  # reference refuses dense batches past 1 GiB (query.py:27)
+
+
+# =========================================================================== containers
+
+
+class RobotSdfBatch:
+    """Dense per-configuration robot distance fields (query.py:30-44).
+
+    ``values`` (C, nx, ny, nz) f32; resident on the GPU, host copy on demand.
+    """
+
+    def __init__(self, values, grid: EnvGrid, d_far_global: float):
+        t = N.torch()
+        self.grid = grid
+        self.d_far_global = float(d_far_global)
+        if isinstance(values, t.Tensor):
+            self._dev = values
+            self._host = None
+        else:
+            self._host = np.asarray(values, dtype=np.float32)
+            self._dev = None
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self._dev.cpu().numpy()
+            self._host.flags.writeable = False
+        return self._host
+
+    def device_values(self):
+        if self._dev is None:
+            self._dev = N.to_device(np.ascontiguousarray(self._host), N.torch().float32)
+        return self._dev
+
+    @property
+    def n_configs(self) -> int:
+        return int((self._dev if self._dev is not None else self._host).shape[0])
+
+
+class ObstacleVoxelSet:
+    """Deduplicated occupied voxels of a point cloud (query.py:47-58).
+
+    ``indices`` (N_occ, 3) int64, lexicographically sorted when produced by
+    :func:`voxelize_pointcloud`.  The GPU occupancy structures (bit map +
+    position grid) are attached lazily and reused by every query.
+    """
+
+    def __init__(self, indices, grid: EnvGrid, n_points: int, n_dropped: int, _occupancy=None,
+                 _sorted_unique=None):
+        self.indices = indices
+        self.grid = grid
+        self.n_points = n_points
+        self.n_dropped = n_dropped
+        self._occ = _occupancy
+        self._sorted = _sorted_unique
+
+    @property
+    def n_occupied(self) -> int:
+        return len(self.indices)
+
+    def occupancy(self):
+        """(workspace tensor, by_position flag) for the query kernels."""
+        if self._occ is None:
+            idx = np.asarray(self.indices, dtype=np.int64).reshape(-1, 3)
+            if len(idx) and (np.any(idx < 0) or np.any(idx >= self.grid.dims)):
+                raise ValidationError("obstacle voxel indices outside the environment grid")
+            if self._sorted is None:
+                lin = (idx[:, 0] * self.grid.dims[1] + idx[:, 1]) * self.grid.dims[2] + idx[:, 2]
+                self._sorted = bool(np.all(np.diff(lin) > 0))
+            t = N.torch()
+            ws = N.empty((int(N.lib().lsdf_occupancy_bytes(ctypes.byref(self.grid.c_struct()))),), t.uint8)
+            d_idx = N.to_device(idx.astype(np.int32), t.int32)
+            N.call("lsdf_occupancy_from_indices", N.ptr(d_idx), len(idx), int(self._sorted),
+                   ctypes.byref(self.grid.c_struct()), N.ptr(ws), N.stream())
+            self._occ = ws
+            self._dev_idx = d_idx
+        return self._occ, (not self._sorted)
+
+    def device_indices(self):
+        if not hasattr(self, "_dev_idx"):
+            self._dev_idx = N.to_device(np.asarray(self.indices, dtype=np.int32).reshape(-1, 3), N.torch().int32)
+        return self._dev_idx
+
+
+def occupancy_workspace(grid: EnvGrid):
+    t = N.torch()
+    return N.empty((int(N.lib().lsdf_occupancy_bytes(ctypes.byref(grid.c_struct()))),), t.uint8)
+
+
+def voxelize_device(points_dev, grid: EnvGrid, workspace=None, indices_out=None):
+    """Launch the voxelizer on a device point tensor (N, 3) f32/f64."""
+    t = N.torch()
+    ws = workspace if workspace is not None else occupancy_workspace(grid)
+    f32 = points_dev.dtype == t.float32
+    if not f32 and points_dev.dtype != t.float64:
+        points_dev = points_dev.to(t.float64)
+    N.call("lsdf_voxelize", N.ptr(points_dev), int(f32), int(points_dev.shape[0]),
+           ctypes.byref(grid.c_struct()), N.ptr(ws), N.ptr(indices_out), N.stream())
+    return ws
+
+
+def voxelize_pointcloud(points, grid: EnvGrid) -> ObstacleVoxelSet:
+    """Snap a cloud to sorted unique occupied voxels, dropping out-of-bounds (query.py:106-125).
+
+    Accepts numpy (any float dtype; f32 and f64 are voxelized exactly as the
+    reference's f64 arithmetic) or a CUDA tensor.
+    """
+    t = N.torch()
+    if isinstance(points, t.Tensor):
+        pts = points.reshape(-1, 3)
+        if pts.dtype not in (t.float32, t.float64):
+            pts = pts.to(t.float64)
+        pts = N.to_device(pts)
+    else:
+        arr = np.asarray(points)
+        if arr.dtype not in (np.float32, np.float64):
+            arr = arr.astype(np.float64)
+        pts = N.to_device(np.ascontiguousarray(arr.reshape(-1, 3)))
+    n = int(pts.shape[0])
+    idx_dev = N.empty((max(1, min(n, grid.n_voxels)), 3), t.int32)
+    ws = voxelize_device(pts, grid, indices_out=idx_dev)
+    counters = ws[:8].view(t.int32).cpu().numpy()
+    n_occ, n_drop = int(counters[0]), int(counters[1])
+    idx = idx_dev[:n_occ].cpu().numpy().astype(np.int64)
+    idx.flags.writeable = False
+    out = ObstacleVoxelSet(indices=idx, grid=grid, n_points=n, n_dropped=n_drop, _occupancy=ws,
+                           _sorted_unique=True)
+    out._dev_idx = idx_dev[:n_occ]
+    return out
+
+
+# =========================================================================== trajectory handle
+
+
+class TrajectorySdf:
+    """Lazy robot-SDF batch for one trajectory (RobotSdfBatch-compatible).
+
+    Holds the geometry-link SDF grids, the window geometry and the device
+    poses (rotation, alignment residual, anchor per waypoint x link).  Queries
+    run the fused direct kernel; ``values`` assembles the dense batch on demand.
+    """
+
+    def __init__(self, sdfs, grid: EnvGrid, window, R_dev, dt_dev, anchor_dev, d_far_global=None,
+                 flags=None):
+        from .placement import _check_links, link_grid_table
+
+        _check_links(sdfs, window)
+        self.sdfs = list(sdfs)
+        self.grid = grid
+        self.window = window
+        self.R = R_dev
+        self.dt = dt_dev
+        self.anchor = anchor_dev
+        self.d_far_global = float(min(s.d_far for s in sdfs) if d_far_global is None else d_far_global)
+        self._table = link_grid_table(self.sdfs)
+        self._dense = None
+        self._flags = flags
+
+    @property
+    def n_configs(self) -> int:
+        return int(self.R.shape[0])
+
+    @property
+    def n_links(self) -> int:
+        return len(self.sdfs)
+
+    @classmethod
+    def from_poses(cls, sdfs, poses, grid: EnvGrid, provider, d_far_global=None) -> "TrajectorySdf":
+        """From geometry-link poses (LinkPoseBatch, C x L) — placement.py:289-295 alignment on GPU."""
+        from .errors import NoOverlapError
+        from .placement import _align_device
+
+        window = provider.window
+        t = N.torch()
+        C_, L = poses.n_configs, poses.n_links
+        if len(sdfs) != L:
+            raise ValidationError(f"{len(sdfs)} SDFs for {L} links")
+        R = N.to_device(np.ascontiguousarray(poses.rotations, dtype=np.float64), t.float64)
+        T = N.to_device(np.ascontiguousarray(np.asarray(poses.translations, np.float64).reshape(-1, 3)), t.float64)
+        anchor, dt, flags = _align_device(T, grid, window.dims)
+        if int(flags[1].item()):
+            raise NoOverlapError(f"{int(flags[1].item())} window(s) miss the grid entirely")
+        return cls(sdfs, grid, window, R, dt.reshape(C_, L, 3), anchor.reshape(C_, L, 3), d_far_global)
+
+    @classmethod
+    def from_configs(cls, robot, configs, sdfs, grid: EnvGrid, window, d_far_global=None,
+                     check=True) -> "TrajectorySdf":
+        """FK + alignment on the GPU for configurations (C, D) (numpy or CUDA tensor)."""
+        from .robot import ConfigBatch, check_limits, fk_device
+
+        t = N.torch()
+        if isinstance(configs, t.Tensor):
+            q = N.to_device(configs, t.float64)
+        else:
+            batch = configs if isinstance(configs, ConfigBatch) else ConfigBatch(configs)
+            if check:
+                check_limits(robot, batch)
+            q = N.to_device(batch.configurations, t.float64)
+        out = fk_device(robot, q, all_links=False, grid=grid, window_dims=window.dims)
+        traj = cls(sdfs, grid, window, out["R_geo"], out["dt_geo"], out["anchor_geo"], d_far_global,
+                   flags=out["flags"])
+        if check:
+            traj.raise_flags()
+        return traj
+
+    def raise_flags(self):
+        from .errors import NoOverlapError
+
+        if self._flags is not None:
+            f = self._flags.cpu().numpy()
+            if f[0]:
+                raise ValidationError(f"{int(f[0])} joint limit violation(s) in the configurations")
+            if f[1]:
+                raise NoOverlapError(f"{int(f[1])} window(s) miss the grid entirely")
+
+    def windows_device(self):
+        from .placement import place_windows_device
+
+        return place_windows_device(self.sdfs, self.R, self.dt, self.window)
+
+    def device_values(self, max_bytes: int = 1 << 36):
+        if self._dense is None:
+            C_, L = self.n_configs, self.n_links
+            need = C_ * self.grid.n_voxels * 4
+            if need > max_bytes:
+                raise ValidationError(f"dense robot SDF batch needs {need / 2**20:.0f} MiB, "
+                                      f"over the {max_bytes / 2**20:.0f} MiB budget")
+            t = N.torch()
+            win = self.windows_device()
+            cfg = t.arange(C_, device=win.device, dtype=t.int32).repeat_interleave(L)
+            out = N.empty((C_,) + tuple(int(d) for d in self.grid.dims), t.float32)
+            N.call("lsdf_assemble", N.ptr(win), N.ptr(self.anchor), N.ptr(cfg), C_ * L, N.i32x3(self.window.dims),
+                   ctypes.byref(self.grid.c_struct()), C_, self.d_far_global, N.ptr(out), N.stream())
+            self._dense = out
+        return self._dense
+
+    @property
+    def values(self) -> np.ndarray:
+        v = self.device_values().cpu().numpy()
+        v.flags.writeable = False
+        return v
+
+    def query_device(self, occupancy, by_position: bool, outputs=None, per_link=False):
+        """Enqueue the fused direct query; returns dict of CUDA tensors (d, link, voxel[, per_link])."""
+        t = N.torch()
+        C_ = self.n_configs
+        out = outputs if outputs is not None else {}
+        if "d" not in out:
+            out["d"] = N.empty((C_,), t.float32)
+            out["link"] = N.empty((C_,), t.int32)
+            out["voxel"] = N.empty((C_,), t.int32)
+        if per_link and "per_link" not in out:
+            out["per_link"] = N.empty((C_, self.n_links), t.float32)
+        ws, _ = self.window.device_tables()
+        N.call("lsdf_query_direct", N.ptr(self.R), N.ptr(self.dt), N.ptr(self.anchor), C_, self.n_links,
+               self._table, ctypes.byref(ws), ctypes.byref(self.grid.c_struct()), N.ptr(occupancy),
+               int(by_position), self.d_far_global, N.ptr(out["d"]), N.ptr(out["link"]), N.ptr(out["voxel"]),
+               N.ptr(out.get("per_link")), N.stream())
+        return out
+
+    def per_link_min_distances(self, obstacles: ObstacleVoxelSet) -> np.ndarray:
+        """(C, L) per-link minima (query.py:153-176) from the same fused kernel."""
+        occ, by_pos = obstacles.occupancy()
+        return self.query_device(occ, by_pos, per_link=True)["per_link"].cpu().numpy()
+
+
+# =========================================================================== reference API
+
+
+def assemble_robot_sdfs(fields: Iterable, grid: EnvGrid, n_configs: int, d_far_global: float,
+                        max_bytes: int = DEFAULT_BATCH_BYTES) -> RobotSdfBatch:
+    """Min-merge (config, field) pairs into dense robot SDFs (query.py:61-103), on the GPU."""
+    need = n_configs * grid.n_voxels * 4
+    if need > max_bytes:
+        raise ValidationError(
+            f"robot SDF batch needs {need / 2**20:.0f} MiB for {n_configs} configurations x "
+            f"{grid.n_voxels} voxels, over the {max_bytes / 2**20:.0f} MiB budget")
+    t = N.torch()
+    groups: dict[tuple, list] = {}
+    for c, field in fields:
+        if not 0 <= c < n_configs:
+            raise ValidationError(f"configuration index {c} out of range")
+        groups.setdefault(tuple(field.window_dims), []).append((c, field))
+    out = N.empty((n_configs,) + tuple(int(d) for d in grid.dims), t.float32)
+    N.call("lsdf_fill", N.ptr(out), out.numel(), float(np.float32(d_far_global)), N.stream())
+    for wd, items in groups.items():
+        vals = np.stack([np.ravel(f.values, order="F") for _, f in items]).astype(np.float32)
+        anchors = np.stack([np.asarray(f.anchor, dtype=np.int64) for _, f in items]).astype(np.int32)
+        cfg = np.asarray([c for c, _ in items], dtype=np.int32)
+        N.call("lsdf_assemble", N.ptr(N.to_device(vals)), N.ptr(N.to_device(anchors)), N.ptr(N.to_device(cfg)),
+               len(items), N.i32x3(wd), ctypes.byref(grid.c_struct()), 0, float(d_far_global), N.ptr(out),
+               N.stream())
+    return RobotSdfBatch(values=out, grid=grid, d_far_global=float(d_far_global))
+
+
+def _clamp_rule(d, link, voxel, clamp):
+    far = d == np.float32(clamp)
+    link = np.where(far, -1, link).astype(np.int32)
+    voxel = np.where(far, -1, voxel).astype(np.int32)
+    return link, voxel
+
+
+def query_min_distances(batch, obstacles: ObstacleVoxelSet, return_stats: bool = False, *,
+                        return_argmin: bool = False):
+    """Minimum robot-obstacle distance per configuration (query.py:128-150).
+
+    ``batch`` is a dense :class:`RobotSdfBatch` (gather + min kernel) or a
+    :class:`TrajectorySdf` (fused direct kernel, same values).  With
+    ``return_argmin`` the result is (d, link, voxel): voxel is the position in
+    ``obstacles.indices`` of the first minimum, link the lowest geometry link
+    attaining it (dense batches carry no link identity: -1); both are -1 when
+    d equals float32(d_far_global).  ``return_stats`` reports the algorithmic
+    gather count C x |occupied| (query.py:144-149).
+    """
+    if not batch.grid.same_geometry(obstacles.grid):
+        raise GridMismatchError("obstacle set was voxelized on a different grid")
+    C_ = batch.n_configs
+    stats = {"gathers": int(C_ * obstacles.n_occupied)}
+    clamp = np.float32(batch.d_far_global)
+    if obstacles.n_occupied == 0:
+        d = np.full(C_, clamp, dtype=np.float32)
+        link = np.full(C_, -1, np.int32)
+        voxel = np.full(C_, -1, np.int32)
+    elif isinstance(batch, TrajectorySdf):
+        occ, by_pos = obstacles.occupancy()
+        out = batch.query_device(occ, by_pos)
+        d, link, voxel = (out["d"].cpu().numpy(), out["link"].cpu().numpy(), out["voxel"].cpu().numpy())
+    else:
+        t = N.torch()
+        d_dev = N.empty((C_,), t.float32)
+        a_dev = N.empty((C_,), t.int32)
+        N.call("lsdf_query_dense", N.ptr(batch.device_values()), C_, ctypes.byref(batch.grid.c_struct()),
+               N.ptr(obstacles.device_indices()), obstacles.n_occupied, N.ptr(d_dev), N.ptr(a_dev), N.stream())
+        d = d_dev.cpu().numpy()
+        link, voxel = _clamp_rule(d, np.full(C_, -1), a_dev.cpu().numpy(), clamp)
+    result = (d, link, voxel) if return_argmin else d
+    return (result, stats) if return_stats else result
+
+
+def per_link_min_distances(fields, obstacles: ObstacleVoxelSet, n_configs: int, n_links: int,
+                           d_far_global: float) -> np.ndarray:
+    """Per-(configuration, link) minima from (config, link, field) triples (query.py:153-176)."""
+    t = N.torch()
+    out = N.empty((n_configs, n_links), t.float32)
+    N.call("lsdf_fill", N.ptr(out), out.numel(), float(np.float32(d_far_global)), N.stream())
+    occ, _ = obstacles.occupancy() if obstacles.n_occupied else (occupancy_workspace(obstacles.grid), False)
+    if obstacles.n_occupied == 0:
+        N.call("lsdf_occupancy_from_indices", None, 0, 1, ctypes.byref(obstacles.grid.c_struct()), N.ptr(occ),
+               N.stream())
+    groups: dict[tuple, list] = {}
+    for c, li, f in fields:
+        groups.setdefault(tuple(f.window_dims), []).append((c, li, f))
+    for wd, items in groups.items():
+        vals = np.stack([np.ravel(f.values, order="F") for *_, f in items]).astype(np.float32)
+        anchors = np.stack([np.asarray(f.anchor) for *_, f in items]).astype(np.int32)
+        cfg = np.asarray([c for c, _, _ in items], np.int32)
+        lnk = np.asarray([li for _, li, _ in items], np.int32)
+        dfar = np.asarray([np.float32(f.d_far) for *_, f in items], np.float32)
+        N.call("lsdf_per_link_fields", N.ptr(N.to_device(vals)), N.ptr(N.to_device(anchors)),
+               N.ptr(N.to_device(cfg)), N.ptr(N.to_device(lnk)), N.ptr(N.to_device(dfar)), len(items),
+               N.i32x3(wd), n_links, ctypes.byref(obstacles.grid.c_struct()), N.ptr(occ), N.ptr(out), N.stream())
+    return out.cpu().numpy()
+
+
+def stream_min_distances(batch, frames: Iterable) -> Iterator[tuple[float, np.ndarray]]:
+    """Per-cycle distance vectors for (timestamp, points) frames (query.py:294-306)."""
+    for timestamp, points in frames:
+        yield timestamp, query_min_distances(batch, voxelize_pointcloud(points, batch.grid))
+
+
+def query_trajectory(robot, configs, sdfs, grid: EnvGrid, provider_or_window, points=None, *,
+                     obstacles: ObstacleVoxelSet | None = None, d_far_global=None):
+    """Configurations + points (or voxels) -> (d f32[C], link i32[C], voxel i32[C]).
+
+    ``link`` indexes the geometry links (``robot.geometry_links``); ``voxel``
+    is the position in the sorted occupied-voxel list.
+    """
+    window = getattr(provider_or_window, "window", provider_or_window)
+    traj = TrajectorySdf.from_configs(robot, configs, sdfs, grid, window, d_far_global)
+    obs = obstacles if obstacles is not None else voxelize_pointcloud(points, grid)
+    return query_min_distances(traj, obs, return_argmin=True)
+
+
+# =========================================================================== sphere baseline
+
+
+@dataclass(frozen=True, eq=False)
+class SphereRobotModel:
+    """Per-link covering spheres in link frames (query.py:179-212)."""
+
+    link_indices: np.ndarray
+    centers: np.ndarray
+    radii: np.ndarray
+
+    def __post_init__(self):
+        if np.any(self.radii <= 0):
+            raise ValidationError("sphere radii must be positive")
+
+    @property
+    def n_spheres(self) -> int:
+        return len(self.radii)
+
+    @classmethod
+    def from_robot(cls, model) -> "SphereRobotModel":
+        li, ce, ra = [], [], []
+        for link_name, spheres in model.sphere_model.items():
+            idx = model.link_index(link_name)
+            for center, radius in spheres:
+                li.append(idx)
+                ce.append(center)
+                ra.append(radius)
+        if not ra:
+            raise ValidationError(f"robot {model.name} declares no spheres")
+        return cls(link_indices=np.int64(li), centers=np.float64(ce), radii=np.float64(ra))
+
+
+def validate_sphere_model(model, spheres: SphereRobotModel, rng: np.random.Generator, n_samples: int = 2048,
+                          tol: float = 1e-9) -> float:
+    """Check the spheres cover each link's surface samples (query.py:215-251); host-side validation."""
+    worst = -np.inf
+    for li, link in enumerate(model.links):
+        if link.geometry is None:
+            continue
+        mine = spheres.link_indices == li
+        if not np.any(mine):
+            raise ValidationError(f"link {link.name} has geometry but no spheres")
+        if isinstance(link.geometry, TriangleMesh):
+            surface = link.geometry.sample_surface(n_samples, rng)
+        else:
+            surface = primitive_surface_points(link.geometry, n_samples, rng)
+        d = (np.linalg.norm(surface[:, None, :] - spheres.centers[None, mine], axis=-1)
+             - spheres.radii[mine]).min(axis=1)
+        worst = max(worst, float(d.max()))
+        if worst > tol:
+            raise ValidationError(f"link {link.name}: surface escapes the covering spheres by {worst:.2e} m")
+    return worst
+
+
+def sphere_baseline_distances(spheres: SphereRobotModel, poses, obstacles: ObstacleVoxelSet, grid: EnvGrid,
+                              chunk: int = 64, return_stats: bool = False):
+    """Covering-sphere comparator (query.py:254-291), evaluated on the GPU in fp64."""
+    if not grid.same_geometry(obstacles.grid):
+        raise GridMismatchError("obstacle set was voxelized on a different grid")
+    C_ = poses.n_configs
+    if obstacles.n_occupied == 0:
+        d = np.full(C_, np.inf, dtype=np.float64)
+        return (d, {"distance_evals": 0}) if return_stats else d
+    t = N.torch()
+    L = poses.n_links
+    R = N.to_device(np.ascontiguousarray(poses.rotations, dtype=np.float64), t.float64)
+    T = N.to_device(np.ascontiguousarray(poses.translations, dtype=np.float64), t.float64)
+    out = N.empty((C_,), t.float64)
+    N.call("lsdf_sphere_baseline", N.ptr(R), N.ptr(T), C_, L,
+           N.ptr(N.to_device(spheres.link_indices.astype(np.int32))),
+           N.ptr(N.to_device(np.ascontiguousarray(spheres.centers, dtype=np.float64))),
+           N.ptr(N.to_device(np.ascontiguousarray(spheres.radii, dtype=np.float64))), spheres.n_spheres,
+           N.ptr(obstacles.device_indices()), obstacles.n_occupied, ctypes.byref(grid.c_struct()), N.ptr(out),
+           N.stream())
+    d = out.cpu().numpy()
+    if return_stats:
+        return d, {"distance_evals": int(C_ * spheres.n_spheres * obstacles.n_occupied)}
+    return d
+
+
+# =========================================================================== frame IO (host plumbing)
+
+
+def write_pointcloud_frame(path, points) -> None:
+    """Count-prefixed little-endian f32 xyz triples."""
+    pts = np.asarray(points, dtype=np.float32).reshape(-1, 3)
+    with open(path, "wb") as fh:
+        fh.write(struct.pack("<I", len(pts)))
+        fh.write(np.ascontiguousarray(pts, dtype="<f4").tobytes())
+
+
+def read_pointcloud_frame(path) -> np.ndarray:
+    with open(path, "rb") as fh:
+        (count,) = struct.unpack("<I", fh.read(4))
+        raw = np.frombuffer(fh.read(12 * count), dtype="<f4")
+        if raw.size != 3 * count:
+            raise ValidationError(f"{path}: truncated point data")
+    return raw.reshape(count, 3).astype(np.float64)
+
+
+def read_cloud_manifest(path) -> list[tuple[float, Path]]:
+    base = Path(path).parent
+    frames = []
+    with open(path) as fh:
+        for line in fh:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            stamp, name = line.split(maxsplit=1)
+            frames.append((float(stamp), base / name))
+    return frames
+
+
+def iter_cloud_frames(manifest_path) -> Iterator[tuple[float, np.ndarray]]:
+    for stamp, frame_path in read_cloud_manifest(manifest_path):
+        yield stamp, read_pointcloud_frame(frame_path)
+
+
+def write_distance_csv(path, rows, n_configs: int) -> None:
+    with open(path, "w") as fh:
+        fh.write(",".join(["timestamp_ms"] + [f"d_{i}" for i in range(n_configs)]) + "\n")
+        for stamp, dists in rows:
+            fh.write(f"{stamp:.3f}," + ",".join(f"{d:.6f}" for d in dists) + "\n")

@@ -1,0 +1,372 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the reference goldens and the oracle.
+
+Bars (north_star): FK <= 1e-12 abs; anchors, voxel indices,
+argmin link/voxel bit-exact; primitive link grids, windows, assembled fields
+and distances bit-exact in fp32 when the poses are the reference's own
+(stage isolation); distances from GPU FK within 1e-6 m (the fp64 sin/cos of
+the device may differ from the host libm in the last ulp); mesh grids within
+1e-5 m; MLP outputs within 1e-5 (normalized).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from tests.conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+D_TOL = 1e-6      # m, distances from device FK vs reference FK
+MESH_TOL = 1e-5   # m, SURVEY §8c
+MLP_TOL = 1e-5    # normalized coordinates
+
+
+@pytest.fixture(scope="module")
+def L():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2309_12543_b200 as lib
+
+    return lib
+
+
+def _doc(g):
+    return json.loads(bytes(g["robot_json"]).decode())
+
+
+def _scene(L, g):
+    robot = L.RobotModel.from_dict(_doc(g))
+    grid = L.EnvGrid(float(g["env_extent"]), float(g["env_res"]))
+    e_r, r_r = float(g["e_r"]), float(g["r_r"])
+    sdfs = [L.build_link_sdf(robot.links[i].geometry, e_r, r_r, link_id=i) for i in robot.geometry_links]
+    window = L.WindowGeometry.build(e_r, grid)
+    return robot, grid, sdfs, window
+
+
+# ----------------------------------------------------------------------------- stage 1
+
+
+@pytest.mark.parametrize("name", ["scene_c1", "scene_arm7", "scene_small"])
+def test_fk_batch(L, name):
+    g = golden(name)
+    robot = L.RobotModel.from_dict(_doc(g))
+    poses = L.forward_kinematics_batch(robot, L.ConfigBatch(g["q"]))
+    assert np.abs(poses.rotations - g["R"]).max() <= 1e-12
+    assert np.abs(poses.translations - g["T"]).max() <= 1e-12
+
+
+def test_fk_known_answers(L, tmp_path):
+    # test_robot.py:114-155
+    doc = {"name": "one", "links": [{"name": "base"}, {"name": "child", "parent_joint": "j",
+                                                         "origin": {"xyz": [1, 0, 0]}}],
+           "joints": [{"name": "j", "type": "revolute", "parent_link": "base", "axis": [0, 0, 1],
+                       "limits": {"position": [-7, 7], "velocity": 1, "acceleration": 1}}]}
+    m = L.RobotModel.from_dict(doc)
+    p = L.forward_kinematics_batch(m, L.ConfigBatch([[np.pi / 2]]))
+    assert np.allclose(p.translations[0, 1], [0, 1, 0], atol=1e-15)
+    doc = {"name": "slider", "links": [{"name": "base"}, {"name": "car", "parent_joint": "j",
+                                                          "origin": {"xyz": [0, 0.1, 0]}}],
+           "joints": [{"name": "j", "type": "prismatic", "parent_link": "base",
+                       "origin": {"rpy": [0, 0, np.pi / 2]}, "axis": [1, 0, 0],
+                       "limits": {"position": [-0.5, 0.5], "velocity": 1, "acceleration": 2}}]}
+    m = L.RobotModel.from_dict(doc)
+    p = L.forward_kinematics_batch(m, L.ConfigBatch([[0.3]]))
+    assert np.allclose(p.translations[0, 1], [-0.1, 0.3, 0], atol=1e-15)
+    with pytest.raises(L.LimitViolationError) as err:
+        L.forward_kinematics_batch(m, L.ConfigBatch([[0.0], [0.9]]))
+    assert (1, 0) in err.value.violations
+
+
+def test_alignment(L):
+    # test_placement.py:55-87
+    grid = L.EnvGrid(1.0, 0.1)
+    a = L.compute_alignment(np.float64([0.10, 0.05, 0.05]), grid, 0.3)
+    assert list(a.anchor) == [8, 7, 7] and np.allclose(a.delta_t, [-0.05, 0, 0], atol=1e-15)
+    a = L.compute_alignment(np.float64([1.05, 0.0, 0.0]), grid, 0.3)
+    assert list(a.anchor) == [17, 7, 7]
+    with pytest.raises(L.NoOverlapError):
+        L.compute_alignment(np.float64([1.7, 0.0, 0.0]), grid, 0.3)
+    rng = np.random.default_rng(5)
+    t = rng.uniform(-0.99, 0.99, size=(100_000, 3))
+    a = L.compute_alignment(t, grid, 0.3)
+    from oracle import linksdf_oracle as O
+
+    ra, rd, _ = O.align(t, O.Env(1.0, 0.1), 0.3)
+    assert np.array_equal(a.anchor, ra) and np.array_equal(a.delta_t, rd)
+
+
+# ----------------------------------------------------------------------------- obstacles
+
+
+@pytest.mark.parametrize("name", ["scene_c1", "scene_c2", "scene_small", "scene_arm7"])
+def test_voxelize(L, name):
+    g = golden(name)
+    grid = L.EnvGrid(float(g["env_extent"]), float(g["env_res"]))
+    v = L.voxelize_pointcloud(g["points"], grid)
+    assert np.array_equal(v.indices, g["indices"])
+    assert v.n_dropped == int(g["n_dropped"]) and v.n_points == int(g["n_points"])
+    v32 = L.voxelize_pointcloud(g["points"].astype(np.float32), grid)
+    from oracle import linksdf_oracle as O
+
+    idx, _, drop = O.voxelize(g["points"].astype(np.float32), O.Env(float(g["env_extent"]), float(g["env_res"])))
+    assert np.array_equal(v32.indices, idx) and v32.n_dropped == drop
+
+
+def test_voxelize_edges(L):
+    # test_query.py:105-136 + face/NaN/empty cases
+    grid = L.EnvGrid(1.0, 0.1)
+    v = L.voxelize_pointcloud(np.empty((0, 3)), grid)
+    assert v.n_occupied == 0 and v.n_points == 0 and v.n_dropped == 0
+    v = L.voxelize_pointcloud(np.tile(np.float64([0.31, 0.02, -0.44]), (1000, 1)), grid)
+    assert v.n_occupied == 1 and v.n_points == 1000
+    v = L.voxelize_pointcloud(np.float64([[0, 0, 0], [2, 0, 0], [0, -3, 0], [1.0, 0, 0], [-1.0, 0, 0],
+                                          [np.nan, 0, 0]]), grid)
+    assert v.n_dropped == 4 and v.indices.tolist() == [[0, 10, 10], [10, 10, 10]]
+    assert np.array_equal(L.voxel_index_of(np.float64([0.05, 0.05, 0.05]), grid), [10, 10, 10])
+    with pytest.raises(L.OutOfBoundsError):
+        L.voxel_index_of(np.float64([1.0, 0.0, 0.0]), grid)
+
+
+# ----------------------------------------------------------------------------- stage 2a
+
+
+def test_build_primitives_bit_exact(L):
+    b = golden("builds")
+    from tests.test_hostcheck import _prim_params  # noqa: F401  (same parameter mapping)
+
+    for key in [k for k in b.files if k.startswith("prim_") and not k.endswith("_json")]:
+        geom = json.loads(bytes(b[key + "_json"]).decode())
+        shape = {"sphere": lambda g: L.Sphere(g["radius"], center=g.get("center", (0, 0, 0))),
+                 "capsule": lambda g: L.Capsule(g["radius"], g["half_length"], axis=g.get("axis", (0, 0, 1))),
+                 "box": lambda g: L.Box(g["half_extents"])}[geom["type"]](geom)
+        s = L.build_link_sdf(shape, 0.2, 0.01)
+        assert np.array_equal(s.values, b[key]), key
+
+
+def test_build_meshes(L):
+    b = golden("builds")
+    for name in ("ico", "box", "tiltbox", "open"):
+        m = L.TriangleMesh(b[f"mesh_{name}_V"], b[f"mesh_{name}_F"])
+        e, r = b[f"mesh_{name}_er"]
+        s = L.build_link_sdf(m, e, r)
+        ref = b[f"mesh_{name}"]
+        assert np.abs(s.values - ref).max() <= MESH_TOL, name
+        assert np.mean(s.values == ref) > 0.999, name
+
+
+def test_scene_grids_bit_exact(L):
+    g = golden("scene_c1")
+    _, _, sdfs, _ = _scene(L, g)
+    for k, s in enumerate(sdfs):
+        assert np.array_equal(s.values, g["grids"][k])
+    g2 = golden("scene_c2")
+    _, _, sdfs2, _ = _scene(L, g2)
+    cells = g2["grid_cells"]
+    for k, s in enumerate(sdfs2):
+        v = s.values
+        assert np.array_equal(v[cells[:, 0], cells[:, 1], cells[:, 2]], g2["grid_samples"][k])
+        assert v.astype(np.float64).sum() == g2["grid_sums"][k]
+
+
+def test_trilinear(L):
+    t = golden("trilinear")
+    s = L.LinkSdf(float(t["extent"]), float(t["res"]), t["values"], 0)
+    assert np.array_equal(L.trilinear_sample(s, t["pts"]), t["out"])
+
+
+# ----------------------------------------------------------------------------- placement / assembly
+
+
+def test_place_and_assemble_bit_exact(L):
+    g = golden("scene_small")
+    robot, grid, sdfs, window = _scene(L, g)
+    gl = g["geometry_links"]
+    poses = L.LinkPoseBatch(rotations=g["R"][:, gl], translations=g["T"][:, gl])
+    prov = L.ExactTransformProvider(window)
+    fields = list(L.place_links_batch(sdfs, poses, grid, prov))
+    for c, li, f in fields:
+        assert np.array_equal(f.anchor, g["anchors"][c, li])
+        assert np.array_equal(f.values, g["windows"][c, li])
+    batch = L.assemble_robot_sdfs(((c, f) for c, _, f in fields), grid, len(g["q"]), float(g["d_far_global"]))
+    assert np.array_equal(batch.values, g["batch"])
+    obs = L.voxelize_pointcloud(g["points"], grid)
+    d, link, voxel = L.query_min_distances(batch, obs, return_argmin=True)
+    assert np.array_equal(d, g["d"]) and np.array_equal(voxel, g["voxel"])
+    pl = L.per_link_min_distances(iter(fields), obs, len(g["q"]), len(gl), float(g["d_far_global"]))
+    assert np.array_equal(pl, g["per_link"])
+    traj = L.TrajectorySdf.from_poses(sdfs, poses, grid, prov)
+    assert np.array_equal(traj.values, g["batch"])
+
+
+# ----------------------------------------------------------------------------- stages 3+4
+
+
+@pytest.mark.parametrize("name", ["scene_c1", "scene_c2", "scene_small", "scene_arm7"])
+def test_direct_query_stage_isolated(L, name):
+    """Reference poses in, (d, link, voxel) out: bit-exact against the reference."""
+    g = golden(name)
+    robot, grid, sdfs, window = _scene(L, g)
+    gl = g["geometry_links"]
+    poses = L.LinkPoseBatch(rotations=g["R"][:, gl], translations=g["T"][:, gl])
+    traj = L.TrajectorySdf.from_poses(sdfs, poses, grid, L.ExactTransformProvider(window))
+    obs = L.voxelize_pointcloud(g["points"], grid)
+    (d, link, voxel), stats = L.query_min_distances(traj, obs, return_stats=True, return_argmin=True)
+    assert stats["gathers"] == len(g["q"]) * len(g["indices"])
+    assert np.array_equal(d, g["d"])
+    assert np.array_equal(link, g["link"])
+    assert np.array_equal(voxel, g["voxel"])
+    assert np.array_equal(traj.per_link_min_distances(obs), g["per_link"])
+
+
+@pytest.mark.parametrize("name", ["scene_c1", "scene_c2", "scene_arm7"])
+def test_full_pipeline_from_configs(L, name):
+    g = golden(name)
+    robot, grid, sdfs, window = _scene(L, g)
+    d, link, voxel = L.query_trajectory(robot, g["q"], sdfs, grid, window, g["points"])
+    assert np.abs(d.astype(np.float64) - g["d"]).max() <= D_TOL
+    assert np.array_equal(link, g["link"]) and np.array_equal(voxel, g["voxel"])
+
+
+def test_checker_graph_path(L):
+    g = golden("scene_c2")
+    robot, grid, sdfs, window = _scene(L, g)
+    chk = L.DistanceChecker(robot, sdfs, grid, window).prepare(len(g["q"]), 40_000, np.float64)
+    for _ in range(3):  # replay determinism
+        d, link, voxel = chk.query(g["q"], g["points"])
+        assert np.abs(d.astype(np.float64) - g["d"]).max() <= D_TOL
+        assert np.array_equal(link, g["link"]) and np.array_equal(voxel, g["voxel"])
+    q_bad = g["q"].copy()
+    q_bad[3, 1] = 9.0
+    with pytest.raises(L.LimitViolationError) as err:
+        chk.query(q_bad, g["points"])
+    assert (3, 1) in err.value.violations
+
+
+def test_known_answer_tie_clamp_empty(L):
+    k = golden("known_answer")
+    grid = L.EnvGrid(1.0, 0.1)
+    sdfs = [L.build_link_sdf(L.Sphere(0.12), 0.3, 0.01, link_id=0),
+            L.build_link_sdf(L.Box([0.05, 0.05, 0.05]), 0.3, 0.01, link_id=1)]
+    for s, ref in zip(sdfs, k["grids"]):
+        assert np.array_equal(s.values, ref)
+    window = L.WindowGeometry.build(0.3, grid)
+    traj = L.TrajectorySdf.from_poses(sdfs, L.LinkPoseBatch(k["R"], k["T"]), grid, L.ExactTransformProvider(window))
+    for name in ("tie", "far", "empty"):
+        idx = k[f"{name}_indices"]
+        obs = L.ObstacleVoxelSet(indices=idx, grid=grid, n_points=len(idx), n_dropped=0)
+        d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
+        assert np.array_equal(d, k[f"{name}_d"]), name
+        assert np.array_equal(link, k[f"{name}_link"]), name
+        assert np.array_equal(voxel, k[f"{name}_voxel"]), name
+
+
+def test_unsorted_and_duplicate_obstacles(L):
+    """General index lists: first-occurrence argmin like numpy (query.py:146)."""
+    from oracle import linksdf_oracle as O
+
+    g = golden("scene_small")
+    robot, grid, sdfs, window = _scene(L, g)
+    gl = g["geometry_links"]
+    poses = L.LinkPoseBatch(rotations=g["R"][:, gl], translations=g["T"][:, gl])
+    traj = L.TrajectorySdf.from_poses(sdfs, poses, grid, L.ExactTransformProvider(window))
+    rng = np.random.default_rng(3)
+    idx = g["indices"][rng.permutation(len(g["indices"]))]
+    idx = np.concatenate([idx, idx[:50]])
+    obs = L.ObstacleVoxelSet(indices=idx, grid=grid, n_points=len(idx), n_dropped=0)
+    d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
+    env = O.Env(float(g["env_extent"]), float(g["env_res"]))
+    anchors = g["anchors"]
+    rd, rl, rv = O.argmin_oracle(g["batch"], g["windows"], anchors, idx, float(g["d_far_global"]))
+    assert np.array_equal(d, rd) and np.array_equal(link, rl) and np.array_equal(voxel, rv)
+    assert env.dims[0] == grid.dims[0]
+
+
+def test_stream_min_distances(L):
+    g = golden("scene_small")
+    robot, grid, sdfs, window = _scene(L, g)
+    traj = L.TrajectorySdf.from_configs(robot, g["q"], sdfs, grid, window)
+    frames = [(float(i), g["points"]) for i in range(3)] + [(3.0, np.empty((0, 3)))]
+    rows = list(L.stream_min_distances(traj, frames))
+    assert all(np.array_equal(r[1], rows[0][1]) for r in rows[:3])
+    assert np.all(rows[3][1] == np.float32(traj.d_far_global))
+
+
+# ----------------------------------------------------------------------------- stage 2b
+
+
+def test_mlp_predict(L):
+    m = golden("mlp")
+    model = L.TinyMlp(m["w1"], m["b1"], m["w2"], m["b2"])
+    y = model.predict(m["R"])
+    assert np.abs(y - m["predict"]).max() <= MLP_TOL
+    g = L.infer_grid_transform(model, m["R"], m["dt"], 0.3)
+    assert np.abs(g - m["infer"]).max() <= MLP_TOL
+    ex = L.grid_transform_exact(m["R"], m["dt"], 0.3, m["masked_points"])
+    assert np.array_equal(ex, m["exact"])
+
+
+def test_sphere_baseline(L):
+    from oracle import linksdf_oracle as O
+
+    g = golden("scene_small")
+    robot = L.RobotModel.from_dict(_doc(g))
+    grid = L.EnvGrid(float(g["env_extent"]), float(g["env_res"]))
+    li = np.int64([1, 2, 3, 6])
+    centers = np.float64([[0, 0, 0.02], [0, 0, -0.03], [0.01, 0, 0], [0, 0, 0]])
+    radii = np.float64([0.08, 0.07, 0.06, 0.05])
+    sph = L.SphereRobotModel(li, centers, radii)
+    poses = L.LinkPoseBatch(g["R"], g["T"])
+    obs = L.voxelize_pointcloud(g["points"], grid)
+    d, st = L.sphere_baseline_distances(sph, poses, obs, grid, return_stats=True)
+    assert st["distance_evals"] == len(g["q"]) * 4 * obs.n_occupied
+    tgt = O.Env(float(g["env_extent"]), float(g["env_res"])).centers(obs.indices)
+    world = np.einsum("bsij,sj->bsi", g["R"][:, li], centers) + g["T"][:, li]
+    ref = (np.linalg.norm(world[:, :, None] - tgt[None, None], axis=-1) - radii[None, :, None]).min(axis=(1, 2))
+    assert np.abs(d - ref).max() <= 1e-12
+    assert robot.n_links == 7
+
+
+# ----------------------------------------------------------------------------- full-size properties
+
+
+def test_config2_full_size_properties(L):
+    """BASELINE config 2 at full size: direct == dense gather, oracle on a subset, invariances."""
+    from oracle import linksdf_oracle as O
+    from paper_2309_12543_b200 import scenarios as S
+
+    shape = S.CONFIG2
+    robot = L.RobotModel.from_dict(shape.robot)
+    grid = L.EnvGrid(shape.grid_extent, shape.grid_res)
+    sdfs = [L.build_link_sdf(robot.links[i].geometry, shape.link_extent, shape.link_res, link_id=i)
+            for i in robot.geometry_links]
+    window = L.WindowGeometry.build(shape.link_extent, grid)
+    q = S.random_configs(shape.robot, shape.n_waypoints, seed=0)
+    pts = S.cloud_for(shape, seed=0)
+    traj = L.TrajectorySdf.from_configs(robot, q, sdfs, grid, window)
+    obs = L.voxelize_pointcloud(pts, grid)
+    d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
+    dense = L.RobotSdfBatch(traj.device_values(), grid, traj.d_far_global)
+    d2, _, v2 = L.query_min_distances(dense, obs, return_argmin=True)
+    assert np.array_equal(d, d2) and np.array_equal(voxel, v2)
+    # oracle (reference restatement) on 12 waypoints of the full cloud
+    sub = np.arange(0, shape.n_waypoints, 42)
+    grids = [s.values for s in sdfs]
+    rd, rl, rv = O.run_pipeline(shape.robot, q[sub], pts, shape.grid_extent, shape.grid_res,
+                                shape.link_extent, grids, [shape.link_res] * len(grids))
+    assert np.abs(d[sub].astype(np.float64) - rd).max() <= D_TOL
+    assert np.array_equal(link[sub], rl) and np.array_equal(voxel[sub], rv)
+    # permutation of the cloud changes nothing; a superset never increases d
+    perm = np.random.default_rng(1).permutation(len(pts))
+    dp = L.query_min_distances(traj, L.voxelize_pointcloud(pts[perm], grid))
+    assert np.array_equal(dp, d)
+    more = np.concatenate([pts, S.human_cloud(20_000, seed=9)])
+    dm = L.query_min_distances(traj, L.voxelize_pointcloud(more, grid))
+    assert np.all(dm <= d)
+    # waypoint sharding (the multi-GPU partition) is exact: shards == whole
+    halves = [L.TrajectorySdf.from_configs(robot, q[s], sdfs, grid, window)
+              for s in (slice(0, 250), slice(250, 500))]
+    ds = np.concatenate([L.query_min_distances(h, obs) for h in halves])
+    assert np.array_equal(ds, d)

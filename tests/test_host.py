@@ -1,0 +1,104 @@
+"""CPU-only tests: the C-ABI library loads and exports the header, host-side
+tables are right, and the product fails loudly without a GPU (no CPU path)."""
+
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+from tests.conftest import REPO
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2309_12543_b200 import _native as N
+    from paper_2309_12543_b200.build import build
+
+    build()
+    lib = ctypes.CDLL(str(N.LIB_PATH))
+    header = (REPO / "include" / "linksdf_b200.h").read_text()
+    declared = set(re.findall(r"^\s*(?:int|int64_t|uint64_t|const char\*)\s+(lsdf_\w+)\s*\(", header, re.M))
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(N.EXPORTS) == declared
+    N.load_library()
+    assert b"sm_100a" in N.lib().lsdf_version()
+
+
+def test_ctypes_struct_layouts_match_header():
+    from paper_2309_12543_b200 import _native as N
+
+    # sizes implied by include/linksdf_b200.h on LP64
+    assert ctypes.sizeof(N.EnvGridT) == 64
+    assert ctypes.sizeof(N.LinkT) == 16 + 45 * 8
+    assert ctypes.sizeof(N.LinkGridT) == 8 + 12 + 4 + 48
+    assert ctypes.sizeof(N.WindowT) == 16 + 8 + 8 + 8 + 8 + 8
+
+
+def test_sass_is_sm100a():
+    import subprocess
+
+    from paper_2309_12543_b200 import _native as N
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(N.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2309_12543_b200 as L
+
+    grid = L.EnvGrid(1.0, 0.1)
+    with pytest.raises(L.LinkSdfError):
+        L.voxelize_pointcloud(np.zeros((4, 3)), grid)
+    with pytest.raises(L.LinkSdfError):
+        L.build_link_sdf(L.Sphere(0.1), 0.2, 0.05)
+
+
+def test_window_tables_match_mask():
+    import paper_2309_12543_b200 as L
+
+    for res, e in ((0.04, 0.32), (0.1, 0.3), (0.04, 1.2), (0.01, 0.64)):
+        grid = L.EnvGrid(1.0 if res > 0.01 else 1.28, res)
+        w = L.WindowGeometry.build(e, grid)
+        W = w.dims
+        m = w.mask
+        for mx in range(0, W[0], max(1, W[0] // 7)):
+            for my in range(W[1]):
+                zs = np.nonzero(m[mx, my])[0]
+                if len(zs):
+                    assert zs[-1] + 1 - zs[0] == len(zs)  # ball rows are intervals along z
+    w = L.WindowGeometry.build(0.32, L.EnvGrid(1.0, 0.04))
+    assert w.n_masked == 2103  # SURVEY §8 probe
+
+
+def test_chain_table_constants():
+    import paper_2309_12543_b200 as L
+    from paper_2309_12543_b200 import scenarios as S
+
+    robot = L.RobotModel.from_dict(S.ARM7G)
+    t = robot.chain_table()
+    assert robot.dof == 7 and robot.n_links == 8 and robot.geometry_links == list(range(1, 8))
+    assert t[0].kind == 0 and t[1].kind == 1 and t[7].geom_slot == 6 and t[7].parent == 6
+    j2 = robot.joint("j2")
+    assert np.array_equal(np.array(t[2].joint_R[:]).reshape(3, 3), j2.origin.rotation)
+
+
+def test_validation_errors_host_side():
+    import paper_2309_12543_b200 as L
+
+    with pytest.raises(L.ValidationError):
+        L.EnvGrid(1.0, 0.3)
+    with pytest.raises(L.ValidationError):
+        L.window_dims(0.25, L.EnvGrid(1.0, 0.1))
+    with pytest.raises(L.ValidationError):
+        L.canonical_points([0.3, 0.3, 0.2], L.EnvGrid(1.0, 0.1))
+    with pytest.raises(L.ValidationError):
+        L.masked_window_points(5)
+    g = L.EnvGrid(1.0, 0.1)
+    with pytest.raises(L.ValidationError):
+        L.assemble_robot_sdfs([], g, 10_000_000, 0.5, max_bytes=1 << 20)
