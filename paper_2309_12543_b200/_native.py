@@ -125,7 +125,15 @@ def lib():
 
 
 def call(name: str, *args) -> int:
-    rc = getattr(lib(), name)(*args)
+    """Invoke an entry point; CUDA tensors may be passed directly (their
+    pointers are taken here, and ``args`` keeps them alive until the launch
+    is enqueued, so temporaries cannot be recycled under a pending copy)."""
+    t = _torch
+    if t is not None:
+        cargs = [a.data_ptr() if isinstance(a, t.Tensor) else a for a in args]
+    else:
+        cargs = args
+    rc = getattr(lib(), name)(*cargs)
     if rc != 0:
         msg = lib().lsdf_last_error().decode(errors="replace")
         raise _ERRORS.get(rc, errors.LinkSdfError)(f"{name}: {msg}")
@@ -170,6 +178,8 @@ def to_device(a, dtype=None):
         out = a.to(device=device(), dtype=dtype) if dtype is not None else a.to(device=device())
         return out.contiguous()
     arr = np.ascontiguousarray(a)
+    if not arr.flags.writeable:
+        arr = arr.copy()
     out = t.from_numpy(arr).to(device(), non_blocking=False)
     if dtype is not None:
         out = out.to(dtype)

@@ -120,8 +120,8 @@ def grid_transform_exact(rotations, delta_t, extent_r, points):
     P = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 3))
     t = N.torch()
     G = N.empty((len(r), len(P), 3), t.float64)
-    N.call("lsdf_grid_transform_exact", N.ptr(N.to_device(r, t.float64)), N.ptr(N.to_device(dt, t.float64)),
-           len(r), N.ptr(N.to_device(P, t.float64)), len(P), e_r, N.ptr(G), N.stream())
+    N.call("lsdf_grid_transform_exact", N.to_device(r, t.float64), N.to_device(dt, t.float64),
+           len(r), N.to_device(P, t.float64), len(P), e_r, N.ptr(G), N.stream())
     g = G.cpu().numpy()
     return g[0] if single else g
 

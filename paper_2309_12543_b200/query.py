@@ -324,7 +324,7 @@ def assemble_robot_sdfs(fields: Iterable, grid: EnvGrid, n_configs: int, d_far_g
         vals = np.stack([np.ravel(f.values, order="F") for _, f in items]).astype(np.float32)
         anchors = np.stack([np.asarray(f.anchor, dtype=np.int64) for _, f in items]).astype(np.int32)
         cfg = np.asarray([c for c, _ in items], dtype=np.int32)
-        N.call("lsdf_assemble", N.ptr(N.to_device(vals)), N.ptr(N.to_device(anchors)), N.ptr(N.to_device(cfg)),
+        N.call("lsdf_assemble", N.to_device(vals), N.to_device(anchors), N.to_device(cfg),
                len(items), N.i32x3(wd), ctypes.byref(grid.c_struct()), 0, float(d_far_global), N.ptr(out),
                N.stream())
     return RobotSdfBatch(values=out, grid=grid, d_far_global=float(d_far_global))
@@ -393,8 +393,8 @@ def per_link_min_distances(fields, obstacles: ObstacleVoxelSet, n_configs: int, 
         cfg = np.asarray([c for c, _, _ in items], np.int32)
         lnk = np.asarray([li for _, li, _ in items], np.int32)
         dfar = np.asarray([np.float32(f.d_far) for *_, f in items], np.float32)
-        N.call("lsdf_per_link_fields", N.ptr(N.to_device(vals)), N.ptr(N.to_device(anchors)),
-               N.ptr(N.to_device(cfg)), N.ptr(N.to_device(lnk)), N.ptr(N.to_device(dfar)), len(items),
+        N.call("lsdf_per_link_fields", N.to_device(vals), N.to_device(anchors),
+               N.to_device(cfg), N.to_device(lnk), N.to_device(dfar), len(items),
                N.i32x3(wd), n_links, ctypes.byref(obstacles.grid.c_struct()), N.ptr(occ), N.ptr(out), N.stream())
     return out.cpu().numpy()
 
@@ -488,9 +488,9 @@ def sphere_baseline_distances(spheres: SphereRobotModel, poses, obstacles: Obsta
     T = N.to_device(np.ascontiguousarray(poses.translations, dtype=np.float64), t.float64)
     out = N.empty((C_,), t.float64)
     N.call("lsdf_sphere_baseline", N.ptr(R), N.ptr(T), C_, L,
-           N.ptr(N.to_device(spheres.link_indices.astype(np.int32))),
-           N.ptr(N.to_device(np.ascontiguousarray(spheres.centers, dtype=np.float64))),
-           N.ptr(N.to_device(np.ascontiguousarray(spheres.radii, dtype=np.float64))), spheres.n_spheres,
+           N.to_device(spheres.link_indices.astype(np.int32)),
+           N.to_device(np.ascontiguousarray(spheres.centers, dtype=np.float64)),
+           N.to_device(np.ascontiguousarray(spheres.radii, dtype=np.float64)), spheres.n_spheres,
            N.ptr(obstacles.device_indices()), obstacles.n_occupied, ctypes.byref(grid.c_struct()), N.ptr(out),
            N.stream())
     d = out.cpu().numpy()
