@@ -76,14 +76,24 @@ typedef struct {
     double link_t[3];
 } lsdf_link;
 
-/* One dense link SDF grid (grids.py:116-152): values x-fastest, f32. */
+/* One dense link SDF grid (grids.py:116-152): values x-fastest, f32.
+ * packed_dev: the same values re-laid out by lsdf_pack_corners — per cell
+ * (i, j, k) < dims-1 its eight corners as two float4 (32 B, one sector), used
+ * by the fused query kernel; NULL where only the plain layout is needed. */
 typedef struct {
     const float* values_dev;
+    const float* packed_dev;
     int32_t dims[3];
     float d_far;          /* float32(min(extent))   grids.py:145-148 */
     double extent[3];
     double resolution[3];
 } lsdf_link_grid;
+
+/* Build the packed-corner layout (dims-1)^3 x 8 f32 from a plain grid. */
+int lsdf_pack_corners(const float* values_dev, const int32_t dims[3], float* packed_dev, void* stream);
+
+/* Bytes of the query workspace for C configurations x n_geo links. */
+int64_t lsdf_query_workspace_bytes(int64_t C, int32_t n_geo);
 
 /* Window geometry (placement.py:172-210).  P tables hold the canonical
  * normalized offsets ((m - W/2) * r_e / e_r, placement.py:119-121) per axis.
@@ -165,12 +175,15 @@ int lsdf_voxel_index(const double* points_dev, int64_t N, const lsdf_env_grid* e
  * i32 (position in the obstacle list; -1/-1 when d equals the clamp or the set
  * is empty).  per_link_dev (C, n_geo) f32 or NULL: per_link_min_distances
  * (query.py:153-176).  by_position != 0 selects the general (unsorted list)
- * tie rule; set it when the occupancy came from an unsorted index list. */
+ * tie rule; set it when the occupancy came from an unsorted index list.
+ * workspace_dev: lsdf_query_workspace_bytes(C, n_geo) bytes, zeroed once at
+ * allocation; every launch leaves it zeroed again (the last warp of each
+ * configuration resets its slots), so graph replays need no memset. */
 int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_dev,
                       const int32_t* anchor_geo_dev, int64_t C, int32_t n_geo,
                       const lsdf_link_grid* grids, const lsdf_window* window,
                       const lsdf_env_grid* env, const void* occupancy_dev,
-                      int32_t by_position, double d_far_global,
+                      int32_t by_position, double d_far_global, void* workspace_dev,
                       float* d_dev, int32_t* link_dev, int32_t* voxel_dev,
                       float* per_link_dev, void* stream);
 

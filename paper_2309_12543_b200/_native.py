@@ -37,7 +37,7 @@ class LinkT(C.Structure):
 
 
 class LinkGridT(C.Structure):
-    _fields_ = [("values_dev", C.c_void_p), ("dims", C.c_int32 * 3), ("d_far", C.c_float),
+    _fields_ = [("values_dev", C.c_void_p), ("packed_dev", C.c_void_p), ("dims", C.c_int32 * 3), ("d_far", C.c_float),
                 ("extent", C.c_double * 3), ("resolution", C.c_double * 3)]
 
 
@@ -62,7 +62,9 @@ _SIGS = {
     "lsdf_occupancy_from_indices": [_P, _I64, _I32, C.POINTER(EnvGridT), _P, _P],
     "lsdf_voxel_index": [_P, _I64, C.POINTER(EnvGridT), _P, _P, _P],
     "lsdf_query_direct": [_P, _P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT),
-                          C.POINTER(EnvGridT), _P, _I32, _D, _P, _P, _P, _P, _P],
+                          C.POINTER(EnvGridT), _P, _I32, _D, _P, _P, _P, _P, _P, _P],
+    "lsdf_query_workspace_bytes": [_I64, _I32],
+    "lsdf_pack_corners": [_P, C.POINTER(_I32), _P, _P],
     "lsdf_place_windows": [_P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT), _P, _P],
     "lsdf_assemble": [_P, _P, _P, _I64, C.POINTER(_I32), C.POINTER(EnvGridT), _I64, _D, _P, _P],
     "lsdf_query_dense": [_P, _I64, C.POINTER(EnvGridT), _P, _I64, _P, _P, _P],
@@ -112,7 +114,7 @@ def load_library(path: Path | None = None):
         for name, argtypes in _SIGS.items():
             fn = getattr(lib, name)
             fn.argtypes = argtypes
-            fn.restype = C.c_int64 if name == "lsdf_occupancy_bytes" else C.c_int
+            fn.restype = C.c_int64 if name.endswith("_bytes") else C.c_int
         lib.lsdf_version.restype = C.c_char_p
         lib.lsdf_last_error.restype = C.c_char_p
         lib.lsdf_launch_count.restype = C.c_uint64

@@ -23,7 +23,8 @@ OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "liblinksdf_b200.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["lsdf_capi.cu", "lsdf_query.cu", "lsdf_build.cu", "lsdf_mlp.cu", "lsdf_mlp_tc.cu"]
+SOURCES = ["lsdf_capi.cu", "lsdf_fk.cu", "lsdf_voxel.cu", "lsdf_query.cu", "lsdf_dense.cu", "lsdf_build.cu",
+           "lsdf_mlp.cu", "lsdf_mlp_tc.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -38,7 +39,7 @@ def _nvcc() -> str:
 
 def _digest() -> str:
     h = hashlib.sha256()
-    for name in SOURCES + ["lsdf_math.cuh", "lsdf_common.cuh"]:
+    for name in SOURCES + ["lsdf_math.cuh", "lsdf_common.cuh", "lsdf_device.cuh"]:
         h.update((CSRC / name).read_bytes())
     h.update((INCLUDE / "linksdf_b200.h").read_bytes())
     h.update(" ".join(ARCH + FLAGS).encode())

@@ -49,8 +49,8 @@ class DistanceChecker:
         self._shape = (C_, int(n_points), np.dtype(points_dtype))
         self.q_host = t.empty((C_, D), dtype=t.float64, pin_memory=True)
         self.p_host = t.full((int(n_points), 3), float("nan"), dtype=tdt, pin_memory=True)
-        self.q_dev = t.empty((C_, D), dtype=t.float64, device=dev)
-        self.p_dev = t.empty((int(n_points), 3), dtype=tdt, device=dev)
+        self.q_dev = t.zeros((C_, D), dtype=t.float64, device=dev)
+        self.p_dev = t.full((int(n_points), 3), float("nan"), dtype=tdt, device=dev)
         self.ws = occupancy_workspace(self.grid)
         self.fk_out = {}
         fk_device(self.robot, self.q_dev, all_links=False, grid=self.grid, window_dims=self.window.dims,
@@ -64,6 +64,9 @@ class DistanceChecker:
         self.voxel_host = t.empty((C_,), dtype=t.int32, pin_memory=True)
         self.flags_host = t.empty((4,), dtype=t.int32, pin_memory=True)
         self.window.device_tables()
+        for sdf in self.sdfs:
+            sdf.packed_values()
+        self._side = t.cuda.Stream()
         t.cuda.synchronize()
         if use_graph:
             self._capture()
@@ -74,22 +77,39 @@ class DistanceChecker:
         return self.q_host.numpy(), self.p_host.numpy()
 
     # ------------------------------------------------------------------ the step
-    def _compute(self):
-        """Device work of one cycle on the current stream (inputs already in q_dev / p_dev)."""
+    # FK+alignment and voxelization are independent: FK runs on a side stream
+    # while the cloud is voxelized, the query joins both (two graph branches).
+    def _fk(self, h2d: bool):
+        if h2d:
+            self.q_dev.copy_(self.q_host, non_blocking=True)
         self.fk_out["flags"].zero_()
         fk_device(self.robot, self.q_dev, all_links=False, grid=self.grid, window_dims=self.window.dims,
                   outputs=self.fk_out)
+
+    def _run(self, h2d: bool):
+        t = N.torch()
+        main = t.cuda.current_stream()
+        self._side.wait_stream(main)
+        with t.cuda.stream(self._side):
+            self._fk(h2d)
+        if h2d:
+            self.p_dev.copy_(self.p_host, non_blocking=True)
         voxelize_device(self.p_dev, self.grid, workspace=self.ws)
+        main.wait_stream(self._side)
         self.traj.query_device(self.ws, False, outputs=self.q_out)
+        if h2d:
+            self.d_host.copy_(self.q_out["d"], non_blocking=True)
+            self.link_host.copy_(self.q_out["link"], non_blocking=True)
+            self.voxel_host.copy_(self.q_out["voxel"], non_blocking=True)
+            self.flags_host.copy_(self.fk_out["flags"], non_blocking=True)
+
+    def _compute(self):
+        """Device work of one cycle (inputs already in q_dev / p_dev)."""
+        self._run(False)
 
     def _step(self):
-        self.q_dev.copy_(self.q_host, non_blocking=True)
-        self.p_dev.copy_(self.p_host, non_blocking=True)
-        self._compute()
-        self.d_host.copy_(self.q_out["d"], non_blocking=True)
-        self.link_host.copy_(self.q_out["link"], non_blocking=True)
-        self.voxel_host.copy_(self.q_out["voxel"], non_blocking=True)
-        self.flags_host.copy_(self.fk_out["flags"], non_blocking=True)
+        """H2D of the inputs, the cycle, D2H of (d, link, voxel, flags)."""
+        self._run(True)
 
     def _capture(self):
         t = N.torch()

@@ -1,0 +1,303 @@
+// lsdf_dense.cu — the paper's materialized mode and the standalone operators.
+//
+//   place_windows_kernel    placement.py:267-313 (every (c, l) window, W^3 cells)
+//   assemble_kernel         query.py:61-103 (scatter-min into dense C x V_e)
+//   query_dense_kernel      query.py:128-150 (gather + first-occurrence argmin)
+//   per_link_fields_kernel  query.py:153-176
+//   sphere_baseline_kernel  query.py:254-291
+//   trilinear_kernel        grids.py:155-191
+//   transform_exact_kernel  placement.py:148-169
+//   pack_corners_kernel     layout change for the fused query (no arithmetic)
+#include "lsdf_device.cuh"
+
+using namespace lsdf;
+
+namespace {
+
+struct PlaceParams {
+    lsdf_link_grid grids[LSDF_MAX_LINKS];
+    const double* R;
+    const double* dt;
+    int32_t n_geo;
+    int32_t W[3];
+    double e_r;
+    const double* P;
+    int32_t Wmax;
+    const uint32_t* mask_bits;
+    float* out;
+};
+
+__global__ void place_windows_kernel(const __grid_constant__ PlaceParams p) {
+    const int64_t f = blockIdx.x;  // field = c * n_geo + l
+    const int l = (int)(f % p.n_geo);
+    const lsdf_link_grid& G = p.grids[l];
+    const GridView gv = view_of(G);
+    const LdgLoad ld{G.values_dev};
+    double R[9], dtinv[3];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) R[e] = p.R[f * 9 + e];
+    shift_inverse(R, p.dt + f * 3, p.e_r, dtinv);
+    const int W0 = p.W[0], W1 = p.W[1];
+    const int n = W0 * W1 * p.W[2];
+    float* dst = p.out + f * (int64_t)n;
+    for (int cell = threadIdx.x; cell < n; cell += blockDim.x) {
+        const bool keep = (__ldg(p.mask_bits + (cell >> 5)) >> (cell & 31)) & 1u;
+        float v = gv.d_far;  // masked cells carry the link sentinel (placement.py:305-308)
+        if (keep) {
+            const int mx = cell % W0, my = (cell / W0) % W1, mz = cell / (W0 * W1);
+            double pt[3];
+            window_point(p.P[mx], p.P[p.Wmax + my], p.P[2 * p.Wmax + mz], R, dtinv, p.e_r, pt);
+            v = trilinear_at(gv, pt[0], pt[1], pt[2], ld);
+        }
+        dst[cell] = v;
+    }
+}
+
+__global__ void fill_kernel(float* out, int64_t n, float v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = v;
+}
+
+// float min via integer atomics: non-negative floats order like ints, negative
+// ones reverse-order like unsigned ints.
+__device__ __forceinline__ void atomic_min_float(float* addr, float v) {
+    if (v >= 0.0f)
+        atomicMin((int*)addr, __float_as_int(v));
+    else
+        atomicMax((unsigned int*)addr, __float_as_uint(v));
+}
+
+__global__ void assemble_kernel(const float* __restrict__ windows, const int32_t* anchors, const int32_t* configs,
+                                int32_t W0, int32_t W1, int32_t W2, lsdf_env_grid env, float* out) {
+    const int64_t f = blockIdx.x;
+    const int64_t c = configs[f];
+    const int ax = anchors[3 * f], ay = anchors[3 * f + 1], az = anchors[3 * f + 2];
+    const int n = W0 * W1 * W2;
+    const int64_t V = n_vox(env);
+    for (int cell = threadIdx.x; cell < n; cell += blockDim.x) {
+        const int x = ax + cell % W0, y = ay + (cell / W0) % W1, z = az + cell / (W0 * W1);
+        if (x < 0 || y < 0 || z < 0 || x >= env.dims[0] || y >= env.dims[1] || z >= env.dims[2]) continue;
+        const float v = windows[f * n + cell];
+        float* dst = out + c * V + ((int64_t)x * env.dims[1] + y) * env.dims[2] + z;
+        if (v < *dst) atomic_min_float(dst, v);
+    }
+}
+
+__global__ void query_dense_kernel(const float* __restrict__ values, int64_t V, lsdf_env_grid env,
+                                   const int32_t* __restrict__ idx, int64_t N, float* d, int32_t* argmin) {
+    __shared__ uint64_t s_key[32];
+    const int64_t c = blockIdx.x;
+    uint64_t best = ~0ull;
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const int64_t lin = ((int64_t)idx[3 * i] * env.dims[1] + idx[3 * i + 1]) * env.dims[2] + idx[3 * i + 2];
+        const float v = __ldg(values + c * V + lin);
+        const uint64_t key = ((uint64_t)orderable(v) << 32) | (uint64_t)i;
+        best = key < best ? key : best;
+    }
+    best = warp_min_u64(best);
+    if ((threadIdx.x & 31) == 0) s_key[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        uint64_t k = threadIdx.x < (blockDim.x >> 5) ? s_key[threadIdx.x] : ~0ull;
+        k = warp_min_u64(k);
+        if (threadIdx.x == 0) {
+            d[c] = from_orderable((uint32_t)(k >> 32));
+            argmin[c] = (int32_t)(uint32_t)k;
+        }
+    }
+}
+
+__global__ void per_link_fields_kernel(const float* __restrict__ windows, const int32_t* anchors,
+                                       const int32_t* configs, const int32_t* links, const float* d_far,
+                                       int32_t W0, int32_t W1, int32_t W2, int32_t n_links, lsdf_env_grid env,
+                                       const uint32_t* __restrict__ bitmap, float* out) {
+    __shared__ float s_min[32];
+    const int64_t f = blockIdx.x;
+    const int ax = anchors[3 * f], ay = anchors[3 * f + 1], az = anchors[3 * f + 2];
+    const int n = W0 * W1 * W2;
+    float m = d_far[f];  // query.py:171: the limit starts at the field's sentinel
+    for (int cell = threadIdx.x; cell < n; cell += blockDim.x) {
+        const int x = ax + cell % W0, y = ay + (cell / W0) % W1, z = az + cell / (W0 * W1);
+        if (x < 0 || y < 0 || z < 0 || x >= env.dims[0] || y >= env.dims[1] || z >= env.dims[2]) continue;
+        const int64_t lin = ((int64_t)x * env.dims[1] + y) * env.dims[2] + z;
+        if ((__ldg(bitmap + (lin >> 5)) >> (lin & 31)) & 1u) m = fminf(m, windows[f * n + cell]);
+    }
+    m = warp_min_f(m);
+    if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (int)(blockDim.x >> 5) ? s_min[threadIdx.x] : INFINITY;
+        m = warp_min_f(m);
+        if (threadIdx.x == 0) atomic_min_float(out + (int64_t)configs[f] * n_links + links[f], m);
+    }
+}
+
+__global__ void sphere_baseline_kernel(const double* __restrict__ R, const double* __restrict__ T, int32_t L,
+                                       const int32_t* sl, const double* sc, const double* sr, int32_t S,
+                                       const int32_t* __restrict__ idx, int64_t N, lsdf_env_grid env, double* out) {
+    extern __shared__ double s_w[];  // S x 4: world centre + radius
+    __shared__ double s_min[32];
+    const int64_t c = blockIdx.x;
+    for (int s = threadIdx.x; s < S; s += blockDim.x) {
+        const double* Rc = R + (c * L + sl[s]) * 9;
+        double w[3];
+        mv_einsum(Rc, sc + 3 * s, w);  // einsum("bsij,sj->bsi")
+        for (int k = 0; k < 3; ++k) s_w[4 * s + k] = DADD(w[k], T[(c * L + sl[s]) * 3 + k]);
+        s_w[4 * s + 3] = sr[s];
+    }
+    __syncthreads();
+    double m = INFINITY;
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        double x[3];
+        for (int k = 0; k < 3; ++k)
+            x[k] = DADD(-env.extent[k], DMUL(DADD((double)idx[3 * i + k], 0.5), env.resolution[k]));
+        for (int s = 0; s < S; ++s) {
+            const double d0 = DSUB(s_w[4 * s], x[0]), d1 = DSUB(s_w[4 * s + 1], x[1]),
+                         d2 = DSUB(s_w[4 * s + 2], x[2]);
+            const double d = DSUB(DSQRT(dot3(d0, d1, d2, d0, d1, d2)), s_w[4 * s + 3]);
+            m = d < m ? d : m;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double u = __shfl_xor_sync(FULL_MASK, m, o);
+        m = u < m ? u : m;
+    }
+    if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = INFINITY;
+        for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) r = s_min[w2] < r ? s_min[w2] : r;
+        out[c] = r;
+    }
+}
+
+__global__ void trilinear_kernel(lsdf_link_grid g, const double* pts, int64_t n, double scale, float* out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = trilinear_at(view_of(g), DMUL(pts[3 * i], scale), DMUL(pts[3 * i + 1], scale),
+                          DMUL(pts[3 * i + 2], scale), LdgLoad{g.values_dev});
+}
+
+__global__ void transform_exact_kernel(const double* R, const double* dt, int64_t B, const double* P, int64_t V,
+                                       double e_r, double* G) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * V) return;
+    const int64_t b = i / V, v = i % V;
+    double Rb[9], dtinv[3];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) Rb[e] = R[b * 9 + e];
+    shift_inverse(Rb, dt + b * 3, e_r, dtinv);
+    const double px = P[3 * v], py = P[3 * v + 1], pz = P[3 * v + 2];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        G[i * 3 + k] = DADD(DFMA(pz, Rb[6 + k], DFMA(py, Rb[3 + k], DMUL(px, Rb[k]))), dtinv[k]);
+}
+
+__global__ void pack_corners_kernel(const float* __restrict__ v, int32_t nx, int32_t ny, int32_t nz, float4* out) {
+    const int64_t cx = nx - 1, cy = ny - 1, cz = nz - 1;
+    const int64_t n = cx * cy * cz;
+    for (int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < n;
+         cell += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = cell % cx, j = (cell / cx) % cy, k = cell / (cx * cy);
+        const int64_t sy = nx, sz = (int64_t)nx * ny;
+        const int64_t b = i + sy * j + sz * k;
+        out[2 * cell] = make_float4(v[b], v[b + 1], v[b + sy], v[b + 1 + sy]);
+        out[2 * cell + 1] = make_float4(v[b + sz], v[b + 1 + sz], v[b + sy + sz], v[b + 1 + sy + sz]);
+    }
+}
+
+}  // namespace
+
+extern "C" int lsdf_pack_corners(const float* values_dev, const int32_t dims[3], float* packed_dev, void* stream) {
+    if (dims[0] < 2 || dims[1] < 2 || dims[2] < 2) return fail(LSDF_ERR_VALIDATION, "grid needs >= 2 cells per axis");
+    pack_corners_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(values_dev, dims[0], dims[1], dims[2],
+                                                                     (float4*)packed_dev);
+    return check_launch("pack_corners_kernel");
+}
+
+extern "C" int lsdf_place_windows(const double* R_geo_dev, const double* dt_geo_dev, int64_t C, int32_t n_geo,
+                                  const lsdf_link_grid* grids, const lsdf_window* window, float* windows_dev,
+                                  void* stream) {
+    if (n_geo < 1 || n_geo > LSDF_MAX_LINKS) return fail(LSDF_ERR_VALIDATION, "place: bad link count %d", n_geo);
+    if (C <= 0) return LSDF_OK;
+    PlaceParams p{};
+    for (int l = 0; l < n_geo; ++l) p.grids[l] = grids[l];
+    p.R = R_geo_dev;
+    p.dt = dt_geo_dev;
+    p.n_geo = n_geo;
+    for (int a = 0; a < 3; ++a) p.W[a] = window->W[a];
+    p.e_r = window->e_r;
+    p.P = window->P_dev;
+    p.Wmax = window->Wmax;
+    p.mask_bits = window->mask_bits_dev;
+    p.out = windows_dev;
+    place_windows_kernel<<<(unsigned)(C * n_geo), 256, 0, (cudaStream_t)stream>>>(p);
+    return check_launch("place_windows_kernel");
+}
+
+extern "C" int lsdf_fill(float* dst_dev, int64_t n, float value, void* stream) {
+    if (n <= 0) return LSDF_OK;
+    const int64_t blocks = (n + 255) / 256;
+    fill_kernel<<<(unsigned)(blocks < 148 * 8 ? blocks : 148 * 8), 256, 0, (cudaStream_t)stream>>>(dst_dev, n, value);
+    return check_launch("fill_kernel");
+}
+
+extern "C" int lsdf_assemble(const float* windows_dev, const int32_t* anchors_dev, const int32_t* config_dev,
+                             int64_t n_fields, const int32_t W[3], const lsdf_env_grid* env, int64_t C,
+                             double d_far_global, float* values_dev, void* stream) {
+    if (C > 0) LSDF_TRY(lsdf_fill(values_dev, C * n_vox(*env), (float)d_far_global, stream));
+    if (n_fields <= 0) return LSDF_OK;
+    assemble_kernel<<<(unsigned)n_fields, 256, 0, (cudaStream_t)stream>>>(windows_dev, anchors_dev, config_dev, W[0],
+                                                                           W[1], W[2], *env, values_dev);
+    return check_launch("assemble_kernel");
+}
+
+extern "C" int lsdf_query_dense(const float* values_dev, int64_t C, const lsdf_env_grid* env,
+                                const int32_t* indices_dev, int64_t N, float* d_dev, int32_t* argmin_dev,
+                                void* stream) {
+    if (C <= 0 || N <= 0) return LSDF_OK;
+    query_dense_kernel<<<(unsigned)C, 256, 0, (cudaStream_t)stream>>>(values_dev, n_vox(*env), *env, indices_dev, N,
+                                                                       d_dev, argmin_dev);
+    return check_launch("query_dense_kernel");
+}
+
+extern "C" int lsdf_per_link_fields(const float* windows_dev, const int32_t* anchors_dev, const int32_t* configs_dev,
+                                    const int32_t* links_dev, const float* d_far_dev, int64_t n_fields,
+                                    const int32_t W[3], int32_t n_links, const lsdf_env_grid* env,
+                                    const void* occupancy_dev, float* out_dev, void* stream) {
+    if (n_fields <= 0) return LSDF_OK;
+    Occupancy o = carve_occupancy(const_cast<void*>(occupancy_dev), *env);
+    per_link_fields_kernel<<<(unsigned)n_fields, 256, 0, (cudaStream_t)stream>>>(
+        windows_dev, anchors_dev, configs_dev, links_dev, d_far_dev, W[0], W[1], W[2], n_links, *env, o.bitmap,
+        out_dev);
+    return check_launch("per_link_fields_kernel");
+}
+
+extern "C" int lsdf_sphere_baseline(const double* R_all_dev, const double* T_all_dev, int64_t C, int32_t L,
+                                    const int32_t* sphere_link_dev, const double* sphere_center_dev,
+                                    const double* sphere_radius_dev, int32_t S, const int32_t* indices_dev, int64_t N,
+                                    const lsdf_env_grid* env, double* out_dev, void* stream) {
+    if (C <= 0) return LSDF_OK;
+    if (S <= 0 || S > 4096) return fail(LSDF_ERR_VALIDATION, "sphere model with %d spheres", S);
+    sphere_baseline_kernel<<<(unsigned)C, 256, (size_t)S * 4 * sizeof(double), (cudaStream_t)stream>>>(
+        R_all_dev, T_all_dev, L, sphere_link_dev, sphere_center_dev, sphere_radius_dev, S, indices_dev, N, *env,
+        out_dev);
+    return check_launch("sphere_baseline_kernel");
+}
+
+extern "C" int lsdf_trilinear(const lsdf_link_grid* grid, const double* pts_dev, int64_t n, double scale,
+                              float* out_dev, void* stream) {
+    if (n <= 0) return LSDF_OK;
+    trilinear_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*grid, pts_dev, n, scale, out_dev);
+    return check_launch("trilinear_kernel");
+}
+
+extern "C" int lsdf_grid_transform_exact(const double* R_dev, const double* dt_dev, int64_t B,
+                                         const double* points_dev, int64_t V, double e_r, double* G_dev,
+                                         void* stream) {
+    if (B * V <= 0) return LSDF_OK;
+    transform_exact_kernel<<<grid_for(B * V, 256), 256, 0, (cudaStream_t)stream>>>(R_dev, dt_dev, B, points_dev, V,
+                                                                                   e_r, G_dev);
+    return check_launch("transform_exact_kernel");
+}

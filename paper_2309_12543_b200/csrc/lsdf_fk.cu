@@ -1,0 +1,187 @@
+// lsdf_fk.cu — stage 1: batched forward kinematics + window alignment.
+//
+//   fk_align_kernel  robot.py:305-347 (FK) + placement.py:60-99 (alignment)
+//   align_kernel     placement.py:60-99 alone (compute_alignment API)
+//
+// One thread per configuration walks the parents-first chain in fp64 with
+// the reference's operation order (lsdf_math.cuh); the per-link world poses
+// of the configuration live in shared memory so children can read any
+// earlier link.  For the geometry links the thread also splits T into the
+// window anchor and residual.  Outputs are written link-major per config,
+// matching LinkPoseBatch (C, L, 3, 3).
+#include "lsdf_device.cuh"
+
+using namespace lsdf;
+
+namespace {
+
+struct FkParams {
+    lsdf_link links[LSDF_MAX_LINKS];
+    int32_t n_links, n_geo, D, pad_;
+    int64_t C;
+    const double* q;
+    const double* limits;
+    lsdf_env_grid env;
+    int32_t W[3];
+    double* R_all;
+    double* T_all;
+    double* R_geo;
+    double* dt_geo;
+    int32_t* anchor_geo;
+    int32_t* flags;
+};
+
+constexpr int FK_THREADS = 64;
+
+__global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_constant__ FkParams p) {
+    // [n_links][12][FK_THREADS]: thread-fastest so the 64 threads of a block
+    // touch consecutive banks when they read or write the same link slot
+    extern __shared__ double s_pose[];
+    const int64_t c = (int64_t)blockIdx.x * FK_THREADS + threadIdx.x;
+    if (c >= p.C) return;
+    double* pose = s_pose + threadIdx.x;
+    auto at = [&](int li, int e) -> double& { return pose[(li * 12 + e) * FK_THREADS]; };
+    const double* q = p.q + c * p.D;
+    if (p.limits != nullptr) {  // robot.py:297-302
+        int bad = 0;
+        for (int j = 0; j < p.D; ++j) {
+            const double v = q[j];
+            bad += (v < p.limits[2 * j] || v > p.limits[2 * j + 1]);
+        }
+        if (bad) atomicAdd(&p.flags[0], bad);
+    }
+    for (int li = 0; li < p.n_links; ++li) {
+        const lsdf_link& L = p.links[li];
+        double rj[9], tj[3];
+        if (L.kind == 0) {
+#pragma unroll
+            for (int e = 0; e < 9; ++e) rj[e] = (e == 0 || e == 4 || e == 8) ? 1.0 : 0.0;
+            tj[0] = tj[1] = tj[2] = 0.0;
+        } else {
+            double rp[9], tp[3];
+#pragma unroll
+            for (int e = 0; e < 9; ++e) rp[e] = at(L.parent, e);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) tp[k] = at(L.parent, 9 + k);
+            double rl[9], tl[3];
+            if (L.kind == 1) {  // revolute: r_o @ rodrigues(q)   robot.py:331-334
+                const double a = q[L.q_col];
+                double M[9];
+                rodrigues(L.skew, L.outer, cos(a), sin(a), M);
+                mm33(L.joint_R, M, rl);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) tl[k] = L.joint_t[k];
+            } else {
+#pragma unroll
+                for (int e = 0; e < 9; ++e) rl[e] = L.joint_R[e];
+                if (L.kind == 2) {  // prismatic: t_o + q * (r_o @ axis)   robot.py:335-337
+                    const double a = q[L.q_col];
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) tl[k] = DADD(L.joint_t[k], DMUL(a, L.R_axis[k]));
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) tl[k] = L.joint_t[k];
+                }
+            }
+            double tmp[3];
+            mm33(rp, rl, rj);         // robot.py:341
+            mv_einsum(rp, tl, tmp);   // robot.py:342
+#pragma unroll
+            for (int k = 0; k < 3; ++k) tj[k] = DADD(tp[k], tmp[k]);
+        }
+        double R[9], T[3], tmp[3];
+        mm33(rj, L.link_R, R);        // robot.py:343
+        mv_einsum(rj, L.link_t, tmp); // robot.py:344-346
+#pragma unroll
+        for (int k = 0; k < 3; ++k) T[k] = DADD(tj[k], tmp[k]);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) at(li, e) = R[e];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) at(li, 9 + k) = T[k];
+        if (p.R_all != nullptr) {
+            double* dr = p.R_all + (c * p.n_links + li) * 9;
+            double* dtt = p.T_all + (c * p.n_links + li) * 3;
+#pragma unroll
+            for (int e = 0; e < 9; ++e) dr[e] = R[e];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) dtt[k] = T[k];
+        }
+        if (L.geom_slot >= 0 && p.R_geo != nullptr) {
+            const int64_t o = c * p.n_geo + L.geom_slot;
+#pragma unroll
+            for (int e = 0; e < 9; ++e) p.R_geo[o * 9 + e] = R[e];
+            int32_t anc[3];
+            double del[3];
+            if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del)) atomicAdd(&p.flags[1], 1);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                p.dt_geo[o * 3 + k] = del[k];
+                p.anchor_geo[o * 3 + k] = anc[k];
+            }
+        }
+    }
+}
+
+__global__ void align_kernel(const double* T, int64_t n, lsdf_env_grid env, int32_t W0, int32_t W1, int32_t W2,
+                             int32_t* anchor, double* dt, int32_t* flags) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t W[3] = {W0, W1, W2};
+    int32_t a[3];
+    double d[3];
+    if (!align_one(T + 3 * i, env.extent, env.resolution, env.dims, W, a, d)) atomicAdd(&flags[1], 1);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        anchor[3 * i + k] = a[k];
+        dt[3 * i + k] = d[k];
+    }
+}
+
+}  // namespace
+
+extern "C" int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_geo, const double* q_dev, int64_t C,
+                             int32_t D, const double* limits_dev, const lsdf_env_grid* env, const int32_t W[3],
+                             double* R_all_dev, double* T_all_dev, double* R_geo_dev, double* dt_geo_dev,
+                             int32_t* anchor_geo_dev, int32_t* flags_dev, void* stream) {
+    if (n_links < 1 || n_links > LSDF_MAX_LINKS || n_geo > LSDF_MAX_LINKS)
+        return fail(LSDF_ERR_VALIDATION, "lsdf_fk_align: %d links outside 1..%d", n_links, LSDF_MAX_LINKS);
+    if (C <= 0) return LSDF_OK;
+    FkParams p{};
+    for (int i = 0; i < n_links; ++i) p.links[i] = links[i];
+    p.n_links = n_links;
+    p.n_geo = n_geo;
+    p.D = D;
+    p.C = C;
+    p.q = q_dev;
+    p.limits = limits_dev;
+    if (env) p.env = *env;
+    if (W) {
+        p.W[0] = W[0];
+        p.W[1] = W[1];
+        p.W[2] = W[2];
+    }
+    p.R_all = R_all_dev;
+    p.T_all = T_all_dev;
+    p.R_geo = R_geo_dev;
+    p.dt_geo = dt_geo_dev;
+    p.anchor_geo = anchor_geo_dev;
+    p.flags = flags_dev;
+    const size_t smem = (size_t)FK_THREADS * n_links * 12 * sizeof(double);
+    if (smem > 48 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(fk_align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr = true;
+        }
+    }
+    fk_align_kernel<<<grid_for(C, FK_THREADS), FK_THREADS, smem, (cudaStream_t)stream>>>(p);
+    return check_launch("fk_align_kernel");
+}
+
+extern "C" int lsdf_align(const double* T_dev, int64_t n, const lsdf_env_grid* env, const int32_t W[3],
+                          int32_t* anchor_dev, double* dt_dev, int32_t* flags_dev, void* stream) {
+    if (n <= 0) return LSDF_OK;
+    align_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(T_dev, n, *env, W[0], W[1], W[2], anchor_dev,
+                                                                       dt_dev, flags_dev);
+    return check_launch("align_kernel");
+}

@@ -1,0 +1,213 @@
+// lsdf_voxel.cu — obstacle voxelization (query.py:106-125, grids.py:93-113).
+//
+// voxel_scatter_kernel: one thread per point, fp64 floor((p + e) / r) exactly
+//   as numpy, clipped; warps merge lanes that hit the same bitmap word
+//   (__match_any_sync) so a dense human blob costs one atomicOr per word per
+//   warp.  The last CTA to finish (ticket counter) turns the bitmap into the
+//   exclusive popcount prefix per word: rank(voxel) = prefix[w] +
+//   popc(word & below) is its position in np.unique(axis=0) order.
+// voxel_compact_kernel: optional, one thread per word, writes the sorted
+//   index list (the ObstacleVoxelSet.indices the API returns) and posgrid.
+#include <cub/block/block_scan.cuh>
+
+#include "lsdf_device.cuh"
+
+using namespace lsdf;
+
+namespace {
+
+constexpr int SCAN_THREADS = 1024;
+
+__device__ void prefix_scan_block(const uint32_t* bitmap, int64_t n_words, int32_t* prefix, int32_t* counters) {
+    using Scan = cub::BlockScan<int, SCAN_THREADS>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    // tiles of SCAN_THREADS * 4 words; each thread owns 4 consecutive words
+    for (int64_t base = 0; base < n_words; base += (int64_t)SCAN_THREADS * 4) {
+        const int64_t w0 = base + threadIdx.x * 4;
+        int c[4], s = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            c[k] = (w0 + k < n_words) ? __popc(__ldcg(bitmap + w0 + k)) : 0;
+            s += c[k];
+        }
+        int excl, total;
+        Scan(tmp).ExclusiveSum(s, excl, total);
+        const int start = carry + excl;
+        int run = start;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (w0 + k < n_words) prefix[w0 + k] = run;
+            run += c[k];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        counters[0] = carry;
+        counters[2] = 0;  // reset the ticket for the next launch (graph replays)
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SCAN_THREADS)
+voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, uint32_t* bitmap, int32_t* prefix,
+                     int32_t* counters, int64_t n_words) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool dropped = false;
+    int64_t word = -1;
+    uint32_t bit = 0;
+    if (i < N) {
+        const double x = (double)pts[3 * i], y = (double)pts[3 * i + 1], z = (double)pts[3 * i + 2];
+        const double ex = env.extent[0], ey = env.extent[1], ez = env.extent[2];
+        // query.py:112: keep -e <= p < e on every axis (NaN fails the test -> dropped)
+        const bool inside = (x >= -ex) && (x < ex) && (y >= -ey) && (y < ey) && (z >= -ez) && (z < ez);
+        if (inside) {
+            int64_t ix = (int64_t)floor(DDIV(DADD(x, ex), env.resolution[0]));
+            int64_t iy = (int64_t)floor(DDIV(DADD(y, ey), env.resolution[1]));
+            int64_t iz = (int64_t)floor(DDIV(DADD(z, ez), env.resolution[2]));
+            ix = ix < 0 ? 0 : (ix > env.dims[0] - 1 ? env.dims[0] - 1 : ix);  // grids.py:111 clip
+            iy = iy < 0 ? 0 : (iy > env.dims[1] - 1 ? env.dims[1] - 1 : iy);
+            iz = iz < 0 ? 0 : (iz > env.dims[2] - 1 ? env.dims[2] - 1 : iz);
+            const int64_t lin = (ix * env.dims[1] + iy) * env.dims[2] + iz;
+            word = lin >> 5;
+            bit = 1u << (lin & 31);
+        } else {
+            dropped = true;
+        }
+    }
+    // one atomicOr per distinct word per warp
+    const unsigned peers = __match_any_sync(FULL_MASK, word);
+    const uint32_t merged = __reduce_or_sync(peers, bit);
+    const int lane = threadIdx.x & 31;
+    if (word >= 0 && lane == __ffs(peers) - 1) atomicOr(bitmap + word, merged);
+    const unsigned b = __ballot_sync(FULL_MASK, dropped);
+    if (lane == 0 && b) atomicAdd(&counters[1], __popc(b));
+    if (prefix == nullptr) return;
+    // last CTA: exclusive popcount prefix over the finished bitmap
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&counters[2], 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (blockDim.x == SCAN_THREADS) prefix_scan_block(bitmap, n_words, prefix, counters);
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) prefix_only_kernel(const uint32_t* bitmap, int64_t n_words,
+                                                                    int32_t* prefix, int32_t* counters) {
+    prefix_scan_block(bitmap, n_words, prefix, counters);
+}
+
+__global__ void voxel_compact_kernel(const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ prefix,
+                                     int64_t n_words, lsdf_env_grid env, int32_t* posgrid, int32_t* indices) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= n_words) return;
+    uint32_t bits = bitmap[w];
+    int rank = prefix[w];
+    const int64_t nyz = (int64_t)env.dims[1] * env.dims[2];
+    while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int64_t lin = w * 32 + b;
+        posgrid[lin] = rank;
+        if (indices != nullptr) {
+            indices[3 * (int64_t)rank] = (int32_t)(lin / nyz);
+            indices[3 * (int64_t)rank + 1] = (int32_t)((lin / env.dims[2]) % env.dims[1]);
+            indices[3 * (int64_t)rank + 2] = (int32_t)(lin % env.dims[2]);
+        }
+        ++rank;
+    }
+}
+
+__global__ void occ_from_indices_kernel(const int32_t* idx, int64_t N, lsdf_env_grid env, uint32_t* bitmap,
+                                        int32_t* posgrid, int mode) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int64_t lin = ((int64_t)idx[3 * i] * env.dims[1] + idx[3 * i + 1]) * env.dims[2] + idx[3 * i + 2];
+    if (mode == 0) {  // sorted unique: position == list index == rank
+        posgrid[lin] = (int32_t)i;
+        atomicOr(bitmap + (lin >> 5), 1u << (lin & 31));
+    } else if (mode == 1) {  // general, pass 1: reset touched entries
+        posgrid[lin] = 0x7fffffff;
+    } else {  // general, pass 2: first occurrence wins (numpy argmin semantics)
+        atomicMin(posgrid + lin, (int32_t)i);
+        atomicOr(bitmap + (lin >> 5), 1u << (lin & 31));
+    }
+}
+
+__global__ void voxel_index_kernel(const double* pts, int64_t N, lsdf_env_grid env, int32_t* out, int32_t* flags) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    bool bad = false;
+    for (int a = 0; a < 3; ++a) {
+        const double x = pts[3 * i + a];
+        if (!(x >= -env.extent[a] && x < env.extent[a])) bad = true;
+        const double f = floor(DDIV(DADD(x, env.extent[a]), env.resolution[a]));
+        int64_t j = (f == f) ? (int64_t)f : 0;
+        j = j < 0 ? 0 : (j > env.dims[a] - 1 ? env.dims[a] - 1 : j);
+        out[3 * i + a] = (int32_t)j;
+    }
+    if (bad) atomicAdd(flags, 1);
+}
+
+}  // namespace
+
+extern "C" int64_t lsdf_occupancy_bytes(const lsdf_env_grid* env) { return occupancy_bytes(*env); }
+
+extern "C" int lsdf_voxelize(const void* points_dev, int32_t points_f32, int64_t N, const lsdf_env_grid* env,
+                             void* occupancy_dev, int32_t* indices_dev, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    Occupancy o = carve_occupancy(occupancy_dev, *env);
+    LSDF_TRY(check_cuda(cudaMemsetAsync(occupancy_dev, 0, 256 + o.n_words * 4, s), "voxelize memset"));
+    if (N > 0) {
+        // the scan needs SCAN_THREADS per CTA in the last block
+        const unsigned blocks = grid_for(N, SCAN_THREADS);
+        if (points_f32)
+            voxel_scatter_kernel<float><<<blocks, SCAN_THREADS, 0, s>>>((const float*)points_dev, N, *env, o.bitmap,
+                                                                        o.prefix, o.counters, o.n_words);
+        else
+            voxel_scatter_kernel<double><<<blocks, SCAN_THREADS, 0, s>>>((const double*)points_dev, N, *env,
+                                                                         o.bitmap, o.prefix, o.counters, o.n_words);
+        LSDF_TRY(check_launch("voxel_scatter_kernel"));
+    } else {
+        prefix_only_kernel<<<1, SCAN_THREADS, 0, s>>>(o.bitmap, o.n_words, o.prefix, o.counters);
+        LSDF_TRY(check_launch("prefix_only_kernel"));
+    }
+    if (indices_dev == nullptr) return LSDF_OK;  // hot path: the query only needs bitmap + prefix
+    voxel_compact_kernel<<<grid_for(o.n_words, 256), 256, 0, s>>>(o.bitmap, o.prefix, o.n_words, *env, o.posgrid,
+                                                                    indices_dev);
+    return check_launch("voxel_compact_kernel");
+}
+
+extern "C" int lsdf_occupancy_from_indices(const int32_t* indices_dev, int64_t N, int32_t sorted_unique,
+                                           const lsdf_env_grid* env, void* occupancy_dev, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    Occupancy o = carve_occupancy(occupancy_dev, *env);
+    LSDF_TRY(check_cuda(cudaMemsetAsync(occupancy_dev, 0, 256 + o.n_words * 4, s), "occupancy memset"));
+    if (N > 0) {
+        if (sorted_unique) {
+            occ_from_indices_kernel<<<grid_for(N, 256), 256, 0, s>>>(indices_dev, N, *env, o.bitmap, o.posgrid, 0);
+            LSDF_TRY(check_launch("occ_from_indices_kernel"));
+        } else {
+            occ_from_indices_kernel<<<grid_for(N, 256), 256, 0, s>>>(indices_dev, N, *env, o.bitmap, o.posgrid, 1);
+            LSDF_TRY(check_launch("occ_from_indices_kernel"));
+            occ_from_indices_kernel<<<grid_for(N, 256), 256, 0, s>>>(indices_dev, N, *env, o.bitmap, o.posgrid, 2);
+            LSDF_TRY(check_launch("occ_from_indices_kernel"));
+        }
+    }
+    prefix_only_kernel<<<1, SCAN_THREADS, 0, s>>>(o.bitmap, o.n_words, o.prefix, o.counters);
+    return check_launch("prefix_only_kernel");
+}
+
+extern "C" int lsdf_voxel_index(const double* points_dev, int64_t N, const lsdf_env_grid* env, int32_t* indices_dev,
+                                int32_t* flags_dev, void* stream) {
+    if (N <= 0) return LSDF_OK;
+    voxel_index_kernel<<<grid_for(N, 256), 256, 0, (cudaStream_t)stream>>>(points_dev, N, *env, indices_dev,
+                                                                           flags_dev);
+    return check_launch("voxel_index_kernel");
+}

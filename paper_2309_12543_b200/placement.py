@@ -220,10 +220,10 @@ class ExactTransformProvider:
         return grid_transform_exact(rotations, delta_t, self.window.extent, self.window.masked_points)
 
 
-def link_grid_table(sdfs: Sequence[LinkSdf]):
+def link_grid_table(sdfs: Sequence[LinkSdf], packed: bool = False):
     table = (N.LinkGridT * len(sdfs))()
     for i, s in enumerate(sdfs):
-        table[i] = s.c_struct()
+        table[i] = s.c_struct(packed)
     return table
 
 

@@ -189,7 +189,8 @@ class TrajectorySdf:
         self.dt = dt_dev
         self.anchor = anchor_dev
         self.d_far_global = float(min(s.d_far for s in sdfs) if d_far_global is None else d_far_global)
-        self._table = link_grid_table(self.sdfs)
+        self._table = link_grid_table(self.sdfs, packed=True)
+        self._ws = None
         self._dense = None
         self._flags = flags
 
@@ -289,10 +290,13 @@ class TrajectorySdf:
         if per_link and "per_link" not in out:
             out["per_link"] = N.empty((C_, self.n_links), t.float32)
         ws, _ = self.window.device_tables()
+        if self._ws is None:  # zeroed once; every launch leaves it zeroed again
+            nbytes = int(N.lib().lsdf_query_workspace_bytes(C_, self.n_links))
+            self._ws = N.zeros((nbytes,), t.uint8)
         N.call("lsdf_query_direct", N.ptr(self.R), N.ptr(self.dt), N.ptr(self.anchor), C_, self.n_links,
                self._table, ctypes.byref(ws), ctypes.byref(self.grid.c_struct()), N.ptr(occupancy),
-               int(by_position), self.d_far_global, N.ptr(out["d"]), N.ptr(out["link"]), N.ptr(out["voxel"]),
-               N.ptr(out.get("per_link")), N.stream())
+               int(by_position), self.d_far_global, N.ptr(self._ws), N.ptr(out["d"]), N.ptr(out["link"]),
+               N.ptr(out["voxel"]), N.ptr(out.get("per_link")), N.stream())
         return out
 
     def per_link_min_distances(self, obstacles: ObstacleVoxelSet) -> np.ndarray:
