@@ -124,6 +124,46 @@ __device__ __forceinline__ int floor_small(double u, double& fl) {
     return i;
 }
 
+// Geometry shared by every link grid of one query launch (the usual case:
+// all links baked with the same extent and resolution); kept in kernel
+// parameters so the compiler holds it in uniform registers.
+struct GridGeom {
+    double ext[3], res[3], rinv[3], hi[3], topd[3];
+    int32_t top[3];
+    int32_t cx, cy;
+};
+
+// grids.py:155-191 at a link-frame point, packed-corner layout, returning
+// `far` outside the stored hull.  Identical arithmetic to trilinear_at.
+__device__ __forceinline__ float trilinear_geom(const GridGeom& g, const float4* __restrict__ cells, float far,
+                                                double px, double py, double pz) {
+    const double ux = cell_coord(px, g.ext[0], g.res[0], g.rinv[0]);
+    const double uy = cell_coord(py, g.ext[1], g.res[1], g.rinv[1]);
+    const double uz = cell_coord(pz, g.ext[2], g.res[2], g.rinv[2]);
+    const bool inside = (ux >= 0.0) & (ux <= g.hi[0]) & (uy >= 0.0) & (uy <= g.hi[1]) & (uz >= 0.0) &
+                        (uz <= g.hi[2]);
+    if (!inside) return far;
+    double fx0, fy0, fz0;
+    int ix = floor_small(ux, fx0), iy = floor_small(uy, fy0), iz = floor_small(uz, fz0);
+    if (ix > g.top[0]) { ix = g.top[0]; fx0 = g.topd[0]; }
+    if (iy > g.top[1]) { iy = g.top[1]; fy0 = g.topd[1]; }
+    if (iz > g.top[2]) { iz = g.top[2]; fz0 = g.topd[2]; }
+    const float fx = __double2float_rn(__dsub_rn(ux, fx0));
+    const float fy = __double2float_rn(__dsub_rn(uy, fy0));
+    const float fz = __double2float_rn(__dsub_rn(uz, fz0));
+    const float gx = __fsub_rn(1.0f, fx), gy = __fsub_rn(1.0f, fy), gz = __fsub_rn(1.0f, fz);
+    const uint32_t cell = (uint32_t)ix + (uint32_t)g.cx * ((uint32_t)iy + (uint32_t)g.cy * (uint32_t)iz);
+    const float4 a = __ldg(cells + 2 * cell);      // v000 v100 v010 v110
+    const float4 b = __ldg(cells + 2 * cell + 1);  // v001 v101 v011 v111
+    const float c00 = __fadd_rn(__fmul_rn(a.x, gx), __fmul_rn(a.y, fx));
+    const float c10 = __fadd_rn(__fmul_rn(a.z, gx), __fmul_rn(a.w, fx));
+    const float c01 = __fadd_rn(__fmul_rn(b.x, gx), __fmul_rn(b.y, fx));
+    const float c11 = __fadd_rn(__fmul_rn(b.z, gx), __fmul_rn(b.w, fx));
+    const float c0 = __fadd_rn(__fmul_rn(c00, gy), __fmul_rn(c10, fy));
+    const float c1 = __fadd_rn(__fmul_rn(c01, gy), __fmul_rn(c11, fy));
+    return __fadd_rn(__fmul_rn(c0, gz), __fmul_rn(c1, fz));
+}
+
 // grids.py:155-191 at a link-frame point, packed-corner layout.  Identical
 // arithmetic to trilinear_at (lsdf_math.cuh).
 __device__ __forceinline__ float trilinear_packed(const PackedGrid& g, double px, double py, double pz) {

@@ -26,7 +26,10 @@ using namespace lsdf;
 namespace {
 
 struct QueryParams {
-    PackedGrid grids[LSDF_MAX_LINKS];
+    GridGeom geom;                          // shared by the links of this launch
+    const float4* cells[LSDF_MAX_LINKS];    // packed-corner grid per link
+    float dfar[LSDF_MAX_LINKS];             // float32 link sentinel per link
+    int32_t group[LSDF_MAX_LINKS];          // links handled by this launch
     const double* R;
     const double* dt;
     const int32_t* anchor;
@@ -64,7 +67,7 @@ __device__ __forceinline__ void finalize(const QueryParams& p, int64_t c) {
         for (int l = 0; l < p.n_geo; ++l) {
             const uint32_t u = ~atomicExch(p.perlink + c * p.n_geo + l, 0u);
             const float v = from_orderable(u);
-            p.per_link[c * p.n_geo + l] = fminf(p.clamp, fminf(p.grids[l].d_far, v));  // query.py:171-175
+            p.per_link[c * p.n_geo + l] = fminf(p.clamp, fminf(p.dfar[l], v));  // query.py:171-175
         }
     }
     const uint32_t hi = (uint32_t)(k >> 32);
@@ -87,19 +90,24 @@ __device__ __forceinline__ void finalize(const QueryParams& p, int64_t c) {
     }
 }
 
-__global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_constant__ QueryParams p) {
-    extern __shared__ uint32_t s_queue[];
+template <bool FULL, bool BY_POS>
+__global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_constant__ QueryParams p,
+                                                                  int64_t blocks_per_link) {
+    extern __shared__ double s_dyn[];
+    double* sP = s_dyn;                                       // 3 x Wmax window offsets
+    uint32_t* s_queue = (uint32_t*)(s_dyn + 3 * p.Wmax);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t task = (int64_t)blockIdx.x * WARPS + warp;
-    if (task >= p.n_tasks) return;
+    for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) sP[i] = p.P[i];
+    __syncthreads();
+    // the link is uniform over the block
+    const int l = p.group[blockIdx.x / blocks_per_link];
+    const int64_t t_in_link = (blockIdx.x % blocks_per_link) * WARPS + warp;
+    const int64_t c = t_in_link / p.split;
+    if (c >= p.C) return;
+    const int sidx = (int)(t_in_link % p.split);
     uint32_t* queue = s_queue + warp * QCAP;
-    const int64_t per_link_tasks = p.C * p.split;
-    const int l = (int)(task / per_link_tasks);
-    const int64_t rem = task % per_link_tasks;
-    const int64_t c = rem / p.split;
-    const int sidx = (int)(rem % p.split);
-
-    const PackedGrid& G = p.grids[l];
+    const float4* __restrict__ cells = p.cells[l];
+    const float far = p.dfar[l];
     const int64_t o = c * p.n_geo + l;
     double R[9], dtinv[3];
 #pragma unroll
@@ -107,62 +115,61 @@ __global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_c
     shift_inverse(R, p.dt + o * 3, p.e_r, dtinv);
     const int ax = __ldg(p.anchor + o * 3), ay = __ldg(p.anchor + o * 3 + 1), az = __ldg(p.anchor + o * 3 + 2);
     const int W0 = p.W[0], W1 = p.W[1], W2 = p.W[2];
-    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
-    const double* Px = p.P;
-    const double* Py = p.P + p.Wmax;
-    const double* Pz = p.P + 2 * p.Wmax;
+    const int ny = p.dims[1], nz = p.dims[2];
     const int n_cols = W0 * W1;
-    const double e_r = p.e_r;
+    const int Wm = p.Wmax;
+    // C-order voxel index of window cell (0, 0, 0); cell (mx, my, mz) adds (mx*ny + my)*nz + mz
+    const int lin0 = (ax * ny + ay) * nz + az;
 
-    uint64_t best = ~0ull;
-    float bestval = INFINITY;
+    float bestv = INFINITY;
+    uint32_t bestpos = 0xffffffffu;
     int qlen = 0;
-
-    auto evaluate = [&](uint32_t cell) {
-        const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = (cell >> 16) & 0xff;
-        float v = G.d_far;
-        bool in_mask = true;
-        if (p.full_window) {
+    auto consider = [&](uint32_t cell) {
+        const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
+        float v = far;
+        bool keep = true;
+        if (FULL) {
             const int bit = mx + W0 * (my + W1 * mz);
-            in_mask = (__ldg(p.mask_bits + (bit >> 5)) >> (bit & 31)) & 1u;
+            keep = (__ldg(p.mask_bits + (bit >> 5)) >> (bit & 31)) & 1u;
         }
-        if (in_mask) {
+        if (keep) {
             double pt[3];
-            window_point(__ldg(Px + mx), __ldg(Py + my), __ldg(Pz + mz), R, dtinv, e_r, pt);
-            v = trilinear_packed(G, pt[0], pt[1], pt[2]);
-            bestval = fminf(bestval, v);
+            window_point(sP[mx], sP[Wm + my], sP[2 * Wm + mz], R, dtinv, p.e_r, pt);
+            v = trilinear_geom(p.geom, cells, far, pt[0], pt[1], pt[2]);
         }
-        const int64_t lin = ((int64_t)(ax + mx) * ny + (ay + my)) * nz + (az + mz);
-        const uint32_t pos = p.by_position ? (uint32_t)__ldg(p.posgrid + lin) : (uint32_t)lin;
-        const uint64_t key = ((uint64_t)orderable(v) << 32) | (uint64_t)(pos * (uint32_t)p.n_geo + l);
-        best = key < best ? key : best;
+        const int lin = lin0 + (mx * ny + my) * nz + mz;
+        const uint32_t pos = BY_POS ? (uint32_t)__ldg(p.posgrid + lin) : (uint32_t)lin;
+        const bool better = (v < bestv) | ((v == bestv) & (pos < bestpos));
+        bestv = better ? v : bestv;
+        bestpos = better ? pos : bestpos;
     };
 
     for (int base = sidx * 32; base < n_cols; base += 32 * p.split) {
         const int col = base + lane;
-        const int mx = col % W0, my = col / W0;
+        const int my = col / W0, mx = col - my * W0;
         int zcur = 0, zend = 0;
-        int64_t bitbase = 0;
+        int bitbase = 0;
         if (col < n_cols) {
             const int x = ax + mx, y = ay + my;
-            if (x >= 0 && x < nx && y >= 0 && y < ny) {
+            if (x >= 0 && x < p.dims[0] && y >= 0 && y < ny) {
                 int zlo = 0, zhi = W2;
-                if (!p.full_window) {
-                    zlo = __ldg(p.zrange + 2 * col);
-                    zhi = __ldg(p.zrange + 2 * col + 1);
+                if (!FULL) {
+                    const uint32_t zr = __ldg((const uint32_t*)p.zrange + col);
+                    zlo = (int)(zr & 0xffff);
+                    zhi = (int)(zr >> 16);
                 }
                 zcur = max(az + zlo, 0);
                 zend = min(az + zhi, nz);
-                bitbase = ((int64_t)x * ny + y) * nz;
+                bitbase = (x * ny + y) * nz;
             }
         }
         // consume each column's z-run in segments of <= 16 bits, all lanes in step
         while (__any_sync(FULL_MASK, zcur < zend)) {
             uint32_t bits = 0;
-            const int zs = zcur;
+            const int zs = zcur - az;
             if (zcur < zend) {
-                const int64_t bp = bitbase + zcur;
-                const int off = (int)(bp & 31);
+                const int bp = bitbase + zcur;
+                const int off = bp & 31;
                 const int n = min(min(zend - zcur, 16), 32 - off);
                 bits = (__ldg(p.bitmap + (bp >> 5)) >> off) & ((1u << n) - 1u);
                 zcur += n;
@@ -171,32 +178,35 @@ __global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_c
             int incl = cnt;
 #pragma unroll
             for (int o2 = 1; o2 < 32; o2 <<= 1) {
-                const int t = __shfl_up_sync(FULL_MASK, incl, o2);
-                if (lane >= o2) incl += t;
+                const int v = __shfl_up_sync(FULL_MASK, incl, o2);
+                if (lane >= o2) incl += v;
             }
             const int total = __shfl_sync(FULL_MASK, incl, 31);
             int slot = qlen + incl - cnt;
+            const uint32_t colkey = (uint32_t)mx | ((uint32_t)my << 8);
             while (bits) {
                 const int b = __ffs(bits) - 1;
                 bits &= bits - 1;
-                queue[slot++] = (uint32_t)mx | ((uint32_t)my << 8) | ((uint32_t)(zs + b - az) << 16);
+                queue[slot++] = colkey | ((uint32_t)(zs + b) << 16);
             }
             qlen += total;
             __syncwarp();
             while (qlen >= 32) {
-                evaluate(queue[qlen - 32 + lane]);
+                consider(queue[qlen - 32 + lane]);
                 qlen -= 32;
             }
             __syncwarp();
         }
     }
-    if (lane < qlen) evaluate(queue[lane]);
+    if (lane < qlen) consider(queue[lane]);
 
+    const uint32_t pos_key = bestpos == 0xffffffffu ? 0xffffffffu : bestpos * (uint32_t)p.n_geo + (uint32_t)l;
+    uint64_t best = bestpos == 0xffffffffu ? ~0ull : (((uint64_t)orderable(bestv) << 32) | pos_key);
     best = warp_min_u64(best);
-    bestval = warp_min_f(bestval);
+    const float wmin = warp_min_f(bestv);
     if (lane == 0) {
         atomicMax(p.keys + c, (unsigned long long)~best);
-        if (p.per_link != nullptr) atomicMax(p.perlink + o, ~orderable(bestval));
+        if (p.per_link != nullptr) atomicMax(p.perlink + o, ~orderable(wmin));
         __threadfence();
         const uint32_t done = atomicAdd(p.counters + c, 1u);
         if (done == (uint32_t)(p.n_geo * p.split - 1)) {
@@ -232,18 +242,8 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
     for (int l = 0; l < n_geo; ++l) {
         const lsdf_link_grid& g = grids[l];
         if (g.packed_dev == nullptr) return fail(LSDF_ERR_VALIDATION, "query: link %d has no packed-corner grid", l);
-        PackedGrid& q = p.grids[l];
-        q.cells = (const float4*)g.packed_dev;
-        for (int a = 0; a < 3; ++a) {
-            q.ext[a] = g.extent[a];
-            q.res[a] = g.resolution[a];
-            q.rinv[a] = 1.0 / g.resolution[a];  // RN(1/r): the Markstein reciprocal
-            q.hi[a] = (double)(g.dims[a] - 1);
-            q.top[a] = g.dims[a] - 2;
-        }
-        q.cx = g.dims[0] - 1;
-        q.cy = g.dims[1] - 1;
-        q.d_far = g.d_far;
+        p.cells[l] = (const float4*)g.packed_dev;
+        p.dfar[l] = g.d_far;
         if (g.d_far < clamp) full = 1;  // masked cells can undercut the clamp
     }
     if (window->zrange_dev == nullptr) full = 1;
@@ -283,8 +283,49 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
     p.link_out = link_dev;
     p.voxel_out = voxel_dev;
     p.per_link = per_link_dev;
-    const size_t smem = (size_t)WARPS * QCAP * sizeof(uint32_t);
-    const int64_t blocks = (p.n_tasks + WARPS - 1) / WARPS;
-    query_direct_kernel<<<(unsigned)blocks, 32 * WARPS, smem, (cudaStream_t)stream>>>(p);
-    return check_launch("query_direct_kernel");
+    const size_t smem = (size_t)3 * window->Wmax * sizeof(double) + (size_t)WARPS * QCAP * sizeof(uint32_t);
+    const int64_t blocks_per_link = (C * split + WARPS - 1) / WARPS;
+    cudaStream_t s = (cudaStream_t)stream;
+    // one launch per group of links with identical grid geometry (normally one)
+    bool done[LSDF_MAX_LINKS] = {false};
+    for (int l0 = 0; l0 < n_geo; ++l0) {
+        if (done[l0]) continue;
+        const lsdf_link_grid& g0 = grids[l0];
+        int n_group = 0;
+        for (int l = l0; l < n_geo; ++l) {
+            const lsdf_link_grid& g = grids[l];
+            bool same = true;
+            for (int a = 0; a < 3; ++a)
+                same &= g.dims[a] == g0.dims[a] && g.extent[a] == g0.extent[a] && g.resolution[a] == g0.resolution[a];
+            if (same && !done[l]) {
+                done[l] = true;
+                p.group[n_group++] = l;
+            }
+        }
+        for (int a = 0; a < 3; ++a) {
+            p.geom.ext[a] = g0.extent[a];
+            p.geom.res[a] = g0.resolution[a];
+            p.geom.rinv[a] = 1.0 / g0.resolution[a];  // RN(1/r): the Markstein reciprocal
+            p.geom.hi[a] = (double)(g0.dims[a] - 1);
+            p.geom.topd[a] = (double)(g0.dims[a] - 2);
+            p.geom.top[a] = g0.dims[a] - 2;
+        }
+        p.geom.cx = g0.dims[0] - 1;
+        p.geom.cy = g0.dims[1] - 1;
+        const unsigned blocks = (unsigned)(blocks_per_link * n_group);
+        if (full) {
+            if (by_position)
+                query_direct_kernel<true, true><<<blocks, 32 * WARPS, smem, s>>>(p, blocks_per_link);
+            else
+                query_direct_kernel<true, false><<<blocks, 32 * WARPS, smem, s>>>(p, blocks_per_link);
+        } else {
+            if (by_position)
+                query_direct_kernel<false, true><<<blocks, 32 * WARPS, smem, s>>>(p, blocks_per_link);
+            else
+                query_direct_kernel<false, false><<<blocks, 32 * WARPS, smem, s>>>(p, blocks_per_link);
+        }
+        LSDF_TRY(check_launch("query_direct_kernel"));
+    }
+    return LSDF_OK;
+
 }
