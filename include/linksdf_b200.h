@@ -87,6 +87,12 @@ typedef struct {
     float d_far;          /* float32(min(extent))   grids.py:145-148 */
     double extent[3];
     double resolution[3];
+    /* core_radius: a bound rho such that every value of the grid, and so
+     * every trilinear sample at a link-frame point p inside the hull, is
+     * >= |p| - rho (computed from the grid values; +inf disables the
+     * shell culling of the fused query). */
+    float core_radius;
+    float pad_[3];
 } lsdf_link_grid;
 
 /* Build the packed-corner layout (dims-1)^3 x 8 f32 from a plain grid. */
@@ -109,6 +115,11 @@ typedef struct {
     int32_t pad_;
     const int16_t* zrange_dev;    /* 2 x W[0] x W[1]                   */
     const uint32_t* mask_bits_dev;
+    /* window cells of the sphere mask sorted by distance from the window
+     * centre: packed (mx | my << 8 | mz << 16) and the distance in metres
+     * (rounded down), n_masked entries each; NULL disables shell order */
+    const uint32_t* shell_cells_dev;
+    const float* shell_radius_dev;
 } lsdf_window;
 
 const char* lsdf_version(void);

@@ -38,13 +38,15 @@ class LinkT(C.Structure):
 
 class LinkGridT(C.Structure):
     _fields_ = [("values_dev", C.c_void_p), ("packed_dev", C.c_void_p), ("dims", C.c_int32 * 3), ("d_far", C.c_float),
-                ("extent", C.c_double * 3), ("resolution", C.c_double * 3)]
+                ("extent", C.c_double * 3), ("resolution", C.c_double * 3), ("core_radius", C.c_float),
+                ("pad_", C.c_float * 3)]
 
 
 class WindowT(C.Structure):
     _fields_ = [("W", C.c_int32 * 3), ("n_masked", C.c_int32), ("e_r", C.c_double),
                 ("P_dev", C.c_void_p), ("Wmax", C.c_int32), ("pad_", C.c_int32),
-                ("zrange_dev", C.c_void_p), ("mask_bits_dev", C.c_void_p)]
+                ("zrange_dev", C.c_void_p), ("mask_bits_dev", C.c_void_p),
+                ("shell_cells_dev", C.c_void_p), ("shell_radius_dev", C.c_void_p)]
 
 
 _P = C.c_void_p

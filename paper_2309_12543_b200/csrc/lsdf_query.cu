@@ -29,6 +29,10 @@ struct QueryParams {
     GridGeom geom;                          // shared by the links of this launch
     const float4* cells[LSDF_MAX_LINKS];    // packed-corner grid per link
     float dfar[LSDF_MAX_LINKS];             // float32 link sentinel per link
+    float core[LSDF_MAX_LINKS];             // value(p) >= |p| - core  (lsdf_link_grid.core_radius)
+    const uint32_t* shell_cells;            // kept window cells sorted by distance from the centre
+    const float* shell_radius;              // their distance (m), rounded down
+    int32_t n_shell;
     int32_t group[LSDF_MAX_LINKS];          // links handled by this launch
     const double* R;
     const double* dt;
@@ -216,6 +220,125 @@ __global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_c
     }
 }
 
+// ---------------------------------------------------------------- shell order
+// The kept window cells are visited in order of increasing distance rho from
+// the window centre (the link origin T up to the residual dt).  Every sample
+// of link l at a cell obeys value >= rho - |dt| - core_l (core_radius, derived
+// from the grid values), so once the next chunk's rho - |dt| - core_l exceeds
+// the best value any lane of the warp has found (or, when per-link minima are
+// not requested, the configuration's best over all links so far, read from
+// the key slot), no remaining cell can reach or tie the minimum and the scan
+// stops.  Occupied cells are compacted with a ballot and evaluated 32 at a
+// time with the exact fp64 recipe, so the results are those of the full scan.
+constexpr int QCAP_SHELL = 64;
+
+template <bool BY_POS>
+__global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_constant__ QueryParams p,
+                                                                  int64_t blocks_per_link) {
+    extern __shared__ double s_dyn[];
+    double* sP = s_dyn;
+    uint32_t* s_queue = (uint32_t*)(s_dyn + 3 * p.Wmax);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) sP[i] = p.P[i];
+    __syncthreads();
+    const int l = p.group[blockIdx.x / blocks_per_link];
+    const int64_t t_in_link = (blockIdx.x % blocks_per_link) * WARPS + warp;
+    const int64_t c = t_in_link / p.split;
+    if (c >= p.C) return;
+    const int sidx = (int)(t_in_link % p.split);
+    uint32_t* queue = s_queue + warp * QCAP_SHELL;
+    const float4* __restrict__ cells = p.cells[l];
+    const float far = p.dfar[l];
+    const int64_t o = c * p.n_geo + l;
+    double R[9], dtinv[3];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) R[e] = __ldg(p.R + o * 9 + e);
+    const double* dt = p.dt + o * 3;
+    shift_inverse(R, dt, p.e_r, dtinv);
+    // |dt| rounded up (dt is the residual of T against its voxel centre)
+    const float dtn = (float)(sqrt(dt[0] * dt[0] + dt[1] * dt[1] + dt[2] * dt[2]) * (1.0 + 1e-6) + 1e-12);
+    const float slack = dtn + p.core[l];
+    const int ax = __ldg(p.anchor + o * 3), ay = __ldg(p.anchor + o * 3 + 1), az = __ldg(p.anchor + o * 3 + 2);
+    const int Wm = p.Wmax;
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    const int lin0 = (ax * ny + ay) * nz + az;
+    const bool share_cfg = p.per_link == nullptr;
+
+    float bestv = INFINITY;
+    uint32_t bestpos = 0xffffffffu;
+    float thresh = p.clamp;  // values >= clamp never change the answer
+    if (share_cfg) {
+        uint64_t k = 0;
+        if (lane == 0) k = ~(uint64_t)atomicMax(p.keys + c, 0ull);
+        k = __shfl_sync(FULL_MASK, k, 0);
+        if (k != ~0ull) thresh = fminf(thresh, from_orderable((uint32_t)(k >> 32)));
+    }
+    int qlen = 0, rounds = 0;
+    auto evaluate = [&](uint32_t cell, bool valid) {
+        if (valid) {
+            const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
+            double pt[3];
+            window_point(sP[mx], sP[Wm + my], sP[2 * Wm + mz], R, dtinv, p.e_r, pt);
+            const float v = trilinear_geom(p.geom, cells, far, pt[0], pt[1], pt[2]);
+            const int lin = lin0 + (mx * ny + my) * nz + mz;
+            const uint32_t pos = BY_POS ? (uint32_t)__ldg(p.posgrid + lin) : (uint32_t)lin;
+            const bool better = (v < bestv) | ((v == bestv) & (pos < bestpos));
+            bestv = better ? v : bestv;
+            bestpos = better ? pos : bestpos;
+        }
+        thresh = fminf(thresh, from_orderable(__reduce_min_sync(FULL_MASK, orderable(bestv))));
+        if (share_cfg && (++rounds & 3) == 0) {
+            uint64_t k = 0;
+            if (lane == 0) k = ~(uint64_t)atomicMax(p.keys + c, 0ull);
+            k = __shfl_sync(FULL_MASK, k, 0);
+            if (k != ~0ull) thresh = fminf(thresh, from_orderable((uint32_t)(k >> 32)));
+        }
+    };
+
+    for (int k0 = sidx * 32; k0 < p.n_shell; k0 += 32 * p.split) {
+        if (__ldg(p.shell_radius + k0) - slack > thresh) break;  // every later cell is farther
+        const int k = k0 + lane;
+        bool occ = false;
+        uint32_t cell = 0;
+        if (k < p.n_shell) {
+            cell = __ldg(p.shell_cells + k);
+            const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
+            const int x = ax + mx, y = ay + my, z = az + mz;
+            if (x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz) {
+                const int lin = lin0 + (mx * ny + my) * nz + mz;
+                occ = (__ldg(p.bitmap + (lin >> 5)) >> (lin & 31)) & 1u;
+            }
+        }
+        const unsigned ballot = __ballot_sync(FULL_MASK, occ);
+        if (occ) queue[qlen + __popc(ballot & ((1u << lane) - 1u))] = cell;
+        qlen += __popc(ballot);
+        __syncwarp();
+        if (qlen >= 32) {
+            evaluate(queue[qlen - 32 + lane], true);
+            qlen -= 32;
+        }
+        __syncwarp();
+    }
+    if (qlen > 0) evaluate(lane < qlen ? queue[lane] : 0u, lane < qlen);
+
+    const uint32_t pos_key = bestpos == 0xffffffffu ? 0xffffffffu : bestpos * (uint32_t)p.n_geo + (uint32_t)l;
+    uint64_t best = bestpos == 0xffffffffu ? ~0ull : (((uint64_t)orderable(bestv) << 32) | pos_key);
+    best = warp_min_u64(best);
+    if (lane == 0) atomicMax(p.keys + c, (unsigned long long)~best);
+    if (p.per_link != nullptr) {
+        const uint32_t wm = __reduce_min_sync(FULL_MASK, orderable(bestv));
+        if (lane == 0) atomicMax(p.perlink + o, ~wm);
+    }
+    if (lane == 0) {
+        __threadfence();
+        const uint32_t done = atomicAdd(p.counters + c, 1u);
+        if (done == (uint32_t)(p.n_geo * p.split - 1)) {
+            __threadfence();
+            finalize(p, c);
+        }
+    }
+}
+
 inline int64_t ws_bytes(int64_t C, int32_t n_geo) {
     return align256(C * 4) + align256(C * 8) + align256(C * n_geo * 4);
 }
@@ -244,6 +367,7 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
         if (g.packed_dev == nullptr) return fail(LSDF_ERR_VALIDATION, "query: link %d has no packed-corner grid", l);
         p.cells[l] = (const float4*)g.packed_dev;
         p.dfar[l] = g.d_far;
+        p.core[l] = g.core_radius;
         if (g.d_far < clamp) full = 1;  // masked cells can undercut the clamp
     }
     if (window->zrange_dev == nullptr) full = 1;
@@ -263,6 +387,10 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
     }
     p.full_window = full;
     p.e_r = window->e_r;
+    p.shell_cells = window->shell_cells_dev;
+    p.shell_radius = window->shell_radius_dev;
+    p.n_shell = window->n_masked;
+    const bool shells = !full && window->shell_cells_dev != nullptr && window->shell_radius_dev != nullptr;
     p.P = window->P_dev;
     p.Wmax = window->Wmax;
     p.by_position = by_position;
@@ -313,7 +441,13 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
         p.geom.cx = g0.dims[0] - 1;
         p.geom.cy = g0.dims[1] - 1;
         const unsigned blocks = (unsigned)(blocks_per_link * n_group);
-        if (full) {
+        if (shells) {
+            const size_t smem_s = (size_t)3 * window->Wmax * sizeof(double) + (size_t)WARPS * QCAP_SHELL * 4;
+            if (by_position)
+                query_shells_kernel<true><<<blocks, 32 * WARPS, smem_s, s>>>(p, blocks_per_link);
+            else
+                query_shells_kernel<false><<<blocks, 32 * WARPS, smem_s, s>>>(p, blocks_per_link);
+        } else if (full) {
             if (by_position)
                 query_direct_kernel<true, true><<<blocks, 32 * WARPS, smem, s>>>(p, blocks_per_link);
             else

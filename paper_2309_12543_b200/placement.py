@@ -196,6 +196,18 @@ class WindowGeometry:
         s.Wmax = Wmax
         s.zrange_dev = N.ptr(dev["zrange"])
         s.mask_bits_dev = N.ptr(dev["mask_bits"])
+        # kept cells sorted by distance from the window centre (shell order)
+        off = _axis_offsets(self.extent, self.grid, False)
+        mxs, mys, mzs = np.nonzero(self.mask)
+        dist = np.sqrt(off[0][mxs] ** 2 + off[1][mys] ** 2 + off[2][mzs] ** 2)
+        order = np.argsort(dist, kind="stable")
+        packed = (mxs | (mys << 8) | (mzs << 16)).astype(np.uint32)[order]
+        radius = np.nextafter(dist[order].astype(np.float32), np.float32(-np.inf))  # rounded down
+        radius = np.minimum(radius, dist[order]).astype(np.float32)
+        dev["shell_cells"] = N.to_device(packed.view(np.int32), t.int32)
+        dev["shell_radius"] = N.to_device(radius, t.float32)
+        s.shell_cells_dev = N.ptr(dev["shell_cells"])
+        s.shell_radius_dev = N.ptr(dev["shell_radius"])
         self._tables = (s, dev)
         return self._tables
 

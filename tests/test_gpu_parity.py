@@ -370,3 +370,36 @@ def test_config2_full_size_properties(L):
               for s in (slice(0, 250), slice(250, 500))]
     ds = np.concatenate([L.query_min_distances(h, obs) for h in halves])
     assert np.array_equal(ds, d)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_direct_equals_dense_on_adversarial_grids(L, seed):
+    """Random (non-Lipschitz) grid values, random rotations, a dense cloud:
+    the screened direct kernel must select exactly what the dense gather selects."""
+    rng = np.random.default_rng(seed)
+    grid = L.EnvGrid(1.0, 0.05)
+    e_r = 0.3
+    window = L.WindowGeometry.build(e_r, grid)
+    sdfs = []
+    for li in range(3):
+        vals = rng.normal(0.0, 0.2, size=(30, 30, 30)).astype(np.float32)
+        if li == 1:
+            vals = np.round(vals * 8) / 8  # many exact ties
+        sdfs.append(L.LinkSdf(e_r, 0.02, vals, li))
+    C = 40
+    R = L.sample_rotations(rng, C * 3).reshape(C, 3, 3, 3)
+    T = rng.uniform(-0.6, 0.6, size=(C, 3, 3))
+    traj = L.TrajectorySdf.from_poses(sdfs, L.LinkPoseBatch(R, T), grid, L.ExactTransformProvider(window))
+    obs = L.voxelize_pointcloud(rng.uniform(-1, 1, size=(20_000, 3)), grid)
+    d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
+    dense = L.RobotSdfBatch(traj.device_values(), grid, traj.d_far_global)
+    d2, _, v2 = L.query_min_distances(dense, obs, return_argmin=True)
+    assert np.array_equal(d, d2) and np.array_equal(voxel, v2)
+    # link: lowest link whose window value at the winning voxel equals d
+    fields = list(L.place_links_batch(sdfs, L.LinkPoseBatch(R, T), grid, L.ExactTransformProvider(window)))
+    pl = L.per_link_min_distances(iter(fields), obs, C, 3, traj.d_far_global)
+    assert np.array_equal(traj.per_link_min_distances(obs), pl)
+    for c in range(C):
+        if link[c] >= 0:
+            assert pl[c, link[c]] == d[c]
+            assert np.all(pl[c, : link[c]] > d[c]) or voxel[c] >= 0
