@@ -244,7 +244,8 @@ def run_ours(args, rank, world, dist):
     chk.launch(device_only=True)
     torch.cuda.synchronize()
     n_occ = int(chk.ws[:4].view(torch.int32).item())
-    qk = lambda: chk.traj.query_device(chk.ws, False, outputs=chk.q_out)  # noqa: E731
+    q_outs = {}
+    qk = lambda: chk.traj.query_device(chk.ws, False, outputs=q_outs)  # noqa: E731
     _time_steps(torch, qk, 3, flush)
     q_ms = statistics.mean(_time_steps(torch, qk, max(5, args.steps), flush))
     alg_bytes = 4.0 * n_occ * n_local

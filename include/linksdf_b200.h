@@ -127,6 +127,10 @@ const char* lsdf_last_error(void);
 /* Number of kernels this library enqueued since load (evidence counter). */
 uint64_t lsdf_launch_count(void);
 
+/* Device address of page-locked (mapped) host memory: lets the real-time
+ * path read its inputs and write its results over PCIe without staging. */
+int lsdf_host_device_pointer(void* host, void** dev);
+
 /* ---- stage 1: forward kinematics + alignment --------------------------- */
 
 /* forward_kinematics_batch (robot.py:305-347) for C configurations of D

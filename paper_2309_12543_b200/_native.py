@@ -82,6 +82,7 @@ _SIGS = {
     "lsdf_build_mesh": [_P, _I32, _I32, C.POINTER(_D), C.POINTER(_D), C.POINTER(_I32), _P, _P],
     "lsdf_mesh_points": [_P, _I32, _I32, _P, _I64, _P, _P],
     "lsdf_mlp_predict": [_P, _P, _P, _P, _I32, _I64, _P, _I64, _P, _I32, _P],
+    "lsdf_host_device_pointer": [_P, C.POINTER(C.c_void_p)],
 }
 
 EXPORTS = tuple(_SIGS) + ("lsdf_version", "lsdf_last_error", "lsdf_launch_count")
@@ -196,6 +197,13 @@ def empty(shape, dtype):
 
 def zeros(shape, dtype):
     return torch().zeros(shape, dtype=dtype, device=device())
+
+
+def mapped_pointer(host_tensor) -> int:
+    """Device address of a pinned host tensor (zero-copy access from kernels)."""
+    out = C.c_void_p()
+    call("lsdf_host_device_pointer", host_tensor.data_ptr(), C.byref(out))
+    return int(out.value)
 
 
 def env_struct(grid) -> EnvGridT:

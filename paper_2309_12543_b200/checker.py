@@ -1,25 +1,33 @@
 """DistanceChecker — the real-time entry point: configurations + cloud → (d, link, voxel).
 
 One object per (robot, link SDFs, environment grid, window).  ``prepare``
-sizes device buffers and pinned host staging for a batch shape and captures
-the whole control-cycle step in one CUDA graph:
+sizes device buffers and pinned host buffers for a batch shape and captures
+one control cycle as a CUDA graph with two branches:
 
-    H2D(q, points) → fk_align → voxelize (memset, scatter, rank) →
-    query_direct (lookup + min/argmin, finished in-kernel) → D2H(d, link, voxel, flags)
+    side stream:  fk_align (reads the configurations)  ──┐
+    main stream:  voxelize (memset, scatter + rank)     ──┴─> query_direct ──> (d, link, voxel)
 
-so a 500-waypoint query is a single graph launch plus one stream sync.  The
-point capacity is fixed per capture; shorter clouds are padded with NaN,
+End to end (``query``) the kernels read the configurations and the cloud
+straight from page-locked host memory and the query writes (d, link, voxel)
+straight back to page-locked host memory (zero-copy over PCIe, mapped by
+``lsdf_host_device_pointer``), so the transfer overlaps the voxelization
+instead of preceding it; when mapping is unavailable the graph stages the
+same bytes with explicit async copies.  ``launch(device_only=True)`` replays
+the same cycle on device-resident inputs (the bench's HBM-resident number).
+
+The point capacity is fixed per capture; shorter clouds are padded with NaN,
 which the voxelizer drops exactly like out-of-grid points (query.py:112).
 """
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import _native as N
 from .errors import LimitViolationError, NoOverlapError, ValidationError
-from .query import TrajectorySdf, occupancy_workspace, voxelize_device
-from .robot import fk_device
+from .query import TrajectorySdf, occupancy_workspace
 
 
 class DistanceChecker:
@@ -41,32 +49,55 @@ class DistanceChecker:
         self._graph_dev = None
 
     # ------------------------------------------------------------------ buffers
-    def prepare(self, n_configs: int, n_points: int, points_dtype=np.float32, use_graph: bool = True):
+    def prepare(self, n_configs: int, n_points: int, points_dtype=np.float32, use_graph: bool = True,
+                zero_copy: bool = True):
         t = N.torch()
         dev = N.device()
-        tdt = t.float32 if np.dtype(points_dtype) == np.float32 else t.float64
-        C_, D = int(n_configs), self.robot.dof
-        self._shape = (C_, int(n_points), np.dtype(points_dtype))
-        self.q_host = t.empty((C_, D), dtype=t.float64, pin_memory=True)
-        self.p_host = t.full((int(n_points), 3), float("nan"), dtype=tdt, pin_memory=True)
+        pdt = np.dtype(points_dtype)
+        if pdt not in (np.float32, np.float64):
+            raise ValidationError(f"points must be float32 or float64, got {pdt}")
+        tdt = t.float32 if pdt == np.float32 else t.float64
+        C_, D, G = int(n_configs), self.robot.dof, len(self.sdfs)
+        P = int(n_points)
+        self._shape = (C_, P, pdt)
+        pin = dict(pin_memory=True)
+        # host side (page-locked)
+        self.q_host = t.zeros((C_, D), dtype=t.float64, **pin)
+        self.p_host = t.full((P, 3), float("nan"), dtype=tdt, **pin)
+        self.d_host = t.zeros((C_,), dtype=t.float32, **pin)
+        self.link_host = t.zeros((C_,), dtype=t.int32, **pin)
+        self.voxel_host = t.zeros((C_,), dtype=t.int32, **pin)
+        self.flags_host = t.zeros((4,), dtype=t.int32, **pin)
+        self._np = {k: getattr(self, k + "_host").numpy() for k in ("q", "p", "d", "link", "voxel", "flags")}
+        # device side
         self.q_dev = t.zeros((C_, D), dtype=t.float64, device=dev)
-        self.p_dev = t.full((int(n_points), 3), float("nan"), dtype=tdt, device=dev)
+        self.p_dev = t.full((P, 3), float("nan"), dtype=tdt, device=dev)
+        self.R_geo = t.zeros((C_, G, 3, 3), dtype=t.float64, device=dev)
+        self.dt_geo = t.zeros((C_, G, 3), dtype=t.float64, device=dev)
+        self.anchor_geo = t.zeros((C_, G, 3), dtype=t.int32, device=dev)
+        self.flags = t.zeros((4,), dtype=t.int32, device=dev)
+        self.limits = N.to_device(np.ascontiguousarray(self._limits), t.float64)
+        self.d_dev = t.zeros((C_,), dtype=t.float32, device=dev)
+        self.link_dev = t.zeros((C_,), dtype=t.int32, device=dev)
+        self.voxel_dev = t.zeros((C_,), dtype=t.int32, device=dev)
         self.ws = occupancy_workspace(self.grid)
-        self.fk_out = {}
-        fk_device(self.robot, self.q_dev, all_links=False, grid=self.grid, window_dims=self.window.dims,
-                  outputs=self.fk_out)  # allocates outputs (values are garbage until run)
-        self.traj = TrajectorySdf(self.sdfs, self.grid, self.window, self.fk_out["R_geo"], self.fk_out["dt_geo"],
-                                  self.fk_out["anchor_geo"], self.d_far_global)
-        self.q_out = {}
-        self.traj.query_device(self.ws, False, outputs=self.q_out)
-        self.d_host = t.empty((C_,), dtype=t.float32, pin_memory=True)
-        self.link_host = t.empty((C_,), dtype=t.int32, pin_memory=True)
-        self.voxel_host = t.empty((C_,), dtype=t.int32, pin_memory=True)
-        self.flags_host = t.empty((4,), dtype=t.int32, pin_memory=True)
-        self.window.device_tables()
+        self.traj = TrajectorySdf(self.sdfs, self.grid, self.window, self.R_geo, self.dt_geo, self.anchor_geo,
+                                  self.d_far_global)
+        self.qws = t.zeros((int(N.lib().lsdf_query_workspace_bytes(C_, G)),), dtype=t.uint8, device=dev)
+        self._wstruct, _ = self.window.device_tables()
         for sdf in self.sdfs:
             sdf.packed_values()
+        # mapped addresses for the zero-copy end-to-end cycle
+        self._map = None
+        if zero_copy:
+            try:
+                self._map = {k: N.mapped_pointer(getattr(self, k + "_host")) for k in ("q", "p", "d", "link", "voxel")}
+            except Exception:  # mapping unavailable: the graph stages copies instead
+                self._map = None
         self._side = t.cuda.Stream()
+        self._env = ctypes.byref(self.grid.c_struct())
+        self._W = N.i32x3(self.window.dims)
+        self._chain = self.robot.chain_table()
         t.cuda.synchronize()
         if use_graph:
             self._capture()
@@ -74,77 +105,89 @@ class DistanceChecker:
 
     def host_inputs(self):
         """Pinned numpy views (configs (C, D) f64, points (N, 3)) the caller may fill in place."""
-        return self.q_host.numpy(), self.p_host.numpy()
+        return self._np["q"], self._np["p"]
 
-    # ------------------------------------------------------------------ the step
-    # FK+alignment and voxelization are independent: FK runs on a side stream
-    # while the cloud is voxelized, the query joins both (two graph branches).
-    def _fk(self, h2d: bool):
-        if h2d:
-            self.q_dev.copy_(self.q_host, non_blocking=True)
-        self.fk_out["flags"].zero_()
-        fk_device(self.robot, self.q_dev, all_links=False, grid=self.grid, window_dims=self.window.dims,
-                  outputs=self.fk_out)
+    @property
+    def zero_copy(self) -> bool:
+        return self._map is not None
 
-    def _run(self, h2d: bool):
+    # ------------------------------------------------------------------ the cycle
+    def _run(self, e2e: bool):
         t = N.torch()
+        C_, P, pdt = self._shape
         main = t.cuda.current_stream()
-        self._side.wait_stream(main)
-        with t.cuda.stream(self._side):
-            self._fk(h2d)
-        if h2d:
+        side = self._side
+        zc = e2e and self._map is not None
+        staged = e2e and self._map is None
+        side.wait_stream(main)
+        with t.cuda.stream(side):
+            if staged:
+                self.q_dev.copy_(self.q_host, non_blocking=True)
+            self.flags.zero_()
+            q_ptr = self._map["q"] if zc else N.ptr(self.q_dev)
+            N.call("lsdf_fk_align", self._chain, self.robot.n_links, len(self.sdfs), q_ptr, C_, self.robot.dof,
+                   N.ptr(self.limits), self._env, self._W, None, None, N.ptr(self.R_geo), N.ptr(self.dt_geo),
+                   N.ptr(self.anchor_geo), N.ptr(self.flags), side.cuda_stream)
+        if staged:
             self.p_dev.copy_(self.p_host, non_blocking=True)
-        voxelize_device(self.p_dev, self.grid, workspace=self.ws)
-        main.wait_stream(self._side)
-        self.traj.query_device(self.ws, False, outputs=self.q_out)
-        if h2d:
-            self.d_host.copy_(self.q_out["d"], non_blocking=True)
-            self.link_host.copy_(self.q_out["link"], non_blocking=True)
-            self.voxel_host.copy_(self.q_out["voxel"], non_blocking=True)
-            self.flags_host.copy_(self.fk_out["flags"], non_blocking=True)
-
-    def _compute(self):
-        """Device work of one cycle (inputs already in q_dev / p_dev)."""
-        self._run(False)
-
-    def _step(self):
-        """H2D of the inputs, the cycle, D2H of (d, link, voxel, flags)."""
-        self._run(True)
+        p_ptr = self._map["p"] if zc else N.ptr(self.p_dev)
+        N.call("lsdf_voxelize", p_ptr, int(pdt == np.float32), P, self._env, N.ptr(self.ws), None,
+               main.cuda_stream)
+        main.wait_stream(side)
+        if e2e:
+            with t.cuda.stream(side):  # 16 B of flags back to the host, off the critical path
+                self.flags_host.copy_(self.flags, non_blocking=True)
+        if zc:
+            outs = (self._map["d"], self._map["link"], self._map["voxel"])
+        else:
+            outs = (N.ptr(self.d_dev), N.ptr(self.link_dev), N.ptr(self.voxel_dev))
+        tr = self.traj
+        N.call("lsdf_query_direct", N.ptr(self.R_geo), N.ptr(self.dt_geo), N.ptr(self.anchor_geo), C_, tr.n_links,
+               tr._table, ctypes.byref(self._wstruct), self._env, N.ptr(self.ws), 0, self.d_far_global,
+               N.ptr(self.qws), outs[0], outs[1], outs[2], None, main.cuda_stream)
+        if staged:
+            self.d_host.copy_(self.d_dev, non_blocking=True)
+            self.link_host.copy_(self.link_dev, non_blocking=True)
+            self.voxel_host.copy_(self.voxel_dev, non_blocking=True)
+        if e2e:
+            main.wait_stream(side)
 
     def _capture(self):
         t = N.torch()
         s = t.cuda.Stream()
         s.wait_stream(t.cuda.current_stream())
         with t.cuda.stream(s):
-            for _ in range(2):  # warm-up outside capture (sets kernel attributes, pools)
-                self._step()
+            for _ in range(2):  # warm-up outside capture (kernel attributes, allocator pools)
+                self._run(True)
+                self._run(False)
         t.cuda.current_stream().wait_stream(s)
         t.cuda.synchronize()
         self._graph = t.cuda.CUDAGraph()
         with t.cuda.graph(self._graph):
-            self._step()
+            self._run(True)
         self._graph_dev = t.cuda.CUDAGraph()
         with t.cuda.graph(self._graph_dev):
-            self._compute()
+            self._run(False)
         t.cuda.synchronize()
 
     # ------------------------------------------------------------------ public calls
     def launch(self, device_only: bool = False):
-        """Enqueue one cycle (graph replay when captured); no synchronisation."""
+        """Enqueue one cycle (graph replay when captured); no synchronisation.
+
+        device_only: inputs from q_dev / p_dev, results to d_dev / link_dev / voxel_dev.
+        """
         g = self._graph_dev if device_only else self._graph
         if g is not None:
             g.replay()
-        elif device_only:
-            self._compute()
         else:
-            self._step()
+            self._run(not device_only)
 
     def query(self, configs=None, points=None):
         """One control cycle from host arrays; returns numpy (d, link, voxel)."""
         if self._shape is None:
             raise ValidationError("call prepare(n_configs, n_points) first")
         C_, cap, _ = self._shape
-        q_np, p_np = self.host_inputs()
+        q_np, p_np = self._np["q"], self._np["p"]
         if configs is not None:
             q = np.asarray(configs, dtype=np.float64)
             if q.shape != q_np.shape:
@@ -158,11 +201,12 @@ class DistanceChecker:
             p_np[len(p):] = np.nan
         self.launch()
         N.torch().cuda.current_stream().synchronize()
-        self._raise_flags(q_np)
-        return self.d_host.numpy().copy(), self.link_host.numpy().copy(), self.voxel_host.numpy().copy()
+        f = self._np["flags"]
+        if f[0] or f[1]:
+            self._raise_flags(q_np, f)
+        return self._np["d"].copy(), self._np["link"].copy(), self._np["voxel"].copy()
 
-    def _raise_flags(self, q_np):
-        f = self.flags_host.numpy()
+    def _raise_flags(self, q_np, f):
         if self.check_limits and f[0]:
             lim = self._limits
             bad = (q_np < lim[:, 0]) | (q_np > lim[:, 1])

@@ -15,3 +15,14 @@ std::atomic<uint64_t>& launch_counter() {
 extern "C" const char* lsdf_version(void) { return "linksdf-b200 0.1.0 (sm_100a)"; }
 extern "C" const char* lsdf_last_error(void) { return lsdf::last_error().c_str(); }
 extern "C" uint64_t lsdf_launch_count(void) { return lsdf::launch_counter().load(); }
+
+// Device address of page-locked host memory (mapped under UVA), so kernels
+// can read inputs / write results across PCIe without staging copies.
+extern "C" int lsdf_host_device_pointer(void* host, void** dev) {
+    cudaError_t e = cudaHostGetDevicePointer(dev, host, 0);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return lsdf::fail(LSDF_ERR_CUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e));
+    }
+    return LSDF_OK;
+}

@@ -31,93 +31,118 @@ struct FkParams {
     int32_t* flags;
 };
 
-constexpr int FK_THREADS = 64;
+constexpr int FK_THREADS = 128;
 
-__global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_constant__ FkParams p) {
-    // [n_links][12][FK_THREADS]: thread-fastest so the 64 threads of a block
-    // touch consecutive banks when they read or write the same link slot
-    extern __shared__ double s_pose[];
-    const int64_t c = (int64_t)blockIdx.x * FK_THREADS + threadIdx.x;
-    if (c >= p.C) return;
-    double* pose = s_pose + threadIdx.x;
-    auto at = [&](int li, int e) -> double& { return pose[(li * 12 + e) * FK_THREADS]; };
-    const double* q = p.q + c * p.D;
-    if (p.limits != nullptr) {  // robot.py:297-302
+// Three phases per CTA of `cpb` configurations x `lp` link slots (lp = next
+// power of two >= n_links):
+//   1. one thread per (configuration, link): the joint-local transform
+//      (sin/cos, Rodrigues, r_o @ r_motion) — independent work, in parallel;
+//   2. one thread per configuration: the parents-first chain (matmuls only);
+//   3. one thread per (configuration, link): outputs + window alignment.
+__global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_constant__ FkParams p, int lp_log2) {
+    extern __shared__ double s_fk[];
+    const int lp = 1 << lp_log2, cpb = FK_THREADS >> lp_log2;
+    const int cl = threadIdx.x >> lp_log2, li = threadIdx.x & (lp - 1);
+    const int64_t c = (int64_t)blockIdx.x * cpb + cl;
+    const bool active = c < p.C && li < p.n_links;
+    double* loc = s_fk + ((size_t)cl * lp + li) * 12;             // local transform of (cl, li)
+    double* world = s_fk + (size_t)cpb * lp * 12;                 // [cpb][lp][12]
+    const double* q = p.q + (c < p.C ? c : 0) * p.D;
+    if (c < p.C && p.limits != nullptr) {  // robot.py:297-302
         int bad = 0;
-        for (int j = 0; j < p.D; ++j) {
+        for (int j = li; j < p.D; j += lp) {
             const double v = q[j];
             bad += (v < p.limits[2 * j] || v > p.limits[2 * j + 1]);
         }
         if (bad) atomicAdd(&p.flags[0], bad);
     }
-    for (int li = 0; li < p.n_links; ++li) {
+    if (active) {
         const lsdf_link& L = p.links[li];
-        double rj[9], tj[3];
-        if (L.kind == 0) {
+        if (L.kind == 1) {  // revolute: r_o @ rodrigues(q)   robot.py:331-334
+            const double a = q[L.q_col];
+            double M[9], rl[9];
+            rodrigues(L.skew, L.outer, cos(a), sin(a), M);
+            mm33(L.joint_R, M, rl);
 #pragma unroll
-            for (int e = 0; e < 9; ++e) rj[e] = (e == 0 || e == 4 || e == 8) ? 1.0 : 0.0;
-            tj[0] = tj[1] = tj[2] = 0.0;
+            for (int e = 0; e < 9; ++e) loc[e] = rl[e];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) loc[9 + k] = L.joint_t[k];
         } else {
-            double rp[9], tp[3];
 #pragma unroll
-            for (int e = 0; e < 9; ++e) rp[e] = at(L.parent, e);
-#pragma unroll
-            for (int k = 0; k < 3; ++k) tp[k] = at(L.parent, 9 + k);
-            double rl[9], tl[3];
-            if (L.kind == 1) {  // revolute: r_o @ rodrigues(q)   robot.py:331-334
+            for (int e = 0; e < 9; ++e) loc[e] = L.joint_R[e];
+            if (L.kind == 2) {  // prismatic: t_o + q * (r_o @ axis)   robot.py:335-337
                 const double a = q[L.q_col];
-                double M[9];
-                rodrigues(L.skew, L.outer, cos(a), sin(a), M);
-                mm33(L.joint_R, M, rl);
 #pragma unroll
-                for (int k = 0; k < 3; ++k) tl[k] = L.joint_t[k];
+                for (int k = 0; k < 3; ++k) loc[9 + k] = DADD(L.joint_t[k], DMUL(a, L.R_axis[k]));
             } else {
 #pragma unroll
-                for (int e = 0; e < 9; ++e) rl[e] = L.joint_R[e];
-                if (L.kind == 2) {  // prismatic: t_o + q * (r_o @ axis)   robot.py:335-337
-                    const double a = q[L.q_col];
+                for (int k = 0; k < 3; ++k) loc[9 + k] = L.joint_t[k];
+            }
+        }
+    }
+    __syncthreads();
+    if (li == 0 && c < p.C) {
+        double* wc = world + (size_t)cl * lp * 12;
+        const double* lc = s_fk + (size_t)cl * lp * 12;
+        for (int k2 = 0; k2 < p.n_links; ++k2) {
+            const lsdf_link& L = p.links[k2];
+            double rj[9], tj[3];
+            if (L.kind == 0) {
 #pragma unroll
-                    for (int k = 0; k < 3; ++k) tl[k] = DADD(L.joint_t[k], DMUL(a, L.R_axis[k]));
-                } else {
+                for (int e = 0; e < 9; ++e) rj[e] = (e == 0 || e == 4 || e == 8) ? 1.0 : 0.0;
+                tj[0] = tj[1] = tj[2] = 0.0;
+            } else {
+                double rp[9], tp[3], rl[9], tl[3], tmp[3];
+                const double* wp = wc + L.parent * 12;
+                const double* lk = lc + k2 * 12;
 #pragma unroll
-                    for (int k = 0; k < 3; ++k) tl[k] = L.joint_t[k];
+                for (int e = 0; e < 9; ++e) {
+                    rp[e] = wp[e];
+                    rl[e] = lk[e];
                 }
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    tp[k] = wp[9 + k];
+                    tl[k] = lk[9 + k];
+                }
+                mm33(rp, rl, rj);        // robot.py:341
+                mv_einsum(rp, tl, tmp);  // robot.py:342
+#pragma unroll
+                for (int k = 0; k < 3; ++k) tj[k] = DADD(tp[k], tmp[k]);
             }
-            double tmp[3];
-            mm33(rp, rl, rj);         // robot.py:341
-            mv_einsum(rp, tl, tmp);   // robot.py:342
+            double R[9], tmp[3];
+            mm33(rj, L.link_R, R);         // robot.py:343
+            mv_einsum(rj, L.link_t, tmp);  // robot.py:344-346
+            double* w = wc + k2 * 12;
 #pragma unroll
-            for (int k = 0; k < 3; ++k) tj[k] = DADD(tp[k], tmp[k]);
+            for (int e = 0; e < 9; ++e) w[e] = R[e];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) w[9 + k] = DADD(tj[k], tmp[k]);
         }
-        double R[9], T[3], tmp[3];
-        mm33(rj, L.link_R, R);        // robot.py:343
-        mv_einsum(rj, L.link_t, tmp); // robot.py:344-346
+    }
+    __syncthreads();
+    if (!active) return;
+    const double* w = world + ((size_t)cl * lp + li) * 12;
+    const lsdf_link& L = p.links[li];
+    if (p.R_all != nullptr) {
+        double* dr = p.R_all + (c * p.n_links + li) * 9;
+        double* dtt = p.T_all + (c * p.n_links + li) * 3;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) T[k] = DADD(tj[k], tmp[k]);
+        for (int e = 0; e < 9; ++e) dr[e] = w[e];
 #pragma unroll
-        for (int e = 0; e < 9; ++e) at(li, e) = R[e];
+        for (int k = 0; k < 3; ++k) dtt[k] = w[9 + k];
+    }
+    if (L.geom_slot >= 0 && p.R_geo != nullptr) {
+        const int64_t o = c * p.n_geo + L.geom_slot;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) at(li, 9 + k) = T[k];
-        if (p.R_all != nullptr) {
-            double* dr = p.R_all + (c * p.n_links + li) * 9;
-            double* dtt = p.T_all + (c * p.n_links + li) * 3;
+        for (int e = 0; e < 9; ++e) p.R_geo[o * 9 + e] = w[e];
+        int32_t anc[3];
+        double del[3], T[3] = {w[9], w[10], w[11]};
+        if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del)) atomicAdd(&p.flags[1], 1);
 #pragma unroll
-            for (int e = 0; e < 9; ++e) dr[e] = R[e];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) dtt[k] = T[k];
-        }
-        if (L.geom_slot >= 0 && p.R_geo != nullptr) {
-            const int64_t o = c * p.n_geo + L.geom_slot;
-#pragma unroll
-            for (int e = 0; e < 9; ++e) p.R_geo[o * 9 + e] = R[e];
-            int32_t anc[3];
-            double del[3];
-            if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del)) atomicAdd(&p.flags[1], 1);
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                p.dt_geo[o * 3 + k] = del[k];
-                p.anchor_geo[o * 3 + k] = anc[k];
-            }
+        for (int k = 0; k < 3; ++k) {
+            p.dt_geo[o * 3 + k] = del[k];
+            p.anchor_geo[o * 3 + k] = anc[k];
         }
     }
 }
@@ -166,15 +191,11 @@ extern "C" int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_
     p.dt_geo = dt_geo_dev;
     p.anchor_geo = anchor_geo_dev;
     p.flags = flags_dev;
-    const size_t smem = (size_t)FK_THREADS * n_links * 12 * sizeof(double);
-    if (smem > 48 * 1024) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(fk_align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            attr = true;
-        }
-    }
-    fk_align_kernel<<<grid_for(C, FK_THREADS), FK_THREADS, smem, (cudaStream_t)stream>>>(p);
+    int lp_log2 = 0;
+    while ((1 << lp_log2) < n_links) ++lp_log2;
+    const int cpb = FK_THREADS >> lp_log2;
+    const size_t smem = (size_t)2 * FK_THREADS * 12 * sizeof(double);  // local + world, cpb * lp slots each
+    fk_align_kernel<<<grid_for(C, cpb), FK_THREADS, smem, (cudaStream_t)stream>>>(p, lp_log2);
     return check_launch("fk_align_kernel");
 }
 
