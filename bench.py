@@ -1,28 +1,30 @@
 """Benchmark of the batched link-SDF distance checker (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload config4|config2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One JSON line on rank 0.  A *step* is one pass of the hot path over one batch:
 FK + alignment for every waypoint, voxelization of the step's obstacle cloud,
-and the fused transform/trilinear/min/argmin query, producing
-(d, link, voxel) per waypoint.
+and the fused transform / trilinear / min / argmin query, producing
+(d, link, voxel) for every waypoint.
 
 * ``value`` — waypoint-queries/s, whole job, on BASELINE config 4 (7-DoF arm,
   65,536 waypoints vs a 1M-point crowd cloud, 64^3 link SDFs, W = 16), inputs
   resident in HBM, device time (CUDA events on the launching stream), L2
   flushed (256 MiB write) before every timed step.  N > 1 GPUs: waypoints are
-  sharded contiguously across ranks (no collective on the data path), time is
-  the max over ranks.
-* ``realtime`` (N = 1) — BASELINE config 2: p50/p99 µs per 500-waypoint query
-  (6-DoF, 100k-point cloud, 64^3), device-only graph and host-to-host e2e.
-* ``e2e`` — the same throughput through the public API (DistanceChecker.query)
-  from pinned host buffers, H2D of configs + cloud and D2H of results inside
-  the timed region.
-* ``roofline`` — query_direct_kernel: algorithmic bytes 4·N_occ per
-  waypoint-query (the reference's gather) over its event-timed
-  duration, against MEASURED_PEAKS.json hbm_gbs.
-* ``cpu_baseline`` — the oracle port of the reference pipeline (numpy) on the
-  host cores, bounded sample, rank 0 at N = 1.
+  sharded contiguously across ranks (each rank voxelizes the full cloud; no
+  collective on the data path), time is the max over ranks -> strong scaling.
+* ``realtime`` (N = 1) — BASELINE config 2: p50 / p99 µs per 500-waypoint
+  query (6-DoF, 100k-point cloud, 64^3): device graph and host-to-host.
+* ``e2e`` — config 4 through the public API (DistanceChecker.query) from
+  pinned host buffers: the kernels read the inputs and write the results
+  across PCIe inside the timed region (host wall clock per step).
+* ``roofline`` — query_shells_kernel (the dominant kernel): algorithmic bytes
+  4 * N_occ per waypoint-query (the reference's gather) over
+  its event-timed duration, against MEASURED_PEAKS.json hbm_gbs.  The kernel
+  culls cells it can prove irrelevant, so frac > 1 means "faster than
+  gathering the dense robot SDF at HBM speed".
+* ``cpu_baseline`` — the oracle port of the reference pipeline (numpy) on
+  this host, bounded sample, rank 0 at N = 1.
 
 ``--impl reference`` times that CPU port alone on the same workload and
 prints the same line with "impl": "reference".
@@ -46,7 +48,7 @@ REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
 METRIC = "p50/p99 µs per 500-waypoint query; waypoint-queries/s at 1/2/4/8 B200"
-KERNELS_PER_STEP = 4  # fk_align, voxel_scatter, voxel_compact, query_direct (+1 memset node)
+KERNELS_PER_STEP = 3  # fk_align, voxel_scatter (+rank prefix), query_shells; plus 2 memset nodes
 
 
 def _peaks():
@@ -66,32 +68,32 @@ def _env_int(name, default):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+    """nvidia-smi clocks + throttle reasons, sampled every 50 ms while the GPU works."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines = []
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except FileNotFoundError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
-    def __exit__(self, *a):
+    def stop(self):
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -99,10 +101,11 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ts, ln in self.lines:
+            if t0 is not None and not (t0 <= ts <= t1):
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -111,7 +114,7 @@ class ClockSampler:
                 mx = float(parts[1])
             except ValueError:
                 continue
-            for n, v in zip(names, parts[2:6]):
+            for n, v in zip(self.NAMES, parts[2:6]):
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
@@ -133,17 +136,14 @@ def _cloud(shape, seed):
     return S.cloud_for(shape, seed).astype(np.float32)  # frames are f32 on disk (query.py:313-327)
 
 
-def _setup_gpu(shape, n_configs, seeds, L):
-    from paper_2309_12543_b200 import scenarios as S
-
+def _checker(shape, n_configs, L):
     robot = L.RobotModel.from_dict(shape.robot)
     grid = L.EnvGrid(shape.grid_extent, shape.grid_res)
     sdfs = [L.build_link_sdf(robot.links[i].geometry, shape.link_extent, shape.link_res, link_id=i)
             for i in robot.geometry_links]
     window = L.WindowGeometry.build(shape.link_extent, grid)
     chk = L.DistanceChecker(robot, sdfs, grid, window).prepare(n_configs, shape.n_points, np.float32)
-    inputs = [(S.random_configs(shape.robot, n_configs, seed=s), _cloud(shape, s)) for s in seeds]
-    return robot, grid, sdfs, window, chk, inputs
+    return robot, chk
 
 
 class L2Flush:
@@ -155,9 +155,9 @@ class L2Flush:
 
 
 def _time_steps(torch, fn, steps, flush, before=None):
-    """Per-step device times (ms) with CUDA events on the launching stream."""
+    """Per-step device times (ms), CUDA events on the launching stream, L2 flushed before each."""
     stream = torch.cuda.current_stream()
-    times = []
+    marks = []
     for k in range(steps):
         if before is not None:
             before(k)
@@ -167,36 +167,40 @@ def _time_steps(torch, fn, steps, flush, before=None):
         e0.record(stream)
         fn()
         e1.record(stream)
-        times.append((e0, e1))
+        marks.append((e0, e1))
     torch.cuda.synchronize()
-    return [a.elapsed_time(b) for a, b in times]
+    return [a.elapsed_time(b) for a, b in marks]
 
 
-def run_ours(args, rank, world, dist):
+def _max_over_ranks(dist, torch, x):
+    if dist is None:
+        return x
+    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_ours(args, rank, world, dist, sampler):
     import torch
 
     import paper_2309_12543_b200 as L
+    from paper_2309_12543_b200 import scenarios as S
 
-    torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
     shape = _shape(args.workload)
     C_total = shape.n_waypoints
     per = C_total // world
     lo = rank * per
     n_local = per if rank < world - 1 else C_total - lo
-    from paper_2309_12543_b200 import scenarios as S
-
+    robot, chk = _checker(shape, n_local, L)
     seeds = [11, 12, 13]
-    robot, grid, sdfs, window, chk, _ = _setup_gpu(shape, n_local, [], L)
-    # shard: each rank owns waypoints [lo, lo + n_local) of every step's trajectory batch
-    dev_inputs = []
-    for s in seeds:
-        q_all = S.random_configs(shape.robot, C_total, seed=s)[lo:lo + n_local]
-        dev_inputs.append((torch.from_numpy(np.ascontiguousarray(q_all)).cuda(),
-                           torch.from_numpy(_cloud(shape, s)).cuda()))
+    # each rank owns waypoints [lo, lo + n_local) of every step's trajectory batch
+    host = [(np.ascontiguousarray(S.random_configs(shape.robot, C_total, seed=s)[lo:lo + n_local]), _cloud(shape, s))
+            for s in seeds]
+    dev = [(torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda()) for q, p in host]
     flush = L2Flush(torch)
 
     def stage(k):
-        q, p = dev_inputs[k % len(dev_inputs)]
+        q, p = dev[k % len(dev)]
         chk.q_dev.copy_(q)
         chk.p_dev.copy_(p)
 
@@ -205,54 +209,46 @@ def run_ours(args, rank, world, dist):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler = ClockSampler(torch.cuda.current_device())
-    with sampler:
-        dev_ms = _time_steps(torch, step, args.steps, flush, stage)
+    t0 = time.perf_counter()
+    dev_ms = _time_steps(torch, step, args.steps, flush, stage)
     torch.cuda.synchronize()
-    total_ms = sum(dev_ms)
+    t1 = time.perf_counter()
     if dist is not None:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
         dist.barrier()
+    total_ms = _max_over_ranks(dist, torch, sum(dev_ms))
     ms_per_step = total_ms / args.steps
     value = C_total / (ms_per_step / 1e3)
 
-    # ---- e2e through the public API from pinned host buffers (host wall clock)
+    # ---- e2e through the public API: pinned host inputs, zero-copy reads, results back in pinned memory
     q_host, p_host = chk.host_inputs()
-    host_np = [(q.cpu().numpy(), p.cpu().numpy()) for q, p in dev_inputs]
-    e2e_t = []
+    e2e = []
     for k in range(args.warmup + args.steps):
-        q, p = host_np[k % len(host_np)]
+        q, p = host[k % len(host)]
         q_host[...] = q
         p_host[: len(p)] = p
         flush()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        d, link, voxel = chk.query()
-        t1 = time.perf_counter()
+        s0 = time.perf_counter()
+        chk.query()
+        s1 = time.perf_counter()
         if k >= args.warmup:
-            e2e_t.append(t1 - t0)
-    e2e_ms = 1e3 * sum(e2e_t) / len(e2e_t)
-    if dist is not None:
-        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+            e2e.append(s1 - s0)
+    e2e_ms = _max_over_ranks(dist, torch, 1e3 * sum(e2e) / len(e2e))
 
-    # ---- roofline of the dominant kernel (query_direct) timed alone
+    # ---- roofline of the dominant kernel (query) timed alone on the staged batch
     stage(0)
     chk.launch(device_only=True)
     torch.cuda.synchronize()
     n_occ = int(chk.ws[:4].view(torch.int32).item())
-    q_outs = {}
-    qk = lambda: chk.traj.query_device(chk.ws, False, outputs=q_outs)  # noqa: E731
+    outs = {}
+    qk = lambda: chk.traj.query_device(chk.ws, False, outputs=outs)  # noqa: E731
     _time_steps(torch, qk, 3, flush)
-    q_ms = statistics.mean(_time_steps(torch, qk, max(5, args.steps), flush))
+    q_ms = statistics.mean(_time_steps(torch, qk, max(5, min(args.steps, 50)), flush))
     alg_bytes = 4.0 * n_occ * n_local
     peak, peak_kind = _peaks()
     achieved = alg_bytes / (q_ms / 1e3) / 1e9
     traffic = None
-    tf = REPO / "profiles" / "query_direct_traffic.json"
+    tf = REPO / "profiles" / "query_traffic.json"
     if tf.exists():
         try:
             traffic = json.loads(tf.read_text()).get(args.workload)
@@ -261,44 +257,48 @@ def run_ours(args, rank, world, dist):
     out = {
         "metric": METRIC, "value": value, "unit": "waypoint-queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64 index math + f32 lerp",
-        "data": "synthetic (seeded scenarios: arm7g/arm6g primitives, human/crowd clouds)",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded arm7g/arm6g primitive robots, random joint configs, human/crowd point clouds",
         "config": {"workload": f"{shape.name}: {shape.robot['name']} {C_total} waypoints vs {shape.n_points} pts "
-                               f"({shape.cloud}), link SDF {round(2 * shape.link_extent / shape.link_res)}^3, "
-                               f"env 50^3 @ 4 cm, W=16", "waypoints": C_total, "points": shape.n_points,
-                   "occupied_voxels": n_occ, "parallelism": f"waypoint shards x{world}",
-                   "l2": "flushed (256 MiB write) before every timed step"},
+                               f"({shape.cloud}), 64^3 link SDFs, env 50^3 @ 4 cm, W=16",
+                   "waypoints": C_total, "points": shape.n_points, "occupied_voxels": n_occ,
+                   "parallelism": f"waypoint shards x{world}",
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "timing": "device: CUDA events around a graph replay of the cycle"},
         "gpu_launches": KERNELS_PER_STEP * args.steps,
         "e2e": {"value": C_total / (e2e_ms / 1e3), "unit": "waypoint-queries/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(n_local * robot.dof * 8 + shape.n_points * 12),
                 "d2h_bytes_per_step": int(n_local * 12 + 16),
-                "path": "DistanceChecker.query() from pinned host buffers, one CUDA graph, host wall clock"},
+                "path": "DistanceChecker.query() from pinned host buffers (zero-copy kernel reads/writes over PCIe), "
+                        "host wall clock" if chk.zero_copy else "DistanceChecker.query() staged copies"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "query_direct_kernel", "kernel_ms": q_ms,
-                     "algorithmic_bytes": alg_bytes, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
-        "clocks": sampler.summary(),
+                     "traffic": traffic, "kernel": "query_shells_kernel", "kernel_ms": q_ms,
+                     "algorithmic_bytes": alg_bytes, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst)"},
+        "clocks": sampler.summary(t0 - 0.2, t1 + 0.2) if sampler else None,
     }
-    return out, (robot, grid, sdfs, window, chk, n_occ)
+    return out
 
 
 def run_realtime(args, L):
     """Config 2: p50/p99 per 500-waypoint query (device graph and host-to-host)."""
     import torch
 
+    from paper_2309_12543_b200 import scenarios as S
+
     shape = _shape("config2")
-    seeds = [21, 22, 23, 24]
-    robot, grid, sdfs, window, chk, inputs = _setup_gpu(shape, shape.n_waypoints, seeds, L)
-    dev_inputs = [(torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda()) for q, p in inputs]
+    robot, chk = _checker(shape, shape.n_waypoints, L)
+    inputs = [(S.random_configs(shape.robot, shape.n_waypoints, seed=s), _cloud(shape, s)) for s in (21, 22, 23, 24)]
+    dev = [(torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda()) for q, p in inputs]
     flush = L2Flush(torch)
 
     def stage(k):
-        q, p = dev_inputs[k % len(dev_inputs)]
+        q, p = dev[k % len(dev)]
         chk.q_dev.copy_(q)
         chk.p_dev.copy_(p)
 
-    n = max(50, args.steps)
+    n = max(200, args.steps)
     _time_steps(torch, lambda: chk.launch(device_only=True), 10, flush, stage)
-    dev = _time_steps(torch, lambda: chk.launch(device_only=True), n, flush, stage)
+    devt = _time_steps(torch, lambda: chk.launch(device_only=True), n, flush, stage)
     q_host, p_host = chk.host_inputs()
     e2e = []
     for k in range(n + 10):
@@ -316,84 +316,95 @@ def run_realtime(args, L):
     n_occ = int(chk.ws[:4].view(torch.int32).item())
     pct = lambda a, p: float(np.percentile(np.asarray(a) * 1e3, p))  # noqa: E731  ms -> µs
     return {"workload": f"{shape.name}: arm6g 500 waypoints vs 100k pts, 64^3, W=16", "occupied_voxels": n_occ,
-            "device_p50_us": pct(dev, 50), "device_p99_us": pct(dev, 99),
+            "device_p50_us": pct(devt, 50), "device_p99_us": pct(devt, 99),
             "e2e_p50_us": pct(e2e, 50), "e2e_p99_us": pct(e2e, 99), "samples": n,
-            "waypoint_queries_per_s_device": 500 / (statistics.mean(dev) / 1e3)}
+            "waypoint_queries_per_s_device": 500 / (statistics.mean(devt) / 1e3),
+            "paper_gpu_ms_per_trajectory": 0.391}
 
 
 # ----------------------------------------------------------------------------- CPU (oracle port)
 
 
-def cpu_baseline(workload: str, budget_s: float = 20.0):
-    """Time the oracle port (numpy restatement of the reference) on a bounded sample."""
-    from oracle import linksdf_oracle as O
-    from paper_2309_12543_b200 import scenarios as S
+class CpuPort:
+    """The oracle port of the reference pipeline (numpy), set up once per workload."""
 
-    shape = _shape(workload)
-    doc = shape.robot
-    chain = O.chain_from_doc(doc)
-    gl = O.geometry_links(chain)
-    grids = [O.build_grid(chain[i]["geometry"], shape.link_extent, shape.link_res) for i in gl]
-    env = O.Env(shape.grid_extent, shape.grid_res)
-    pts = _cloud(shape, 11)
-    t0 = time.perf_counter()
-    idx, _, _ = O.voxelize(pts, env)
-    t_vox = time.perf_counter() - t0
-    sample = 64 if workload == "config4" else shape.n_waypoints
-    q = S.random_configs(doc, sample, seed=11)
-    reps, t_run = 0, 0.0
-    while reps < 2 or (t_run < budget_s and reps < 5):
+    def __init__(self, workload: str, sample: int):
+        from oracle import linksdf_oracle as O
+        from paper_2309_12543_b200 import scenarios as S
+
+        self.O = O
+        self.shape = shape = _shape(workload)
+        chain = O.chain_from_doc(shape.robot)
+        self.chain = chain
+        self.gl = O.geometry_links(chain)
+        self.grids = [O.build_grid(chain[i]["geometry"], shape.link_extent, shape.link_res) for i in self.gl]
+        self.env = O.Env(shape.grid_extent, shape.grid_res)
+        pts = _cloud(shape, 11)
         t0 = time.perf_counter()
-        R, T = O.fk(chain, q)
-        windows, anchors = O.place_windows(grids, [shape.link_extent] * len(gl), [shape.link_res] * len(gl),
-                                           R[:, gl], T[:, gl], env, shape.link_extent)
-        batch = O.assemble(windows, anchors, env, shape.link_extent)
-        O.argmin_oracle(batch, windows, anchors, idx, shape.link_extent)
-        t_run += time.perf_counter() - t0
-        reps += 1
-    t_sample = t_run / reps
-    # per-waypoint rate with the cloud's voxelization charged pro rata (it runs
-    # once per step for all waypoints of the step)
-    t_per_wp = t_sample / sample + t_vox / shape.n_waypoints
-    threads = os.environ.get("OPENBLAS_NUM_THREADS") or "default"
-    return {"value": 1.0 / t_per_wp, "unit": "waypoint-queries/s", "cores": len(os.sched_getaffinity(0)),
-            "kind": "port",
-            "sample": f"{shape.name}: {sample} waypoints x {reps} reps through FK+placement+assembly+gather+argmin "
-                      f"({t_sample:.2f} s each) + voxelize of the full {shape.n_points}-pt cloud ({t_vox:.2f} s, "
-                      f"charged per waypoint over {shape.n_waypoints}); numpy single process, "
-                      f"OPENBLAS_NUM_THREADS={threads}",
-            "seconds_per_waypoint": t_per_wp}
+        self.idx, _, _ = O.voxelize(pts, self.env)
+        self.t_vox = time.perf_counter() - t0
+        self.sample = min(sample, shape.n_waypoints)
+        self.q = S.random_configs(shape.robot, self.sample, seed=11)
+
+    def step(self) -> float:
+        """Seconds per waypoint-query for one bounded sample (voxelize charged pro rata)."""
+        O, shape, gl = self.O, self.shape, self.gl
+        t0 = time.perf_counter()
+        R, T = O.fk(self.chain, self.q)
+        windows, anchors = O.place_windows(self.grids, [shape.link_extent] * len(gl), [shape.link_res] * len(gl),
+                                           R[:, gl], T[:, gl], self.env, shape.link_extent)
+        batch = O.assemble(windows, anchors, self.env, shape.link_extent)
+        O.argmin_oracle(batch, windows, anchors, self.idx, shape.link_extent)
+        t_sample = time.perf_counter() - t0
+        return t_sample / self.sample + self.t_vox / shape.n_waypoints
+
+    def describe(self, reps):
+        shape = self.shape
+        threads = os.environ.get("OPENBLAS_NUM_THREADS") or "default"
+        return (f"{shape.name}: {self.sample} waypoints x {reps} reps through FK + placement + assembly + gather + "
+                f"argmin (oracle port of the reference, numpy, one process) against the full {shape.n_points}-pt "
+                f"cloud voxelized once ({self.t_vox:.2f} s, charged per waypoint over {shape.n_waypoints}); "
+                f"OPENBLAS_NUM_THREADS={threads}")
+
+
+def cpu_baseline(workload: str, budget_s: float = 15.0, sample: int = 64):
+    port = CpuPort(workload, sample)
+    per_wp, t_start = [], time.perf_counter()
+    while len(per_wp) < 2 or (time.perf_counter() - t_start < budget_s and len(per_wp) < 20):
+        per_wp.append(port.step())
+    v = 1.0 / statistics.median(per_wp)
+    return {"value": v, "unit": "waypoint-queries/s", "cores": 1, "kind": "port",
+            "sample": port.describe(len(per_wp)), "host_cores_available": len(os.sched_getaffinity(0))}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    shape = _shape(args.workload)
-    samples = []
-    base = None
-    for k in range(args.warmup + args.steps):
-        base = cpu_baseline(args.workload, budget_s=0.0)
-        if k >= args.warmup:
-            samples.append(base["value"])
-        if sum(1 for _ in samples) and time.perf_counter() - _T0 > 240:
+    port = CpuPort(args.workload, 64)
+    for _ in range(args.warmup):
+        port.step()
+    per_wp = []
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
+        per_wp.append(port.step())
+        if time.perf_counter() - t_start > 240:
             break
-    value = statistics.mean(samples) if samples else base["value"]
+    value = len(per_wp) / sum(per_wp)
+    shape = port.shape
     return {"metric": METRIC, "value": value, "unit": "waypoint-queries/s", "n_gpus": world,
-            "steps": len(samples), "warmup": args.warmup, "ms_per_step": 1e3 * shape.n_waypoints / value,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 index math + f32 lerp",
+            "steps": len(per_wp), "warmup": args.warmup, "ms_per_step": 1e3 * shape.n_waypoints / value,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": shape.name, "waypoints": shape.n_waypoints, "points": shape.n_points},
-            "cpu_baseline": {**base, "value": value},
+            "cpu_baseline": {"value": value, "unit": "waypoint-queries/s", "cores": 1, "kind": "port",
+                             "sample": port.describe(len(per_wp))},
             "e2e": {"value": value, "unit": "waypoint-queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-
-
-_T0 = time.perf_counter()
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["config4", "config2", "config1"], default="config4")
@@ -402,26 +413,31 @@ def main():
     args.warmup = max(3, args.warmup)
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
-    dist = None
     if args.impl == "reference":
         out = run_reference(args, rank, world)
         if out is not None:
             print(json.dumps(out), flush=True)
         return
+    import torch
+
+    torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
+    dist = None
     if world > 1:
-        import torch
         import torch.distributed as tdist
 
-        torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
         tdist.init_process_group("nccl")
         dist = tdist
     import paper_2309_12543_b200 as L
 
-    out, _ = run_ours(args, rank, world, dist)
-    if world == 1:
-        out["realtime"] = run_realtime(args, L)
-        if not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(args.workload)
+    sampler = ClockSampler(torch.cuda.current_device()).start()
+    try:
+        out = run_ours(args, rank, world, dist, sampler)
+        if world == 1:
+            out["realtime"] = run_realtime(args, L)
+    finally:
+        sampler.stop()
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.workload)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist is not None:

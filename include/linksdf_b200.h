@@ -138,8 +138,9 @@ int lsdf_host_device_pointer(void* host, void** dev);
  * (C, n_links, 3) fp64.  For geometry links (geom_slot >= 0) also writes the
  * alignment of compute_alignment (placement.py:60-99) for window width W:
  *   R_geo (C, n_geo, 9), dt_geo (C, n_geo, 3) fp64, anchor_geo (C, n_geo, 3) i32.
- * flags_dev[0] += #limit violations (robot.py:291-302), flags_dev[1] += #windows
- * that miss the grid (placement.py:86-93); limits_dev is (D, 2) fp64 or NULL. */
+ * flags_dev[0] = #limit violations (robot.py:291-302), flags_dev[1] = #windows
+ * that miss the grid (placement.py:86-93), both reset by this call;
+ * limits_dev is (D, 2) fp64 or NULL. */
 int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_geo,
                   const double* q_dev, int64_t C, int32_t D, const double* limits_dev,
                   const lsdf_env_grid* env, const int32_t W[3],

@@ -123,7 +123,6 @@ class DistanceChecker:
         with t.cuda.stream(side):
             if staged:
                 self.q_dev.copy_(self.q_host, non_blocking=True)
-            self.flags.zero_()
             q_ptr = self._map["q"] if zc else N.ptr(self.q_dev)
             N.call("lsdf_fk_align", self._chain, self.robot.n_links, len(self.sdfs), q_ptr, C_, self.robot.dof,
                    N.ptr(self.limits), self._env, self._W, None, None, N.ptr(self.R_geo), N.ptr(self.dt_geo),

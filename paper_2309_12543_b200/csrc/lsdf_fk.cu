@@ -195,6 +195,8 @@ extern "C" int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_
     while ((1 << lp_log2) < n_links) ++lp_log2;
     const int cpb = FK_THREADS >> lp_log2;
     const size_t smem = (size_t)2 * FK_THREADS * 12 * sizeof(double);  // local + world, cpb * lp slots each
+    if (flags_dev != nullptr)
+        LSDF_TRY(check_cuda(cudaMemsetAsync(flags_dev, 0, 2 * sizeof(int32_t), (cudaStream_t)stream), "fk flags memset"));
     fk_align_kernel<<<grid_for(C, cpb), FK_THREADS, smem, (cudaStream_t)stream>>>(p, lp_log2);
     return check_launch("fk_align_kernel");
 }
