@@ -403,3 +403,21 @@ def test_direct_equals_dense_on_adversarial_grids(L, seed):
         if link[c] >= 0:
             assert pl[c, link[c]] == d[c]
             assert np.all(pl[c, : link[c]] > d[c]) or voxel[c] >= 0
+
+
+def test_mlp_tensor_cores(L):
+    """tcgen05 kind::tf32 (3xTF32) layer 2 vs the reference prediction and the CUDA-core kernel."""
+    import torch
+
+    m = golden("mlp")
+    model = L.TinyMlp(m["w1"], m["b1"], m["w2"], m["b2"])
+    R = torch.from_numpy(np.ascontiguousarray(m["R"].reshape(-1, 9))).cuda()
+    y_tc = model.predict_device(R, use_tensor_cores=True).cpu().numpy().reshape(m["predict"].shape)
+    assert np.abs(y_tc - m["predict"]).max() <= MLP_TOL
+    rng = np.random.default_rng(4)
+    big = L.TinyMlp.random(2103, hidden=32, seed=3)   # the W = 16 window of configs 1-2
+    Rb = torch.from_numpy(L.sample_rotations(rng, 300).reshape(-1, 9)).cuda()
+    a = big.predict_device(Rb, use_tensor_cores=True).cpu().numpy()
+    b = big.predict_device(Rb, use_tensor_cores=False).cpu().numpy()
+    scale = np.abs(b).max()
+    assert np.abs(a - b).max() <= 1e-6 * max(1.0, scale) * 8
