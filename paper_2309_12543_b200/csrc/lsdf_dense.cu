@@ -179,19 +179,43 @@ __global__ void trilinear_kernel(lsdf_link_grid g, const double* pts, int64_t n,
                           DMUL(pts[3 * i + 2], scale), LdgLoad{g.values_dev});
 }
 
-__global__ void transform_exact_kernel(const double* R, const double* dt, int64_t B, const double* P, int64_t V,
-                                       double e_r, double* G) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= B * V) return;
-    const int64_t b = i / V, v = i % V;
-    double Rb[9], dtinv[3];
+// One CTA per (rotation b, slice of points): R and dt_inv are computed once
+// per CTA; each thread writes its points' 24-byte fp64 triples (consecutive
+// threads -> consecutive points -> coalesced).
+constexpr int TX_THREADS = 256, TX_PER_THREAD = 4;
+
+__global__ void __launch_bounds__(TX_THREADS) transform_exact_kernel(const double* R, const double* dt, int64_t B,
+                                                                      const double* __restrict__ P, int64_t V,
+                                                                      double e_r, double* G) {
+    __shared__ double s_R[9], s_dti[3];
+    const int64_t b = blockIdx.y;
+    if (threadIdx.x == 0) {
+        double Rb[9], dti[3];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) Rb[e] = R[b * 9 + e];
-    shift_inverse(Rb, dt + b * 3, e_r, dtinv);
-    const double px = P[3 * v], py = P[3 * v + 1], pz = P[3 * v + 2];
+        for (int e = 0; e < 9; ++e) Rb[e] = R[b * 9 + e];
+        shift_inverse(Rb, dt + b * 3, e_r, dti);
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
-        G[i * 3 + k] = DADD(DFMA(pz, Rb[6 + k], DFMA(py, Rb[3 + k], DMUL(px, Rb[k]))), dtinv[k]);
+        for (int e = 0; e < 9; ++e) s_R[e] = Rb[e];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) s_dti[k] = dti[k];
+    }
+    __syncthreads();
+    double Rb[9], dti[3];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) Rb[e] = s_R[e];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dti[k] = s_dti[k];
+    const int64_t v0 = (int64_t)blockIdx.x * TX_THREADS * TX_PER_THREAD + threadIdx.x;
+    double* out = G + b * V * 3;
+#pragma unroll
+    for (int r = 0; r < TX_PER_THREAD; ++r) {
+        const int64_t v = v0 + (int64_t)r * TX_THREADS;
+        if (v >= V) break;
+        const double px = __ldg(P + 3 * v), py = __ldg(P + 3 * v + 1), pz = __ldg(P + 3 * v + 2);
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            out[3 * v + k] = DADD(DFMA(pz, Rb[6 + k], DFMA(py, Rb[3 + k], DMUL(px, Rb[k]))), dti[k]);
+    }
 }
 
 __global__ void pack_corners_kernel(const float* __restrict__ v, int32_t nx, int32_t ny, int32_t nz, float4* out) {
@@ -297,7 +321,7 @@ extern "C" int lsdf_grid_transform_exact(const double* R_dev, const double* dt_d
                                          const double* points_dev, int64_t V, double e_r, double* G_dev,
                                          void* stream) {
     if (B * V <= 0) return LSDF_OK;
-    transform_exact_kernel<<<grid_for(B * V, 256), 256, 0, (cudaStream_t)stream>>>(R_dev, dt_dev, B, points_dev, V,
-                                                                                   e_r, G_dev);
+    dim3 grid((unsigned)((V + TX_THREADS * TX_PER_THREAD - 1) / (TX_THREADS * TX_PER_THREAD)), (unsigned)B);
+    transform_exact_kernel<<<grid, TX_THREADS, 0, (cudaStream_t)stream>>>(R_dev, dt_dev, B, points_dev, V, e_r, G_dev);
     return check_launch("transform_exact_kernel");
 }

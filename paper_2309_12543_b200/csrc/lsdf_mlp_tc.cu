@@ -1,19 +1,23 @@
 // lsdf_mlp_tc.cu — TinyMlp layer 2 on the 5th-generation tensor cores (tcgen05).
 //
 // y = h W2 + b2 with h = relu(x W1 + b1) (approx.py:123-130): M = rotations,
-// N = 3V window coordinates (up to 3.3 M), K = hidden (32).  One CTA owns a
-// 128-row M tile: it computes its h rows on CUDA cores (K = 9 layer), splits
-// them into TF32 hi/lo halves and keeps them in shared memory (K-major,
-// 128-byte swizzle).  It then streams N tiles of 256 outputs: the matching
-// W2^T tile (pre-split hi/lo and pre-swizzled at model upload, so the copy is
-// a single bulk async copy — cp.async.bulk, the TMA engine — completing on an
-// mbarrier) lands in shared memory, one elected thread issues the 3xTF32
-// product as tcgen05.mma kind::tf32 (hi*hi + hi*lo + lo*hi, K = 8 per
-// instruction) into a 128 x 256 fp32 TMEM accumulator, commits to an mbarrier,
-// and the four warps drain TMEM with tcgen05.ld, add b2 and store y.
-// 3xTF32 keeps ~fp32 accuracy (|err| <= ~1e-6 relative), well inside the
-// 1e-5 (normalized) contract; the CUDA-core kernel (lsdf_mlp.cu) stays the
-// bit-reproducing path.
+// N = 3V window coordinates (up to 3.3 M), K = hidden (32).
+//
+// layer1_pack_kernel (CUDA cores, K = 9) writes h for every row, split into
+// TF32 hi/lo halves, straight into the GEMM's A-tile layout (K-major, 128-byte
+// swizzle).  W2^T is split and swizzled the same way once per weight buffer
+// (pack_w2_kernel), so every operand tile is one contiguous bulk async copy
+// (cp.async.bulk -> UBLKCP, completing on an mbarrier).
+//
+// mlp_tc_kernel is warp-specialized and persistent over N tiles of 256
+// outputs (each W2 tile read once, all M tiles of 128 rows streamed past it):
+// warp 0 issues the copies, one thread of warp 1 issues the 3xTF32 product as
+// tcgen05.mma kind::tf32 (hi*hi + hi*lo + lo*hi, K = 8 per instruction) into a
+// double-buffered 128 x 256 fp32 TMEM accumulator and commits to mbarriers,
+// warps 2-5 drain TMEM with tcgen05.ld, add b2 and write y through a padded
+// shared-memory transpose as coalesced 128-byte row segments.  3xTF32 keeps
+// ~fp32 accuracy, inside the 1e-5 (normalized) contract; the CUDA-core kernel
+// (lsdf_mlp.cu) stays the bit-reproducing path.
 #include "lsdf_common.cuh"
 
 namespace {
@@ -22,7 +26,6 @@ constexpr int TM = 128;   // rows per tile (tcgen05 M)
 constexpr int TN = 256;   // outputs per tile (tcgen05 N)
 constexpr int KB_BYTES_A = TM * 128;  // one 32-wide k-block of A: 128 rows x 128 B
 constexpr int KB_BYTES_B = TN * 128;  // one 32-wide k-block of B: 256 rows x 128 B
-constexpr int THREADS = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -118,119 +121,187 @@ __global__ void pack_w2_kernel(const float* __restrict__ w2, int H, int64_t N, i
     }
 }
 
+// Layer 1 (K = 9, CUDA cores) for every row, split into TF32 hi/lo and stored
+// in the GEMM's A-tile layout: [m_tile][k_block][128 rows x 128 B, swizzled].
+__global__ void layer1_pack_kernel(const float* __restrict__ w1, const float* __restrict__ b1, int H, int kblocks,
+                                   const double* __restrict__ R, int64_t B, int64_t m_tiles, float* a_hi,
+                                   float* a_lo) {
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= m_tiles * TM) return;
+    float x[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) x[k] = row < B ? (float)R[row * 9 + k] : 0.0f;
+    const int64_t mt = row / TM;
+    const uint32_t r = (uint32_t)(row % TM);
+    for (int j = 0; j < kblocks * 32; ++j) {
+        float h = 0.0f;
+        if (row < B && j < H) {
+            float acc = __fmul_rn(x[0], __ldg(w1 + j));
+#pragma unroll
+            for (int k = 1; k < 9; ++k) acc = __fmaf_rn(x[k], __ldg(w1 + k * H + j), acc);
+            acc = __fadd_rn(acc, __ldg(b1 + j));
+            h = acc > 0.0f ? acc : 0.0f;
+        }
+        const float hh = tf32_rna(h);
+        const float hl = tf32_rna(h - hh);
+        const int64_t base = (mt * kblocks + (j >> 5)) * (int64_t)TM * 32;
+        const uint32_t off = sw128_offset(r, (uint32_t)(j & 31)) >> 2;
+        a_hi[base + off] = hh;
+        a_lo[base + off] = hl;
+    }
+}
+
 struct MlpTcParams {
-    const float* w1;
-    const float* b1;
-    const float* b2;
+    const float* a_hi;
+    const float* a_lo;
     const float* w2t_hi;
     const float* w2t_lo;
-    const double* R;
+    const float* b2;
     float* y;
-    int64_t B, N, n_tiles;
-    int32_t H, kblocks;
+    int64_t B, N, n_tiles, m_tiles;
+    int32_t kblocks;
 };
 
-__global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(const __grid_constant__ MlpTcParams p) {
+// Warp roles: warp 0 = bulk-copy producer, warp 1 = MMA issuer, warps 2-5 =
+// epilogue (warp w drains TMEM lanes 32*(w % 4) .. +31).  Persistent over N
+// tiles (each W2 tile is read once), looping over all M tiles inside; A tiles
+// and TMEM accumulators are double-buffered so the epilogue of one tile
+// overlaps the copies and MMAs of the next.
+constexpr int TC_THREADS = 192;
+constexpr int EP_STRIDE = 33;  // padded staging row (floats)
+
+__global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(const __grid_constant__ MlpTcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-B alignment for the swizzled tiles
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int kb = p.kblocks;
-    uint8_t* A_hi = smem;
-    uint8_t* A_lo = A_hi + kb * KB_BYTES_A;
-    uint8_t* B_hi = A_lo + kb * KB_BYTES_A;
-    uint8_t* B_lo = B_hi + kb * KB_BYTES_B;
-    uint64_t* bars = (uint64_t*)(B_lo + kb * KB_BYTES_B);  // [0] load, [1] mma
-    uint32_t* tmem_slot = (uint32_t*)(bars + 2);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t m0 = (int64_t)blockIdx.y * TM;
+    const uint32_t a_bytes = (uint32_t)kb * KB_BYTES_A;  // one term (hi or lo)
+    const uint32_t b_bytes = (uint32_t)kb * KB_BYTES_B;
+    uint8_t* Bt = smem;                       // [hi | lo]
+    uint8_t* At = Bt + 2 * b_bytes;           // [stage][hi | lo]
+    float* stage_ep = (float*)(At + 4 * a_bytes);  // 4 epilogue warps x 32 x 33
+    uint64_t* bars = (uint64_t*)(stage_ep + 4 * 32 * EP_STRIDE);
+    uint64_t* bfull = bars + 0;
+    uint64_t* bempty = bars + 1;
+    uint64_t* afull = bars + 2;   // [2]
+    uint64_t* aempty = bars + 4;  // [2]
+    uint64_t* tfull = bars + 6;   // [2]
+    uint64_t* tempty = bars + 8;  // [2]
+    uint32_t* tmem_slot = (uint32_t*)(bars + 10);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    // ---- layer 1 (K = 9) on CUDA cores: row tid of this tile
-    {
-        const int64_t row = m0 + tid;
-        float x[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) x[k] = row < p.B ? (float)p.R[row * 9 + k] : 0.0f;
-        for (int j = 0; j < kb * 32; ++j) {
-            float h = 0.0f;
-            if (row < p.B && j < p.H) {
-                float acc = __fmul_rn(x[0], __ldg(p.w1 + j));
-#pragma unroll
-                for (int k = 1; k < 9; ++k) acc = __fmaf_rn(x[k], __ldg(p.w1 + k * p.H + j), acc);
-                acc = __fadd_rn(acc, __ldg(p.b1 + j));
-                h = acc > 0.0f ? acc : 0.0f;
-            }
-            const float hh = tf32_rna(h);
-            const float hl = tf32_rna(h - hh);
-            const uint32_t off = (uint32_t)(j >> 5) * KB_BYTES_A + sw128_offset((uint32_t)tid, (uint32_t)(j & 31));
-            *(float*)(A_hi + off) = hh;
-            *(float*)(A_lo + off) = hl;
-        }
-    }
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic stores -> async proxy (MMA)
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TN));
+                     "r"(2 * TN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
-    if (tid == 32) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+    if (threadIdx.x == 32) {
+        mbar_init(bfull, 1);
+        mbar_init(bempty, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(afull + i, 1);
+            mbar_init(aempty + i, 1);
+            mbar_init(tfull + i, 1);
+            mbar_init(tempty + i, 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tile_bytes = (uint32_t)kb * KB_BYTES_B;
-    uint32_t phase = 0;
 
-    for (int64_t nt = blockIdx.x; nt < p.n_tiles; nt += gridDim.x) {
-        if (tid == 0) {
-            mbar_expect_tx(&bars[0], 2 * tile_bytes);
-            bulk_copy(B_hi, p.w2t_hi + nt * (int64_t)kb * TN * 32, tile_bytes, &bars[0]);
-            bulk_copy(B_lo, p.w2t_lo + nt * (int64_t)kb * TN * 32, tile_bytes, &bars[0]);
-            mbar_wait(&bars[0], phase);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint8_t* As[3] = {A_hi, A_hi, A_lo};
-            const uint8_t* Bs[3] = {B_hi, B_lo, B_hi};
-            uint32_t acc = 0;
-#pragma unroll
-            for (int term = 0; term < 3; ++term)
-                for (int b = 0; b < kb; ++b)
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {  // K = 8 tf32 (32 B) per instruction
-                        const uint64_t ad = sdesc(smem_u32(As[term] + b * KB_BYTES_A + kk * 32));
-                        const uint64_t bd = sdesc(smem_u32(Bs[term] + b * KB_BYTES_B + kk * 32));
-                        mma_tf32(tmem, ad, bd, acc);
-                        acc = 1;
-                    }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                             smem_u32(&bars[1]))
-                         : "memory");
-        }
-        __syncwarp();
-        mbar_wait(&bars[1], phase);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        // ---- epilogue: warp w owns TMEM lanes [32w, 32w + 32) = rows of the tile
-        const int64_t row = m0 + warp * 32 + lane;
-        const int64_t n0 = nt * TN;
-        for (int c0 = 0; c0 < TN; c0 += 16) {
-            float v[16];
-            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-            if (row < p.B) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int64_t n = n0 + c0 + i;
-                    if (n < p.N) p.y[row * p.N + n] = v[i] + __ldg(p.b2 + n);
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- producer
+            uint32_t it = 0, nc = 0;
+            for (int64_t nt = blockIdx.x; nt < p.n_tiles; nt += gridDim.x, ++nc) {
+                if (nc > 0) mbar_wait(bempty, (nc - 1) & 1);
+                mbar_expect_tx(bfull, 2 * b_bytes);
+                bulk_copy(Bt, p.w2t_hi + nt * (int64_t)kb * TN * 32, b_bytes, bfull);
+                bulk_copy(Bt + b_bytes, p.w2t_lo + nt * (int64_t)kb * TN * 32, b_bytes, bfull);
+                for (int64_t m = 0; m < p.m_tiles; ++m, ++it) {
+                    const uint32_t s = it & 1, use = it >> 1;
+                    if (it >= 2) mbar_wait(aempty + s, (use - 1) & 1);
+                    uint8_t* dst = At + s * 2 * a_bytes;
+                    mbar_expect_tx(afull + s, 2 * a_bytes);
+                    bulk_copy(dst, p.a_hi + m * (int64_t)kb * TM * 32, a_bytes, afull + s);
+                    bulk_copy(dst + a_bytes, p.a_lo + m * (int64_t)kb * TM * 32, a_bytes, afull + s);
                 }
             }
         }
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        __syncthreads();
-        phase ^= 1;
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            uint32_t it = 0, nc = 0;
+            for (int64_t nt = blockIdx.x; nt < p.n_tiles; nt += gridDim.x, ++nc) {
+                mbar_wait(bfull, nc & 1);
+                for (int64_t m = 0; m < p.m_tiles; ++m, ++it) {
+                    const uint32_t s = it & 1, acc_buf = it & 1;
+                    mbar_wait(afull + s, (it >> 1) & 1);
+                    if (it >= 2) mbar_wait(tempty + acc_buf, ((it >> 1) - 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                    const uint8_t* Ah = At + s * 2 * a_bytes;
+                    const uint8_t* As[3] = {Ah, Ah, Ah + a_bytes};
+                    const uint8_t* Bs[3] = {Bt, Bt + b_bytes, Bt};
+                    const uint32_t d = tmem + acc_buf * TN;
+                    uint32_t accumulate = 0;
+#pragma unroll
+                    for (int term = 0; term < 3; ++term)
+                        for (int b = 0; b < kb; ++b)
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk) {
+                                mma_tf32(d, sdesc(smem_u32(As[term] + b * KB_BYTES_A + kk * 32)),
+                                         sdesc(smem_u32(Bs[term] + b * KB_BYTES_B + kk * 32)), accumulate);
+                                accumulate = 1;
+                            }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                                     smem_u32(aempty + s))
+                                 : "memory");
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                                     smem_u32(tfull + acc_buf))
+                                 : "memory");
+                    if (m == p.m_tiles - 1)
+                        asm volatile(
+                            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                                smem_u32(bempty))
+                            : "memory");
+                }
+            }
+        }
+    } else {  // ---------------- epilogue warps 2..5
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        float* st = stage_ep + (warp - 2) * 32 * EP_STRIDE;
+        uint32_t it = 0;
+        for (int64_t nt = blockIdx.x; nt < p.n_tiles; nt += gridDim.x) {
+            const int64_t n0 = nt * TN;
+            for (int64_t m = 0; m < p.m_tiles; ++m, ++it) {
+                const uint32_t acc_buf = it & 1;
+                mbar_wait(tfull + acc_buf, (it >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                const int64_t row0 = m * TM + q * 32;
+                for (int c0 = 0; c0 < TN; c0 += 32) {
+                    float v[32];
+                    const uint32_t ta = tmem + acc_buf * TN + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+                    tmem_ld16(ta, v);
+                    tmem_ld16(ta + 16, v + 16);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) st[lane * EP_STRIDE + j] = v[j];
+                    __syncwarp();
+                    const int64_t n = n0 + c0 + lane;
+                    const float bias = n < p.N ? __ldg(p.b2 + n) : 0.0f;
+                    for (int r = 0; r < 32; ++r) {  // one coalesced 128-B row segment per store
+                        const int64_t row = row0 + r;
+                        if (row < p.B && n < p.N) p.y[row * p.N + n] = st[r * EP_STRIDE + lane] + bias;
+                    }
+                    __syncwarp();
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tempty + acc_buf))
+                                            : "memory");
+            }
+        }
     }
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TN));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * TN));
 }
 
 struct PackCache {
@@ -263,30 +334,38 @@ int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const
         g_pack.N = n_out;
         g_pack.H = H;
     }
+    const int64_t m_tiles = (B + TM - 1) / TM;
+    const size_t a_bytes = (size_t)m_tiles * kblocks * TM * 32 * sizeof(float);
+    float *a_hi = nullptr, *a_lo = nullptr;
+    LSDF_TRY(check_cuda(cudaMallocAsync((void**)&a_hi, a_bytes, s), "mlp A alloc"));
+    LSDF_TRY(check_cuda(cudaMallocAsync((void**)&a_lo, a_bytes, s), "mlp A alloc"));
+    layer1_pack_kernel<<<grid_for(m_tiles * TM, 128), 128, 0, s>>>(w1, b1, H, kblocks, R, B, m_tiles, a_hi, a_lo);
+    LSDF_TRY(check_launch("layer1_pack_kernel"));
     MlpTcParams p{};
-    p.w1 = w1;
-    p.b1 = b1;
-    p.b2 = b2;
+    p.a_hi = a_hi;
+    p.a_lo = a_lo;
     p.w2t_hi = g_pack.hi;
     p.w2t_lo = g_pack.lo;
-    p.R = R;
+    p.b2 = b2;
     p.y = y;
     p.B = B;
     p.N = n_out;
     p.n_tiles = n_tiles;
-    p.H = H;
+    p.m_tiles = m_tiles;
     p.kblocks = kblocks;
-    const size_t smem = 1024 + (size_t)kblocks * (2 * KB_BYTES_A + 2 * KB_BYTES_B) + 64;
+    const size_t smem = 1024 + (size_t)kblocks * (2 * KB_BYTES_B + 4 * KB_BYTES_A) + 4 * 32 * EP_STRIDE * 4 + 128;
     static bool attr = false;
     if (!attr) {
         LSDF_TRY(check_cuda(cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
                             "mlp smem attribute"));
         attr = true;
     }
-    const int64_t m_tiles = (B + TM - 1) / TM;
-    int64_t gx = (148 + m_tiles - 1) / m_tiles;  // enough CTAs to fill the machine
-    gx = gx < 1 ? 1 : (gx > n_tiles ? n_tiles : gx);
-    dim3 grid((unsigned)gx, (unsigned)m_tiles);
-    mlp_tc_kernel<<<grid, THREADS, smem, s>>>(p);
-    return check_launch("mlp_tc_kernel");
+    if (smem > 227 * 1024) return fail(LSDF_ERR_UNSUPPORTED, "tcgen05 TinyMlp: hidden %d needs too much smem", H);
+    const unsigned grid = (unsigned)(n_tiles < 148 ? n_tiles : 148);
+    mlp_tc_kernel<<<grid, TC_THREADS, smem, s>>>(p);
+    LSDF_TRY(check_launch("mlp_tc_kernel"));
+    cudaFreeAsync(a_hi, s);
+    cudaFreeAsync(a_lo, s);
+    return LSDF_OK;
+
 }

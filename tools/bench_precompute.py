@@ -1,0 +1,158 @@
+"""BASELINE config 3 — per-link precompute at 128^3 and the grid transform at W = 128.
+
+    python tools/bench_precompute.py [--cpu]
+
+(i)   exact link-SDF build at 128^3 (e_r 0.64, r_r 0.01) for the six arm6g
+      primitives and one 1,280-triangle mesh (icosphere, 3 subdivisions);
+(ii)  exact grid transform G = P R + dt_inv (fp64, placement.py:148-169) for
+      B = 3,000 rotations x V_mask = 1,097,911 cells (W = 128, r_e = 0.01);
+(iii) TinyMlp prediction of the same G (approx.py:123-130) on tcgen05 tensor
+      cores (3xTF32) and on CUDA cores.
+Prints one JSON object: device times (CUDA events), achieved bandwidth/flops
+and their roofline fractions, and (with --cpu) the oracle port timed on a
+bounded, extrapolated sample.
+"""
+
+import argparse
+import json
+import statistics
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(REPO))
+
+
+def _time(torch, fn, reps=3, warm=1):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    out = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        out.append(a.elapsed_time(b))
+    return statistics.median(out)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cpu", action="store_true")
+    ap.add_argument("--rotations", type=int, default=3000)
+    ap.add_argument("--chunk", type=int, default=1000, help="rotations per exact-transform launch (fp64 G)")
+    ap.add_argument("--mlp-chunk", type=int, default=3000, help="rotations per MLP launch (f32 y)")
+    args = ap.parse_args()
+    import torch
+
+    import paper_2309_12543_b200 as L
+    from paper_2309_12543_b200 import _native as N
+    from paper_2309_12543_b200 import scenarios as S
+
+    peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    tf32_peak = float(peaks.get("bf16_tflops", 1590.0)) / 2.0  # dense TF32 = bf16 / 2 (B200_PROFILING.md)
+    out = {"config": "config3_precompute"}
+
+    # (i) builds
+    robot = L.RobotModel.from_dict(S.ARM6G)
+    e_r, r_r = 0.64, 0.01
+    builds = {}
+    for i in robot.geometry_links:
+        g = robot.links[i].geometry
+        ms = _time(torch, lambda: L.build_link_sdf(g, e_r, r_r, link_id=i))
+        builds[robot.links[i].name] = ms
+    ico = L.make_icosphere(0.08, subdivisions=3)
+    assert len(ico.triangles) == 1280
+    ms_mesh = _time(torch, lambda: L.build_link_sdf(ico, e_r, r_r), reps=2)
+    cells = 128 ** 3
+    prim_ms = statistics.mean(builds.values())
+    out["build"] = {
+        "primitive_ms_per_link": builds, "cells": cells,
+        "primitive_write_GBps": 4 * cells / (prim_ms / 1e3) / 1e9,
+        "primitive_frac_hbm": 4 * cells / (prim_ms / 1e3) / 1e9 / hbm,
+        "mesh_ms": ms_mesh, "mesh_triangles": 1280,
+        "mesh_pairs_per_s": cells * 1280 / (ms_mesh / 1e3),
+        "mesh_fp64_flop_per_s": 110.0 * cells * 1280 / (ms_mesh / 1e3),
+    }
+
+    # (ii)/(iii) transform at W = 128
+    grid = L.EnvGrid(1.28, 0.01)
+    window = L.WindowGeometry.build(0.64, grid)
+    V = window.n_masked
+    rng = np.random.default_rng(0)
+    B, ch = args.rotations, args.chunk
+    Rall = L.sample_rotations(rng, B)
+    dt = rng.uniform(-0.005, 0.005, size=(B, 3))
+    P = N.to_device(window.masked_points, torch.float64)
+    Rd = torch.from_numpy(Rall.reshape(B, 9)).cuda()
+    dtd = torch.from_numpy(dt).cuda()
+    G = torch.empty((ch, V, 3), dtype=torch.float64, device="cuda")
+
+    def exact_all():
+        for s in range(0, B, ch):
+            N.call("lsdf_grid_transform_exact", N.ptr(Rd[s:s + ch]), N.ptr(dtd[s:s + ch]), ch, N.ptr(P), V, 0.64,
+                   N.ptr(G), N.stream())
+
+    ms_exact = _time(torch, exact_all, reps=2)
+    del G
+    model = L.TinyMlp.initial(V, hidden=32, seed=0)
+    model.w2 = np.random.default_rng(1).normal(0, 0.05, size=model.w2.shape).astype(np.float32)
+    model._dev = None
+    mch = args.mlp_chunk
+    Y = torch.empty((mch, 3 * V), dtype=torch.float32, device="cuda")
+
+    def mlp_all(tc):
+        for s in range(0, B, mch):
+            model.predict_device(Rd[s:s + mch], use_tensor_cores=tc, out=Y)
+
+    ms_tc = _time(torch, lambda: mlp_all(True), reps=2)
+    ms_cc = _time(torch, lambda: mlp_all(False), reps=2)
+    flops = 2.0 * B * (9 * 32 + 32 * 3 * V)
+    out["transform"] = {
+        "rotations": B, "V_mask": V, "W": int(window.dims[0]), "chunk_exact": ch, "chunk_mlp": mch,
+        "exact_fp64_ms": ms_exact, "exact_write_GBps": B * V * 24 / (ms_exact / 1e3) / 1e9,
+        "exact_frac_hbm": B * V * 24 / (ms_exact / 1e3) / 1e9 / hbm,
+        "mlp_tcgen05_ms": ms_tc, "mlp_cuda_core_ms": ms_cc,
+        "mlp_algorithmic_flop": flops,
+        "mlp_tcgen05_TFLOPs": flops / (ms_tc / 1e3) / 1e12,
+        "mlp_tcgen05_frac_tf32_dense": flops / (ms_tc / 1e3) / 1e12 / tf32_peak,
+        "mlp_tcgen05_write_GBps": B * V * 12 / (ms_tc / 1e3) / 1e9,
+        "mlp_tcgen05_frac_hbm_write": B * V * 12 / (ms_tc / 1e3) / 1e9 / hbm,
+        "tf32_dense_peak_TFLOPs": tf32_peak,
+        "note": "the MLP costs 32 MACs per output coordinate vs 3 for the exact product; with both writing G the "
+                "MLP is output-write bound (12 B/point f32) and the exact transform writes 24 B/point (fp64)",
+    }
+    if args.cpu:
+        from oracle import linksdf_oracle as O
+
+        geo = [l for l in S.ARM6G["links"] if l.get("geometry")][0]["geometry"]
+        t0 = time.perf_counter()
+        O.build_grid(geo, e_r, r_r)
+        cpu_prim = time.perf_counter() - t0
+        axes = O.cell_centers(e_r, r_r)
+        sub = np.stack(np.meshgrid(axes[0][::16], axes[1][::16], axes[2][::16], indexing="ij"), -1).reshape(-1, 3)
+        t0 = time.perf_counter()
+        O.mesh_sdf(ico.vertices, ico.triangles, sub, signed=True)
+        cpu_mesh_s = (time.perf_counter() - t0) * cells / len(sub)
+        pts = window.masked_points
+        t0 = time.perf_counter()
+        O.transform_exact(Rall[:2], dt[:2], 0.64, pts)
+        cpu_exact_s = (time.perf_counter() - t0) / 2 * B
+        t0 = time.perf_counter()
+        O.mlp_predict(model.w1, model.b1, model.w2, model.b2, Rall[:2])
+        cpu_mlp_s = (time.perf_counter() - t0) / 2 * B
+        out["cpu_port"] = {"primitive_build_s": cpu_prim, "mesh_build_s_extrapolated": cpu_mesh_s,
+                           "exact_transform_s_extrapolated": cpu_exact_s, "mlp_predict_s_extrapolated": cpu_mlp_s,
+                           "sample": "oracle port (numpy, 1 process); mesh: every 16th cell per axis; transforms: "
+                                     "2 rotations scaled to 3,000"}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
