@@ -1,0 +1,136 @@
+"""Multi-GPU partitioning of the batched query.
+
+One process per GPU (torchrun), ``torch.distributed`` for the plumbing.
+
+* **Waypoint shards** (the throughput sweep, config 4): waypoints are
+  independent ("partitioned by configuration is the contract"),
+  so rank r runs the query on its contiguous slice and nothing crosses the
+  interconnect on the data path; :func:`gather_waypoint_results` collects the
+  (d, link, voxel) slices when a caller wants them in one place.
+* **Obstacle shards** (huge clouds, few waypoints): each rank evaluates every
+  waypoint against its slice of the sorted occupied-voxel list; the per-rank
+  winners are combined with ONE min all-reduce of a packed 64-bit key
+  (orderable f32 distance, global voxel rank, link) — the same lexicographic
+  key the kernel reduces with, so the tie rule (lowest rank, then lowest link)
+  and the clamp rule survive the reduction exactly.  C = 500 keys = 4 KB.
+
+The key helpers are plain numpy so the reduction logic is tested on CPU
+(gloo, world size 2) in tests/test_sharding.py.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+_SIGN = np.uint64(1 << 63)
+_NONE = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) slice of n items for rank (the last rank takes the remainder)."""
+    per = n // world
+    lo = rank * per
+    hi = n if rank == world - 1 else lo + per
+    return lo, hi
+
+
+def orderable(d: np.ndarray) -> np.ndarray:
+    """f32 -> u32 preserving order, -0.0 == +0.0 (lsdf_math.cuh::orderable)."""
+    d = np.asarray(d, dtype=np.float32).copy()
+    d[d == 0] = 0.0
+    b = d.view(np.uint32)
+    return np.where(b & np.uint32(0x80000000), ~b, b | np.uint32(0x80000000)).astype(np.uint32)
+
+
+def from_orderable(k: np.ndarray) -> np.ndarray:
+    k = np.asarray(k, dtype=np.uint32)
+    b = np.where(k & np.uint32(0x80000000), k & np.uint32(0x7FFFFFFF), ~k).astype(np.uint32)
+    return b.view(np.float32)
+
+
+def pack_keys(d, link, voxel, n_links: int, voxel_offset: int = 0) -> np.ndarray:
+    """(d, link, voxel) of one shard -> u64 keys; -1 entries (nothing below the clamp) -> max key."""
+    d = np.asarray(d, dtype=np.float32)
+    link = np.asarray(link, dtype=np.int64)
+    voxel = np.asarray(voxel, dtype=np.int64)
+    lo = (voxel + voxel_offset) * n_links + link
+    keys = (orderable(d).astype(np.uint64) << np.uint64(32)) | lo.astype(np.uint64)
+    return np.where(link < 0, _NONE, keys)
+
+
+def unpack_keys(keys, n_links: int, clamp: float):
+    keys = np.asarray(keys, dtype=np.uint64)
+    none = keys == _NONE
+    hi = (keys >> np.uint64(32)).astype(np.uint32)
+    lo = (keys & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    d = np.where(none, np.float32(clamp), from_orderable(hi)).astype(np.float32)
+    link = np.where(none, -1, lo % n_links).astype(np.int32)
+    voxel = np.where(none, -1, lo // n_links).astype(np.int32)
+    return d, link, voxel
+
+
+def _to_signed(keys: np.ndarray) -> np.ndarray:
+    """u64 order -> i64 order (torch's MIN reduction is signed)."""
+    return (np.asarray(keys, dtype=np.uint64) ^ _SIGN).view(np.int64)
+
+
+def _from_signed(keys: np.ndarray) -> np.ndarray:
+    return np.asarray(keys, dtype=np.int64).view(np.uint64) ^ _SIGN
+
+
+def allreduce_min_keys(keys: np.ndarray, group=None, device=None) -> np.ndarray:
+    """Element-wise min of u64 keys over all ranks (NCCL on GPUs, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(_to_signed(keys).copy())
+    if device is not None:
+        t = t.to(device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return _from_signed(t.cpu().numpy())
+
+
+def query_obstacle_sharded(traj, obstacles, group=None):
+    """(d, link, voxel) over the full obstacle set, each rank evaluating its voxel slice.
+
+    ``obstacles`` is the full (replicated) ObstacleVoxelSet; rank r keeps the
+    occupied voxels of rank [lo, hi) in the sorted list, queries them on its
+    GPU, and the packed keys meet in one MIN all-reduce.
+    """
+    import torch.distributed as dist
+
+    from .query import ObstacleVoxelSet, query_min_distances
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    lo, hi = shard_range(obstacles.n_occupied, rank, world)
+    part = ObstacleVoxelSet(indices=obstacles.indices[lo:hi], grid=obstacles.grid, n_points=obstacles.n_points,
+                            n_dropped=obstacles.n_dropped, _sorted_unique=True)
+    d, link, voxel = query_min_distances(traj, part, return_argmin=True)
+    keys = pack_keys(d, link, voxel, traj.n_links, voxel_offset=lo)
+    dev = None
+    if dist.get_backend(group) == "nccl":
+        import torch
+
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return unpack_keys(allreduce_min_keys(keys, group, dev), traj.n_links, traj.d_far_global)
+
+
+def gather_waypoint_results(d, link, voxel, group=None):
+    """All-gather the per-rank waypoint slices (variable lengths) into full arrays on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    n = torch.tensor([len(d)], dtype=torch.int64)
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    m = int(max(s.item() for s in sizes))
+    packed = np.zeros((m, 3), dtype=np.float64)
+    packed[: len(d), 0] = d
+    packed[: len(d), 1] = link
+    packed[: len(d), 2] = voxel
+    mine = torch.from_numpy(packed)
+    parts = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    rows = np.concatenate([p.numpy()[: int(s.item())] for p, s in zip(parts, sizes)])
+    return rows[:, 0].astype(np.float32), rows[:, 1].astype(np.int32), rows[:, 2].astype(np.int32)

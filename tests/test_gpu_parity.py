@@ -421,3 +421,24 @@ def test_mlp_tensor_cores(L):
     b = big.predict_device(Rb, use_tensor_cores=False).cpu().numpy()
     scale = np.abs(b).max()
     assert np.abs(a - b).max() <= 1e-6 * max(1.0, scale) * 8
+
+
+def test_obstacle_shards_recombine_exactly(L):
+    """Obstacle sharding: per-shard GPU queries + packed-key min == the full query."""
+    from paper_2309_12543_b200 import sharding as Sh
+
+    g = golden("scene_c1")
+    robot, grid, sdfs, window = _scene(L, g)
+    traj = L.TrajectorySdf.from_configs(robot, g["q"], sdfs, grid, window)
+    obs = L.voxelize_pointcloud(g["points"], grid)
+    full = L.query_min_distances(traj, obs, return_argmin=True)
+    for world in (2, 3):
+        keys = []
+        for r in range(world):
+            lo, hi = Sh.shard_range(obs.n_occupied, r, world)
+            part = L.ObstacleVoxelSet(indices=obs.indices[lo:hi], grid=grid, n_points=hi - lo, n_dropped=0)
+            d, link, voxel = L.query_min_distances(traj, part, return_argmin=True)
+            keys.append(Sh.pack_keys(d, link, voxel, traj.n_links, voxel_offset=lo))
+        red = np.minimum.reduce([Sh._to_signed(k) for k in keys])
+        d, link, voxel = Sh.unpack_keys(Sh._from_signed(red), traj.n_links, traj.d_far_global)
+        assert np.array_equal(d, full[0]) and np.array_equal(link, full[1]) and np.array_equal(voxel, full[2])
