@@ -41,6 +41,16 @@ constexpr int FK_THREADS = 128;
 //   3. one thread per (configuration, link): outputs + window alignment.
 __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_constant__ FkParams p, int lp_log2) {
     extern __shared__ double s_fk[];
+    // the chain table in shared memory: lanes of a warp read different links,
+    // which the constant cache would serialize
+    __shared__ lsdf_link s_links[LSDF_MAX_LINKS];
+    {
+        const double* src = (const double*)p.links;
+        double* dst = (double*)s_links;
+        const int n = p.n_links * (int)(sizeof(lsdf_link) / sizeof(double));
+        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
     const int lp = 1 << lp_log2, cpb = FK_THREADS >> lp_log2;
     const int cl = threadIdx.x >> lp_log2, li = threadIdx.x & (lp - 1);
     const int64_t c = (int64_t)blockIdx.x * cpb + cl;
@@ -57,7 +67,7 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
         if (bad) atomicAdd(&p.flags[0], bad);
     }
     if (active) {
-        const lsdf_link& L = p.links[li];
+        const lsdf_link& L = s_links[li];
         if (L.kind == 1) {  // revolute: r_o @ rodrigues(q)   robot.py:331-334
             const double a = q[L.q_col];
             double M[9], rl[9];
@@ -85,7 +95,7 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
         double* wc = world + (size_t)cl * lp * 12;
         const double* lc = s_fk + (size_t)cl * lp * 12;
         for (int k2 = 0; k2 < p.n_links; ++k2) {
-            const lsdf_link& L = p.links[k2];
+            const lsdf_link& L = s_links[k2];
             double rj[9], tj[3];
             if (L.kind == 0) {
 #pragma unroll
@@ -123,7 +133,7 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
     __syncthreads();
     if (!active) return;
     const double* w = world + ((size_t)cl * lp + li) * 12;
-    const lsdf_link& L = p.links[li];
+    const lsdf_link& L = s_links[li];
     if (p.R_all != nullptr) {
         double* dr = p.R_all + (c * p.n_links + li) * 9;
         double* dtt = p.T_all + (c * p.n_links + li) * 3;

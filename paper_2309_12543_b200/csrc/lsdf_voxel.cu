@@ -1,11 +1,10 @@
 // lsdf_voxel.cu — obstacle voxelization (query.py:106-125, grids.py:93-113).
 //
 // voxel_scatter_kernel: one thread per point, fp64 floor((p + e) / r) exactly
-//   as numpy, clipped; warps merge lanes that hit the same bitmap word
-//   (__match_any_sync) so a dense human blob costs one atomicOr per word per
-//   warp.  The last CTA to finish (ticket counter) turns the bitmap into the
-//   exclusive popcount prefix per word: rank(voxel) = prefix[w] +
-//   popc(word & below) is its position in np.unique(axis=0) order.
+//   as numpy, clipped; each CTA merges its points in a shared-memory bitmap
+//   and ORs the touched words into the global one.
+// prefix_only_kernel: the exclusive popcount prefix per word: rank(voxel) =
+//   prefix[w] + popc(word & below) is its position in np.unique(axis=0) order.
 // voxel_compact_kernel: optional, one thread per word, writes the sorted
 //   index list (the ObstacleVoxelSet.indices the API returns) and posgrid.
 #include <cub/block/block_scan.cuh>
@@ -17,6 +16,8 @@ using namespace lsdf;
 namespace {
 
 constexpr int SCAN_THREADS = 1024;
+constexpr int SCATTER_THREADS = 1024;
+constexpr int64_t PRIVATE_WORDS_MAX = 12288;  // 48 KiB of shared bitmap
 
 __device__ void prefix_scan_block(const uint32_t* bitmap, int64_t n_words, int32_t* prefix, int32_t* counters) {
     using Scan = cub::BlockScan<int, SCAN_THREADS>;
@@ -52,50 +53,60 @@ __device__ void prefix_scan_block(const uint32_t* bitmap, int64_t n_words, int32
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(SCAN_THREADS)
-voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, uint32_t* bitmap, int32_t* prefix,
-                     int32_t* counters, int64_t n_words) {
+// floor((p + e) / r) exactly as numpy: correctly rounded quotient via
+// q0 = x * RN(1/r) plus one FMA residual step (Markstein), then floor.
+__device__ __forceinline__ int64_t voxel_coord(double p, double e, double r, double rinv) {
+    const double x = __dadd_rn(p, e);
+    const double q0 = __dmul_rn(x, rinv);
+    const double q = __fma_rn(__fma_rn(-q0, r, x), rinv, q0);
+    return (int64_t)floor(q);
+}
+
+// One thread per point.  With a small grid the CTA first merges its points
+// into a shared-memory copy of the bitmap (fast shared atomics), then ORs the
+// non-empty words into the global bitmap: a dense human blob costs one global
+// atomic per touched word per CTA instead of one per point.
+template <typename T, bool PRIVATE>
+__global__ void __launch_bounds__(SCATTER_THREADS)
+voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, double rx, double ry, double rz,
+                     uint32_t* bitmap, int32_t* counters, int64_t n_words) {
+    extern __shared__ uint32_t s_bits[];
+    if (PRIVATE) {
+        for (int64_t w = threadIdx.x; w < n_words; w += blockDim.x) s_bits[w] = 0u;
+        __syncthreads();
+    }
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool dropped = false;
-    int64_t word = -1;
-    uint32_t bit = 0;
     if (i < N) {
         const double x = (double)pts[3 * i], y = (double)pts[3 * i + 1], z = (double)pts[3 * i + 2];
         const double ex = env.extent[0], ey = env.extent[1], ez = env.extent[2];
         // query.py:112: keep -e <= p < e on every axis (NaN fails the test -> dropped)
         const bool inside = (x >= -ex) && (x < ex) && (y >= -ey) && (y < ey) && (z >= -ez) && (z < ez);
         if (inside) {
-            int64_t ix = (int64_t)floor(DDIV(DADD(x, ex), env.resolution[0]));
-            int64_t iy = (int64_t)floor(DDIV(DADD(y, ey), env.resolution[1]));
-            int64_t iz = (int64_t)floor(DDIV(DADD(z, ez), env.resolution[2]));
+            int64_t ix = voxel_coord(x, ex, env.resolution[0], rx);
+            int64_t iy = voxel_coord(y, ey, env.resolution[1], ry);
+            int64_t iz = voxel_coord(z, ez, env.resolution[2], rz);
             ix = ix < 0 ? 0 : (ix > env.dims[0] - 1 ? env.dims[0] - 1 : ix);  // grids.py:111 clip
             iy = iy < 0 ? 0 : (iy > env.dims[1] - 1 ? env.dims[1] - 1 : iy);
             iz = iz < 0 ? 0 : (iz > env.dims[2] - 1 ? env.dims[2] - 1 : iz);
             const int64_t lin = (ix * env.dims[1] + iy) * env.dims[2] + iz;
-            word = lin >> 5;
-            bit = 1u << (lin & 31);
+            if (PRIVATE)
+                atomicOr(s_bits + (lin >> 5), 1u << (lin & 31));
+            else
+                atomicOr(bitmap + (lin >> 5), 1u << (lin & 31));
         } else {
             dropped = true;
         }
     }
-    // one atomicOr per distinct word per warp
-    const unsigned peers = __match_any_sync(FULL_MASK, word);
-    const uint32_t merged = __reduce_or_sync(peers, bit);
-    const int lane = threadIdx.x & 31;
-    if (word >= 0 && lane == __ffs(peers) - 1) atomicOr(bitmap + word, merged);
     const unsigned b = __ballot_sync(FULL_MASK, dropped);
-    if (lane == 0 && b) atomicAdd(&counters[1], __popc(b));
-    if (prefix == nullptr) return;
-    // last CTA: exclusive popcount prefix over the finished bitmap
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(&counters[2], 1) == (int)gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    if (blockDim.x == SCAN_THREADS) prefix_scan_block(bitmap, n_words, prefix, counters);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(&counters[1], __popc(b));
+    if (PRIVATE) {
+        __syncthreads();
+        for (int64_t w = threadIdx.x; w < n_words; w += blockDim.x) {
+            const uint32_t v = s_bits[w];
+            if (v) atomicOr(bitmap + w, v);
+        }
+    }
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) prefix_only_kernel(const uint32_t* bitmap, int64_t n_words,
@@ -165,19 +176,29 @@ extern "C" int lsdf_voxelize(const void* points_dev, int32_t points_f32, int64_t
     Occupancy o = carve_occupancy(occupancy_dev, *env);
     LSDF_TRY(check_cuda(cudaMemsetAsync(occupancy_dev, 0, 256 + o.n_words * 4, s), "voxelize memset"));
     if (N > 0) {
-        // the scan needs SCAN_THREADS per CTA in the last block
-        const unsigned blocks = grid_for(N, SCAN_THREADS);
-        if (points_f32)
-            voxel_scatter_kernel<float><<<blocks, SCAN_THREADS, 0, s>>>((const float*)points_dev, N, *env, o.bitmap,
-                                                                        o.prefix, o.counters, o.n_words);
-        else
-            voxel_scatter_kernel<double><<<blocks, SCAN_THREADS, 0, s>>>((const double*)points_dev, N, *env,
-                                                                         o.bitmap, o.prefix, o.counters, o.n_words);
+        const unsigned blocks = grid_for(N, SCATTER_THREADS);
+        const double rx = 1.0 / env->resolution[0], ry = 1.0 / env->resolution[1], rz = 1.0 / env->resolution[2];
+        const bool priv = o.n_words <= PRIVATE_WORDS_MAX;
+        const size_t smem = priv ? (size_t)o.n_words * 4 : 0;
+        if (points_f32) {
+            if (priv)
+                voxel_scatter_kernel<float, true><<<blocks, SCATTER_THREADS, smem, s>>>(
+                    (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+            else
+                voxel_scatter_kernel<float, false><<<blocks, SCATTER_THREADS, 0, s>>>(
+                    (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+        } else {
+            if (priv)
+                voxel_scatter_kernel<double, true><<<blocks, SCATTER_THREADS, smem, s>>>(
+                    (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+            else
+                voxel_scatter_kernel<double, false><<<blocks, SCATTER_THREADS, 0, s>>>(
+                    (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+        }
         LSDF_TRY(check_launch("voxel_scatter_kernel"));
-    } else {
-        prefix_only_kernel<<<1, SCAN_THREADS, 0, s>>>(o.bitmap, o.n_words, o.prefix, o.counters);
-        LSDF_TRY(check_launch("prefix_only_kernel"));
     }
+    prefix_only_kernel<<<1, SCAN_THREADS, 0, s>>>(o.bitmap, o.n_words, o.prefix, o.counters);
+    LSDF_TRY(check_launch("prefix_only_kernel"));
     if (indices_dev == nullptr) return LSDF_OK;  // hot path: the query only needs bitmap + prefix
     voxel_compact_kernel<<<grid_for(o.n_words, 256), 256, 0, s>>>(o.bitmap, o.prefix, o.n_words, *env, o.posgrid,
                                                                     indices_dev);

@@ -21,15 +21,17 @@ KEYS = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
 def main(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
-    h, v = r[0], r[2]
-    d = dict(zip(h, v))
-    for k in KEYS:
-        if k in d:
-            print(f"  {k:62s} {d[k]}")
-    stalls = {k: float(d[k].replace(",", "")) for k in h
-              if "issue_stalled" in k and k.endswith("per_issue_active.ratio")}
-    top = sorted(stalls.items(), key=lambda kv: -kv[1])[:8]
-    print("  stalls/issue: " + ", ".join(f"{k.split('stalled_')[1].split('_per')[0]}={x:.2f}" for k, x in top))
+    h = r[0]
+    for v in r[2:]:
+        d = dict(zip(h, v))
+        print(f" [{d.get('Kernel Name', '?')[:70]}]")
+        for k in KEYS:
+            if k in d:
+                print(f"  {k:62s} {d[k]}")
+        stalls = {k: float(d[k].replace(",", "")) for k in h
+                  if "issue_stalled" in k and k.endswith("per_issue_active.ratio") and d.get(k)}
+        top = sorted(stalls.items(), key=lambda kv: -kv[1])[:8]
+        print("  stalls/issue: " + ", ".join(f"{k.split('stalled_')[1].split('_per')[0]}={x:.2f}" for k, x in top))
 
 
 if __name__ == "__main__":
