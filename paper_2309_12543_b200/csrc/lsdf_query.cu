@@ -65,11 +65,12 @@ constexpr int WARPS = 8;
 constexpr int QCAP = 32 * 16 + 32;  // queue entries per warp: <= 16 bits per lane per round
 
 __device__ __forceinline__ void finalize(const QueryParams& p, int64_t c) {
-    const uint64_t k = ~(uint64_t)atomicExch(p.keys + c, 0ull);
-    p.counters[c] = 0;
+    const uint64_t k = ~(uint64_t)p.keys[c];
+    p.keys[c] = 0ull;  // leave the workspace zeroed for the next launch
     if (p.per_link != nullptr) {
         for (int l = 0; l < p.n_geo; ++l) {
-            const uint32_t u = ~atomicExch(p.perlink + c * p.n_geo + l, 0u);
+            const uint32_t u = ~p.perlink[c * p.n_geo + l];
+            p.perlink[c * p.n_geo + l] = 0u;
             const float v = from_orderable(u);
             p.per_link[c * p.n_geo + l] = fminf(p.clamp, fminf(p.dfar[l], v));  // query.py:171-175
         }
@@ -211,12 +212,6 @@ __global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_c
     if (lane == 0) {
         atomicMax(p.keys + c, (unsigned long long)~best);
         if (p.per_link != nullptr) atomicMax(p.perlink + o, ~orderable(wmin));
-        __threadfence();
-        const uint32_t done = atomicAdd(p.counters + c, 1u);
-        if (done == (uint32_t)(p.n_geo * p.split - 1)) {
-            __threadfence();
-            finalize(p, c);
-        }
     }
 }
 
@@ -267,10 +262,8 @@ __global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_c
     float bestv = INFINITY;
     uint32_t bestpos = 0xffffffffu;
     float thresh = p.clamp;  // values >= clamp never change the answer
-    if (share_cfg) {
-        uint64_t k = 0;
-        if (lane == 0) k = ~(uint64_t)atomicMax(p.keys + c, 0ull);
-        k = __shfl_sync(FULL_MASK, k, 0);
+    if (share_cfg) {  // best key any link of this configuration has published so far
+        const uint64_t k = ~(uint64_t)__ldcg(p.keys + c);
         if (k != ~0ull) thresh = fminf(thresh, from_orderable((uint32_t)(k >> 32)));
     }
     int qlen = 0, rounds = 0;
@@ -288,9 +281,7 @@ __global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_c
         }
         thresh = fminf(thresh, from_orderable(__reduce_min_sync(FULL_MASK, orderable(bestv))));
         if (share_cfg && (++rounds & 3) == 0) {
-            uint64_t k = 0;
-            if (lane == 0) k = ~(uint64_t)atomicMax(p.keys + c, 0ull);
-            k = __shfl_sync(FULL_MASK, k, 0);
+            const uint64_t k = ~(uint64_t)__ldcg(p.keys + c);
             if (k != ~0ull) thresh = fminf(thresh, from_orderable((uint32_t)(k >> 32)));
         }
     };
@@ -329,14 +320,12 @@ __global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_c
         const uint32_t wm = __reduce_min_sync(FULL_MASK, orderable(bestv));
         if (lane == 0) atomicMax(p.perlink + o, ~wm);
     }
-    if (lane == 0) {
-        __threadfence();
-        const uint32_t done = atomicAdd(p.counters + c, 1u);
-        if (done == (uint32_t)(p.n_geo * p.split - 1)) {
-            __threadfence();
-            finalize(p, c);
-        }
-    }
+}
+
+// (d, link, voxel) per configuration from the reduced keys; resets the slots.
+__global__ void finalize_kernel(const __grid_constant__ QueryParams p) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < p.C) finalize(p, c);
 }
 
 inline int64_t ws_bytes(int64_t C, int32_t n_geo) {
@@ -376,8 +365,11 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
     p.anchor = anchor_geo_dev;
     p.C = C;
     p.n_geo = n_geo;
-    const int64_t target = 148LL * 64;  // warps for a full machine
-    int64_t split = (target + C * n_geo - 1) / (C * n_geo);
+    const bool shells = !full && window->shell_cells_dev != nullptr && window->shell_radius_dev != nullptr;
+    // the column scan needs enough warps in flight for small batches; the
+    // shell scan stops early, so one warp per (configuration, link) is best
+    const int64_t target = 148LL * 64;
+    int64_t split = shells ? 1 : (target + C * n_geo - 1) / (C * n_geo);
     split = split < 1 ? 1 : (split > 8 ? 8 : split);
     p.split = (int32_t)split;
     p.n_tasks = C * n_geo * split;
@@ -390,7 +382,6 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
     p.shell_cells = window->shell_cells_dev;
     p.shell_radius = window->shell_radius_dev;
     p.n_shell = window->n_masked;
-    const bool shells = !full && window->shell_cells_dev != nullptr && window->shell_radius_dev != nullptr;
     p.P = window->P_dev;
     p.Wmax = window->Wmax;
     p.by_position = by_position;
@@ -460,6 +451,7 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
         }
         LSDF_TRY(check_launch("query_direct_kernel"));
     }
-    return LSDF_OK;
+    finalize_kernel<<<grid_for(C, 128), 128, 0, s>>>(p);
+    return check_launch("finalize_kernel");
 
 }
