@@ -52,7 +52,7 @@ struct QueryParams {
     const uint32_t* bitmap;
     const int32_t* prefix;
     const int32_t* posgrid;
-    uint32_t* counters;          // C: tasks finished per configuration
+    uint32_t* counters;          // [LSDF_MAX_LINKS] shell-scan work counters (zero between launches)
     unsigned long long* keys;    // C: ~best key (atomicMax of the complement, zero = empty)
     uint32_t* perlink;           // C x n_geo: ~orderable(min value)
     float* d_out;
@@ -226,22 +226,20 @@ __global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_c
 // stops.  Occupied cells are compacted with a ballot and evaluated 32 at a
 // time with the exact fp64 recipe, so the results are those of the full scan.
 constexpr int QCAP_SHELL = 64;
+constexpr int SHELL_STAGE_MAX = 4096;   // kept cells staged in shared memory (W <= 20)
+constexpr int BITMAP_STAGE_MAX = 8192;  // occupancy words staged in shared memory (<= 262k voxels)
 
+struct ShellView {
+    const uint32_t* cells;   // shell-ordered kept cells (shared or global)
+    const float* radius;
+    const uint32_t* bits;    // occupancy bitmap (shared or global)
+    const double* P;         // window offsets (shared)
+};
+
+// One warp, one (configuration c, link l, slice sidx) task.
 template <bool BY_POS>
-__global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_constant__ QueryParams p,
-                                                                  int64_t blocks_per_link) {
-    extern __shared__ double s_dyn[];
-    double* sP = s_dyn;
-    uint32_t* s_queue = (uint32_t*)(s_dyn + 3 * p.Wmax);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) sP[i] = p.P[i];
-    __syncthreads();
-    const int l = p.group[blockIdx.x / blocks_per_link];
-    const int64_t t_in_link = (blockIdx.x % blocks_per_link) * WARPS + warp;
-    const int64_t c = t_in_link / p.split;
-    if (c >= p.C) return;
-    const int sidx = (int)(t_in_link % p.split);
-    uint32_t* queue = s_queue + warp * QCAP_SHELL;
+__device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView& sv, uint32_t* queue, int l,
+                                           int64_t c, int sidx, int lane) {
     const float4* __restrict__ cells = p.cells[l];
     const float far = p.dfar[l];
     const int64_t o = c * p.n_geo + l;
@@ -271,7 +269,7 @@ __global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_c
         if (valid) {
             const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
             double pt[3];
-            window_point(sP[mx], sP[Wm + my], sP[2 * Wm + mz], R, dtinv, p.e_r, pt);
+            window_point(sv.P[mx], sv.P[Wm + my], sv.P[2 * Wm + mz], R, dtinv, p.e_r, pt);
             const float v = trilinear_geom(p.geom, cells, far, pt[0], pt[1], pt[2]);
             const int lin = lin0 + (mx * ny + my) * nz + mz;
             const uint32_t pos = BY_POS ? (uint32_t)__ldg(p.posgrid + lin) : (uint32_t)lin;
@@ -287,17 +285,17 @@ __global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_c
     };
 
     for (int k0 = sidx * 32; k0 < p.n_shell; k0 += 32 * p.split) {
-        if (__ldg(p.shell_radius + k0) - slack > thresh) break;  // every later cell is farther
+        if (sv.radius[k0] - slack > thresh) break;  // every later cell is farther
         const int k = k0 + lane;
         bool occ = false;
         uint32_t cell = 0;
         if (k < p.n_shell) {
-            cell = __ldg(p.shell_cells + k);
+            cell = sv.cells[k];
             const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
             const int x = ax + mx, y = ay + my, z = az + mz;
             if (x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz) {
                 const int lin = lin0 + (mx * ny + my) * nz + mz;
-                occ = (__ldg(p.bitmap + (lin >> 5)) >> (lin & 31)) & 1u;
+                occ = (sv.bits[lin >> 5] >> (lin & 31)) & 1u;
             }
         }
         const unsigned ballot = __ballot_sync(FULL_MASK, occ);
@@ -322,9 +320,60 @@ __global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_c
     }
 }
 
+// Persistent over groups of 8 tasks (a group never mixes links).  The window
+// offsets, the shell-ordered cell list and the occupancy bitmap are staged in
+// shared memory once per CTA when they fit, so the per-chunk loads of the
+// scan are shared-memory loads.
+template <bool BY_POS>
+__global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_constant__ QueryParams p,
+                                                                  int n_group, int launch, int grab,
+                                                                  int stage_shell, int stage_bits, int64_t n_words) {
+    extern __shared__ double s_dyn[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* sP = s_dyn;
+    uint32_t* s_queue = (uint32_t*)(sP + 3 * p.Wmax);
+    uint32_t* s_cells = s_queue + WARPS * QCAP_SHELL;
+    float* s_radius = (float*)(s_cells + (stage_shell ? p.n_shell : 0));
+    uint32_t* s_bits = (uint32_t*)(s_radius + (stage_shell ? p.n_shell : 0));
+    for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) sP[i] = p.P[i];
+    if (stage_shell)
+        for (int i = threadIdx.x; i < p.n_shell; i += blockDim.x) {
+            s_cells[i] = __ldg(p.shell_cells + i);
+            s_radius[i] = __ldg(p.shell_radius + i);
+        }
+    if (stage_bits)
+        for (int64_t i = threadIdx.x; i < n_words; i += blockDim.x) s_bits[i] = __ldcg(p.bitmap + i);
+    __syncthreads();
+    ShellView sv;
+    sv.cells = stage_shell ? s_cells : p.shell_cells;
+    sv.radius = stage_shell ? s_radius : p.shell_radius;
+    sv.bits = stage_bits ? s_bits : p.bitmap;
+    sv.P = sP;
+    uint32_t* queue = s_queue + warp * QCAP_SHELL;
+    // dynamic task fetch: task durations vary by orders of magnitude (early
+    // stop), so each warp takes `grab` tasks at a time from a global counter
+    // (reset by finalize_kernel).  Task order is link-major, so consecutive
+    // tasks share the link grid.
+    const uint32_t per_link = (uint32_t)(p.C * p.split);
+    const uint32_t n_tasks = per_link * (uint32_t)n_group;
+    for (;;) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(p.counters + launch, (uint32_t)grab);
+        base = __shfl_sync(FULL_MASK, base, 0);
+        if (base >= n_tasks) break;
+        const uint32_t end = min(base + (uint32_t)grab, n_tasks);
+        for (uint32_t t = base; t < end; ++t) {
+            const int l = p.group[t / per_link];
+            const uint32_t r = t % per_link;
+            shell_task<BY_POS>(p, sv, queue, l, (int64_t)(r / p.split), (int)(r % p.split), lane);
+        }
+    }
+}
+
 // (d, link, voxel) per configuration from the reduced keys; resets the slots.
 __global__ void finalize_kernel(const __grid_constant__ QueryParams p) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < LSDF_MAX_LINKS) p.counters[c] = 0;  // shell-scan work counters
     if (c < p.C) finalize(p, c);
 }
 
@@ -345,6 +394,8 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
     if (window->W[0] > LSDF_MAX_WINDOW || window->W[1] > LSDF_MAX_WINDOW || window->W[2] > LSDF_MAX_WINDOW)
         return fail(LSDF_ERR_UNSUPPORTED, "query: window wider than %d cells", LSDF_MAX_WINDOW);
     const int64_t V = n_vox(*env);
+    if ((double)C * 4 * n_geo >= 4294967295.0)
+        return fail(LSDF_ERR_UNSUPPORTED, "query: %lld configurations overflow the 32-bit task counter", (long long)C);
     if ((double)V * n_geo >= 4294967295.0)
         return fail(LSDF_ERR_UNSUPPORTED, "query: %lld voxels x %d links overflow the 32-bit key", (long long)V, n_geo);
     if (C <= 0) return LSDF_OK;
@@ -369,8 +420,9 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
     // the column scan needs enough warps in flight for small batches; the
     // shell scan stops early, so one warp per (configuration, link) is best
     const int64_t target = 148LL * 64;
-    int64_t split = shells ? 1 : (target + C * n_geo - 1) / (C * n_geo);
-    split = split < 1 ? 1 : (split > 8 ? 8 : split);
+    // shells: about one resident wave (148 SMs x 32 warps) in flight for small batches
+    int64_t split = shells ? (148LL * 32 + C * n_geo - 1) / (C * n_geo) : (target + C * n_geo - 1) / (C * n_geo);
+    split = split < 1 ? 1 : (split > (shells ? 4 : 8) ? (shells ? 4 : 8) : split);
     p.split = (int32_t)split;
     p.n_tasks = C * n_geo * split;
     for (int a = 0; a < 3; ++a) {
@@ -407,6 +459,7 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
     cudaStream_t s = (cudaStream_t)stream;
     // one launch per group of links with identical grid geometry (normally one)
     bool done[LSDF_MAX_LINKS] = {false};
+    int n_launch = 0;
     for (int l0 = 0; l0 < n_geo; ++l0) {
         if (done[l0]) continue;
         const lsdf_link_grid& g0 = grids[l0];
@@ -433,11 +486,44 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
         p.geom.cy = g0.dims[1] - 1;
         const unsigned blocks = (unsigned)(blocks_per_link * n_group);
         if (shells) {
-            const size_t smem_s = (size_t)3 * window->Wmax * sizeof(double) + (size_t)WARPS * QCAP_SHELL * 4;
+            const int stage_shell = p.n_shell <= SHELL_STAGE_MAX;
+            const int stage_bits = o.n_words <= BITMAP_STAGE_MAX;
+            const size_t smem_s = (size_t)3 * window->Wmax * sizeof(double) + (size_t)WARPS * QCAP_SHELL * 4 +
+                                  (stage_shell ? (size_t)p.n_shell * 8 : 0) + (stage_bits ? (size_t)o.n_words * 4 : 0);
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(query_shells_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+                cudaFuncSetAttribute(query_shells_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+                attr = true;
+            }
+            // residency cache: (device, by_position, smem bytes) -> CTAs per SM
+            static int c_dev = -1, c_bp = -1, c_sm = 148, c_per = 1;
+            static size_t c_smem = 0;
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev != c_dev || (int)by_position != c_bp || smem_s != c_smem) {
+                cudaDeviceGetAttribute(&c_sm, cudaDevAttrMultiProcessorCount, dev);
+                if (by_position)
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per, query_shells_kernel<true>, 32 * WARPS, smem_s);
+                else
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per, query_shells_kernel<false>, 32 * WARPS, smem_s);
+                c_dev = dev;
+                c_bp = by_position;
+                c_smem = smem_s;
+            }
+            const int per_sm = c_per, n_sm = c_sm;
+            const int64_t resident = (int64_t)n_sm * (per_sm < 1 ? 1 : per_sm);
+            const unsigned grid = (unsigned)((int64_t)blocks < resident ? (int64_t)blocks : resident);
+            const int64_t n_tasks = C * split * n_group;
+            int64_t grab = n_tasks / (resident * WARPS * 16);
+            grab = grab < 1 ? 1 : (grab > 8 ? 8 : grab);
             if (by_position)
-                query_shells_kernel<true><<<blocks, 32 * WARPS, smem_s, s>>>(p, blocks_per_link);
+                query_shells_kernel<true><<<grid, 32 * WARPS, smem_s, s>>>(p, n_group, n_launch, (int)grab,
+                                                                          stage_shell, stage_bits, o.n_words);
             else
-                query_shells_kernel<false><<<blocks, 32 * WARPS, smem_s, s>>>(p, blocks_per_link);
+                query_shells_kernel<false><<<grid, 32 * WARPS, smem_s, s>>>(p, n_group, n_launch, (int)grab,
+                                                                           stage_shell, stage_bits, o.n_words);
+            ++n_launch;
         } else if (full) {
             if (by_position)
                 query_direct_kernel<true, true><<<blocks, 32 * WARPS, smem, s>>>(p, blocks_per_link);
@@ -451,7 +537,7 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
         }
         LSDF_TRY(check_launch("query_direct_kernel"));
     }
-    finalize_kernel<<<grid_for(C, 128), 128, 0, s>>>(p);
+    finalize_kernel<<<grid_for(C > LSDF_MAX_LINKS ? C : LSDF_MAX_LINKS, 128), 128, 0, s>>>(p);
     return check_launch("finalize_kernel");
 
 }

@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--workload", default="config2", choices=["config1", "config2", "config4"])
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--device-only", action="store_true", help="inputs staged in HBM (the bench's value path)")
     args = ap.parse_args()
     import torch
 
@@ -33,8 +34,16 @@ def main():
                                                                 use_graph=not args.no_graph)
     q = S.random_configs(shape.robot, shape.n_waypoints, seed=11)
     pts = S.cloud_for(shape, 11).astype(np.float32)
-    for _ in range(args.steps):
-        d, link, voxel = chk.query(q, pts)
+    if args.device_only:
+        chk.q_dev.copy_(torch.from_numpy(q).cuda())
+        chk.p_dev.copy_(torch.from_numpy(pts).cuda())
+        for _ in range(args.steps):
+            chk.launch(device_only=True)
+        torch.cuda.synchronize()
+        d, link = chk.d_dev.cpu().numpy(), chk.link_dev.cpu().numpy()
+    else:
+        for _ in range(args.steps):
+            d, link, voxel = chk.query(q, pts)
     torch.cuda.synchronize()
     print("min d", float(d.min()), "links hit", int((link >= 0).sum()))
 
