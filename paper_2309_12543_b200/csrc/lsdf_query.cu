@@ -236,22 +236,64 @@ struct ShellView {
     const double* P;         // window offsets (shared)
 };
 
+// Per-task constants, computed by one lane per task (up to GRAB_MAX tasks at a
+// time) and read back from shared memory by the warp that scans the task.
+constexpr int GRAB_MAX = 8;
+struct __align__(16) ShellSetup {
+    double R[9];
+    double dtinv[3];
+    float slack;     // |dt| (rounded up) + core radius of the link
+    int32_t l;       // geometry link
+    int32_t c;       // configuration
+    int32_t sidx;    // slice of the shell list
+    int32_t ax, ay, az;
+    int32_t pad_;
+};
+
+__device__ __forceinline__ void shell_setup(const QueryParams& p, uint32_t t, ShellSetup& s) {
+    const uint32_t per_link = (uint32_t)(p.C * p.split);
+    const int l = p.group[t / per_link];
+    const uint32_t r = t % per_link;
+    const int64_t c = p.split == 1 ? r : r / p.split;
+    const int64_t o = c * p.n_geo + l;
+    double R[9], dtinv[3], dt[3];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) R[e] = __ldg(p.R + o * 9 + e);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) dt[e] = __ldg(p.dt + o * 3 + e);
+    shift_inverse(R, dt, p.e_r, dtinv);
+    // |dt| rounded up (dt is the residual of T against its voxel centre)
+    const float dtn = (float)(sqrt(dt[0] * dt[0] + dt[1] * dt[1] + dt[2] * dt[2]) * (1.0 + 1e-6) + 1e-12);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) s.R[e] = R[e];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) s.dtinv[e] = dtinv[e];
+    s.slack = dtn + p.core[l];
+    s.l = l;
+    s.c = (int32_t)c;
+    s.sidx = p.split == 1 ? 0 : (int32_t)(r % p.split);
+    s.ax = __ldg(p.anchor + o * 3);
+    s.ay = __ldg(p.anchor + o * 3 + 1);
+    s.az = __ldg(p.anchor + o * 3 + 2);
+}
+
 // One warp, one (configuration c, link l, slice sidx) task.
 template <bool BY_POS>
-__device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView& sv, uint32_t* queue, int l,
-                                           int64_t c, int sidx, int lane) {
+__device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView& sv, uint32_t* queue,
+                                           const ShellSetup& st, int lane) {
+    const int l = st.l;
+    const int64_t c = st.c;
+    const int sidx = st.sidx;
     const float4* __restrict__ cells = p.cells[l];
     const float far = p.dfar[l];
     const int64_t o = c * p.n_geo + l;
     double R[9], dtinv[3];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) R[e] = __ldg(p.R + o * 9 + e);
-    const double* dt = p.dt + o * 3;
-    shift_inverse(R, dt, p.e_r, dtinv);
-    // |dt| rounded up (dt is the residual of T against its voxel centre)
-    const float dtn = (float)(sqrt(dt[0] * dt[0] + dt[1] * dt[1] + dt[2] * dt[2]) * (1.0 + 1e-6) + 1e-12);
-    const float slack = dtn + p.core[l];
-    const int ax = __ldg(p.anchor + o * 3), ay = __ldg(p.anchor + o * 3 + 1), az = __ldg(p.anchor + o * 3 + 2);
+    for (int e = 0; e < 9; ++e) R[e] = st.R[e];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) dtinv[e] = st.dtinv[e];
+    const float slack = st.slack;
+    const int ax = st.ax, ay = st.ay, az = st.az;
     const int Wm = p.Wmax;
     const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
     const int lin0 = (ax * ny + ay) * nz + az;
@@ -325,7 +367,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
 // shared memory once per CTA when they fit, so the per-chunk loads of the
 // scan are shared-memory loads.
 template <bool BY_POS>
-__global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_constant__ QueryParams p,
+__global__ void __launch_bounds__(32 * WARPS, 4) query_shells_kernel(const __grid_constant__ QueryParams p,
                                                                   int n_group, int launch, int grab,
                                                                   int stage_shell, int stage_bits, int64_t n_words) {
     extern __shared__ double s_dyn[];
@@ -335,6 +377,7 @@ __global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_c
     uint32_t* s_cells = s_queue + WARPS * QCAP_SHELL;
     float* s_radius = (float*)(s_cells + (stage_shell ? p.n_shell : 0));
     uint32_t* s_bits = (uint32_t*)(s_radius + (stage_shell ? p.n_shell : 0));
+    __shared__ ShellSetup s_setup[WARPS][GRAB_MAX];
     for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) sP[i] = p.P[i];
     if (stage_shell)
         for (int i = threadIdx.x; i < p.n_shell; i += blockDim.x) {
@@ -354,19 +397,19 @@ __global__ void __launch_bounds__(32 * WARPS) query_shells_kernel(const __grid_c
     // stop), so each warp takes `grab` tasks at a time from a global counter
     // (reset by finalize_kernel).  Task order is link-major, so consecutive
     // tasks share the link grid.
-    const uint32_t per_link = (uint32_t)(p.C * p.split);
-    const uint32_t n_tasks = per_link * (uint32_t)n_group;
+    // The per-task constants of a grab are computed lane-parallel (lane j
+    // for task base + j) into shared memory.
+    const uint32_t n_tasks = (uint32_t)(p.C * p.split) * (uint32_t)n_group;
     for (;;) {
         uint32_t base = 0;
         if (lane == 0) base = atomicAdd(p.counters + launch, (uint32_t)grab);
         base = __shfl_sync(FULL_MASK, base, 0);
         if (base >= n_tasks) break;
-        const uint32_t end = min(base + (uint32_t)grab, n_tasks);
-        for (uint32_t t = base; t < end; ++t) {
-            const int l = p.group[t / per_link];
-            const uint32_t r = t % per_link;
-            shell_task<BY_POS>(p, sv, queue, l, (int64_t)(r / p.split), (int)(r % p.split), lane);
-        }
+        const uint32_t cnt = min((uint32_t)grab, n_tasks - base);
+        if ((uint32_t)lane < cnt) shell_setup(p, base + lane, s_setup[warp][lane]);
+        __syncwarp();
+        for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS>(p, sv, queue, s_setup[warp][j], lane);
+        __syncwarp();
     }
 }
 
@@ -516,7 +559,7 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
             const unsigned grid = (unsigned)((int64_t)blocks < resident ? (int64_t)blocks : resident);
             const int64_t n_tasks = C * split * n_group;
             int64_t grab = n_tasks / (resident * WARPS * 16);
-            grab = grab < 1 ? 1 : (grab > 8 ? 8 : grab);
+            grab = grab < 1 ? 1 : (grab > GRAB_MAX ? GRAB_MAX : grab);
             if (by_position)
                 query_shells_kernel<true><<<grid, 32 * WARPS, smem_s, s>>>(p, n_group, n_launch, (int)grab,
                                                                           stage_shell, stage_bits, o.n_words);
