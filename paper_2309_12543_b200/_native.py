@@ -10,6 +10,7 @@ raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -108,7 +109,8 @@ def load_library(path: Path | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # LINKSDF_B200_LIB: an alternative build of the same library (A/B timing)
+        p = Path(path) if path else Path(os.environ.get("LINKSDF_B200_LIB", LIB_PATH))
         if not p.exists():
             raise ImportError(
                 f"linksdf-b200 CUDA extension not built ({p}); run "
