@@ -346,8 +346,8 @@ class CpuPort:
         self.sample = min(sample, shape.n_waypoints)
         self.q = S.random_configs(shape.robot, self.sample, seed=11)
 
-    def step(self) -> float:
-        """Seconds per waypoint-query for one bounded sample (voxelize charged pro rata)."""
+    def sample_seconds(self) -> float:
+        """Wall seconds of FK + placement + assembly + gather + argmin on the sample."""
         O, shape, gl = self.O, self.shape, self.gl
         t0 = time.perf_counter()
         R, T = O.fk(self.chain, self.q)
@@ -355,49 +355,88 @@ class CpuPort:
                                            R[:, gl], T[:, gl], self.env, shape.link_extent)
         batch = O.assemble(windows, anchors, self.env, shape.link_extent)
         O.argmin_oracle(batch, windows, anchors, self.idx, shape.link_extent)
-        t_sample = time.perf_counter() - t0
-        return t_sample / self.sample + self.t_vox / shape.n_waypoints
+        return time.perf_counter() - t0
 
-    def describe(self, reps):
+    def describe(self, reps, procs):
         shape = self.shape
-        threads = os.environ.get("OPENBLAS_NUM_THREADS") or "default"
-        return (f"{shape.name}: {self.sample} waypoints x {reps} reps through FK + placement + assembly + gather + "
-                f"argmin (oracle port of the reference, numpy, one process) against the full {shape.n_points}-pt "
-                f"cloud voxelized once ({self.t_vox:.2f} s, charged per waypoint over {shape.n_waypoints}); "
-                f"OPENBLAS_NUM_THREADS={threads}")
+        return (f"{shape.name}: {procs} processes x {self.sample} waypoints per step, {reps} steps, through FK + "
+                f"placement + assembly + gather + argmin (oracle port of the reference, numpy, one BLAS thread per "
+                f"process) against the full {shape.n_points}-pt cloud voxelized once ({self.t_vox:.2f} s, charged "
+                f"per waypoint over {shape.n_waypoints})")
+
+
+_PORT = None  # inherited by the forked workers
+
+
+def _port_task(_):
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(1):
+        return _PORT.sample_seconds()
+
+
+class PortPool:
+    """The port on every host core: one forked process per core, each running
+    the bounded sample; a step = all processes once (wall clock)."""
+
+    def __init__(self, workload: str, sample: int = 64):
+        import multiprocessing as mp
+
+        global _PORT
+        _PORT = self.port = CpuPort(workload, sample)
+        self.procs = len(os.sched_getaffinity(0))
+        self.pool = mp.get_context("fork").Pool(self.procs)
+
+    def step(self) -> float:
+        """Seconds per waypoint-query of one parallel step (voxelize charged pro rata)."""
+        t0 = time.perf_counter()
+        self.pool.map(_port_task, range(self.procs), chunksize=1)
+        wall = time.perf_counter() - t0
+        port = self.port
+        return wall / (self.procs * port.sample) + port.t_vox / port.shape.n_waypoints
+
+    def close(self):
+        self.pool.terminate()
 
 
 def cpu_baseline(workload: str, budget_s: float = 15.0, sample: int = 64):
-    port = CpuPort(workload, sample)
-    per_wp, t_start = [], time.perf_counter()
-    while len(per_wp) < 2 or (time.perf_counter() - t_start < budget_s and len(per_wp) < 20):
-        per_wp.append(port.step())
+    pool = PortPool(workload, sample)
+    try:
+        pool.step()  # warm-up (worker start)
+        per_wp, t_start = [], time.perf_counter()
+        while len(per_wp) < 2 or (time.perf_counter() - t_start < budget_s and len(per_wp) < 20):
+            per_wp.append(pool.step())
+    finally:
+        pool.close()
     v = 1.0 / statistics.median(per_wp)
-    return {"value": v, "unit": "waypoint-queries/s", "cores": 1, "kind": "port",
-            "sample": port.describe(len(per_wp)), "host_cores_available": len(os.sched_getaffinity(0))}
+    return {"value": v, "unit": "waypoint-queries/s", "cores": pool.procs, "kind": "port",
+            "sample": pool.port.describe(len(per_wp), pool.procs)}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    port = CpuPort(args.workload, 64)
-    for _ in range(args.warmup):
-        port.step()
-    per_wp = []
-    t_start = time.perf_counter()
-    for _ in range(args.steps):
-        per_wp.append(port.step())
-        if time.perf_counter() - t_start > 240:
-            break
+    pool = PortPool(args.workload, 64)
+    try:
+        for _ in range(max(args.warmup, 1)):
+            pool.step()
+        per_wp = []
+        t_start = time.perf_counter()
+        for _ in range(args.steps):
+            per_wp.append(pool.step())
+            if time.perf_counter() - t_start > 240:
+                break
+    finally:
+        pool.close()
     value = len(per_wp) / sum(per_wp)
-    shape = port.shape
+    shape = pool.port.shape
     return {"metric": METRIC, "value": value, "unit": "waypoint-queries/s", "n_gpus": world,
             "steps": len(per_wp), "warmup": args.warmup, "ms_per_step": 1e3 * shape.n_waypoints / value,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": shape.name, "waypoints": shape.n_waypoints, "points": shape.n_points},
-            "cpu_baseline": {"value": value, "unit": "waypoint-queries/s", "cores": 1, "kind": "port",
-                             "sample": port.describe(len(per_wp))},
+            "cpu_baseline": {"value": value, "unit": "waypoint-queries/s", "cores": pool.procs, "kind": "port",
+                             "sample": pool.port.describe(len(per_wp), pool.procs)},
             "e2e": {"value": value, "unit": "waypoint-queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
