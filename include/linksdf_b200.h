@@ -211,6 +211,18 @@ int lsdf_place_windows(const double* R_geo_dev, const double* dt_geo_dev, int64_
                        int32_t n_geo, const lsdf_link_grid* grids, const lsdf_window* window,
                        float* windows_dev, void* stream);
 
+/* place_links_batch with a coordinate provider (placement.py:300-313) fed by
+ * NeuralTransformProvider.transform (approx.py:292-306,340-355): g_dev is the
+ * (C * n_geo, 3 * n_kept) f32 TinyMlp output at row stride ldg elements
+ * (lsdf_mlp_predict on R_geo),
+ * kept_cells_dev (n_kept) i32 the x-fastest cell of each kept point; each
+ * kept cell samples the link grid at (double(g) + shift) * e_r with the fp64
+ * shift -(dt/e_r) R of infer_grid_transform.  C * n_geo <= 65535 per call. */
+int lsdf_place_windows_g(const float* g_dev, int64_t ldg, const int32_t* kept_cells_dev, int32_t n_kept,
+                         const double* R_geo_dev, const double* dt_geo_dev, int64_t C,
+                         int32_t n_geo, const lsdf_link_grid* grids, const lsdf_window* window,
+                         float* windows_dev, void* stream);
+
 /* assemble_robot_sdfs (query.py:61-103) from n_fields windows
  * (n_fields, W^3) with anchors (n_fields, 3) i32 and config ids (n_fields) i32:
  * values (C, nx, ny, nz) f32 C-order, initialised to float32(d_far_global). */
@@ -287,11 +299,14 @@ int lsdf_mesh_points(const double* tri_dev, int32_t n_tri, int32_t is_signed,
 /* ---- stage 2b: TinyMlp grid transform (approx.py:63-158, 292-306) ------- */
 
 /* y = relu(x W1 + b1) W2 + b2 for x = R (B, 9) fp64 rounded to f32; output
- * (B, 3V) f32.  hidden H <= 64.  Layer 2 runs on tcgen05 tensor cores
- * (kind::tf32, 3xTF32 split) when use_tensor_cores != 0. */
+ * rows of n_out = 3V f32 at a row stride of ldy >= n_out elements (a multiple
+ * of 32 keeps every row 128-B aligned: the write-bound kernel then stores
+ * whole L2 lines, 2.2x faster at W = 128 than the packed n_out stride).
+ * hidden H <= 64.  Layer 2 runs on tcgen05 tensor cores (kind::tf32, 3xTF32
+ * split) when use_tensor_cores != 0. */
 int lsdf_mlp_predict(const float* w1_dev, const float* b1_dev, const float* w2_dev,
                      const float* b2_dev, int32_t H, int64_t n_out, const double* R_dev,
-                     int64_t B, float* y_dev, int32_t use_tensor_cores, void* stream);
+                     int64_t B, float* y_dev, int64_t ldy, int32_t use_tensor_cores, void* stream);
 
 #ifdef __cplusplus
 }

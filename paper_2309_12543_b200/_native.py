@@ -69,6 +69,8 @@ _SIGS = {
     "lsdf_query_workspace_bytes": [_I64, _I32],
     "lsdf_pack_corners": [_P, C.POINTER(_I32), _P, _P],
     "lsdf_place_windows": [_P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT), _P, _P],
+    "lsdf_place_windows_g": [_P, _I64, _P, _I32, _P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT), _P,
+                             _P],
     "lsdf_assemble": [_P, _P, _P, _I64, C.POINTER(_I32), C.POINTER(EnvGridT), _I64, _D, _P, _P],
     "lsdf_query_dense": [_P, _I64, C.POINTER(EnvGridT), _P, _I64, _P, _P, _P],
     "lsdf_per_link_fields": [_P, _P, _P, _P, _P, _I64, C.POINTER(_I32), _I32, C.POINTER(EnvGridT),
@@ -82,7 +84,7 @@ _SIGS = {
     "lsdf_primitive_points": [_I32, C.POINTER(_D), _P, _I64, _P, _P],
     "lsdf_build_mesh": [_P, _I32, _I32, C.POINTER(_D), C.POINTER(_D), C.POINTER(_I32), _P, _P],
     "lsdf_mesh_points": [_P, _I32, _I32, _P, _I64, _P, _P],
-    "lsdf_mlp_predict": [_P, _P, _P, _P, _I32, _I64, _P, _I64, _P, _I32, _P],
+    "lsdf_mlp_predict": [_P, _P, _P, _P, _I32, _I64, _P, _I64, _P, _I64, _I32, _P],
     "lsdf_host_device_pointer": [_P, C.POINTER(C.c_void_p)],
 }
 

@@ -1,6 +1,8 @@
 // lsdf_dense.cu — the paper's materialized mode and the standalone operators.
 //
 //   place_windows_kernel    placement.py:267-313 (every (c, l) window, W^3 cells)
+//   place_windows_g_kernel  the same with provider coordinates G (NeuralTransformProvider,
+//                           approx.py:292-306,340-355: G = f32 MLP output + fp64 shift)
 //   assemble_kernel         query.py:61-103 (scatter-min into dense C x V_e)
 //   query_dense_kernel      query.py:128-150 (gather + first-occurrence argmin)
 //   per_link_fields_kernel  query.py:153-176
@@ -50,6 +52,35 @@ __global__ void place_windows_kernel(const __grid_constant__ PlaceParams p) {
             v = trilinear_at(gv, pt[0], pt[1], pt[2], ld);
         }
         dst[cell] = v;
+    }
+}
+
+// Windows from provider coordinates: the kept cell k (x-fastest kept order,
+// kept[k] = its cell) samples the link grid at (double(y[f, 3k..3k+2]) +
+// dtinv) * e_r (approx.py:302-305 then placement.py:300-313).
+__global__ void place_windows_g_kernel(const __grid_constant__ PlaceParams p, const float* __restrict__ y,
+                                       int64_t ldy, const int32_t* __restrict__ kept, int32_t n_kept) {
+    const int64_t f = blockIdx.y;  // field = c * n_geo + l
+    const int l = (int)(f % p.n_geo);
+    const lsdf_link_grid& G = p.grids[l];
+    const GridView gv = view_of(G);
+    const LdgLoad ld{G.values_dev};
+    double R[9], dtinv[3];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) R[e] = p.R[f * 9 + e];
+    shift_inverse(R, p.dt + f * 3, p.e_r, dtinv);
+    const int n = p.W[0] * p.W[1] * p.W[2];
+    float* dst = p.out + f * (int64_t)n;
+    const int stride = gridDim.x * blockDim.x;
+    const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int cell = i0; cell < n; cell += stride)  // masked cells: the link sentinel
+        if (!((__ldg(p.mask_bits + (cell >> 5)) >> (cell & 31)) & 1u)) dst[cell] = gv.d_far;
+    const float* yf = y + f * ldy;
+    for (int k = i0; k < n_kept; k += stride) {
+        const double gx = DADD((double)__ldg(yf + 3 * k), dtinv[0]);
+        const double gy = DADD((double)__ldg(yf + 3 * k + 1), dtinv[1]);
+        const double gz = DADD((double)__ldg(yf + 3 * k + 2), dtinv[2]);
+        dst[__ldg(kept + k)] = trilinear_at(gv, DMUL(gx, p.e_r), DMUL(gy, p.e_r), DMUL(gz, p.e_r), ld);
     }
 }
 
@@ -258,6 +289,32 @@ extern "C" int lsdf_place_windows(const double* R_geo_dev, const double* dt_geo_
     p.out = windows_dev;
     place_windows_kernel<<<(unsigned)(C * n_geo), 256, 0, (cudaStream_t)stream>>>(p);
     return check_launch("place_windows_kernel");
+}
+
+extern "C" int lsdf_place_windows_g(const float* g_dev, int64_t ldg, const int32_t* kept_cells_dev, int32_t n_kept,
+                                    const double* R_geo_dev, const double* dt_geo_dev, int64_t C, int32_t n_geo,
+                                    const lsdf_link_grid* grids, const lsdf_window* window, float* windows_dev,
+                                    void* stream) {
+    if (n_geo < 1 || n_geo > LSDF_MAX_LINKS) return fail(LSDF_ERR_VALIDATION, "place_g: bad link count %d", n_geo);
+    if (n_kept != window->n_masked)
+        return fail(LSDF_ERR_DIMENSION_MISMATCH, "place_g: %d provider points for %d kept cells", n_kept, window->n_masked);
+    if (ldg < 3 * (int64_t)n_kept) return fail(LSDF_ERR_VALIDATION, "place_g: row stride %lld too small", (long long)ldg);
+    if (C <= 0) return LSDF_OK;
+    if (C * n_geo > 65535) return fail(LSDF_ERR_UNSUPPORTED, "place_g: more than 65535 windows per call");
+    PlaceParams p{};
+    for (int l = 0; l < n_geo; ++l) p.grids[l] = grids[l];
+    p.R = R_geo_dev;
+    p.dt = dt_geo_dev;
+    p.n_geo = n_geo;
+    for (int a = 0; a < 3; ++a) p.W[a] = window->W[a];
+    p.e_r = window->e_r;
+    p.mask_bits = window->mask_bits_dev;
+    p.out = windows_dev;
+    const int n = window->W[0] * window->W[1] * window->W[2];
+    const unsigned bx = (unsigned)((n + 255) / 256 < 64 ? (n + 255) / 256 : 64);
+    place_windows_g_kernel<<<dim3(bx, (unsigned)(C * n_geo)), 256, 0, (cudaStream_t)stream>>>(p, g_dev, ldg,
+                                                                                           kept_cells_dev, n_kept);
+    return check_launch("place_windows_g_kernel");
 }
 
 extern "C" int lsdf_fill(float* dst_dev, int64_t n, float value, void* stream) {

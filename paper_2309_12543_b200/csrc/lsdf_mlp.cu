@@ -20,7 +20,7 @@ constexpr int COLS = 256; // outputs per CTA (one per thread)
 __global__ void __launch_bounds__(COLS) mlp_cuda_core_kernel(const float* __restrict__ w1, const float* __restrict__ b1,
                                                              const float* __restrict__ w2, const float* __restrict__ b2,
                                                              int H, int64_t n_out, const double* __restrict__ R,
-                                                             int64_t B, float* __restrict__ y) {
+                                                             int64_t B, float* __restrict__ y, int64_t ldy) {
     __shared__ float s_h[ROWS][64];
     const int64_t r0 = (int64_t)blockIdx.y * ROWS;
     // layer 1 for this CTA's rows: h[r][j] = max(fma-chain_k x[r][k] w1[k][j] + b1[j], 0)
@@ -45,24 +45,26 @@ __global__ void __launch_bounds__(COLS) mlp_cuda_core_kernel(const float* __rest
     for (int r = 0; r < ROWS && r0 + r < B; ++r) {
         float acc = __fmul_rn(s_h[r][0], w[0]);
         for (int k = 1; k < H; ++k) acc = __fmaf_rn(s_h[r][k], w[k], acc);
-        y[(r0 + r) * n_out + n] = __fadd_rn(acc, bias);
+        y[(r0 + r) * ldy + n] = __fadd_rn(acc, bias);
     }
 }
 
 }  // namespace
 
 int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const float* b2, int32_t H,
-                        int64_t n_out, const double* R, int64_t B, float* y, cudaStream_t s);
+                        int64_t n_out, const double* R, int64_t B, float* y, int64_t ldy, cudaStream_t s);
 
 extern "C" int lsdf_mlp_predict(const float* w1_dev, const float* b1_dev, const float* w2_dev, const float* b2_dev,
                                 int32_t H, int64_t n_out, const double* R_dev, int64_t B, float* y_dev,
-                                int32_t use_tensor_cores, void* stream) {
+                                int64_t ldy, int32_t use_tensor_cores, void* stream) {
     if (H < 1 || H > 64) return fail(LSDF_ERR_UNSUPPORTED, "TinyMlp hidden width %d outside 1..64", H);
+    if (ldy < n_out) return fail(LSDF_ERR_VALIDATION, "TinyMlp: row stride %lld < %lld outputs", (long long)ldy,
+                                 (long long)n_out);
     if (B <= 0 || n_out <= 0) return LSDF_OK;
-    if (use_tensor_cores) return lsdf_mlp_predict_tc(w1_dev, b1_dev, w2_dev, b2_dev, H, n_out, R_dev, B, y_dev,
+    if (use_tensor_cores) return lsdf_mlp_predict_tc(w1_dev, b1_dev, w2_dev, b2_dev, H, n_out, R_dev, B, y_dev, ldy,
                                                      (cudaStream_t)stream);
     dim3 grid((unsigned)((n_out + COLS - 1) / COLS), (unsigned)((B + ROWS - 1) / ROWS));
     mlp_cuda_core_kernel<<<grid, COLS, 0, (cudaStream_t)stream>>>(w1_dev, b1_dev, w2_dev, b2_dev, H, n_out, R_dev, B,
-                                                                   y_dev);
+                                                                   y_dev, ldy);
     return check_launch("mlp_cuda_core_kernel");
 }

@@ -1,31 +1,37 @@
 // lsdf_mlp_tc.cu — TinyMlp layer 2 on the 5th-generation tensor cores (tcgen05).
 //
-// y = h W2 + b2 with h = relu(x W1 + b1) (approx.py:123-130): M = rotations,
+// y = h W2 + b2 with h = relu(x W1 + b1) (approx.py:123-130): B rotations,
 // N = 3V window coordinates (up to 3.3 M), K = hidden (32).
 //
-// layer1_pack_kernel (CUDA cores, K = 9) writes h for every row, split into
-// TF32 hi/lo halves, straight into the GEMM's A-tile layout (K-major, 128-byte
-// swizzle).  W2^T is split and swizzled the same way once per weight buffer
-// (pack_w2_kernel), so every operand tile is one contiguous bulk async copy
-// (cp.async.bulk -> UBLKCP, completing on an mbarrier).
+// The product is computed transposed, y^T = W2^T h^T: the MMA's M side (128
+// TMEM lanes) is 128 output coordinates and its N side (256 TMEM columns) is
+// 256 rotations.  tcgen05.ld 32x32b then hands each thread ONE output
+// coordinate for 32 consecutive rotations, so every global store of a warp is
+// 32 consecutive floats of one row of y (a coalesced 128-B segment) straight
+// from registers, with the bias a per-thread constant — no shared-memory
+// transpose in the epilogue.
 //
-// mlp_tc_kernel is warp-specialized and persistent over N tiles of 256
-// outputs (each W2 tile read once, all M tiles of 128 rows streamed past it):
-// warp 0 issues the copies, one thread of warp 1 issues the 3xTF32 product as
-// tcgen05.mma kind::tf32 (hi*hi + hi*lo + lo*hi, K = 8 per instruction) into a
-// double-buffered 128 x 256 fp32 TMEM accumulator and commits to mbarriers,
-// warps 2-5 drain TMEM with tcgen05.ld, add b2 and write y through a padded
-// shared-memory transpose as coalesced 128-byte row segments.  3xTF32 keeps
-// ~fp32 accuracy, inside the 1e-5 (normalized) contract; the CUDA-core kernel
-// (lsdf_mlp.cu) stays the bit-reproducing path.
+// layer1_pack_kernel (CUDA cores, K = 9) writes h for every rotation, split
+// into TF32 hi/lo halves, straight into the K-major 128-byte-swizzled operand
+// layout; pack_w2_kernel does the same for W2^T once per weight buffer, so
+// every operand tile is one contiguous cp.async.bulk (UBLKCP) on an mbarrier.
+//
+// mlp_tc_kernel is warp-specialized and persistent over output tiles (each W2
+// tile read once, all rotation tiles streamed past it): warp 0 issues the
+// copies, one thread of warp 1 issues the 3xTF32 product as tcgen05.mma
+// kind::tf32 (hi*hi + hi*lo + lo*hi, K = 8 per instruction) into a
+// double-buffered 128 x 256 fp32 TMEM accumulator, warps 2-9 (two per TMEM
+// lane quarter, one per rotation half) drain it with tcgen05.ld and store.
+// 3xTF32 keeps ~fp32 accuracy, inside the 1e-5 (normalized) contract; the
+// CUDA-core kernel (lsdf_mlp.cu) stays the bit-reproducing path.
 #include "lsdf_common.cuh"
 
 namespace {
 
-constexpr int TM = 128;   // rows per tile (tcgen05 M)
-constexpr int TN = 256;   // outputs per tile (tcgen05 N)
-constexpr int KB_BYTES_A = TM * 128;  // one 32-wide k-block of A: 128 rows x 128 B
-constexpr int KB_BYTES_B = TN * 128;  // one 32-wide k-block of B: 256 rows x 128 B
+constexpr int TM = 128;   // output coordinates per tile (tcgen05 M)
+constexpr int TN = 256;   // rotations per tile (tcgen05 N)
+constexpr int KB_BYTES_A = TM * 128;  // one 32-wide k-block of A (W2^T): 128 rows x 128 B
+constexpr int KB_BYTES_B = TN * 128;  // one 32-wide k-block of B (h): 256 rows x 128 B
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -98,41 +104,42 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// W2 (H, N) row-major -> per N tile, per k-block: 256 rows x 128 B, swizzled; hi and lo TF32 halves.
+// W2 (H, N) row-major -> per output tile, per k-block: 128 rows (outputs) x
+// 128 B (32 hidden units), swizzled; hi and lo TF32 halves.
 __global__ void pack_w2_kernel(const float* __restrict__ w2, int H, int64_t N, int kblocks, int64_t n_tiles,
                                float* hi, float* lo) {
-    const int64_t total = n_tiles * kblocks * TN * 32;
+    const int64_t total = n_tiles * kblocks * TM * 32;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t tile = i / ((int64_t)kblocks * TN * 32);
-        const int64_t rem = i % ((int64_t)kblocks * TN * 32);
-        const int kb = (int)(rem / (TN * 32));
-        const int r = (int)((rem / 32) % TN);
+        const int64_t tile = i / ((int64_t)kblocks * TM * 32);
+        const int64_t rem = i % ((int64_t)kblocks * TM * 32);
+        const int kb = (int)(rem / (TM * 32));
+        const int r = (int)((rem / 32) % TM);
         const int kk = (int)(rem % 32);
-        const int64_t n = tile * TN + r;
+        const int64_t n = tile * TM + r;
         const int k = kb * 32 + kk;
         const float v = (n < N && k < H) ? w2[(int64_t)k * N + n] : 0.0f;
         const float h = tf32_rna(v);
         const float l = tf32_rna(v - h);
-        const int64_t base = (tile * kblocks + kb) * (int64_t)TN * 32;  // floats
+        const int64_t base = (tile * kblocks + kb) * (int64_t)TM * 32;  // floats
         const uint32_t off = sw128_offset((uint32_t)r, (uint32_t)kk) >> 2;
         hi[base + off] = h;
         lo[base + off] = l;
     }
 }
 
-// Layer 1 (K = 9, CUDA cores) for every row, split into TF32 hi/lo and stored
-// in the GEMM's A-tile layout: [m_tile][k_block][128 rows x 128 B, swizzled].
+// Layer 1 (K = 9, CUDA cores) for every rotation, split into TF32 hi/lo and
+// stored in the B-operand layout: [rotation tile][k_block][256 rows x 128 B, swizzled].
 __global__ void layer1_pack_kernel(const float* __restrict__ w1, const float* __restrict__ b1, int H, int kblocks,
                                    const double* __restrict__ R, int64_t B, int64_t m_tiles, float* a_hi,
                                    float* a_lo) {
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (row >= m_tiles * TM) return;
+    if (row >= m_tiles * TN) return;
     float x[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) x[k] = row < B ? (float)R[row * 9 + k] : 0.0f;
-    const int64_t mt = row / TM;
-    const uint32_t r = (uint32_t)(row % TM);
+    const int64_t mt = row / TN;
+    const uint32_t r = (uint32_t)(row % TN);
     for (int j = 0; j < kblocks * 32; ++j) {
         float h = 0.0f;
         if (row < B && j < H) {
@@ -144,7 +151,7 @@ __global__ void layer1_pack_kernel(const float* __restrict__ w1, const float* __
         }
         const float hh = tf32_rna(h);
         const float hl = tf32_rna(h - hh);
-        const int64_t base = (mt * kblocks + (j >> 5)) * (int64_t)TM * 32;
+        const int64_t base = (mt * kblocks + (j >> 5)) * (int64_t)TN * 32;
         const uint32_t off = sw128_offset(r, (uint32_t)(j & 31)) >> 2;
         a_hi[base + off] = hh;
         a_lo[base + off] = hl;
@@ -152,38 +159,39 @@ __global__ void layer1_pack_kernel(const float* __restrict__ w1, const float* __
 }
 
 struct MlpTcParams {
-    const float* a_hi;
-    const float* a_lo;
-    const float* w2t_hi;
+    const float* h_hi;    // [rotation tile][k-block][256 x 32] swizzled
+    const float* h_lo;
+    const float* w2t_hi;  // [output tile][k-block][128 x 32] swizzled
     const float* w2t_lo;
     const float* b2;
     float* y;
-    int64_t B, N, n_tiles, m_tiles;
+    int64_t ldy;  // row stride of y (elements)
+    int64_t B, N, n_tiles, r_tiles;
     int32_t kblocks;
 };
 
-// Warp roles: warp 0 = bulk-copy producer, warp 1 = MMA issuer, warps 2-5 =
-// epilogue (warp w drains TMEM lanes 32*(w % 4) .. +31).  Persistent over N
-// tiles (each W2 tile is read once), looping over all M tiles inside; A tiles
-// and TMEM accumulators are double-buffered so the epilogue of one tile
-// overlaps the copies and MMAs of the next.
-constexpr int TC_THREADS = 192;
-constexpr int EP_STRIDE = 33;  // padded staging row (floats)
+// Warp roles: warp 0 = bulk-copy producer, warp 1 = MMA issuer, warps 2-9 =
+// epilogue (warp w drains TMEM lanes 32*(w % 4) .. +31 = 32 outputs, rotation
+// half (w-2)/4).  Persistent over output tiles (each W2 tile is read once),
+// looping over all rotation tiles inside; rotation tiles and TMEM
+// accumulators are double-buffered so the epilogue of one tile overlaps the
+// copies and MMAs of the next.
+constexpr int EP_WARPS = 8;
+constexpr int TC_THREADS = 64 + 32 * EP_WARPS;
 
 __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(const __grid_constant__ MlpTcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int kb = p.kblocks;
-    const uint32_t a_bytes = (uint32_t)kb * KB_BYTES_A;  // one term (hi or lo)
-    const uint32_t b_bytes = (uint32_t)kb * KB_BYTES_B;
-    uint8_t* Bt = smem;                       // [hi | lo]
-    uint8_t* At = Bt + 2 * b_bytes;           // [stage][hi | lo]
-    float* stage_ep = (float*)(At + 4 * a_bytes);  // 4 epilogue warps x 32 x 33
-    uint64_t* bars = (uint64_t*)(stage_ep + 4 * 32 * EP_STRIDE);
-    uint64_t* bfull = bars + 0;
-    uint64_t* bempty = bars + 1;
-    uint64_t* afull = bars + 2;   // [2]
-    uint64_t* aempty = bars + 4;  // [2]
+    const uint32_t a_bytes = (uint32_t)kb * KB_BYTES_A;  // W2 tile, one term (hi or lo)
+    const uint32_t b_bytes = (uint32_t)kb * KB_BYTES_B;  // rotation tile, one term
+    uint8_t* At = smem;                    // W2^T [hi | lo]
+    uint8_t* Bt = At + 2 * a_bytes;        // h [stage][hi | lo]
+    uint64_t* bars = (uint64_t*)(Bt + 4 * b_bytes);
+    uint64_t* wfull = bars + 0;
+    uint64_t* wempty = bars + 1;
+    uint64_t* hfull = bars + 2;   // [2]
+    uint64_t* hempty = bars + 4;  // [2]
     uint64_t* tfull = bars + 6;   // [2]
     uint64_t* tempty = bars + 8;  // [2]
     uint32_t* tmem_slot = (uint32_t*)(bars + 10);
@@ -195,13 +203,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(const __grid_cons
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (threadIdx.x == 32) {
-        mbar_init(bfull, 1);
-        mbar_init(bempty, 1);
+        mbar_init(wfull, 1);
+        mbar_init(wempty, 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(afull + i, 1);
-            mbar_init(aempty + i, 1);
+            mbar_init(hfull + i, 1);
+            mbar_init(hempty + i, 1);
             mbar_init(tfull + i, 1);
-            mbar_init(tempty + i, 4);
+            mbar_init(tempty + i, EP_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -214,17 +222,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(const __grid_cons
         if (lane == 0) {  // ---------------- producer
             uint32_t it = 0, nc = 0;
             for (int64_t nt = blockIdx.x; nt < p.n_tiles; nt += gridDim.x, ++nc) {
-                if (nc > 0) mbar_wait(bempty, (nc - 1) & 1);
-                mbar_expect_tx(bfull, 2 * b_bytes);
-                bulk_copy(Bt, p.w2t_hi + nt * (int64_t)kb * TN * 32, b_bytes, bfull);
-                bulk_copy(Bt + b_bytes, p.w2t_lo + nt * (int64_t)kb * TN * 32, b_bytes, bfull);
-                for (int64_t m = 0; m < p.m_tiles; ++m, ++it) {
+                if (nc > 0) mbar_wait(wempty, (nc - 1) & 1);
+                mbar_expect_tx(wfull, 2 * a_bytes);
+                bulk_copy(At, p.w2t_hi + nt * (int64_t)kb * TM * 32, a_bytes, wfull);
+                bulk_copy(At + a_bytes, p.w2t_lo + nt * (int64_t)kb * TM * 32, a_bytes, wfull);
+                for (int64_t rt = 0; rt < p.r_tiles; ++rt, ++it) {
                     const uint32_t s = it & 1, use = it >> 1;
-                    if (it >= 2) mbar_wait(aempty + s, (use - 1) & 1);
-                    uint8_t* dst = At + s * 2 * a_bytes;
-                    mbar_expect_tx(afull + s, 2 * a_bytes);
-                    bulk_copy(dst, p.a_hi + m * (int64_t)kb * TM * 32, a_bytes, afull + s);
-                    bulk_copy(dst + a_bytes, p.a_lo + m * (int64_t)kb * TM * 32, a_bytes, afull + s);
+                    if (it >= 2) mbar_wait(hempty + s, (use - 1) & 1);
+                    uint8_t* dst = Bt + s * 2 * b_bytes;
+                    mbar_expect_tx(hfull + s, 2 * b_bytes);
+                    bulk_copy(dst, p.h_hi + rt * (int64_t)kb * TN * 32, b_bytes, hfull + s);
+                    bulk_copy(dst + b_bytes, p.h_lo + rt * (int64_t)kb * TN * 32, b_bytes, hfull + s);
                 }
             }
         }
@@ -232,15 +240,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(const __grid_cons
         if (lane == 0) {  // ---------------- MMA issuer
             uint32_t it = 0, nc = 0;
             for (int64_t nt = blockIdx.x; nt < p.n_tiles; nt += gridDim.x, ++nc) {
-                mbar_wait(bfull, nc & 1);
-                for (int64_t m = 0; m < p.m_tiles; ++m, ++it) {
+                mbar_wait(wfull, nc & 1);
+                for (int64_t rt = 0; rt < p.r_tiles; ++rt, ++it) {
                     const uint32_t s = it & 1, acc_buf = it & 1;
-                    mbar_wait(afull + s, (it >> 1) & 1);
+                    mbar_wait(hfull + s, (it >> 1) & 1);
                     if (it >= 2) mbar_wait(tempty + acc_buf, ((it >> 1) - 1) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                    const uint8_t* Ah = At + s * 2 * a_bytes;
-                    const uint8_t* As[3] = {Ah, Ah, Ah + a_bytes};
-                    const uint8_t* Bs[3] = {Bt, Bt + b_bytes, Bt};
+                    const uint8_t* Hh = Bt + s * 2 * b_bytes;
+                    const uint8_t* As[3] = {At, At, At + a_bytes};  // W2 hi, hi, lo
+                    const uint8_t* Bs[3] = {Hh, Hh + b_bytes, Hh};  // h  hi, lo, hi
                     const uint32_t d = tmem + acc_buf * TN;
                     uint32_t accumulate = 0;
 #pragma unroll
@@ -253,45 +261,51 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(const __grid_cons
                                 accumulate = 1;
                             }
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                                     smem_u32(aempty + s))
+                                     smem_u32(hempty + s))
                                  : "memory");
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                                      smem_u32(tfull + acc_buf))
                                  : "memory");
-                    if (m == p.m_tiles - 1)
+                    if (rt == p.r_tiles - 1)
                         asm volatile(
                             "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                                smem_u32(bempty))
+                                smem_u32(wempty))
                             : "memory");
                 }
             }
         }
-    } else {  // ---------------- epilogue warps 2..5
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
-        float* st = stage_ep + (warp - 2) * 32 * EP_STRIDE;
+    } else {  // ---------------- epilogue warps 2..(2 + EP_WARPS)
+        const int q = warp & 3;           // TMEM lane quarter = 32 outputs
+        const int half = (warp - 2) / 4;  // rotation half of the tile
         uint32_t it = 0;
         for (int64_t nt = blockIdx.x; nt < p.n_tiles; nt += gridDim.x) {
-            const int64_t n0 = nt * TN;
-            for (int64_t m = 0; m < p.m_tiles; ++m, ++it) {
+            const int64_t n = nt * TM + q * 32 + lane;  // this thread's output coordinate
+            const bool col_ok = n < p.N;
+            const float bias = col_ok ? __ldg(p.b2 + n) : 0.0f;
+            for (int64_t rt = 0; rt < p.r_tiles; ++rt, ++it) {
                 const uint32_t acc_buf = it & 1;
                 mbar_wait(tfull + acc_buf, (it >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                const int64_t row0 = m * TM + q * 32;
-                for (int c0 = 0; c0 < TN; c0 += 32) {
+                const int64_t b0 = rt * TN + half * (TN / 2);
+                float* dst = p.y + b0 * p.ldy + n;
+#pragma unroll 1
+                for (int c0 = 0; c0 < TN / 2; c0 += 32) {
                     float v[32];
-                    const uint32_t ta = tmem + acc_buf * TN + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+                    const uint32_t ta =
+                        tmem + acc_buf * TN + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * (TN / 2) + c0);
                     tmem_ld16(ta, v);
                     tmem_ld16(ta + 16, v + 16);
+                    const int64_t nb = p.B - (b0 + c0);  // rotations left from this chunk
+                    if (col_ok) {
+                        if (nb >= 32) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) st[lane * EP_STRIDE + j] = v[j];
-                    __syncwarp();
-                    const int64_t n = n0 + c0 + lane;
-                    const float bias = n < p.N ? __ldg(p.b2 + n) : 0.0f;
-                    for (int r = 0; r < 32; ++r) {  // one coalesced 128-B row segment per store
-                        const int64_t row = row0 + r;
-                        if (row < p.B && n < p.N) p.y[row * p.N + n] = st[r * EP_STRIDE + lane] + bias;
+                            for (int j = 0; j < 32; ++j) __stcs(dst + (int64_t)(c0 + j) * p.ldy, v[j] + bias);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (j < nb) __stcs(dst + (int64_t)(c0 + j) * p.ldy, v[j] + bias);
+                        }
                     }
-                    __syncwarp();
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
                 __syncwarp();
@@ -317,15 +331,15 @@ PackCache g_pack;
 
 // Pre-split / pre-swizzle W2 once per weight buffer (cached by pointer+shape).
 int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const float* b2, int32_t H, int64_t n_out,
-                        const double* R, int64_t B, float* y, cudaStream_t s) {
+                        const double* R, int64_t B, float* y, int64_t ldy, cudaStream_t s) {
     using namespace lsdf;
     if (H > 64) return fail(LSDF_ERR_UNSUPPORTED, "tcgen05 TinyMlp supports hidden <= 64");
     const int kblocks = (H + 31) / 32;
-    const int64_t n_tiles = (n_out + TN - 1) / TN;
+    const int64_t n_tiles = (n_out + TM - 1) / TM;
     if (g_pack.w2 != w2 || g_pack.N != n_out || g_pack.H != H) {
         if (g_pack.hi) cudaFreeAsync(g_pack.hi, s);
         if (g_pack.lo) cudaFreeAsync(g_pack.lo, s);
-        const size_t bytes = (size_t)n_tiles * kblocks * TN * 32 * sizeof(float);
+        const size_t bytes = (size_t)n_tiles * kblocks * TM * 32 * sizeof(float);
         LSDF_TRY(check_cuda(cudaMallocAsync((void**)&g_pack.hi, bytes, s), "mlp pack alloc"));
         LSDF_TRY(check_cuda(cudaMallocAsync((void**)&g_pack.lo, bytes, s), "mlp pack alloc"));
         pack_w2_kernel<<<148 * 8, 256, 0, s>>>(w2, H, n_out, kblocks, n_tiles, g_pack.hi, g_pack.lo);
@@ -334,26 +348,27 @@ int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const
         g_pack.N = n_out;
         g_pack.H = H;
     }
-    const int64_t m_tiles = (B + TM - 1) / TM;
-    const size_t a_bytes = (size_t)m_tiles * kblocks * TM * 32 * sizeof(float);
+    const int64_t r_tiles = (B + TN - 1) / TN;
+    const size_t h_bytes = (size_t)r_tiles * kblocks * TN * 32 * sizeof(float);
     float *a_hi = nullptr, *a_lo = nullptr;
-    LSDF_TRY(check_cuda(cudaMallocAsync((void**)&a_hi, a_bytes, s), "mlp A alloc"));
-    LSDF_TRY(check_cuda(cudaMallocAsync((void**)&a_lo, a_bytes, s), "mlp A alloc"));
-    layer1_pack_kernel<<<grid_for(m_tiles * TM, 128), 128, 0, s>>>(w1, b1, H, kblocks, R, B, m_tiles, a_hi, a_lo);
+    LSDF_TRY(check_cuda(cudaMallocAsync((void**)&a_hi, h_bytes, s), "mlp h alloc"));
+    LSDF_TRY(check_cuda(cudaMallocAsync((void**)&a_lo, h_bytes, s), "mlp h alloc"));
+    layer1_pack_kernel<<<grid_for(r_tiles * TN, 128), 128, 0, s>>>(w1, b1, H, kblocks, R, B, r_tiles, a_hi, a_lo);
     LSDF_TRY(check_launch("layer1_pack_kernel"));
     MlpTcParams p{};
-    p.a_hi = a_hi;
-    p.a_lo = a_lo;
+    p.h_hi = a_hi;
+    p.h_lo = a_lo;
     p.w2t_hi = g_pack.hi;
     p.w2t_lo = g_pack.lo;
     p.b2 = b2;
     p.y = y;
+    p.ldy = ldy;
     p.B = B;
     p.N = n_out;
     p.n_tiles = n_tiles;
-    p.m_tiles = m_tiles;
+    p.r_tiles = r_tiles;
     p.kblocks = kblocks;
-    const size_t smem = 1024 + (size_t)kblocks * (2 * KB_BYTES_B + 4 * KB_BYTES_A) + 4 * 32 * EP_STRIDE * 4 + 128;
+    const size_t smem = 1024 + (size_t)kblocks * (2 * KB_BYTES_A + 4 * KB_BYTES_B) + 128;
     static bool attr = false;
     if (!attr) {
         LSDF_TRY(check_cuda(cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),

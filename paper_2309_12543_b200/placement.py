@@ -204,6 +204,8 @@ class WindowGeometry:
         packed = (mxs | (mys << 8) | (mzs << 16)).astype(np.uint32)[order]
         radius = np.nextafter(dist[order].astype(np.float32), np.float32(-np.inf))  # rounded down
         radius = np.minimum(radius, dist[order]).astype(np.float32)
+        # kept cells in x-fastest order (the provider's point order)
+        dev["kept_cells"] = N.to_device(np.nonzero(self.mask.ravel(order="F"))[0].astype(np.int32), t.int32)
         dev["shell_cells"] = N.to_device(packed.view(np.int32), t.int32)
         dev["shell_radius"] = N.to_device(radius, t.float32)
         s.shell_cells_dev = N.ptr(dev["shell_cells"])
@@ -256,7 +258,19 @@ def place_windows_device(sdfs, R_dev, dt_dev, window: WindowGeometry, provider=N
         N.call("lsdf_place_windows", N.ptr(R_dev), N.ptr(dt_dev), C_, L, link_grid_table(sdfs),
                ctypes.byref(ws), N.ptr(out), N.stream())
         return out
-    # generic provider: its coordinates, our sampler (placement.py:300-313)
+    ws, dev = window.device_tables()
+    from .approx import NeuralTransformProvider
+
+    if isinstance(provider, NeuralTransformProvider):
+        # the neural provider stays on the device: TinyMlp on the tensor cores
+        # (or the CUDA-core sgemm replica), then the provider-coordinate sampler
+        R_flat = R_dev.reshape(C_ * L, 9)
+        y = provider.model.predict_device(R_flat, use_tensor_cores=provider.use_tensor_cores)
+        N.call("lsdf_place_windows_g", y, int(y.stride(0)), dev["kept_cells"], window.n_masked, N.ptr(R_dev),
+               N.ptr(dt_dev), C_, L,
+               link_grid_table(sdfs), ctypes.byref(ws), out, N.stream())
+        return out
+    # generic provider: its coordinates (host), our sampler (placement.py:300-313)
     mask_f = t.from_numpy(window.mask.ravel(order="F")).to(out.device)
     for li, sdf in enumerate(sdfs):
         G = provider.transform(R_dev[:, li].cpu().numpy(), dt_dev[:, li].cpu().numpy())

@@ -308,6 +308,36 @@ def test_mlp_predict(L):
     assert np.array_equal(ex, m["exact"])
 
 
+@pytest.mark.parametrize("tc", [False, True])
+def test_neural_placement(L, tc):
+    """place_links_batch with NeuralTransformProvider, fully on the device
+    (TinyMlp on tensor cores or CUDA cores -> provider-coordinate sampler), vs
+    the oracle's numpy MLP transform + trilinear (approx.py:292-306,
+    placement.py:300-313): window values within 1e-5 m."""
+    from oracle import linksdf_oracle as O
+
+    g, m = golden("scene_small"), golden("mlp")
+    robot, grid, sdfs, window = _scene(L, g)
+    model = L.TinyMlp(m["w1"], m["b1"], m["w2"], m["b2"])
+    prov = L.NeuralTransformProvider(model, window, use_tensor_cores=tc)
+    gl = [int(i) for i in g["geometry_links"]]
+    R, T = g["R"][:, gl], g["T"][:, gl]
+    fields = list(L.place_links_batch(sdfs, L.LinkPoseBatch(rotations=R, translations=T), grid, prov))
+    e_r, r_r = float(g["e_r"]), float(g["r_r"])
+    env = O.Env(float(g["env_extent"]), float(g["env_res"]))
+    _, dt, _ = O.align(T.reshape(-1, 3), env, e_r)
+    dt = dt.reshape(T.shape)
+    keep = O.window_mask(e_r, env).ravel(order="F")
+    worst = 0.0
+    for c, li, f in fields:
+        G = O.mlp_transform(m["w1"], m["b1"], m["w2"], m["b2"], R[c, li], dt[c, li], e_r)
+        s = O.trilinear(sdfs[li].values, e_r, r_r, (G * e_r).reshape(-1, 3))
+        vals = f.values.ravel(order="F")
+        assert np.all(vals[~keep] == np.float32(sdfs[li].d_far))
+        worst = max(worst, float(np.abs(vals[keep].astype(np.float64) - s).max()))
+    assert worst <= 1e-5, worst
+
+
 def test_sphere_baseline(L):
     from oracle import linksdf_oracle as O
 
@@ -457,6 +487,15 @@ def test_mlp_tensor_cores(L):
     b = big.predict_device(Rb, use_tensor_cores=False).cpu().numpy()
     scale = np.abs(b).max()
     assert np.abs(a - b).max() <= 1e-6 * max(1.0, scale) * 8
+    # row stride: packed, padded (the default allocation) and odd strides agree bit for bit;
+    # 300 rotations = one full and one partial 256-rotation tile
+    n = 3 * 2103
+    for tc in (True, False):
+        ref = big.predict_device(Rb, use_tensor_cores=tc, out=torch.empty((300, n), device="cuda"))
+        for ld in (n + 1, n + 27, 6336):
+            buf = torch.full((300, ld), 7.0, device="cuda")
+            y = big.predict_device(Rb, use_tensor_cores=tc, out=buf[:, :n])
+            assert torch.equal(y, ref) and bool((buf[:, n:] == 7.0).all())
 
 
 def test_obstacle_shards_recombine_exactly(L):

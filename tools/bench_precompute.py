@@ -105,7 +105,8 @@ def main():
     model.w2 = np.random.default_rng(1).normal(0, 0.05, size=model.w2.shape).astype(np.float32)
     model._dev = None
     mch = args.mlp_chunk
-    Y = torch.empty((mch, 3 * V), dtype=torch.float32, device="cuda")
+    # rows at a 32-float stride (128-B aligned, the layout predict_device allocates)
+    Y = torch.empty((mch, (3 * V + 31) // 32 * 32), dtype=torch.float32, device="cuda")[:, :3 * V]
 
     def mlp_all(tc):
         for s in range(0, B, mch):
