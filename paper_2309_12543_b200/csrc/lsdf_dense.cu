@@ -236,16 +236,25 @@ __global__ void __launch_bounds__(TX_THREADS) transform_exact_kernel(const doubl
     for (int e = 0; e < 9; ++e) Rb[e] = s_R[e];
 #pragma unroll
     for (int k = 0; k < 3; ++k) dti[k] = s_dti[k];
-    const int64_t v0 = (int64_t)blockIdx.x * TX_THREADS * TX_PER_THREAD + threadIdx.x;
+    // each round: TX_THREADS points -> 3 * TX_THREADS contiguous doubles of G,
+    // staged in shared memory so the stores are unit-stride (full sectors)
+    __shared__ double s_out[3 * TX_THREADS];
+    const int64_t blk0 = (int64_t)blockIdx.x * TX_THREADS * TX_PER_THREAD;
     double* out = G + b * V * 3;
-#pragma unroll
     for (int r = 0; r < TX_PER_THREAD; ++r) {
-        const int64_t v = v0 + (int64_t)r * TX_THREADS;
-        if (v >= V) break;
-        const double px = __ldg(P + 3 * v), py = __ldg(P + 3 * v + 1), pz = __ldg(P + 3 * v + 2);
+        const int64_t base = blk0 + (int64_t)r * TX_THREADS;
+        if (base >= V) break;
+        const int64_t v = base + threadIdx.x;
+        if (v < V) {
+            const double px = __ldg(P + 3 * v), py = __ldg(P + 3 * v + 1), pz = __ldg(P + 3 * v + 2);
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
-            out[3 * v + k] = DADD(DFMA(pz, Rb[6 + k], DFMA(py, Rb[3 + k], DMUL(px, Rb[k]))), dti[k]);
+            for (int k = 0; k < 3; ++k)
+                s_out[3 * threadIdx.x + k] = DADD(DFMA(pz, Rb[6 + k], DFMA(py, Rb[3 + k], DMUL(px, Rb[k]))), dti[k]);
+        }
+        __syncthreads();
+        const int64_t n = 3 * ((V - base) < TX_THREADS ? (V - base) : TX_THREADS);
+        for (int i = threadIdx.x; i < n; i += TX_THREADS) __stcs(out + 3 * base + i, s_out[i]);
+        __syncthreads();
     }
 }
 

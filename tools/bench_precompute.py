@@ -62,20 +62,31 @@ def main():
     # (i) builds
     robot = L.RobotModel.from_dict(S.ARM6G)
     e_r, r_r = 0.64, 0.01
-    builds = {}
+    builds, kernel_us = {}, {}
+    from paper_2309_12543_b200.meshes import _primitive_params
+
+    vals = torch.empty((128, 128, 128), dtype=torch.float32, device="cuda")
     for i in robot.geometry_links:
         g = robot.links[i].geometry
         ms = _time(torch, lambda: L.build_link_sdf(g, e_r, r_r, link_id=i))
         builds[robot.links[i].name] = ms
+        kind, prm = _primitive_params(g)
+        # the kernel alone (one launch through the C ABI), 20 back-to-back launches per sample
+        kernel_us[robot.links[i].name] = 1e3 / 20 * _time(torch, lambda: [N.call(
+            "lsdf_build_primitive", kind, prm, N.f64s([e_r] * 3, 3), N.f64s([r_r] * 3, 3), N.i32x3([128] * 3),
+            N.ptr(vals), N.stream()) for _ in range(20)])
     ico = L.make_icosphere(0.08, subdivisions=3)
     assert len(ico.triangles) == 1280
     ms_mesh = _time(torch, lambda: L.build_link_sdf(ico, e_r, r_r), reps=2)
     cells = 128 ** 3
     prim_ms = statistics.mean(builds.values())
+    k_us = statistics.mean(kernel_us.values())
     out["build"] = {
         "primitive_ms_per_link": builds, "cells": cells,
-        "primitive_write_GBps": 4 * cells / (prim_ms / 1e3) / 1e9,
-        "primitive_frac_hbm": 4 * cells / (prim_ms / 1e3) / 1e9 / hbm,
+        "primitive_kernel_us_per_link": kernel_us,
+        "primitive_kernel_write_GBps": 4 * cells / (k_us / 1e6) / 1e9,
+        "primitive_kernel_frac_hbm": 4 * cells / (k_us / 1e6) / 1e9 / hbm,
+        "primitive_api_write_GBps": 4 * cells / (prim_ms / 1e3) / 1e9,
         "mesh_ms": ms_mesh, "mesh_triangles": 1280,
         "mesh_pairs_per_s": cells * 1280 / (ms_mesh / 1e3),
         "mesh_fp64_flop_per_s": 110.0 * cells * 1280 / (ms_mesh / 1e3),
