@@ -213,3 +213,110 @@ class DistanceChecker:
             raise LimitViolationError(list(zip(cs.tolist(), js.tolist())))
         if f[1]:
             raise NoOverlapError(f"{int(f[1])} window(s) miss the grid entirely")
+
+
+class CheckerPipeline:
+    """Throughput form of DistanceChecker: ``depth`` cycles in flight.
+
+    Each slot is a prepared DistanceChecker (its own device buffers and
+    device-input graph) plus page-locked host buffers.  A cycle is three
+    stream-ordered pieces:
+
+        copy stream:    H2D configurations + cloud of slot s (copy engine)
+        compute stream: the slot's graph (fk_align || voxelize -> query)
+        d2h stream:     (d, link, voxel) + FK flags of slot s back to the host
+
+    so the PCIe transfers of cycle i+1 and the read-back of cycle i-1 run on
+    the copy engines while cycle i computes (zero-copy reads, as used by the
+    latency path, would need SMs the persistent query kernel occupies).
+    Producers write the next cycle's inputs straight into ``inputs()`` (pinned
+    numpy views), then ``submit()``; ``result(ticket)`` waits for that cycle.
+    """
+
+    def __init__(self, robot, sdfs, grid, window, n_configs: int, n_points: int, points_dtype=np.float32,
+                 depth: int = 2, **kw):
+        t = N.torch()
+        if depth < 1:
+            raise ValidationError("pipeline depth must be >= 1")
+        self.slots = []
+        for _ in range(depth):
+            chk = DistanceChecker(robot, sdfs, grid, window, **kw).prepare(n_configs, n_points, points_dtype,
+                                                                           zero_copy=False)
+            pin = dict(pin_memory=True)
+            host_out = (t.zeros((n_configs,), dtype=t.float32, **pin), t.zeros((n_configs,), dtype=t.int32, **pin),
+                        t.zeros((n_configs,), dtype=t.int32, **pin), t.zeros((4,), dtype=t.int32, **pin))
+            ev = {k: t.cuda.Event() for k in ("h2d", "compute", "d2h")}
+            self.slots.append({"chk": chk, "out": host_out, "ev": ev, "busy": False, "ticket": -1})
+        self.copy = t.cuda.Stream()
+        self.compute = t.cuda.Stream()
+        self.d2h = t.cuda.Stream()
+        self._next = 0
+        self._done_upto = -1
+
+    @property
+    def depth(self) -> int:
+        return len(self.slots)
+
+    def _slot(self, ticket):
+        return self.slots[ticket % len(self.slots)]
+
+    def inputs(self):
+        """Pinned (configs, points) views of the next cycle's slot (waits if it is still in flight)."""
+        s = self._slot(self._next)
+        if s["busy"]:
+            self.result(s["ticket"])
+        return s["chk"].host_inputs()
+
+    def submit(self, configs=None, points=None) -> int:
+        """Enqueue the next cycle; optional arrays are copied into the slot's pinned inputs first."""
+        t = N.torch()
+        ticket = self._next
+        s = self._slot(ticket)
+        if s["busy"]:
+            self.result(s["ticket"])
+        chk = s["chk"]
+        q_np, p_np = chk.host_inputs()
+        if configs is not None:
+            q_np[...] = np.asarray(configs, dtype=np.float64)
+        if points is not None:
+            p = np.asarray(points).reshape(-1, 3)
+            if len(p) > len(p_np):
+                raise ValidationError(f"{len(p)} points exceed the prepared capacity {len(p_np)}")
+            p_np[: len(p)] = p
+            p_np[len(p):] = np.nan
+        ev = s["ev"]
+        with t.cuda.stream(self.copy):
+            self.copy.wait_event(ev["compute"])  # the slot's device inputs are free again
+            chk.q_dev.copy_(chk.q_host, non_blocking=True)
+            chk.p_dev.copy_(chk.p_host, non_blocking=True)
+            ev["h2d"].record(self.copy)
+        with t.cuda.stream(self.compute):
+            self.compute.wait_event(ev["h2d"])
+            self.compute.wait_event(ev["d2h"])  # the previous results of this slot were read back
+            chk.launch(device_only=True)
+            ev["compute"].record(self.compute)
+        d, link, voxel, flags = s["out"]
+        with t.cuda.stream(self.d2h):
+            self.d2h.wait_event(ev["compute"])
+            d.copy_(chk.d_dev, non_blocking=True)
+            link.copy_(chk.link_dev, non_blocking=True)
+            voxel.copy_(chk.voxel_dev, non_blocking=True)
+            flags.copy_(chk.flags, non_blocking=True)
+            ev["d2h"].record(self.d2h)
+        s["busy"], s["ticket"] = True, ticket
+        self._next += 1
+        return ticket
+
+    def result(self, ticket: int):
+        """(d, link, voxel) numpy copies of a submitted cycle (blocks until it is back on the host)."""
+        s = self._slot(ticket)
+        if s["ticket"] != ticket:
+            raise ValidationError(f"cycle {ticket} is no longer held (pipeline depth {self.depth})")
+        s["ev"]["d2h"].synchronize()
+        d, link, voxel, flags = (a.numpy() for a in s["out"])
+        if s["busy"]:
+            s["busy"] = False
+            if flags[0] or flags[1]:
+                chk = s["chk"]
+                chk._raise_flags(chk.host_inputs()[0], flags)
+        return d.copy(), link.copy(), voxel.copy()

@@ -245,6 +245,33 @@ def test_checker_graph_path(L):
     assert (3, 1) in err.value.violations
 
 
+@pytest.mark.parametrize("depth", [2, 3])
+def test_checker_pipeline(L, depth):
+    """CheckerPipeline (cycles in flight, copy-engine transfers) == one-at-a-time checker, cycle by cycle."""
+    from paper_2309_12543_b200 import scenarios as S
+
+    g = golden("scene_c2")
+    robot, grid, sdfs, window = _scene(L, g)
+    C = len(g["q"])
+    chk = L.DistanceChecker(robot, sdfs, grid, window).prepare(C, 40_000, np.float32)
+    pipe = L.CheckerPipeline(robot, sdfs, grid, window, C, 40_000, np.float32, depth=depth)
+    cycles = [(S.random_configs(_doc(g), C, seed=k), S.human_cloud(30_000 + 1000 * k, seed=k).astype(np.float32))
+              for k in range(7)]
+    want = [chk.query(q, p) for q, p in cycles]
+    tickets = [pipe.submit(q, p) for q, p in cycles[:depth]]
+    got = []
+    for k in range(len(cycles)):
+        got.append(pipe.result(tickets[k]))
+        if k + depth < len(cycles):
+            tickets.append(pipe.submit(*cycles[k + depth]))
+    for (d0, l0, v0), (d1, l1, v1) in zip(want, got):
+        assert np.array_equal(d0, d1) and np.array_equal(l0, l1) and np.array_equal(v0, v1)
+    q_bad = cycles[0][0].copy()
+    q_bad[5, 2] = 9.0
+    with pytest.raises(L.LimitViolationError):
+        pipe.result(pipe.submit(q_bad, cycles[0][1]))
+
+
 def test_known_answer_tie_clamp_empty(L):
     k = golden("known_answer")
     grid = L.EnvGrid(1.0, 0.1)
