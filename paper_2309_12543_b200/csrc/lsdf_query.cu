@@ -367,7 +367,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
 // shared memory once per CTA when they fit, so the per-chunk loads of the
 // scan are shared-memory loads.
 template <bool BY_POS>
-__global__ void __launch_bounds__(32 * WARPS, 4) query_shells_kernel(const __grid_constant__ QueryParams p,
+__global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __grid_constant__ QueryParams p,
                                                                   int n_group, int launch, int grab,
                                                                   int stage_shell, int stage_bits, int64_t n_words) {
     extern __shared__ double s_dyn[];
