@@ -32,6 +32,10 @@ struct FkParams {
 };
 
 constexpr int FK_THREADS = 128;
+constexpr int64_t FK_SERIAL_MIN = 4096;
+#ifndef FK_STAGE_OUTPUTS
+#define FK_STAGE_OUTPUTS 1
+#endif  // configurations from which one thread per configuration wins
 
 // Three phases per CTA of `cpb` configurations x `lp` link slots (lp = next
 // power of two >= n_links):
@@ -157,6 +161,151 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
     }
 }
 
+// Large batches: one thread per configuration walks the whole chain with the
+// same arithmetic as the three phases above (identical results), world poses
+// in a per-thread local array (any parent order).  The joint sin/cos of all
+// links are computed up front (independent, so they overlap), and the
+// geometry-link outputs are staged in shared memory in their global layout
+// and written by the whole CTA as contiguous, coalesced blocks.  The 3-phase
+// kernel keeps small batches latency-short.
+constexpr int FKS_THREADS = 64;
+
+template <bool STAGE>
+__global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __grid_constant__ FkParams p) {
+    // every thread walks the same link at the same time: the chain table is
+    // read straight from the kernel parameters (uniform constant-bank loads)
+    const lsdf_link* s_links = p.links;
+    __shared__ bool s_far_child[LSDF_MAX_LINKS];  // link k is the parent of a link other than k + 1
+    extern __shared__ double s_out[];  // [FKS_THREADS * n_geo * 9] R, [.. * 3] dt, then i32 anchors
+    {
+        if (threadIdx.x < LSDF_MAX_LINKS) {
+            bool f = false;
+            for (int j = 0; j < p.n_links; ++j)
+                f |= p.links[j].kind != 0 && p.links[j].parent == (int)threadIdx.x && j != (int)threadIdx.x + 1;
+            s_far_child[threadIdx.x] = f;
+        }
+    }
+    __syncthreads();
+    const int G = p.n_geo;
+    double* sR = s_out;
+    double* sdt = sR + FKS_THREADS * G * 9;
+    int32_t* sanc = (int32_t*)(sdt + FKS_THREADS * G * 3);
+    const int64_t c0 = (int64_t)blockIdx.x * FKS_THREADS;
+    const int64_t c = c0 + threadIdx.x;
+    const int nc = (int)(p.C - c0 < FKS_THREADS ? p.C - c0 : FKS_THREADS);
+    if (c < p.C) {
+        const double* q = p.q + c * p.D;
+        if (p.limits != nullptr) {  // robot.py:297-302
+            int bad = 0;
+            for (int j = 0; j < p.D; ++j) {
+                const double v = q[j];
+                bad += (v < p.limits[2 * j] || v > p.limits[2 * j + 1]);
+            }
+            if (bad) atomicAdd(&p.flags[0], bad);
+        }
+        // world pose of the previous link in registers (serial chains); poses
+        // a later non-adjacent child needs go to a per-thread local array
+        double prev[12];
+        double world[LSDF_MAX_LINKS][12];
+        for (int k2 = 0; k2 < p.n_links; ++k2) {
+            const lsdf_link& L = s_links[k2];
+            double rl[9], tl[3];  // joint-local transform (phase 1)
+            if (L.kind == 1) {    // revolute: r_o @ rodrigues(q)   robot.py:331-334
+                const double a = q[L.q_col];
+                double M[9];
+                rodrigues(L.skew, L.outer, cos(a), sin(a), M);
+                mm33(L.joint_R, M, rl);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) tl[k] = L.joint_t[k];
+            } else {
+#pragma unroll
+                for (int e = 0; e < 9; ++e) rl[e] = L.joint_R[e];
+                if (L.kind == 2) {  // prismatic: t_o + q * (r_o @ axis)   robot.py:335-337
+                    const double a = q[L.q_col];
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) tl[k] = DADD(L.joint_t[k], DMUL(a, L.R_axis[k]));
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) tl[k] = L.joint_t[k];
+                }
+            }
+            double rj[9], tj[3];  // joint frame in the world (phase 2)
+            if (L.kind == 0) {
+#pragma unroll
+                for (int e = 0; e < 9; ++e) rj[e] = (e == 0 || e == 4 || e == 8) ? 1.0 : 0.0;
+                tj[0] = tj[1] = tj[2] = 0.0;
+            } else {
+                double rp[9], tp[3], tmp[3];
+                if (L.parent == k2 - 1) {
+#pragma unroll
+                    for (int e = 0; e < 9; ++e) rp[e] = prev[e];
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) tp[k] = prev[9 + k];
+                } else {
+                    const double* wp = world[L.parent];
+#pragma unroll
+                    for (int e = 0; e < 9; ++e) rp[e] = wp[e];
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) tp[k] = wp[9 + k];
+                }
+                mm33(rp, rl, rj);        // robot.py:341
+                mv_einsum(rp, tl, tmp);  // robot.py:342
+#pragma unroll
+                for (int k = 0; k < 3; ++k) tj[k] = DADD(tp[k], tmp[k]);
+            }
+            double R[9], T[3], tmp[3];
+            mm33(rj, L.link_R, R);         // robot.py:343
+            mv_einsum(rj, L.link_t, tmp);  // robot.py:344-346
+#pragma unroll
+            for (int k = 0; k < 3; ++k) T[k] = DADD(tj[k], tmp[k]);
+#pragma unroll
+            for (int e = 0; e < 9; ++e) prev[e] = R[e];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) prev[9 + k] = T[k];
+            if (s_far_child[k2]) {
+                double* w = world[k2];
+#pragma unroll
+                for (int e = 0; e < 12; ++e) w[e] = prev[e];
+            }
+            // outputs + window alignment (phase 3)
+            if (p.R_all != nullptr) {
+                double* dr = p.R_all + (c * p.n_links + k2) * 9;
+                double* dtt = p.T_all + (c * p.n_links + k2) * 3;
+#pragma unroll
+                for (int e = 0; e < 9; ++e) dr[e] = R[e];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) dtt[k] = T[k];
+            }
+            if (L.geom_slot >= 0 && (STAGE || p.R_geo != nullptr)) {
+                const int64_t o = STAGE ? (int64_t)threadIdx.x * G + L.geom_slot : c * G + L.geom_slot;
+                double* oR = STAGE ? sR : p.R_geo;
+                double* odt = STAGE ? sdt : p.dt_geo;
+                int32_t* oanc = STAGE ? sanc : p.anchor_geo;
+#pragma unroll
+                for (int e = 0; e < 9; ++e) oR[o * 9 + e] = R[e];
+                int32_t anc[3];
+                double del[3];
+                if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del))
+                    atomicAdd(&p.flags[1], 1);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    odt[o * 3 + k] = del[k];
+                    oanc[o * 3 + k] = anc[k];
+                }
+            }
+        }
+    }
+    if (!STAGE) return;
+    __syncthreads();
+    if (p.R_geo == nullptr) return;
+    // this CTA's configurations are contiguous in every output
+    for (int i = threadIdx.x; i < nc * G * 9; i += FKS_THREADS) p.R_geo[c0 * G * 9 + i] = sR[i];
+    for (int i = threadIdx.x; i < nc * G * 3; i += FKS_THREADS) {
+        p.dt_geo[c0 * G * 3 + i] = sdt[i];
+        p.anchor_geo[c0 * G * 3 + i] = sanc[i];
+    }
+}
+
 __global__ void align_kernel(const double* T, int64_t n, lsdf_env_grid env, int32_t W0, int32_t W1, int32_t W2,
                              int32_t* anchor, double* dt, int32_t* flags) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -207,6 +356,23 @@ extern "C" int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_
     const size_t smem = (size_t)2 * FK_THREADS * 12 * sizeof(double);  // local + world, cpb * lp slots each
     if (flags_dev != nullptr)
         LSDF_TRY(check_cuda(cudaMemsetAsync(flags_dev, 0, 2 * sizeof(int32_t), (cudaStream_t)stream), "fk flags memset"));
+    if (C >= FK_SERIAL_MIN) {
+        if (FK_STAGE_OUTPUTS) {
+            const size_t smem_s = (size_t)FKS_THREADS * n_geo * (12 * sizeof(double) + 3 * sizeof(int32_t));
+            static bool attr = false;
+            if (!attr) {
+                LSDF_TRY(check_cuda(cudaFuncSetAttribute(fk_align_serial_kernel<true>,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024),
+                                    "fk smem attribute"));
+                attr = true;
+            }
+            fk_align_serial_kernel<true>
+                <<<grid_for(C, FKS_THREADS), FKS_THREADS, smem_s, (cudaStream_t)stream>>>(p);
+        } else {
+            fk_align_serial_kernel<false><<<grid_for(C, FKS_THREADS), FKS_THREADS, 0, (cudaStream_t)stream>>>(p);
+        }
+        return check_launch("fk_align_serial_kernel");
+    }
     fk_align_kernel<<<grid_for(C, cpb), FK_THREADS, smem, (cudaStream_t)stream>>>(p, lp_log2);
     return check_launch("fk_align_kernel");
 }
