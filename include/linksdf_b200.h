@@ -92,7 +92,17 @@ typedef struct {
      * >= |p| - rho (computed from the grid values; +inf disables the
      * shell culling of the fused query). */
     float core_radius;
-    float pad_[3];
+    /* Segment bound (link frame, computed from the grid values): with
+     * d(p) = distance from p to the segment seg_a + t seg_u, t in [0, seg_len],
+     * every trilinear sample inside the hull satisfies
+     *     d(p) - seg_kappa_lo <= value(p) <= d(p) + seg_kappa_hi.
+     * The fused query skips the exact lookup of a cell whose lower bound
+     * exceeds the running minimum.  seg_kappa_lo < 0 disables it. */
+    float seg_kappa_lo;
+    float seg_kappa_hi;
+    float seg_len;
+    float seg_a[3];
+    float seg_u[3];
 } lsdf_link_grid;
 
 /* Build the packed-corner layout (dims-1)^3 x 8 f32 from a plain grid. */

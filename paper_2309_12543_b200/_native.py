@@ -40,7 +40,8 @@ class LinkT(C.Structure):
 class LinkGridT(C.Structure):
     _fields_ = [("values_dev", C.c_void_p), ("packed_dev", C.c_void_p), ("dims", C.c_int32 * 3), ("d_far", C.c_float),
                 ("extent", C.c_double * 3), ("resolution", C.c_double * 3), ("core_radius", C.c_float),
-                ("pad_", C.c_float * 3)]
+                ("seg_kappa_lo", C.c_float), ("seg_kappa_hi", C.c_float), ("seg_len", C.c_float),
+                ("seg_a", C.c_float * 3), ("seg_u", C.c_float * 3)]
 
 
 class WindowT(C.Structure):

@@ -30,6 +30,10 @@ struct QueryParams {
     const float4* cells[LSDF_MAX_LINKS];    // packed-corner grid per link
     float dfar[LSDF_MAX_LINKS];             // float32 link sentinel per link
     float core[LSDF_MAX_LINKS];             // value(p) >= |p| - core  (lsdf_link_grid.core_radius)
+    float4 seg_a[LSDF_MAX_LINKS];           // segment bound: (a.xyz, kappa_lo); kappa_lo < 0 disables it
+    float4 seg_u[LSDF_MAX_LINKS];           // (u.xyz, length)
+    float seg_hi[LSDF_MAX_LINKS];           // kappa_hi
+    int32_t seg_filter;                     // apply the segment bound (throughput-sized batches)
     const uint32_t* shell_cells;            // kept window cells sorted by distance from the centre
     const float* shell_radius;              // their distance (m), rounded down
     int32_t n_shell;
@@ -234,14 +238,18 @@ struct ShellView {
     const float* radius;
     const uint32_t* bits;    // occupancy bitmap (shared or global)
     const double* P;         // window offsets (shared)
+    const float* Pf;         // the same in f32 (shared), for the segment bound
 };
 
 // Per-task constants, computed by one lane per task (up to GRAB_MAX tasks at a
 // time) and read back from shared memory by the warp that scans the task.
 constexpr int GRAB_MAX = 8;
+constexpr int64_t SEG_FILTER_MIN_TASKS = 148LL * 32 * 8;  // ~8 tasks per resident warp
 struct __align__(16) ShellSetup {
     double R[9];
     double dtinv[3];
+    float A[9];  // f32 link-frame point of window offset P minus the segment origin:
+    float b[3];  //   p_k - a_k = Px A[k] + Py A[3+k] + Pz A[6+k] + b[k]
     float slack;     // |dt| (rounded up) + core radius of the link
     int32_t l;       // geometry link
     int32_t c;       // configuration
@@ -268,6 +276,12 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, uint32_t t, Sh
     for (int e = 0; e < 9; ++e) s.R[e] = R[e];
 #pragma unroll
     for (int e = 0; e < 3; ++e) s.dtinv[e] = dtinv[e];
+    const float4 sa = p.seg_a[l];
+    const float a3[3] = {sa.x, sa.y, sa.z};
+#pragma unroll
+    for (int e = 0; e < 9; ++e) s.A[e] = (float)(R[e] * p.e_r);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s.b[k] = (float)(dtinv[k] * p.e_r - (double)a3[k]);
     s.slack = dtn + p.core[l];
     s.l = l;
     s.c = (int32_t)c;
@@ -326,6 +340,14 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
         }
     };
 
+    // Segment bound (f32, conservative): d(p) - k_lo <= value(p) <= d(p) + k_hi
+    // with d the distance to the link's axis segment.  An occupied cell whose
+    // lower bound exceeds the threshold can neither undercut nor tie the
+    // minimum and skips the exact lookup; every cell that is queued WILL be
+    // looked up, so its upper bound may lower the threshold at once.
+    const float4 sa = p.seg_a[l], su = p.seg_u[l];
+    const float k_lo = sa.w, k_hi = p.seg_hi[l];
+    const bool use_seg = p.seg_filter && k_lo >= 0.0f;
     for (int k0 = sidx * 32; k0 < p.n_shell; k0 += 32 * p.split) {
         if (sv.radius[k0] - slack > thresh) break;  // every later cell is farther
         const int k = k0 + lane;
@@ -339,6 +361,23 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
                 const int lin = lin0 + (mx * ny + my) * nz + mz;
                 occ = (sv.bits[lin >> 5] >> (lin & 31)) & 1u;
             }
+        }
+        if (use_seg && __any_sync(FULL_MASK, occ)) {
+            float ub = INFINITY;
+            if (occ) {
+                const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
+                const float px = sv.Pf[mx], py = sv.Pf[Wm + my], pz = sv.Pf[2 * Wm + mz];
+                float q[3];
+#pragma unroll
+                for (int e = 0; e < 3; ++e) q[e] = fmaf(pz, st.A[6 + e], fmaf(py, st.A[3 + e], fmaf(px, st.A[e], st.b[e])));
+                const float t = fminf(fmaxf(fmaf(q[2], su.z, fmaf(q[1], su.y, q[0] * su.x)), 0.0f), su.w);
+                const float ex = fmaf(-t, su.x, q[0]), ey = fmaf(-t, su.y, q[1]), ez = fmaf(-t, su.z, q[2]);
+                const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+                const float lim = thresh + k_lo;
+                occ = lim >= 0.0f && d2 <= lim * lim;
+                if (occ) ub = sqrtf(d2) + k_hi;
+            }
+            thresh = fminf(thresh, from_orderable(__reduce_min_sync(FULL_MASK, orderable(ub))));
         }
         const unsigned ballot = __ballot_sync(FULL_MASK, occ);
         if (occ) queue[qlen + __popc(ballot & ((1u << lane) - 1u))] = cell;
@@ -373,12 +412,16 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     extern __shared__ double s_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* sP = s_dyn;
-    uint32_t* s_queue = (uint32_t*)(sP + 3 * p.Wmax);
+    float* sPf = (float*)(sP + 3 * p.Wmax);
+    uint32_t* s_queue = (uint32_t*)(sPf + 3 * p.Wmax + (p.Wmax & 1) * 3);  // keep 8-B alignment
     uint32_t* s_cells = s_queue + WARPS * QCAP_SHELL;
     float* s_radius = (float*)(s_cells + (stage_shell ? p.n_shell : 0));
     uint32_t* s_bits = (uint32_t*)(s_radius + (stage_shell ? p.n_shell : 0));
     __shared__ ShellSetup s_setup[WARPS][GRAB_MAX];
-    for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) sP[i] = p.P[i];
+    for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) {
+        sP[i] = p.P[i];
+        sPf[i] = (float)p.P[i];
+    }
     if (stage_shell)
         for (int i = threadIdx.x; i < p.n_shell; i += blockDim.x) {
             s_cells[i] = __ldg(p.shell_cells + i);
@@ -392,6 +435,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     sv.radius = stage_shell ? s_radius : p.shell_radius;
     sv.bits = stage_bits ? s_bits : p.bitmap;
     sv.P = sP;
+    sv.Pf = sPf;
     uint32_t* queue = s_queue + warp * QCAP_SHELL;
     // dynamic task fetch: task durations vary by orders of magnitude (early
     // stop), so each warp takes `grab` tasks at a time from a global counter
@@ -451,6 +495,9 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
         p.cells[l] = (const float4*)g.packed_dev;
         p.dfar[l] = g.d_far;
         p.core[l] = g.core_radius;
+        p.seg_a[l] = make_float4(g.seg_a[0], g.seg_a[1], g.seg_a[2], g.seg_kappa_lo);
+        p.seg_u[l] = make_float4(g.seg_u[0], g.seg_u[1], g.seg_u[2], g.seg_len);
+        p.seg_hi[l] = g.seg_kappa_hi;
         if (g.d_far < clamp) full = 1;  // masked cells can undercut the clamp
     }
     if (window->zrange_dev == nullptr) full = 1;
@@ -477,6 +524,9 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
     p.shell_cells = window->shell_cells_dev;
     p.shell_radius = window->shell_radius_dev;
     p.n_shell = window->n_masked;
+    // the bound saves lookups but lengthens each warp's dependent chain: a
+    // win when the GPU is full of tasks, a loss on the latency path
+    p.seg_filter = C * n_geo >= SEG_FILTER_MIN_TASKS;
     p.P = window->P_dev;
     p.Wmax = window->Wmax;
     p.by_position = by_position;
@@ -531,7 +581,8 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
         if (shells) {
             const int stage_shell = p.n_shell <= SHELL_STAGE_MAX;
             const int stage_bits = o.n_words <= BITMAP_STAGE_MAX;
-            const size_t smem_s = (size_t)3 * window->Wmax * sizeof(double) + (size_t)WARPS * QCAP_SHELL * 4 +
+            const size_t smem_s = (size_t)3 * window->Wmax * (sizeof(double) + sizeof(float)) + 12 +
+                                  (size_t)WARPS * QCAP_SHELL * 4 +
                                   (stage_shell ? (size_t)p.n_shell * 8 : 0) + (stage_bits ? (size_t)o.n_words * 4 : 0);
             static bool attr = false;
             if (!attr) {

@@ -32,7 +32,7 @@ def test_ctypes_struct_layouts_match_header():
     # sizes implied by include/linksdf_b200.h on LP64
     assert ctypes.sizeof(N.EnvGridT) == 64
     assert ctypes.sizeof(N.LinkT) == 16 + 45 * 8
-    assert ctypes.sizeof(N.LinkGridT) == 8 + 8 + 12 + 4 + 48 + 16
+    assert ctypes.sizeof(N.LinkGridT) == 8 + 8 + 12 + 4 + 48 + 4 + 36
     assert ctypes.sizeof(N.WindowT) == 16 + 8 + 8 + 8 + 8 + 8 + 8 + 8
 
 
