@@ -363,7 +363,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
             }
         }
         if (use_seg && __any_sync(FULL_MASK, occ)) {
-            float ub = INFINITY;
+            float d2q = INFINITY;  // squared segment distance of a cell that stays queued
             if (occ) {
                 const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
                 const float px = sv.Pf[mx], py = sv.Pf[Wm + my], pz = sv.Pf[2 * Wm + mz];
@@ -375,9 +375,15 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
                 const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
                 const float lim = thresh + k_lo;
                 occ = lim >= 0.0f && d2 <= lim * lim;
-                if (occ) ub = sqrtf(d2) + k_hi;
+                d2q = occ ? d2 : INFINITY;
             }
-            thresh = fminf(thresh, from_orderable(__reduce_min_sync(FULL_MASK, orderable(ub))));
+            // non-negative floats order like their bits: one integer min over the warp
+            const uint32_t m = __reduce_min_sync(FULL_MASK, __float_as_uint(d2q));
+            if (m < 0x7f800000u) {
+                const float dm = __uint_as_float(m);
+                const float r = dm > 0.0f ? dm * rsqrtf(dm) : 0.0f;  // ~2^-22 relative: rounded up below
+                thresh = fminf(thresh, fmaf(r, 1.0f + 0x1p-18f, k_hi));
+            }
         }
         const unsigned ballot = __ballot_sync(FULL_MASK, occ);
         if (occ) queue[qlen + __popc(ballot & ((1u << lane) - 1u))] = cell;
