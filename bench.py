@@ -180,6 +180,19 @@ def _max_over_ranks(dist, torch, x):
     return float(t.item())
 
 
+def _e2e_entry(C_total, pipe_ms, single_ms, h2d, d2h):
+    """The public-API end-to-end number: the faster of the pipelined and the
+    one-cycle-at-a-time paths (both copy every cycle's inputs in and results out)."""
+    pipe_path = ("CheckerPipeline (2 cycles in flight): per cycle H2D of configs + cloud from pinned host memory on "
+                 "a copy stream, the cycle graph, D2H of (d, link, voxel) + flags; host wall clock over K cycles")
+    single_path = ("DistanceChecker.query() one cycle at a time from pinned host buffers (zero-copy kernel "
+                   "reads/writes over PCIe); median cycle, host wall clock")
+    best_ms, path = (pipe_ms, pipe_path) if pipe_ms <= single_ms else (single_ms, single_path)
+    return {"value": C_total / (best_ms / 1e3), "unit": "waypoint-queries/s", "ms_per_step": best_ms,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "path": path,
+            "pipelined_ms_per_step": pipe_ms, "single_cycle_ms": single_ms}
+
+
 def run_ours(args, rank, world, dist, sampler):
     import torch
 
@@ -292,15 +305,8 @@ def run_ours(args, rank, world, dist, sampler):
                    "l2": "flushed (256 MiB write) before every timed step",
                    "timing": "device: CUDA events around a graph replay of the cycle"},
         "gpu_launches": KERNELS_PER_STEP * args.steps,
-        "e2e": {"value": C_total / (e2e_ms / 1e3), "unit": "waypoint-queries/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": int(n_local * robot.dof * 8 + shape.n_points * 12),
-                "d2h_bytes_per_step": int(n_local * 12 + 16),
-                "path": "CheckerPipeline (2 cycles in flight): per cycle H2D of configs + cloud from pinned host "
-                        "memory on a copy stream, the cycle graph, D2H of (d, link, voxel) + flags; host wall clock "
-                        "over K cycles",
-                "single_cycle_ms": single_ms,
-                "single_cycle_path": "DistanceChecker.query() from pinned host buffers (zero-copy kernel "
-                                     "reads/writes over PCIe), median of one-at-a-time cycles"},
+        "e2e": _e2e_entry(C_total, e2e_ms, single_ms, int(n_local * robot.dof * 8 + shape.n_points * 12),
+                          int(n_local * 12 + 16)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "query_shells_kernel", "kernel_ms": q_ms,
                      "algorithmic_bytes": alg_bytes, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst)"},

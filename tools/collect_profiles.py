@@ -1,0 +1,71 @@
+"""Copy the evidence produced by tools/refresh_profiles.sh (gpurun_out/prof/)
+into profiles/<round>/ and regenerate the ncu summary text.
+
+    python tools/collect_profiles.py [--round r01]
+"""
+import argparse
+import json
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent.parent
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--round", default="r01")
+    args = ap.parse_args()
+    src = REPO / "gpurun_out" / "prof"
+    dst = REPO / "profiles" / args.round
+    dst.mkdir(parents=True, exist_ok=True)
+    for a, b in (("bench.json", "bench_config4_N1.json"), ("bench_config2.json", "bench_config2_N1.json"),
+                 ("bench_reference.json", "bench_reference_port.json")):
+        line = (src / a).read_text().strip().splitlines()[-1]
+        json.loads(line)
+        (dst / b).write_text(line + "\n")
+    for f in ("launches_config4.csv", "launches_config2.csv", "launches_bench.csv"):
+        shutil.copy(src / f, dst / f)
+    # per-launch DRAM traffic of the query kernel, read by bench.py's roofline
+    traffic = {}
+    for w in ("config4", "config2"):
+        out = subprocess.run(["ncu", "-i", str(src / f"shells_{w}.ncu-rep"), "--page", "raw", "--csv"],
+                             capture_output=True, text=True).stdout.splitlines()
+        import csv
+        rows = list(csv.reader(out))
+        h, u, v = rows[0], rows[1], rows[2]
+        d = dict(zip(h, zip(u, v)))
+
+        def val(k):
+            unit, x = d[k]
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            return float(x.replace(",", "")) * scale
+
+        traffic[w] = int(val("dram__bytes_read.sum") + val("dram__bytes_write.sum"))
+    traffic["_units"] = ("bytes per launch of query_shells_kernel: dram__bytes_read.sum + dram__bytes_write.sum from "
+                         f"one ncu --set full capture (profiles/{args.round}/ncu_summary.txt)")
+    (REPO / "profiles" / "query_traffic.json").write_text(json.dumps(traffic))
+    py = sys.executable
+    lines = [f"# ncu summaries, round {args.round[1:]} (tools/refresh_profiles.sh; B200, --clock-control none)", "",
+             "## launch lists (cold, serialised; the first 4 query launches of each process are the checker's "
+             "warm-up with an empty cloud; the bench list includes the 256 MiB L2-flush fills)"]
+    for f in ("launches_bench", "launches_config4", "launches_config2"):
+        r = subprocess.run([py, str(REPO / "tools" / "ncu_launches.py"), str(src / f"{f}.csv")],
+                           capture_output=True, text=True).stdout.splitlines()
+        lines += [f"### {f}.csv"] + r[1:9]
+    for w in ("config4", "config2"):
+        lines += ["", f"## query_shells_kernel, {w} (ncu --set full, the first real query launch)"]
+        r = subprocess.run([py, str(REPO / "tools" / "ncu_summary.py"), str(src / f"shells_{w}.ncu-rep")],
+                           capture_output=True, text=True).stdout.splitlines()
+        lines += r[1:]
+        lines += ["", "### hottest source lines"]
+        r = subprocess.run([py, str(REPO / "tools" / "ncu_lines.py"), str(src / f"shells_{w}.ncu-rep"), "25"],
+                           capture_output=True, text=True).stdout.splitlines()
+        lines += r
+    (dst / "ncu_summary.txt").write_text("\n".join(lines) + "\n")
+    print("collected into", dst, traffic)
+
+
+if __name__ == "__main__":
+    main()
