@@ -134,3 +134,47 @@ def gather_waypoint_results(d, link, voxel, group=None):
     dist.all_gather(parts, mine, group=group)
     rows = np.concatenate([p.numpy()[: int(s.item())] for p, s in zip(parts, sizes)])
     return rows[:, 0].astype(np.float32), rows[:, 1].astype(np.int32), rows[:, 2].astype(np.int32)
+
+
+def build_link_sdfs_sharded(geometries, extent, resolution, group=None, build=None):
+    """Per-link SDF precompute partitioned by link.
+
+    Rank r builds links r, r + world, ... (``build_link_sdf`` on its GPU by
+    default), then ONE all-gather of the padded (links-per-rank, cells) f32
+    block gives every rank every grid (NCCL on GPUs — 8 MiB per 128^3 link —
+    gloo on CPU).  Returns the LinkSdf list in link order on every rank.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from .grids import LinkSdf
+
+    if build is None:
+        from .meshes import build_link_sdf as build
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    n = len(geometries)
+    per = -(-n // world)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+    mine = list(range(rank, n, world))
+    built = [build(geometries[i], extent, resolution, link_id=i) for i in mine]
+    from .grids import _cells, _vec3  # a rank without links still needs the block shape
+
+    dims = tuple(int(d) for d in _cells(_vec3(extent, "extent"), _vec3(resolution, "resolution"), "LinkSdf"))
+    ncell = int(np.prod(dims))
+    block = torch.zeros((per, ncell), dtype=torch.float32, device=dev)
+    for j, sdf in enumerate(built):
+        if nccl:
+            block[j] = sdf.device_values()
+        else:
+            block[j] = torch.from_numpy(np.ascontiguousarray(np.asarray(sdf.values).ravel(order="F")))
+    parts = [torch.empty_like(block) for _ in range(world)]
+    dist.all_gather(parts, block, group=group)
+    out = []
+    for i in range(n):
+        flat = parts[i % world][i // world]
+        if nccl:
+            out.append(LinkSdf(extent, resolution, flat.clone(), link_id=i))
+        else:
+            out.append(LinkSdf(extent, resolution, flat.numpy().reshape(dims, order="F"), link_id=i))
+    return out

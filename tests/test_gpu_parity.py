@@ -544,3 +544,35 @@ def test_obstacle_shards_recombine_exactly(L):
         red = np.minimum.reduce([Sh._to_signed(k) for k in keys])
         d, link, voxel = Sh.unpack_keys(Sh._from_signed(red), traj.n_links, traj.d_far_global)
         assert np.array_equal(d, full[0]) and np.array_equal(link, full[1]) and np.array_equal(voxel, full[2])
+
+
+def test_nccl_sharding_paths_world1(L):
+    """The NCCL code paths of sharding.py on one GPU (world size 1): link-sharded
+    build == local builds bit for bit; obstacle-sharded query == the full query."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2309_12543_b200 import sharding as Sh
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        g = golden("scene_c1")
+        robot, grid, sdfs, window = _scene(L, g)
+        geoms = [robot.links[i].geometry for i in robot.geometry_links]
+        e_r, r_r = float(g["e_r"]), float(g["r_r"])
+        built = Sh.build_link_sdfs_sharded(geoms, e_r, r_r)
+        for a, b in zip(built, sdfs):
+            assert np.array_equal(np.asarray(a.values), np.asarray(b.values))
+        traj = L.TrajectorySdf.from_configs(robot, g["q"], built, grid, window)
+        obs = L.voxelize_pointcloud(g["points"], grid)
+        full = L.query_min_distances(traj, obs, return_argmin=True)
+        d, link, voxel = Sh.query_obstacle_sharded(traj, obs)
+        assert np.array_equal(d, full[0]) and np.array_equal(link, full[1]) and np.array_equal(voxel, full[2])
+    finally:
+        dist.destroy_process_group()
