@@ -1,7 +1,8 @@
 // lsdf_build.cu — stage 2a: exact link-SDF precompute (meshes.py:64-82, 144-371).
 //
-// Primitives: one thread per cell, fp64 analytic distance, f32 store; the
-// write is the whole cost (HBM-store bound, 4 B per cell).
+// Primitives: one thread per cell, fp64 analytic distance, f32 store
+// (fp64-issue bound: the distance with the reference's operation order is
+// ~100 instructions per 4 B written).
 // Meshes: brute force over all triangles (the spec rejects propagation
 // transforms).  A CTA owns 128 cells and streams the
 // triangle list through shared memory in tiles, so every triangle is read
@@ -16,9 +17,11 @@ namespace {
 
 __device__ __forceinline__ void cell_center(int64_t cell, const int32_t* dims, const double* ext, const double* res,
                                             double* p) {
-    const int64_t ix = cell % dims[0];
-    const int64_t iy = (cell / dims[0]) % dims[1];
-    const int64_t iz = cell / ((int64_t)dims[0] * dims[1]);
+    // 32-bit index arithmetic (grids stay far below 2^32 cells; 64-bit
+    // division is a long instruction sequence)
+    const uint32_t c = (uint32_t)cell, d0 = (uint32_t)dims[0], d1 = (uint32_t)dims[1];
+    const uint32_t t = c / d0;
+    const uint32_t ix = c - t * d0, iy = t % d1, iz = t / d1;
     // meshes.py:356-358: -e + (i + 0.5) * r
     p[0] = DADD(-ext[0], DMUL(DADD((double)ix, 0.5), res[0]));
     p[1] = DADD(-ext[1], DMUL(DADD((double)iy, 0.5), res[1]));
@@ -32,14 +35,17 @@ struct BuildParams {
     int32_t dims[3];
 };
 
-__global__ void build_primitive_kernel(const __grid_constant__ BuildParams p, float* out) {
-    const int64_t n = (int64_t)p.dims[0] * p.dims[1] * p.dims[2];
-    for (int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < n;
-         cell += (int64_t)gridDim.x * blockDim.x) {
-        double c[3];
-        cell_center(cell, p.dims, p.ext, p.res, c);
-        out[cell] = (float)primitive_at(p.kind, p.prm, c[0], c[1], c[2]);
-    }
+// grid (ceil(nx / 128), ny, nz): one x-row segment per CTA, no index division
+template <int KIND>
+__global__ void __launch_bounds__(128) build_primitive_kernel(const __grid_constant__ BuildParams p, float* out) {
+    const int ix = blockIdx.x * 128 + threadIdx.x;
+    if (ix >= p.dims[0]) return;
+    const uint32_t iy = blockIdx.y, iz = blockIdx.z, row = iz * (uint32_t)p.dims[1] + iy;
+    // meshes.py:356-358: -e + (i + 0.5) * r
+    const double x = DADD(-p.ext[0], DMUL(DADD((double)ix, 0.5), p.res[0]));
+    const double y = DADD(-p.ext[1], DMUL(DADD((double)iy, 0.5), p.res[1]));
+    const double z = DADD(-p.ext[2], DMUL(DADD((double)iz, 0.5), p.res[2]));
+    out[(int64_t)row * p.dims[0] + ix] = (float)primitive_at(KIND, p.prm, x, y, z);
 }
 
 __global__ void primitive_points_kernel(int32_t kind, BuildParams p, const double* pts, int64_t n, double* out) {
@@ -182,10 +188,17 @@ extern "C" int lsdf_build_primitive(int32_t kind, const double params[8], const 
         p.dims[a] = dims[a];
     }
     const int64_t n = (int64_t)dims[0] * dims[1] * dims[2];
+    if (n >= 4294967296LL) return fail(LSDF_ERR_UNSUPPORTED, "link grid of %lld cells (>= 2^32)", (long long)n);
     if (n <= 0) return LSDF_OK;
-    const int64_t blocks = (n + 255) / 256;
-    build_primitive_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, (cudaStream_t)stream>>>(
-        p, values_dev);
+    if (dims[1] > 65535 || dims[2] > 65535) return fail(LSDF_ERR_UNSUPPORTED, "link grid wider than 65535 cells");
+    const dim3 grid((unsigned)((dims[0] + 127) / 128), (unsigned)dims[1], (unsigned)dims[2]);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (kind == 0)
+        build_primitive_kernel<0><<<grid, 128, 0, s>>>(p, values_dev);
+    else if (kind == 1)
+        build_primitive_kernel<1><<<grid, 128, 0, s>>>(p, values_dev);
+    else
+        build_primitive_kernel<2><<<grid, 128, 0, s>>>(p, values_dev);
     return check_launch("build_primitive_kernel");
 }
 
@@ -212,6 +225,7 @@ extern "C" int lsdf_build_mesh(const double* tri_dev, int32_t n_tri, int32_t is_
         p.dims[a] = dims[a];
     }
     p.n = (int64_t)dims[0] * dims[1] * dims[2];
+    if (p.n >= 4294967296LL) return fail(LSDF_ERR_UNSUPPORTED, "link grid of %lld cells (>= 2^32)", (long long)p.n);
     p.out_f = values_dev;
     if (p.n <= 0) return LSDF_OK;
     return launch_mesh(p, (cudaStream_t)stream);
