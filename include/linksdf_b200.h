@@ -178,6 +178,14 @@ int lsdf_voxelize(const void* points_dev, int32_t points_f32, int64_t N,
                   const lsdf_env_grid* env, void* occupancy_dev,
                   int32_t* indices_dev, void* stream);
 
+/* The two halves of lsdf_voxelize for callers that overlap them with other
+ * work: the bitmap (memset + scatter; all the scan of lsdf_query_scan needs)
+ * and the per-word popcount prefix (rank = np.unique position; needed by
+ * lsdf_query_finalize and the compact index list). */
+int lsdf_voxelize_bitmap(const void* points_dev, int32_t points_f32, int64_t N,
+                         const lsdf_env_grid* env, void* occupancy_dev, void* stream);
+int lsdf_occupancy_prefix(const lsdf_env_grid* env, void* occupancy_dev, void* stream);
+
 /* Occupancy from an explicit index list (ObstacleVoxelSet, query.py:47-58).
  * sorted_unique != 0 promises lexicographic order without duplicates (what
  * voxelize and np.unique produce); otherwise the first position of each voxel
@@ -212,6 +220,26 @@ int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_dev,
                       int32_t by_position, double d_far_global, void* workspace_dev,
                       float* d_dev, int32_t* link_dev, int32_t* voxel_dev,
                       float* per_link_dev, void* stream);
+
+/* lsdf_query_direct in two launches with the same arguments: the scan
+ * (reduces into the workspace keys; needs only the occupancy bitmap) and the
+ * finalize (keys -> d, link, voxel rank; needs the occupancy prefix and
+ * re-zeroes the workspace).  A caller can run lsdf_occupancy_prefix on
+ * another stream between them. */
+int lsdf_query_scan(const double* R_geo_dev, const double* dt_geo_dev,
+                    const int32_t* anchor_geo_dev, int64_t C, int32_t n_geo,
+                    const lsdf_link_grid* grids, const lsdf_window* window,
+                    const lsdf_env_grid* env, const void* occupancy_dev,
+                    int32_t by_position, double d_far_global, void* workspace_dev,
+                    float* d_dev, int32_t* link_dev, int32_t* voxel_dev,
+                    float* per_link_dev, void* stream);
+int lsdf_query_finalize(const double* R_geo_dev, const double* dt_geo_dev,
+                        const int32_t* anchor_geo_dev, int64_t C, int32_t n_geo,
+                        const lsdf_link_grid* grids, const lsdf_window* window,
+                        const lsdf_env_grid* env, const void* occupancy_dev,
+                        int32_t by_position, double d_far_global, void* workspace_dev,
+                        float* d_dev, int32_t* link_dev, int32_t* voxel_dev,
+                        float* per_link_dev, void* stream);
 
 /* ---- materialized (paper) mode ----------------------------------------- */
 

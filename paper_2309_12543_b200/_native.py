@@ -63,9 +63,15 @@ _SIGS = {
     "lsdf_align": [_P, _I64, C.POINTER(EnvGridT), C.POINTER(_I32), _P, _P, _P, _P],
     "lsdf_occupancy_bytes": [C.POINTER(EnvGridT)],
     "lsdf_voxelize": [_P, _I32, _I64, C.POINTER(EnvGridT), _P, _P, _P],
+    "lsdf_voxelize_bitmap": [_P, _I32, _I64, C.POINTER(EnvGridT), _P, _P],
+    "lsdf_occupancy_prefix": [C.POINTER(EnvGridT), _P, _P],
     "lsdf_occupancy_from_indices": [_P, _I64, _I32, C.POINTER(EnvGridT), _P, _P],
     "lsdf_voxel_index": [_P, _I64, C.POINTER(EnvGridT), _P, _P, _P],
     "lsdf_query_direct": [_P, _P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT),
+                          C.POINTER(EnvGridT), _P, _I32, _D, _P, _P, _P, _P, _P, _P],
+    "lsdf_query_scan": [_P, _P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT),
+                          C.POINTER(EnvGridT), _P, _I32, _D, _P, _P, _P, _P, _P, _P],
+    "lsdf_query_finalize": [_P, _P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT),
                           C.POINTER(EnvGridT), _P, _I32, _D, _P, _P, _P, _P, _P, _P],
     "lsdf_query_workspace_bytes": [_I64, _I32],
     "lsdf_pack_corners": [_P, C.POINTER(_I32), _P, _P],

@@ -4,8 +4,9 @@ One object per (robot, link SDFs, environment grid, window).  ``prepare``
 sizes device buffers and pinned host buffers for a batch shape and captures
 one control cycle as a CUDA graph with two branches:
 
-    side stream:  fk_align (reads the configurations)  ──┐
-    main stream:  voxelize (memset, scatter + rank)     ──┴─> query_direct ──> (d, link, voxel)
+    side stream:    fk_align (reads the configurations)  ──┐
+    main stream:    voxelize bitmap (memset, scatter)   ──┴─> query scan ──┬─> finalize ──> (d, link, voxel)
+    prefix stream:                   └─> rank prefix ───────────────────────┘
 
 End to end (``query``) the kernels read the configurations and the cloud
 straight from page-locked host memory and the query writes (d, link, voxel)
@@ -95,6 +96,7 @@ class DistanceChecker:
             except Exception:  # mapping unavailable: the graph stages copies instead
                 self._map = None
         self._side = t.cuda.Stream()
+        self._prefix_stream = t.cuda.Stream()
         self._env = ctypes.byref(self.grid.c_struct())
         self._W = N.i32x3(self.window.dims)
         self._chain = self.robot.chain_table()
@@ -130,8 +132,13 @@ class DistanceChecker:
         if staged:
             self.p_dev.copy_(self.p_host, non_blocking=True)
         p_ptr = self._map["p"] if zc else N.ptr(self.p_dev)
-        N.call("lsdf_voxelize", p_ptr, int(pdt == np.float32), P, self._env, N.ptr(self.ws), None,
+        # the rank prefix is only needed by the finalize: it runs on a third
+        # stream while the scan (which needs the bitmap alone) runs
+        N.call("lsdf_voxelize_bitmap", p_ptr, int(pdt == np.float32), P, self._env, N.ptr(self.ws),
                main.cuda_stream)
+        pre = self._prefix_stream
+        pre.wait_stream(main)
+        N.call("lsdf_occupancy_prefix", self._env, N.ptr(self.ws), pre.cuda_stream)
         main.wait_stream(side)
         if e2e:
             with t.cuda.stream(side):  # 16 B of flags back to the host, off the critical path
@@ -141,9 +148,12 @@ class DistanceChecker:
         else:
             outs = (N.ptr(self.d_dev), N.ptr(self.link_dev), N.ptr(self.voxel_dev))
         tr = self.traj
-        N.call("lsdf_query_direct", N.ptr(self.R_geo), N.ptr(self.dt_geo), N.ptr(self.anchor_geo), C_, tr.n_links,
-               tr._table, ctypes.byref(self._wstruct), self._env, N.ptr(self.ws), 0, self.d_far_global,
-               N.ptr(self.qws), outs[0], outs[1], outs[2], None, main.cuda_stream)
+        args = (N.ptr(self.R_geo), N.ptr(self.dt_geo), N.ptr(self.anchor_geo), C_, tr.n_links, tr._table,
+                ctypes.byref(self._wstruct), self._env, N.ptr(self.ws), 0, self.d_far_global, N.ptr(self.qws),
+                outs[0], outs[1], outs[2], None, main.cuda_stream)
+        N.call("lsdf_query_scan", *args)
+        main.wait_stream(pre)
+        N.call("lsdf_query_finalize", *args)
         if staged:
             self.d_host.copy_(self.d_dev, non_blocking=True)
             self.link_host.copy_(self.link_dev, non_blocking=True)

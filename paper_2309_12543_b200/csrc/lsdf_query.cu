@@ -478,11 +478,14 @@ inline int64_t ws_bytes(int64_t C, int32_t n_geo) {
 
 extern "C" int64_t lsdf_query_workspace_bytes(int64_t C, int32_t n_geo) { return ws_bytes(C, n_geo); }
 
-extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_dev, const int32_t* anchor_geo_dev,
-                                 int64_t C, int32_t n_geo, const lsdf_link_grid* grids, const lsdf_window* window,
-                                 const lsdf_env_grid* env, const void* occupancy_dev, int32_t by_position,
-                                 double d_far_global, void* workspace_dev, float* d_dev, int32_t* link_dev,
-                                 int32_t* voxel_dev, float* per_link_dev, void* stream) {
+namespace {
+
+constexpr int STAGE_SCAN = 1, STAGE_FINALIZE = 2;
+
+int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t* anchor_geo_dev, int64_t C,
+               int32_t n_geo, const lsdf_link_grid* grids, const lsdf_window* window, const lsdf_env_grid* env,
+               const void* occupancy_dev, int32_t by_position, double d_far_global, void* workspace_dev, float* d_dev,
+               int32_t* link_dev, int32_t* voxel_dev, float* per_link_dev, void* stream, int stages) {
     if (n_geo < 1 || n_geo > LSDF_MAX_LINKS) return fail(LSDF_ERR_VALIDATION, "query: %d geometry links", n_geo);
     if (window->W[0] > LSDF_MAX_WINDOW || window->W[1] > LSDF_MAX_WINDOW || window->W[2] > LSDF_MAX_WINDOW)
         return fail(LSDF_ERR_UNSUPPORTED, "query: window wider than %d cells", LSDF_MAX_WINDOW);
@@ -559,7 +562,7 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
     // one launch per group of links with identical grid geometry (normally one)
     bool done[LSDF_MAX_LINKS] = {false};
     int n_launch = 0;
-    for (int l0 = 0; l0 < n_geo; ++l0) {
+    for (int l0 = 0; l0 < n_geo && (stages & STAGE_SCAN); ++l0) {
         if (done[l0]) continue;
         const lsdf_link_grid& g0 = grids[l0];
         int n_group = 0;
@@ -637,7 +640,23 @@ extern "C" int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_d
         }
         LSDF_TRY(check_launch("query_direct_kernel"));
     }
+    if (!(stages & STAGE_FINALIZE)) return LSDF_OK;
     finalize_kernel<<<grid_for(C > LSDF_MAX_LINKS ? C : LSDF_MAX_LINKS, 128), 128, 0, s>>>(p);
     return check_launch("finalize_kernel");
 
 }
+
+}  // namespace
+
+#define LSDF_QUERY_ARGS                                                                                            \
+    const double *R_geo_dev, const double *dt_geo_dev, const int32_t *anchor_geo_dev, int64_t C, int32_t n_geo,   \
+        const lsdf_link_grid *grids, const lsdf_window *window, const lsdf_env_grid *env, const void *occupancy_dev, \
+        int32_t by_position, double d_far_global, void *workspace_dev, float *d_dev, int32_t *link_dev,           \
+        int32_t *voxel_dev, float *per_link_dev, void *stream
+#define LSDF_QUERY_FWD                                                                                   \
+    R_geo_dev, dt_geo_dev, anchor_geo_dev, C, n_geo, grids, window, env, occupancy_dev, by_position,    \
+        d_far_global, workspace_dev, d_dev, link_dev, voxel_dev, per_link_dev, stream
+
+extern "C" int lsdf_query_direct(LSDF_QUERY_ARGS) { return query_impl(LSDF_QUERY_FWD, STAGE_SCAN | STAGE_FINALIZE); }
+extern "C" int lsdf_query_scan(LSDF_QUERY_ARGS) { return query_impl(LSDF_QUERY_FWD, STAGE_SCAN); }
+extern "C" int lsdf_query_finalize(LSDF_QUERY_ARGS) { return query_impl(LSDF_QUERY_FWD, STAGE_FINALIZE); }

@@ -170,39 +170,60 @@ __global__ void voxel_index_kernel(const double* pts, int64_t N, lsdf_env_grid e
 
 extern "C" int64_t lsdf_occupancy_bytes(const lsdf_env_grid* env) { return occupancy_bytes(*env); }
 
+namespace {
+
+// memset + scatter: the bitmap (and the dropped-point counter) of a cloud
+int scatter_bitmap(const void* points_dev, int32_t points_f32, int64_t N, const lsdf_env_grid* env, Occupancy& o,
+                   void* occupancy_dev, cudaStream_t s) {
+    LSDF_TRY(check_cuda(cudaMemsetAsync(occupancy_dev, 0, 256 + o.n_words * 4, s), "voxelize memset"));
+    if (N <= 0) return LSDF_OK;
+    const unsigned blocks = grid_for(N, SCATTER_THREADS);
+    const double rx = 1.0 / env->resolution[0], ry = 1.0 / env->resolution[1], rz = 1.0 / env->resolution[2];
+    const bool priv = o.n_words <= PRIVATE_WORDS_MAX;
+    const size_t smem = priv ? (size_t)o.n_words * 4 : 0;
+    if (points_f32) {
+        if (priv)
+            voxel_scatter_kernel<float, true><<<blocks, SCATTER_THREADS, smem, s>>>(
+                (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+        else
+            voxel_scatter_kernel<float, false><<<blocks, SCATTER_THREADS, 0, s>>>(
+                (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+    } else {
+        if (priv)
+            voxel_scatter_kernel<double, true><<<blocks, SCATTER_THREADS, smem, s>>>(
+                (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+        else
+            voxel_scatter_kernel<double, false><<<blocks, SCATTER_THREADS, 0, s>>>(
+                (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+    }
+    return check_launch("voxel_scatter_kernel");
+}
+
+}  // namespace
+
 extern "C" int lsdf_voxelize(const void* points_dev, int32_t points_f32, int64_t N, const lsdf_env_grid* env,
                              void* occupancy_dev, int32_t* indices_dev, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     Occupancy o = carve_occupancy(occupancy_dev, *env);
-    LSDF_TRY(check_cuda(cudaMemsetAsync(occupancy_dev, 0, 256 + o.n_words * 4, s), "voxelize memset"));
-    if (N > 0) {
-        const unsigned blocks = grid_for(N, SCATTER_THREADS);
-        const double rx = 1.0 / env->resolution[0], ry = 1.0 / env->resolution[1], rz = 1.0 / env->resolution[2];
-        const bool priv = o.n_words <= PRIVATE_WORDS_MAX;
-        const size_t smem = priv ? (size_t)o.n_words * 4 : 0;
-        if (points_f32) {
-            if (priv)
-                voxel_scatter_kernel<float, true><<<blocks, SCATTER_THREADS, smem, s>>>(
-                    (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
-            else
-                voxel_scatter_kernel<float, false><<<blocks, SCATTER_THREADS, 0, s>>>(
-                    (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
-        } else {
-            if (priv)
-                voxel_scatter_kernel<double, true><<<blocks, SCATTER_THREADS, smem, s>>>(
-                    (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
-            else
-                voxel_scatter_kernel<double, false><<<blocks, SCATTER_THREADS, 0, s>>>(
-                    (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
-        }
-        LSDF_TRY(check_launch("voxel_scatter_kernel"));
-    }
+    LSDF_TRY(scatter_bitmap(points_dev, points_f32, N, env, o, occupancy_dev, s));
     prefix_only_kernel<<<1, SCAN_THREADS, 0, s>>>(o.bitmap, o.n_words, o.prefix, o.counters);
     LSDF_TRY(check_launch("prefix_only_kernel"));
     if (indices_dev == nullptr) return LSDF_OK;  // hot path: the query only needs bitmap + prefix
     voxel_compact_kernel<<<grid_for(o.n_words, 256), 256, 0, s>>>(o.bitmap, o.prefix, o.n_words, *env, o.posgrid,
                                                                     indices_dev);
     return check_launch("voxel_compact_kernel");
+}
+
+extern "C" int lsdf_voxelize_bitmap(const void* points_dev, int32_t points_f32, int64_t N, const lsdf_env_grid* env,
+                                    void* occupancy_dev, void* stream) {
+    Occupancy o = carve_occupancy(occupancy_dev, *env);
+    return scatter_bitmap(points_dev, points_f32, N, env, o, occupancy_dev, (cudaStream_t)stream);
+}
+
+extern "C" int lsdf_occupancy_prefix(const lsdf_env_grid* env, void* occupancy_dev, void* stream) {
+    Occupancy o = carve_occupancy(occupancy_dev, *env);
+    prefix_only_kernel<<<1, SCAN_THREADS, 0, (cudaStream_t)stream>>>(o.bitmap, o.n_words, o.prefix, o.counters);
+    return check_launch("prefix_only_kernel");
 }
 
 extern "C" int lsdf_occupancy_from_indices(const int32_t* indices_dev, int64_t N, int32_t sorted_unique,
