@@ -576,3 +576,23 @@ def test_nccl_sharding_paths_world1(L):
         assert np.array_equal(d, full[0]) and np.array_equal(link, full[1]) and np.array_equal(voxel, full[2])
     finally:
         dist.destroy_process_group()
+
+
+def test_training_matches_reference(L):
+    """train_approximator on the GPU (same init, rotation stream, L1 + Adam and
+    early-stop rule, approx.py:212-289) vs the reference's own run
+    (tests/golden/make_training.py): weights within 1e-6 after 300 steps,
+    the same checkpoints, errors within 1e-6 relative."""
+    g = golden("training")
+    cfg = L.TrainingConfig(steps=300, eval_every=100, screen_size=128, val_size=512, target_max_error=1.0, seed=3)
+    m = L.train_approximator(g["points"], cfg)
+    for k in ("w1", "b1", "w2", "b2"):
+        assert np.abs(getattr(m, k) - g[k]).max() <= 1e-6, k
+    hist = np.asarray(m.history, dtype=np.float64)
+    assert hist.shape == g["history"].shape and np.array_equal(hist[:, 0], g["history"][:, 0])
+    assert np.allclose(hist[:, 1:], g["history"][:, 1:], rtol=1e-6, atol=0)
+    assert abs(m.validation_max_error - float(g["val_max"])) <= 1e-6 * float(g["val_max"])
+    with pytest.raises(L.NotConvergedError):
+        L.train_approximator(g["points"], L.TrainingConfig(steps=100, eval_every=100, screen_size=64, val_size=128,
+                                                           target_max_error=0.01, seed=3))
+
