@@ -3,11 +3,13 @@
 // Primitives: one thread per cell, fp64 analytic distance, f32 store
 // (fp64-issue bound: the distance with the reference's operation order is
 // ~100 instructions per 4 B written).
-// Meshes: brute force over all triangles (the spec rejects propagation
-// transforms).  A CTA owns 128 cells and streams the
-// triangle list through shared memory in tiles, so every triangle is read
-// from L2 once per CTA; the per-pair closest-point and ray-crossing tests
-// run in fp64 with the reference's operation order.
+// Meshes: exact per-(cell, triangle) tests (the spec rejects propagation
+// transforms) with conservative box culling.  A CTA owns a
+// compact 8 x 4 x 4 block of cells and streams the triangle list through
+// shared memory in tiles, nearest tile first, skipping tiles / triangles that
+// provably cannot change any of its cells' results; the per-pair
+// closest-point and ray-crossing tests run in fp64 with the reference's
+// operation order.
 #include "lsdf_common.cuh"
 #include "lsdf_math.cuh"
 
@@ -96,34 +98,163 @@ struct MeshParams {
     double* out_d;
 };
 
-__global__ void __launch_bounds__(MESH_CELLS) mesh_kernel(const __grid_constant__ MeshParams p) {
-    __shared__ double s_tri[MESH_TILE * 9];
-    __shared__ RayTri s_ray[MESH_TILE];
-    const int64_t i = (int64_t)blockIdx.x * MESH_CELLS + threadIdx.x;
-    const bool active = i < p.n;
-    double pt[3] = {0.0, 0.0, 0.0};
-    if (active) {
-        if (p.pts) {
-            pt[0] = p.pts[3 * i];
-            pt[1] = p.pts[3 * i + 1];
-            pt[2] = p.pts[3 * i + 2];
-        } else {
-            cell_center(i, p.dims, p.ext, p.res, pt);
+// Per-triangle and per-tile (MESH_TILE triangles) axis-aligned bounds, fp64:
+// [min x, min y, min z, max x, max y, max z].
+__global__ void mesh_bounds_kernel(const double* __restrict__ tri, int32_t n_tri, double* tri_bb, double* tile_bb) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n_tri) {
+        const double* v = tri + 9 * (int64_t)t;
+        for (int a = 0; a < 3; ++a) {
+            tri_bb[6 * (int64_t)t + a] = fmin(v[a], fmin(v[3 + a], v[6 + a]));
+            tri_bb[6 * (int64_t)t + 3 + a] = fmax(v[a], fmax(v[3 + a], v[6 + a]));
         }
     }
+    const int n_tiles = (n_tri + MESH_TILE - 1) / MESH_TILE;
+    if (t < n_tiles) {
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        const int end = (t + 1) * MESH_TILE < n_tri ? (t + 1) * MESH_TILE : n_tri;
+        for (int k = t * MESH_TILE; k < end; ++k)
+            for (int a = 0; a < 9; ++a) {
+                const double x = tri[9 * (int64_t)k + a];
+                lo[a % 3] = fmin(lo[a % 3], x);
+                hi[a % 3] = fmax(hi[a % 3], x);
+            }
+        for (int a = 0; a < 3; ++a) {
+            tile_bb[6 * t + a] = lo[a];
+            tile_bb[6 * t + 3 + a] = hi[a];
+        }
+    }
+}
+
+// squared gap between two boxes (0 when they overlap); a lower bound of the
+// squared distance between any point of one and any point of the other
+__device__ __forceinline__ double box_gap2(const double* A, const double* B) {
+    double g2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double g = fmax(0.0, fmax(B[a] - A[3 + a], A[a] - B[3 + a]));
+        g2 += g * g;
+    }
+    return g2;
+}
+
+// no point of box B can be hit by a ray p + t dir, t > 0, from any p in box A
+// (B lies behind A along an axis the direction advances on), with slack
+__device__ __forceinline__ bool behind(const double* A, const double* B, const double* dir) {
+    constexpr double slack = 1e-6;
+    bool out = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        out |= (dir[a] > 0.0) & (B[3 + a] < A[a] - slack);
+        out |= (dir[a] < 0.0) & (B[a] > A[3 + a] + slack);
+    }
+    return out;
+}
+
+// Exact mesh SDF with conservative culling.  A CTA owns a compact 8 x 4 x 4
+// block of cells (or 128 consecutive explicit points); its box bounds every
+// point.  Unsigned distance: tiles are visited nearest-box first, and a tile
+// or triangle whose box gap to the cell box exceeds the largest running
+// minimum of the CTA (squared, with a relative margin far above the fp64
+// rounding of closest_sq) cannot be any cell's minimum and is skipped.  Ray
+// parity: a triangle whose box lies behind the cell box along an axis the
+// ray advances on cannot give a hit with t > 0 (ray_cross returns 0 for it,
+// never "suspect").  Both leave every result identical to the full
+// brute force (meshes.py:217-246, 259-305).
+template <bool CELLS>
+__global__ void __launch_bounds__(MESH_CELLS) mesh_kernel(const __grid_constant__ MeshParams p,
+                                                          const double* __restrict__ tri_bb,
+                                                          const double* __restrict__ tile_bb) {
+    __shared__ double s_tri[MESH_TILE * 9];
+    __shared__ RayTri s_ray[MESH_TILE];
+    __shared__ unsigned char s_keep[MESH_TILE];
+    __shared__ double s_blk[6];
+    __shared__ double s_wbox[MESH_CELLS / 32][6];
+    __shared__ unsigned long long s_key;
+    __shared__ unsigned long long s_maxbest;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int64_t i;
+    bool active;
+    double pt[3] = {0.0, 0.0, 0.0};
+    if (CELLS) {
+        const int ix = blockIdx.x * 8 + (tid & 7), iy = blockIdx.y * 4 + ((tid >> 3) & 3), iz = blockIdx.z * 4 + (tid >> 5);
+        active = ix < p.dims[0] && iy < p.dims[1] && iz < p.dims[2];
+        i = ix + (int64_t)p.dims[0] * (iy + (int64_t)p.dims[1] * iz);
+        if (active) {  // meshes.py:356-358: -e + (i + 0.5) * r
+            pt[0] = DADD(-p.ext[0], DMUL(DADD((double)ix, 0.5), p.res[0]));
+            pt[1] = DADD(-p.ext[1], DMUL(DADD((double)iy, 0.5), p.res[1]));
+            pt[2] = DADD(-p.ext[2], DMUL(DADD((double)iz, 0.5), p.res[2]));
+        }
+    } else {
+        i = (int64_t)blockIdx.x * MESH_CELLS + tid;
+        active = i < p.n;
+        if (active)
+            for (int a = 0; a < 3; ++a) pt[a] = p.pts[3 * i + a];
+    }
+    // the CTA's point box
+    {
+        double lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = active ? pt[a] : INFINITY;
+            hi[a] = active ? pt[a] : -INFINITY;
+        }
+        for (int o = 16; o; o >>= 1)
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+                hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+            }
+        if (lane == 0)
+            for (int a = 0; a < 3; ++a) {
+                s_wbox[warp][a] = lo[a];
+                s_wbox[warp][3 + a] = hi[a];
+            }
+        if (tid == 0) s_key = ~0ull;
+        __syncthreads();
+        if (tid < 6) {
+            double v = s_wbox[0][tid];
+            for (int w = 1; w < MESH_CELLS / 32; ++w) v = tid < 3 ? fmin(v, s_wbox[w][tid]) : fmax(v, s_wbox[w][tid]);
+            s_blk[tid] = v;
+        }
+        __syncthreads();
+    }
+    const int n_tiles = (p.n_tri + MESH_TILE - 1) / MESH_TILE;
+    // nearest tile first (box gap, ties to the lower index)
+    for (int t = tid; t < n_tiles; t += MESH_CELLS) {
+        const float g = (float)box_gap2(s_blk, tile_bb + 6 * t);
+        atomicMin(&s_key, ((unsigned long long)__float_as_uint(g) << 32) | (unsigned)t);
+    }
+    __syncthreads();
+    const int first = (int)(s_key & 0xffffffffu);
     // exact unsigned distance: min over every triangle (meshes.py:217-246)
     double best = INFINITY;
-    for (int t0 = 0; t0 < p.n_tri; t0 += MESH_TILE) {
+    double maxbest = INFINITY;  // the CTA's largest running minimum (uniform)
+    for (int k = 0; k < n_tiles; ++k) {
+        const int tile = first + k < n_tiles ? first + k : first + k - n_tiles;
+        if (box_gap2(s_blk, tile_bb + 6 * tile) > maxbest * (1.0 + 1e-9)) continue;  // uniform
+        const int t0 = tile * MESH_TILE;
         const int nt = p.n_tri - t0 < MESH_TILE ? p.n_tri - t0 : MESH_TILE;
         __syncthreads();
-        for (int k = threadIdx.x; k < nt * 9; k += MESH_CELLS) s_tri[k] = p.tri[(int64_t)t0 * 9 + k];
+        for (int q = tid; q < nt * 9; q += MESH_CELLS) s_tri[q] = p.tri[(int64_t)t0 * 9 + q];
+        for (int q = tid; q < nt; q += MESH_CELLS)
+            s_keep[q] = box_gap2(s_blk, tri_bb + 6 * (int64_t)(t0 + q)) <= maxbest * (1.0 + 1e-9);
+        if (tid == 0) s_maxbest = 0ull;
         __syncthreads();
         if (active)
             for (int t = 0; t < nt; ++t) {
+                if (!s_keep[t]) continue;
                 const double* tr = s_tri + 9 * t;
                 const double d2 = closest_sq(pt, tr, tr + 3, tr + 6);
                 best = d2 < best ? d2 : best;
             }
+        // non-negative doubles order like their bits
+        unsigned long long mb = active ? (unsigned long long)__double_as_longlong(best) : 0ull;
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long u = __shfl_xor_sync(0xffffffffu, mb, o);
+            mb = u > mb ? u : mb;
+        }
+        if (lane == 0) atomicMax(&s_maxbest, mb);
+        __syncthreads();
+        maxbest = __longlong_as_double((long long)s_maxbest);
     }
     double d = DSQRT(best);
     if (p.is_signed) {
@@ -133,13 +264,19 @@ __global__ void __launch_bounds__(MESH_CELLS) mesh_kernel(const __grid_constant_
             if (!__syncthreads_or(pending)) break;
             int count = 0;
             bool suspect = false;
-            for (int t0 = 0; t0 < p.n_tri; t0 += MESH_TILE) {
+            for (int tile = 0; tile < n_tiles; ++tile) {
+                if (behind(s_blk, tile_bb + 6 * tile, c_dirs[dir])) continue;  // uniform
+                const int t0 = tile * MESH_TILE;
                 const int nt = p.n_tri - t0 < MESH_TILE ? p.n_tri - t0 : MESH_TILE;
                 __syncthreads();
-                for (int k = threadIdx.x; k < nt; k += MESH_CELLS) s_ray[k] = p.ray[(int64_t)dir * p.n_tri + t0 + k];
+                for (int q = tid; q < nt; q += MESH_CELLS) {
+                    s_ray[q] = p.ray[(int64_t)dir * p.n_tri + t0 + q];
+                    s_keep[q] = !behind(s_blk, tri_bb + 6 * (int64_t)(t0 + q), c_dirs[dir]);
+                }
                 __syncthreads();
                 if (pending)
                     for (int t = 0; t < nt; ++t) {
+                        if (!s_keep[t]) continue;
                         const int h = ray_cross(pt, s_ray[t], c_dirs[dir]);
                         count += h != 0;
                         suspect |= h == 2;
@@ -161,15 +298,27 @@ __global__ void __launch_bounds__(MESH_CELLS) mesh_kernel(const __grid_constant_
 
 int launch_mesh(MeshParams& p, cudaStream_t s) {
     RayTri* ray = nullptr;
+    const int n_tiles = (p.n_tri + MESH_TILE - 1) / MESH_TILE;
+    double* bb = nullptr;  // [n_tri * 6 | n_tiles * 6]
+    LSDF_TRY(check_cuda(cudaMallocAsync((void**)&bb, sizeof(double) * 6 * ((size_t)p.n_tri + n_tiles), s),
+                        "mesh bounds alloc"));
+    mesh_bounds_kernel<<<grid_for(p.n_tri, 128), 128, 0, s>>>(p.tri, p.n_tri, bb, bb + 6 * (size_t)p.n_tri);
+    LSDF_TRY(check_launch("mesh_bounds_kernel"));
     if (p.is_signed) {
         LSDF_TRY(check_cuda(cudaMallocAsync((void**)&ray, sizeof(RayTri) * 4 * (size_t)p.n_tri, s), "mesh ray alloc"));
         ray_setup_kernel<<<grid_for(4LL * p.n_tri, 128), 128, 0, s>>>(p.tri, p.n_tri, ray);
         LSDF_TRY(check_launch("ray_setup_kernel"));
     }
     p.ray = ray;
-    mesh_kernel<<<grid_for(p.n, MESH_CELLS), MESH_CELLS, 0, s>>>(p);
+    if (p.pts == nullptr) {
+        const dim3 grid((unsigned)((p.dims[0] + 7) / 8), (unsigned)((p.dims[1] + 3) / 4), (unsigned)((p.dims[2] + 3) / 4));
+        mesh_kernel<true><<<grid, MESH_CELLS, 0, s>>>(p, bb, bb + 6 * (size_t)p.n_tri);
+    } else {
+        mesh_kernel<false><<<grid_for(p.n, MESH_CELLS), MESH_CELLS, 0, s>>>(p, bb, bb + 6 * (size_t)p.n_tri);
+    }
     int rc = check_launch("mesh_kernel");
     if (ray) cudaFreeAsync(ray, s);
+    cudaFreeAsync(bb, s);
     return rc;
 }
 

@@ -88,6 +88,22 @@ def primitive_sdf(shape, points) -> np.ndarray:
     return d[0] if scalar else d.reshape(pts.shape[:-1])
 
 
+def _morton_order(points: np.ndarray) -> np.ndarray:
+    """Permutation sorting points along a 3-D Z-order curve (10 bits per axis)."""
+    p = np.asarray(points, dtype=np.float64)
+    lo, hi = p.min(axis=0), p.max(axis=0)
+    q = np.clip(((p - lo) / np.maximum(hi - lo, 1e-300) * 1023.0).astype(np.int64), 0, 1023)
+
+    def spread(v):
+        v = (v | (v << 16)) & 0x030000FF
+        v = (v | (v << 8)) & 0x0300F00F
+        v = (v | (v << 4)) & 0x030C30C3
+        return (v | (v << 2)) & 0x09249249
+
+    code = spread(q[:, 0]) | (spread(q[:, 1]) << 1) | (spread(q[:, 2]) << 2)
+    return np.argsort(code, kind="stable")
+
+
 class TriangleMesh:
     """Triangle soup with load-time removal of degenerate faces (meshes.py:85-141)."""
 
@@ -126,11 +142,18 @@ class TriangleMesh:
         return v[t[:, 0]], v[t[:, 1]], v[t[:, 2]]
 
     def device_corners(self):
-        """(T, 9) fp64 corner table on the GPU (a, b, c per row), cached."""
+        """(T, 9) fp64 corner table on the GPU (a, b, c per row), cached.
+
+        Rows are in Morton order of the triangle centroids, so each 128-row
+        tile of the build kernel covers a compact patch of the surface and its
+        box culls well; every per-cell result (a min and a crossing parity)
+        is independent of the triangle order.
+        """
         if self._dev is None:
             a, b, c = self.triangle_corners()
-            self._dev = N.to_device(np.ascontiguousarray(np.concatenate([a, b, c], axis=1)),
-                                    N.torch().float64)
+            table = np.concatenate([a, b, c], axis=1)
+            table = table[_morton_order((a + b + c) / 3.0)]
+            self._dev = N.to_device(np.ascontiguousarray(table), N.torch().float64)
         return self._dev
 
     def sample_surface(self, n: int, rng: np.random.Generator) -> np.ndarray:
