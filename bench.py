@@ -48,7 +48,15 @@ REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
 METRIC = "p50/p99 µs per 500-waypoint query; waypoint-queries/s at 1/2/4/8 B200"
-KERNELS_PER_STEP = 3  # fk_align, voxel_scatter (+rank prefix), query_shells; plus 2 memset nodes
+def _kernels_per_cycle(chk, N) -> int:
+    """Our kernel launches in one cycle: the library's launch counter around
+    one un-captured cycle (the graph replays exactly these launches)."""
+    import torch
+
+    before = int(N.lib().lsdf_launch_count())
+    chk._run(False)
+    torch.cuda.synchronize()
+    return int(N.lib().lsdf_launch_count()) - before
 
 
 def _peaks():
@@ -274,6 +282,10 @@ def run_ours(args, rank, world, dist, sampler):
     e2e_ms = _max_over_ranks(dist, torch, 1e3 * (time.perf_counter() - s0) / args.steps)
     del pipe
 
+    from paper_2309_12543_b200 import _native as N
+
+    per_cycle = _kernels_per_cycle(chk, N)
+
     # ---- roofline of the dominant kernel (query) timed alone on the staged batch
     stage(0)
     chk.launch(device_only=True)
@@ -304,7 +316,8 @@ def run_ours(args, rank, world, dist, sampler):
                    "parallelism": f"waypoint shards x{world}",
                    "l2": "flushed (256 MiB write) before every timed step",
                    "timing": "device: CUDA events around a graph replay of the cycle"},
-        "gpu_launches": KERNELS_PER_STEP * args.steps,
+        "gpu_launches": per_cycle * args.steps,
+        "gpu_launches_per_step": per_cycle,
         "e2e": _e2e_entry(C_total, e2e_ms, single_ms, int(n_local * robot.dof * 8 + shape.n_points * 12),
                           int(n_local * 12 + 16)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
