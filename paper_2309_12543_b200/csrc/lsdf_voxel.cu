@@ -54,12 +54,14 @@ __device__ void prefix_scan_block(const uint32_t* bitmap, int64_t n_words, int32
 }
 
 // floor((p + e) / r) exactly as numpy: correctly rounded quotient via
-// q0 = x * RN(1/r) plus one FMA residual step (Markstein), then floor.
-__device__ __forceinline__ int64_t voxel_coord(double p, double e, double r, double rinv) {
+// q0 = x * RN(1/r) plus one FMA residual step (Markstein), then floor
+// (q >= 0 here: the magic-number floor of floor_small, no conversion).
+__device__ __forceinline__ int voxel_floor(double p, double e, double r, double rinv) {
     const double x = __dadd_rn(p, e);
     const double q0 = __dmul_rn(x, rinv);
     const double q = __fma_rn(__fma_rn(-q0, r, x), rinv, q0);
-    return (int64_t)floor(q);
+    double fl;
+    return floor_small(q, fl);
 }
 
 // One thread per point.  With a small grid the CTA first merges its points
@@ -75,31 +77,38 @@ voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, do
         for (int64_t w = threadIdx.x; w < n_words; w += blockDim.x) s_bits[w] = 0u;
         __syncthreads();
     }
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool dropped = false;
-    if (i < N) {
-        const double x = (double)pts[3 * i], y = (double)pts[3 * i + 1], z = (double)pts[3 * i + 2];
-        const double ex = env.extent[0], ey = env.extent[1], ez = env.extent[2];
-        // query.py:112: keep -e <= p < e on every axis (NaN fails the test -> dropped)
-        const bool inside = (x >= -ex) && (x < ex) && (y >= -ey) && (y < ey) && (z >= -ez) && (z < ez);
-        if (inside) {
-            int64_t ix = voxel_coord(x, ex, env.resolution[0], rx);
-            int64_t iy = voxel_coord(y, ey, env.resolution[1], ry);
-            int64_t iz = voxel_coord(z, ez, env.resolution[2], rz);
-            ix = ix < 0 ? 0 : (ix > env.dims[0] - 1 ? env.dims[0] - 1 : ix);  // grids.py:111 clip
-            iy = iy < 0 ? 0 : (iy > env.dims[1] - 1 ? env.dims[1] - 1 : iy);
-            iz = iz < 0 ? 0 : (iz > env.dims[2] - 1 ? env.dims[2] - 1 : iz);
-            const int64_t lin = (ix * env.dims[1] + iy) * env.dims[2] + iz;
-            if (PRIVATE)
-                atomicOr(s_bits + (lin >> 5), 1u << (lin & 31));
-            else
-                atomicOr(bitmap + (lin >> 5), 1u << (lin & 31));
-        } else {
-            dropped = true;
+    // grid-stride: a persistent grid of a few CTAs per SM amortises the
+    // private bitmap's clear and merge over many points
+    int dropped_count = 0;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < N; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        bool dropped = false;
+        if (i < N) {
+            const double x = (double)pts[3 * i], y = (double)pts[3 * i + 1], z = (double)pts[3 * i + 2];
+            const double ex = env.extent[0], ey = env.extent[1], ez = env.extent[2];
+            // query.py:112: keep -e <= p < e on every axis (NaN fails the test -> dropped)
+            const bool inside = (x >= -ex) && (x < ex) && (y >= -ey) && (y < ey) && (z >= -ez) && (z < ez);
+            if (inside) {
+                // inside => 0 <= (p + e) / r, so the exact floor fits 32 bits
+                int ix = voxel_floor(x, ex, env.resolution[0], rx);
+                int iy = voxel_floor(y, ey, env.resolution[1], ry);
+                int iz = voxel_floor(z, ez, env.resolution[2], rz);
+                ix = ix > env.dims[0] - 1 ? env.dims[0] - 1 : ix;  // grids.py:111 clip
+                iy = iy > env.dims[1] - 1 ? env.dims[1] - 1 : iy;
+                iz = iz > env.dims[2] - 1 ? env.dims[2] - 1 : iz;
+                const uint32_t lin = ((uint32_t)ix * (uint32_t)env.dims[1] + (uint32_t)iy) * (uint32_t)env.dims[2] +
+                                     (uint32_t)iz;
+                if (PRIVATE)
+                    atomicOr(s_bits + (lin >> 5), 1u << (lin & 31));
+                else
+                    atomicOr(bitmap + (lin >> 5), 1u << (lin & 31));
+            } else {
+                dropped = true;
+            }
         }
+        dropped_count += __popc(__ballot_sync(FULL_MASK, dropped));
     }
-    const unsigned b = __ballot_sync(FULL_MASK, dropped);
-    if ((threadIdx.x & 31) == 0 && b) atomicAdd(&counters[1], __popc(b));
+    if ((threadIdx.x & 31) == 0 && dropped_count) atomicAdd(&counters[1], dropped_count);
     if (PRIVATE) {
         __syncthreads();
         for (int64_t w = threadIdx.x; w < n_words; w += blockDim.x) {
@@ -177,23 +186,28 @@ int scatter_bitmap(const void* points_dev, int32_t points_f32, int64_t N, const 
                    void* occupancy_dev, cudaStream_t s) {
     LSDF_TRY(check_cuda(cudaMemsetAsync(occupancy_dev, 0, 256 + o.n_words * 4, s), "voxelize memset"));
     if (N <= 0) return LSDF_OK;
-    const unsigned blocks = grid_for(N, SCATTER_THREADS);
     const double rx = 1.0 / env->resolution[0], ry = 1.0 / env->resolution[1], rz = 1.0 / env->resolution[2];
+    // CTA-private shared bitmaps (a dense blob costs one global atomic per
+    // touched word per CTA; measured: global atomics straight away, or
+    // smaller CTAs, are slower even at 100k points), grid-stride over at most
+    // two CTAs per SM so large clouds amortise the clear and merge
     const bool priv = o.n_words <= PRIVATE_WORDS_MAX;
+    const unsigned threads = SCATTER_THREADS;
+    const unsigned blocks = grid_for(N, threads) < 148u * 2u ? grid_for(N, threads) : 148u * 2u;
     const size_t smem = priv ? (size_t)o.n_words * 4 : 0;
     if (points_f32) {
         if (priv)
-            voxel_scatter_kernel<float, true><<<blocks, SCATTER_THREADS, smem, s>>>(
+            voxel_scatter_kernel<float, true><<<blocks, threads, smem, s>>>(
                 (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
         else
-            voxel_scatter_kernel<float, false><<<blocks, SCATTER_THREADS, 0, s>>>(
+            voxel_scatter_kernel<float, false><<<blocks, threads, 0, s>>>(
                 (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
     } else {
         if (priv)
-            voxel_scatter_kernel<double, true><<<blocks, SCATTER_THREADS, smem, s>>>(
+            voxel_scatter_kernel<double, true><<<blocks, threads, smem, s>>>(
                 (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
         else
-            voxel_scatter_kernel<double, false><<<blocks, SCATTER_THREADS, 0, s>>>(
+            voxel_scatter_kernel<double, false><<<blocks, threads, 0, s>>>(
                 (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
     }
     return check_launch("voxel_scatter_kernel");
