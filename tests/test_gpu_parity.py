@@ -616,3 +616,33 @@ def test_training_matches_reference(L):
         L.train_approximator(g["points"], L.TrainingConfig(steps=100, eval_every=100, screen_size=64, val_size=128,
                                                            target_max_error=0.01, seed=3))
 
+
+def test_unstaged_shell_paths(L):
+    """A fine environment grid (100^3: the occupancy bitmap does not fit the
+    shared-memory stage) and a wide window (W = 32: 17k kept cells, the shell
+    list is read from L2): direct == dense gather bit for bit, and the
+    oracle on a subset."""
+    from oracle import linksdf_oracle as O
+    from paper_2309_12543_b200 import scenarios as S
+
+    doc = S.ARM6G
+    robot = L.RobotModel.from_dict(doc)
+    grid = L.EnvGrid(1.0, 0.02)
+    e_r, r_r = 0.32, 0.02
+    sdfs = [L.build_link_sdf(robot.links[i].geometry, e_r, r_r, link_id=i) for i in robot.geometry_links]
+    window = L.WindowGeometry.build(e_r, grid)
+    assert window.n_masked > 4096
+    q = S.random_configs(doc, 64, seed=8)
+    pts = S.human_cloud(20_000, seed=8)
+    traj = L.TrajectorySdf.from_configs(robot, q, sdfs, grid, window)
+    obs = L.voxelize_pointcloud(pts, grid)
+    d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
+    dense = L.RobotSdfBatch(traj.device_values(), grid, traj.d_far_global)
+    d2, _, v2 = L.query_min_distances(dense, obs, return_argmin=True)
+    assert np.array_equal(d, d2) and np.array_equal(voxel, v2)
+    sub = np.arange(0, 64, 8)
+    grids = [s.values for s in sdfs]
+    rd, rl, rv = O.run_pipeline(doc, q[sub], pts, 1.0, 0.02, e_r, grids, [r_r] * len(grids))
+    assert np.abs(d[sub].astype(np.float64) - rd).max() <= D_TOL
+    assert np.array_equal(link[sub], rl) and np.array_equal(voxel[sub], rv)
+
