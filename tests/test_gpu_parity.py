@@ -518,6 +518,41 @@ def test_direct_equals_dense_on_adversarial_grids(L, seed):
             assert np.all(pl[c, : link[c]] > d[c]) or voxel[c] >= 0
 
 
+def test_segment_bound_exact_on_noisy_grids(L):
+    """Throughput-sized batch (segment bound active) on capsule-like grids
+    with noise (the bound's kappas come from the values): direct == dense
+    gather, and == the same waypoints in small chunks (bound inactive)."""
+    rng = np.random.default_rng(11)
+    grid = L.EnvGrid(1.0, 0.05)
+    e_r, r_r = 0.3, 0.02
+    window = L.WindowGeometry.build(e_r, grid)
+    ax = -e_r + (np.arange(30) + 0.5) * r_r
+    X, Y, Z = np.meshgrid(ax, ax, ax, indexing="ij")
+    sdfs = []
+    for li, (r, hl) in enumerate(((0.06, 0.08), (0.04, 0.0), (0.05, 0.05))):
+        t = np.clip(Z, -hl, hl)
+        v = np.sqrt(X * X + Y * Y + (Z - t) ** 2) - r + rng.normal(0.0, 0.004, size=X.shape)
+        if li == 2:
+            v = np.round(v * 64) / 64  # exact ties
+        sdfs.append(L.LinkSdf(e_r, r_r, v.astype(np.float32), li))
+    C = 13_000  # 39,000 tasks: above the segment-bound threshold
+    R = L.sample_rotations(rng, C * 3).reshape(C, 3, 3, 3)
+    T = rng.uniform(-0.6, 0.6, size=(C, 3, 3))
+    poses = L.LinkPoseBatch(R, T)
+    prov = L.ExactTransformProvider(window)
+    traj = L.TrajectorySdf.from_poses(sdfs, poses, grid, prov)
+    obs = L.voxelize_pointcloud(rng.uniform(-1, 1, size=(20_000, 3)), grid)
+    d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
+    dense = L.RobotSdfBatch(traj.device_values(), grid, traj.d_far_global)
+    d2, _, v2 = L.query_min_distances(dense, obs, return_argmin=True)
+    assert np.array_equal(d, d2) and np.array_equal(voxel, v2)
+    for a in range(0, C, 2600):
+        part = L.TrajectorySdf.from_poses(sdfs, L.LinkPoseBatch(R[a:a + 2600], T[a:a + 2600]), grid, prov)
+        dc, lc, vc = L.query_min_distances(part, obs, return_argmin=True)
+        assert np.array_equal(dc, d[a:a + 2600]) and np.array_equal(lc, link[a:a + 2600])
+        assert np.array_equal(vc, voxel[a:a + 2600])
+
+
 def test_mlp_tensor_cores(L):
     """tcgen05 kind::tf32 (3xTF32) layer 2 vs the reference prediction and the CUDA-core kernel."""
     import torch
