@@ -211,7 +211,7 @@ int lsdf_voxel_index(const double* points_dev, int64_t N, const lsdf_env_grid* e
  * (query.py:153-176).  by_position != 0 selects the general (unsorted list)
  * tie rule; set it when the occupancy came from an unsorted index list.
  * workspace_dev: lsdf_query_workspace_bytes(C, n_geo) bytes, zeroed once at
- * allocation; every launch leaves it zeroed again (the last warp of each
+ * allocation; every launch leaves it zeroed again (the finalize pass of each
  * configuration resets its slots), so graph replays need no memset. */
 int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_dev,
                       const int32_t* anchor_geo_dev, int64_t C, int32_t n_geo,

@@ -4,21 +4,25 @@
 // links of each link's resampled window, clamped at d_far_global;
 // placement.py:267-313, query.py:61-103) and gathers it at the occupied
 // voxels (query.py:128-150).  Only the occupied voxels inside a link's
-// sphere-masked window can differ from the clamp, so this kernel evaluates
-// exactly those: for each (c, l) it walks the window's (x, y) columns, takes
-// the column's kept z-interval from the occupancy bitmap, and for every
-// occupied cell recomputes the reference's resampled value
+// sphere-masked window can differ from the clamp, so the query evaluates
+// exactly those, recomputing for every occupied cell the reference's
+// resampled value
 //   g = P R + dt_inv (fp64, placement.py:164-167), point = g * e_r,
 //   trilinear_sample(sdf_l, point) (grids.py:155-191),
 // bit-identical to the assembled field.  Keys (value, rank, link) reduce with
-// a warp shuffle and one 64-bit atomic per warp; the last warp of a
-// configuration finishes (d, link, voxel) and resets the workspace.
+// a warp shuffle and one 64-bit atomic per task into a per-configuration
+// slot; finalize_kernel turns the slots into (d, link, voxel) and re-zeroes
+// them (graph replays need no memset).
 //
-// Work decomposition: one warp = one task (link l, configuration c, column
-// slice s).  Tasks are link-major, so the SMs sweep one link grid at a time
-// (its packed-corner copy stays hot in L2/L1); warps are independent (no
-// block barrier), `split` slices per (c, l) keep >= 148 x 64 warps in flight
-// for small batches.
+// query_shells_kernel (the hot path): one warp = one task (link l,
+// configuration c, slice s), persistent CTAs with dynamic task fetch; the
+// window's kept cells are visited in order of distance from the window
+// centre and the scan stops as soon as no remaining cell can reach the
+// running minimum (core radius of the link grid), optionally gated per cell
+// by the link's segment bound.
+// query_direct_kernel (fallback when a link's far value is below the clamp or
+// the mask has no column intervals): walks the window's (x, y) columns over
+// the kept z-interval of each, with `split` column slices per (c, l).
 #include "lsdf_device.cuh"
 
 using namespace lsdf;
