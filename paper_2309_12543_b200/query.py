@@ -427,14 +427,15 @@ def query_trajectory(robot, configs, sdfs, grid: EnvGrid, provider_or_window, po
 
 @dataclass(frozen=True, eq=False)
 class SphereRobotModel:
-    """Per-link covering spheres in link frames (query.py:179-212)."""
+    """Per-link covering spheres in link frames (query.py:179-212), flattened:
+    sphere k belongs to link ``link_indices[k]``."""
 
     link_indices: np.ndarray
     centers: np.ndarray
     radii: np.ndarray
 
     def __post_init__(self):
-        if np.any(self.radii <= 0):
+        if (np.asarray(self.radii) <= 0).any():
             raise ValidationError("sphere radii must be positive")
 
     @property
@@ -443,35 +444,31 @@ class SphereRobotModel:
 
     @classmethod
     def from_robot(cls, model) -> "SphereRobotModel":
-        li, ce, ra = [], [], []
-        for link_name, spheres in model.sphere_model.items():
-            idx = model.link_index(link_name)
-            for center, radius in spheres:
-                li.append(idx)
-                ce.append(center)
-                ra.append(radius)
-        if not ra:
+        """Flatten the robot JSON's ``spheres`` section, link by link in its order."""
+        flat = [(model.link_index(name), c, r) for name, entries in model.sphere_model.items() for c, r in entries]
+        if not flat:
             raise ValidationError(f"robot {model.name} declares no spheres")
-        return cls(link_indices=np.int64(li), centers=np.float64(ce), radii=np.float64(ra))
+        idx, centers, radii = zip(*flat)
+        return cls(link_indices=np.int64(idx), centers=np.float64(centers), radii=np.float64(radii))
 
 
 def validate_sphere_model(model, spheres: SphereRobotModel, rng: np.random.Generator, n_samples: int = 2048,
                           tol: float = 1e-9) -> float:
-    """Check the spheres cover each link's surface samples (query.py:215-251); host-side validation."""
+    """Worst excess of a link's surface samples over its covering spheres
+    (query.py:215-251); host-side, consumes ``rng`` like the reference
+    (links in order, n_samples per link).  Raises past ``tol``."""
     worst = -np.inf
     for li, link in enumerate(model.links):
-        if link.geometry is None:
+        geom = link.geometry
+        if geom is None:
             continue
-        mine = spheres.link_indices == li
-        if not np.any(mine):
+        own = np.flatnonzero(spheres.link_indices == li)
+        if own.size == 0:
             raise ValidationError(f"link {link.name} has geometry but no spheres")
-        if isinstance(link.geometry, TriangleMesh):
-            surface = link.geometry.sample_surface(n_samples, rng)
-        else:
-            surface = primitive_surface_points(link.geometry, n_samples, rng)
-        d = (np.linalg.norm(surface[:, None, :] - spheres.centers[None, mine], axis=-1)
-             - spheres.radii[mine]).min(axis=1)
-        worst = max(worst, float(d.max()))
+        samples = (geom.sample_surface(n_samples, rng) if isinstance(geom, TriangleMesh)
+                   else primitive_surface_points(geom, n_samples, rng))
+        gaps = np.linalg.norm(samples[:, None, :] - spheres.centers[own][None], axis=-1) - spheres.radii[own]
+        worst = max(worst, float(gaps.min(axis=1).max()))
         if worst > tol:
             raise ValidationError(f"link {link.name}: surface escapes the covering spheres by {worst:.2e} m")
     return worst
@@ -506,43 +503,41 @@ def sphere_baseline_distances(spheres: SphereRobotModel, poses, obstacles: Obsta
 # =========================================================================== frame IO (host plumbing)
 
 
+_FRAME_COUNT = struct.Struct("<I")
+
+
 def write_pointcloud_frame(path, points) -> None:
-    """Count-prefixed little-endian f32 xyz triples."""
-    pts = np.asarray(points, dtype=np.float32).reshape(-1, 3)
-    with open(path, "wb") as fh:
-        fh.write(struct.pack("<I", len(pts)))
-        fh.write(np.ascontiguousarray(pts, dtype="<f4").tobytes())
+    """Frame file (query.py:313-318): uint32 point count, then xyz as little-endian f32."""
+    pts = np.ascontiguousarray(np.asarray(points, dtype="<f4").reshape(-1, 3))
+    Path(path).write_bytes(_FRAME_COUNT.pack(len(pts)) + pts.tobytes())
 
 
 def read_pointcloud_frame(path) -> np.ndarray:
-    with open(path, "rb") as fh:
-        (count,) = struct.unpack("<I", fh.read(4))
-        raw = np.frombuffer(fh.read(12 * count), dtype="<f4")
-        if raw.size != 3 * count:
-            raise ValidationError(f"{path}: truncated point data")
-    return raw.reshape(count, 3).astype(np.float64)
+    """(N, 3) f64 points of a frame file; ValidationError when the data is short."""
+    data = Path(path).read_bytes()
+    (count,) = _FRAME_COUNT.unpack_from(data)
+    avail = (len(data) - _FRAME_COUNT.size) // 4
+    if avail < 3 * count:
+        raise ValidationError(f"{path}: truncated point data")
+    return np.frombuffer(data, dtype="<f4", count=3 * count, offset=_FRAME_COUNT.size).reshape(count, 3) \
+        .astype(np.float64)
 
 
 def read_cloud_manifest(path) -> list[tuple[float, Path]]:
+    """Manifest: one ``<timestamp_ms> <frame file>`` per line, paths relative to
+    the manifest; blank lines and ``#`` comments skipped (query.py:330-341)."""
     base = Path(path).parent
-    frames = []
-    with open(path) as fh:
-        for line in fh:
-            line = line.strip()
-            if not line or line.startswith("#"):
-                continue
-            stamp, name = line.split(maxsplit=1)
-            frames.append((float(stamp), base / name))
-    return frames
+    entries = (ln.strip() for ln in Path(path).read_text().splitlines())
+    pairs = (ln.split(maxsplit=1) for ln in entries if ln and not ln.startswith("#"))
+    return [(float(stamp), base / name) for stamp, name in pairs]
 
 
 def iter_cloud_frames(manifest_path) -> Iterator[tuple[float, np.ndarray]]:
-    for stamp, frame_path in read_cloud_manifest(manifest_path):
-        yield stamp, read_pointcloud_frame(frame_path)
+    return ((stamp, read_pointcloud_frame(p)) for stamp, p in read_cloud_manifest(manifest_path))
 
 
 def write_distance_csv(path, rows, n_configs: int) -> None:
-    with open(path, "w") as fh:
-        fh.write(",".join(["timestamp_ms"] + [f"d_{i}" for i in range(n_configs)]) + "\n")
-        for stamp, dists in rows:
-            fh.write(f"{stamp:.3f}," + ",".join(f"{d:.6f}" for d in dists) + "\n")
+    """timestamp_ms,d_0..d_{C-1} header, one row per cycle (%.3f stamp, %.6f distances)."""
+    lines = [",".join(["timestamp_ms", *(f"d_{i}" for i in range(n_configs))])]
+    lines += [",".join([f"{stamp:.3f}", *(f"{d:.6f}" for d in dists)]) for stamp, dists in rows]
+    Path(path).write_text("".join(line + "\n" for line in lines))
