@@ -22,13 +22,19 @@ from .errors import NonWatertightError, ValidationError
 log = logging.getLogger(__name__)
 
 
+def _vec(v) -> np.ndarray:
+    return np.asarray(v, dtype=np.float64)
+
+
 @dataclass(frozen=True, eq=False)
 class Sphere:
+    """Ball of ``radius`` about ``center`` (link frame)."""
+
     radius: float
     center: np.ndarray = field(default_factory=lambda: np.zeros(3))
 
     def __post_init__(self):
-        object.__setattr__(self, "center", np.asarray(self.center, dtype=np.float64))
+        object.__setattr__(self, "center", _vec(self.center))
 
 
 @dataclass(frozen=True, eq=False)
@@ -40,19 +46,21 @@ class Capsule:
     axis: np.ndarray = field(default_factory=lambda: np.float64([0.0, 0.0, 1.0]))
 
     def __post_init__(self):
-        axis = np.asarray(self.axis, dtype=np.float64)
-        n = np.linalg.norm(axis)
-        if n == 0:
+        direction = _vec(self.axis)
+        length = np.linalg.norm(direction)
+        if not length:
             raise ValidationError("capsule axis must be nonzero")
-        object.__setattr__(self, "axis", axis / n)
+        object.__setattr__(self, "axis", direction / length)
 
 
 @dataclass(frozen=True, eq=False)
 class Box:
+    """Axis-aligned box of the given half extents about the link origin."""
+
     half_extents: np.ndarray
 
     def __post_init__(self):
-        object.__setattr__(self, "half_extents", np.asarray(self.half_extents, dtype=np.float64))
+        object.__setattr__(self, "half_extents", _vec(self.half_extents))
 
 
 Primitive = Sphere | Capsule | Box
@@ -105,36 +113,37 @@ def _morton_order(points: np.ndarray) -> np.ndarray:
 
 
 class TriangleMesh:
-    """Triangle soup with load-time removal of degenerate faces (meshes.py:85-141)."""
+    """Indexed triangle soup (meshes.py:85-141); zero-area faces are dropped
+    (with a warning) when the mesh is built."""
 
     def __init__(self, vertices, triangles):
-        vertices = np.asarray(vertices, dtype=np.float64).reshape(-1, 3)
-        triangles = np.asarray(triangles, dtype=np.int64).reshape(-1, 3)
-        if triangles.size and (triangles.min() < 0 or triangles.max() >= len(vertices)):
+        v = np.asarray(vertices, dtype=np.float64).reshape(-1, 3)
+        f = np.asarray(triangles, dtype=np.int64).reshape(-1, 3)
+        if f.size and not (0 <= f.min() and f.max() < len(v)):
             raise ValidationError("triangle indices out of range")
-        a, b, c = vertices[triangles[:, 0]], vertices[triangles[:, 1]], vertices[triangles[:, 2]]
-        keep = np.linalg.norm(np.cross(b - a, c - a), axis=-1) > 1e-14
-        dropped = int((~keep).sum())
-        if dropped:
-            log.warning("dropped %d degenerate triangle(s)", dropped)
-            triangles = triangles[keep]
-        if len(triangles) == 0:
+        corners = v[f]  # (T, 3 corners, 3)
+        twice_area = np.linalg.norm(np.cross(corners[:, 1] - corners[:, 0], corners[:, 2] - corners[:, 0]), axis=-1)
+        degenerate = twice_area <= 1e-14
+        if degenerate.any():
+            log.warning("dropped %d degenerate triangle(s)", int(degenerate.sum()))
+            f = f[~degenerate]
+        if not len(f):
             raise ValidationError("mesh has no non-degenerate triangles")
-        self.vertices = vertices
-        self.triangles = triangles
-        self.vertices.flags.writeable = False
-        self.triangles.flags.writeable = False
+        v.flags.writeable = False
+        f.flags.writeable = False
+        self.vertices, self.triangles = v, f
         self._watertight = None
         self._dev = None
 
     @property
     def is_watertight(self) -> bool:
-        """Every undirected edge is shared by exactly two triangles."""
+        """Closed 2-manifold test: each undirected edge belongs to exactly two faces."""
         if self._watertight is None:
-            t = self.triangles
-            edges = np.sort(np.concatenate([t[:, [0, 1]], t[:, [1, 2]], t[:, [2, 0]]]), axis=1)
-            _, counts = np.unique(edges, axis=0, return_counts=True)
-            self._watertight = bool(np.all(counts == 2))
+            f = self.triangles
+            ends = np.sort(np.stack([f, np.roll(f, -1, axis=1)], axis=-1).reshape(-1, 2), axis=1)
+            key = ends[:, 0] * (int(f.max()) + 1) + ends[:, 1]
+            _, uses = np.unique(key, return_counts=True)
+            self._watertight = bool((uses == 2).all())
         return self._watertight
 
     def triangle_corners(self):
@@ -157,15 +166,15 @@ class TriangleMesh:
         return self._dev
 
     def sample_surface(self, n: int, rng: np.random.Generator) -> np.ndarray:
+        """n area-weighted surface points; draws from ``rng`` in the reference's
+        order (face choice, then u, then v; folded barycentrics)."""
         a, b, c = self.triangle_corners()
-        areas = 0.5 * np.linalg.norm(np.cross(b - a, c - a), axis=-1)
-        which = rng.choice(len(areas), size=n, p=areas / areas.sum())
-        u = rng.random(n)
-        v = rng.random(n)
-        flip = u + v > 1.0
-        u[flip] = 1.0 - u[flip]
-        v[flip] = 1.0 - v[flip]
-        return a[which] + u[:, None] * (b[which] - a[which]) + v[:, None] * (c[which] - a[which])
+        weight = np.linalg.norm(np.cross(b - a, c - a), axis=-1) * 0.5
+        face = rng.choice(len(weight), size=n, p=weight / weight.sum())
+        uv = np.stack([rng.random(n), rng.random(n)], axis=1)
+        outside = uv.sum(axis=1) > 1.0
+        uv[outside] = 1.0 - uv[outside]
+        return a[face] + uv[:, :1] * (b[face] - a[face]) + uv[:, 1:] * (c[face] - a[face])
 
 
 def exact_point_distance(mesh: TriangleMesh, points, signed: bool = True) -> np.ndarray:
@@ -276,34 +285,32 @@ def primitive_surface_points(shape, n: int, rng: np.random.Generator):
 
 
 def load_stl(path) -> TriangleMesh:
-    with open(path, "rb") as fh:
-        data = fh.read()
-    if data[:5] == b"solid" and b"facet" in data[:2048]:
-        coords = [[float(x) for x in ln.split()[1:]] for ln in data.decode("ascii", "replace").splitlines()
-                  if len(ln.split()) == 4 and ln.split()[0] == "vertex"]
-        return _from_soup(np.float64(coords).reshape(-1, 3, 3))
+    """STL, ASCII ("solid ... facet ... vertex x y z") or binary (80-byte
+    header, uint32 count, 50-byte facets); vertices deduplicated."""
+    data = open(path, "rb").read()
+    if data.startswith(b"solid") and b"facet" in data[:2048]:
+        words = (ln.split() for ln in data.decode("ascii", "replace").splitlines())
+        xyz = [[float(t) for t in w[1:]] for w in words if len(w) == 4 and w[0] == "vertex"]
+        return _from_soup(np.float64(xyz).reshape(-1, 3, 3))
     if len(data) < 84:
         raise ValidationError(f"{path}: truncated STL")
-    (count,) = struct.unpack_from("<I", data, 80)
-    if len(data) < 84 + 50 * count:
+    n = int.from_bytes(data[80:84], "little")
+    if len(data) < 84 + 50 * n:
         raise ValidationError(f"{path}: STL facet data truncated")
-    raw = np.frombuffer(data, dtype=np.uint8, count=50 * count, offset=84).reshape(count, 50)
-    return _from_soup(raw[:, 12:48].copy().view("<f4").reshape(count, 3, 3).astype(np.float64))
+    facets = np.frombuffer(data, dtype=np.uint8, count=50 * n, offset=84).reshape(n, 50)
+    return _from_soup(facets[:, 12:48].copy().view("<f4").reshape(n, 3, 3).astype(np.float64))
 
 
 def load_obj(path) -> TriangleMesh:
-    vertices, faces = [], []
-    with open(path) as fh:
-        for line in fh:
-            parts = line.split()
-            if not parts:
-                continue
-            if parts[0] == "v":
-                vertices.append([float(x) for x in parts[1:4]])
-            elif parts[0] == "f":
-                idx = [int(p.split("/")[0]) - 1 for p in parts[1:]]
-                faces += [(idx[0], idx[i], idx[i + 1]) for i in range(1, len(idx) - 1)]
-    return TriangleMesh(np.float64(vertices), np.int64(faces))
+    """OBJ 'v' and 'f' records; polygons are fan-triangulated, 'v/t/n' indices accepted."""
+    verts, faces = [], []
+    for words in (ln.split() for ln in open(path)):
+        if words[:1] == ["v"]:
+            verts.append([float(t) for t in words[1:4]])
+        elif words[:1] == ["f"]:
+            ring = [int(t.split("/")[0]) - 1 for t in words[1:]]
+            faces.extend(zip([ring[0]] * (len(ring) - 2), ring[1:-1], ring[2:]))
+    return TriangleMesh(np.float64(verts), np.int64(faces))
 
 
 def load_mesh(path) -> TriangleMesh:
