@@ -261,27 +261,29 @@ def make_icosphere(radius: float, subdivisions: int = 1) -> TriangleMesh:
     return TriangleMesh(np.float64(verts) * radius, np.int64(faces))
 
 
+def _unit_normals(rng: np.random.Generator, n: int) -> np.ndarray:
+    d = rng.normal(size=(n, 3))
+    return d / np.linalg.norm(d, axis=-1, keepdims=True)
+
+
 def primitive_surface_points(shape, n: int, rng: np.random.Generator):
-    """Random points on a primitive's surface (coverage validation)."""
-    if isinstance(shape, Sphere):
-        d = rng.normal(size=(n, 3))
-        d /= np.linalg.norm(d, axis=-1, keepdims=True)
-        return shape.center + shape.radius * d
-    if isinstance(shape, Capsule):
-        d = rng.normal(size=(n, 3))
-        d /= np.linalg.norm(d, axis=-1, keepdims=True)
-        t = rng.uniform(-shape.half_length, shape.half_length, size=n)
-        axial = d @ shape.axis
-        radial = d - axial[:, None] * shape.axis
-        on_cap = rng.random(n) < (2 * shape.radius / (2 * shape.radius + 2 * shape.half_length))
-        return np.where(
-            on_cap[:, None],
-            np.sign(axial)[:, None] * shape.half_length * shape.axis + shape.radius * d,
-            t[:, None] * shape.axis
-            + shape.radius * radial / np.maximum(np.linalg.norm(radial, axis=-1, keepdims=True), 1e-12))
+    """Random points on a primitive's surface (sphere-model validation); the
+    draws from ``rng`` follow the reference (meshes.py:108-141)."""
     if isinstance(shape, Box):
         return make_box_mesh(shape.half_extents).sample_surface(n, rng)
-    raise ValidationError(f"unknown primitive {type(shape).__name__}")
+    if not isinstance(shape, (Sphere, Capsule)):
+        raise ValidationError(f"unknown primitive {type(shape).__name__}")
+    d = _unit_normals(rng, n)
+    if isinstance(shape, Sphere):
+        return shape.center + shape.radius * d
+    r, h, k = shape.radius, shape.half_length, shape.axis
+    t = rng.uniform(-h, h, size=n)
+    along = d @ k
+    across = d - along[:, None] * k
+    cap = (rng.random(n) < (2 * r / (2 * r + 2 * h)))[:, None]
+    on_caps = np.sign(along)[:, None] * h * k + r * d
+    on_side = t[:, None] * k + r * across / np.maximum(np.linalg.norm(across, axis=-1, keepdims=True), 1e-12)
+    return np.where(cap, on_caps, on_side)
 
 
 def load_stl(path) -> TriangleMesh:
