@@ -261,6 +261,30 @@ int lsdf_place_windows_g(const float* g_dev, int64_t ldg, const int32_t* kept_ce
                          int32_t n_geo, const lsdf_link_grid* grids, const lsdf_window* window,
                          float* windows_dev, void* stream);
 
+/* The paper's materialized mode, voxel-major: the
+ * assembled robot SDF of a fixed trajectory as field (V, C) f32 — voxel v's
+ * C values contiguous (v = C-order (ix*ny+iy)*nz+iz), f32(d_far_global) where
+ * no window reaches (placement.py:267-313 + query.py:61-103, exact). */
+int lsdf_materialize_vm(const double* R_geo_dev, const double* dt_geo_dev,
+                        const int32_t* anchor_geo_dev, int64_t C, int32_t n_geo,
+                        const lsdf_link_grid* grids, const lsdf_window* window,
+                        const lsdf_env_grid* env, double d_far_global, float* field_dev,
+                        void* stream);
+
+/* One cycle against a materialized field: d, voxel (position in the obstacle
+ * list, first occurrence) and link (the lowest link whose window value at
+ * that voxel equals d, exact lookups) — query_min_distances (query.py:128-150)
+ * with the Appendix-B argmin and the clamp rule.  indices_dev (n, 3) i32: the
+ * obstacle list; n_list >= 0 its length, or -1 to take the occupied count of
+ * occupancy_dev (the sorted list lsdf_voxelize writes).  workspace_dev: C x 8
+ * bytes, zeroed once (left zeroed). */
+int lsdf_query_vm(const float* field_dev, const double* R_geo_dev, const double* dt_geo_dev,
+                  const int32_t* anchor_geo_dev, int64_t C, int32_t n_geo,
+                  const lsdf_link_grid* grids, const lsdf_window* window,
+                  const lsdf_env_grid* env, const void* occupancy_dev, const int32_t* indices_dev,
+                  int64_t n_list, double d_far_global, void* workspace_dev, float* d_dev,
+                  int32_t* link_dev, int32_t* voxel_dev, void* stream);
+
 /* assemble_robot_sdfs (query.py:61-103) from n_fields windows
  * (n_fields, W^3) with anchors (n_fields, 3) i32 and config ids (n_fields) i32:
  * values (C, nx, ny, nz) f32 C-order, initialised to float32(d_far_global). */

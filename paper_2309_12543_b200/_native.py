@@ -75,6 +75,10 @@ _SIGS = {
                           C.POINTER(EnvGridT), _P, _I32, _D, _P, _P, _P, _P, _P, _P],
     "lsdf_query_workspace_bytes": [_I64, _I32],
     "lsdf_pack_corners": [_P, C.POINTER(_I32), _P, _P],
+    "lsdf_materialize_vm": [_P, _P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT),
+                            C.POINTER(EnvGridT), _D, _P, _P],
+    "lsdf_query_vm": [_P, _P, _P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT), C.POINTER(EnvGridT),
+                      _P, _P, _I64, _D, _P, _P, _P, _P, _P],
     "lsdf_place_windows": [_P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT), _P, _P],
     "lsdf_place_windows_g": [_P, _I64, _P, _I32, _P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT), _P,
                              _P],

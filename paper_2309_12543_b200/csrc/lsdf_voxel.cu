@@ -5,7 +5,7 @@
 //   and ORs the touched words into the global one.
 // prefix_only_kernel: the exclusive popcount prefix per word: rank(voxel) =
 //   prefix[w] + popc(word & below) is its position in np.unique(axis=0) order.
-// voxel_compact_kernel: optional, one thread per word, writes the sorted
+// voxel_compact_kernel: optional, one thread per voxel, writes the sorted
 //   index list (the ObstacleVoxelSet.indices the API returns) and posgrid.
 #include <cub/block/block_scan.cuh>
 
@@ -123,24 +123,22 @@ __global__ void __launch_bounds__(SCAN_THREADS) prefix_only_kernel(const uint32_
     prefix_scan_block(bitmap, n_words, prefix, counters);
 }
 
+// one thread per voxel (bit): an occupied voxel's rank is prefix[w] +
+// popc(word & below), so every write is independent (no per-word loop)
 __global__ void voxel_compact_kernel(const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ prefix,
                                      int64_t n_words, lsdf_env_grid env, int32_t* posgrid, int32_t* indices) {
-    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= n_words) return;
-    uint32_t bits = bitmap[w];
-    int rank = prefix[w];
-    const int64_t nyz = (int64_t)env.dims[1] * env.dims[2];
-    while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const int64_t lin = w * 32 + b;
-        posgrid[lin] = rank;
-        if (indices != nullptr) {
-            indices[3 * (int64_t)rank] = (int32_t)(lin / nyz);
-            indices[3 * (int64_t)rank + 1] = (int32_t)((lin / env.dims[2]) % env.dims[1]);
-            indices[3 * (int64_t)rank + 2] = (int32_t)(lin % env.dims[2]);
-        }
-        ++rank;
+    const int64_t lin = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (lin >= n_words * 32) return;
+    const uint32_t word = __ldg(bitmap + (lin >> 5));
+    const uint32_t bit = 1u << (lin & 31);
+    if (!(word & bit)) return;
+    const int rank = __ldg(prefix + (lin >> 5)) + __popc(word & (bit - 1u));
+    posgrid[lin] = rank;
+    if (indices != nullptr) {
+        const int64_t nyz = (int64_t)env.dims[1] * env.dims[2];
+        indices[3 * (int64_t)rank] = (int32_t)(lin / nyz);
+        indices[3 * (int64_t)rank + 1] = (int32_t)((lin / env.dims[2]) % env.dims[1]);
+        indices[3 * (int64_t)rank + 2] = (int32_t)(lin % env.dims[2]);
     }
 }
 
@@ -223,7 +221,7 @@ extern "C" int lsdf_voxelize(const void* points_dev, int32_t points_f32, int64_t
     prefix_only_kernel<<<1, SCAN_THREADS, 0, s>>>(o.bitmap, o.n_words, o.prefix, o.counters);
     LSDF_TRY(check_launch("prefix_only_kernel"));
     if (indices_dev == nullptr) return LSDF_OK;  // hot path: the query only needs bitmap + prefix
-    voxel_compact_kernel<<<grid_for(o.n_words, 256), 256, 0, s>>>(o.bitmap, o.prefix, o.n_words, *env, o.posgrid,
+    voxel_compact_kernel<<<grid_for(o.n_words * 32, 256), 256, 0, s>>>(o.bitmap, o.prefix, o.n_words, *env, o.posgrid,
                                                                     indices_dev);
     return check_launch("voxel_compact_kernel");
 }

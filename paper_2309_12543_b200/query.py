@@ -305,6 +305,64 @@ class TrajectorySdf:
         return self.query_device(occ, by_pos, per_link=True)["per_link"].cpu().numpy()
 
 
+class VoxelMajorSdf:
+    """The paper's materialized mode: the assembled
+    robot SDF of one fixed trajectory, prepared once on the GPU as a
+    voxel-major (V, C) f32 field, so that each control cycle is one coalesced
+    gather (``lsdf_query_vm``) instead of a window scan.  RobotSdfBatch-like:
+    ``grid``, ``n_configs``, ``d_far_global`` and a lazily transposed ``values``.
+    """
+
+    def __init__(self, traj: TrajectorySdf):
+        t = N.torch()
+        self.traj = traj
+        self.grid = traj.grid
+        self.d_far_global = traj.d_far_global
+        C_ = traj.n_configs
+        self.field = N.empty((self.grid.n_voxels, C_), t.float32)
+        ws, _ = traj.window.device_tables()
+        N.call("lsdf_materialize_vm", N.ptr(traj.R), N.ptr(traj.dt), N.ptr(traj.anchor), C_, traj.n_links,
+               traj._table, ctypes.byref(ws), ctypes.byref(self.grid.c_struct()), self.d_far_global,
+               self.field, N.stream())
+        self._keys = N.zeros((C_,), t.int64)  # the kernels leave it zeroed
+
+    @property
+    def n_configs(self) -> int:
+        return self.traj.n_configs
+
+    @property
+    def values(self) -> np.ndarray:
+        """(C, nx, ny, nz) like RobotSdfBatch.values (a transposed host copy)."""
+        v = self.field.T.contiguous().cpu().numpy().reshape((self.n_configs,) + tuple(int(d) for d in self.grid.dims))
+        v.flags.writeable = False
+        return v
+
+    def query_device(self, occupancy, indices_dev, n_list: int, outputs=None):
+        """Enqueue one cycle: (d, link, voxel) CUDA tensors; n_list < 0 reads the
+        occupied count from ``occupancy`` (a voxelized cloud's sorted list)."""
+        t = N.torch()
+        C_ = self.n_configs
+        out = outputs if outputs is not None else {}
+        if "d" not in out:
+            out["d"] = N.empty((C_,), t.float32)
+            out["link"] = N.empty((C_,), t.int32)
+            out["voxel"] = N.empty((C_,), t.int32)
+        tr = self.traj
+        ws, _ = tr.window.device_tables()
+        N.call("lsdf_query_vm", self.field, N.ptr(tr.R), N.ptr(tr.dt), N.ptr(tr.anchor), C_, tr.n_links, tr._table,
+               ctypes.byref(ws), ctypes.byref(self.grid.c_struct()), N.ptr(occupancy), N.ptr(indices_dev), int(n_list),
+               self.d_far_global, self._keys, out["d"], out["link"], out["voxel"], N.stream())
+        return out
+
+
+def _materialize(self) -> VoxelMajorSdf:
+    """The voxel-major materialized field of this trajectory (prepare once, query many cycles)."""
+    return VoxelMajorSdf(self)
+
+
+TrajectorySdf.materialize = _materialize
+
+
 # =========================================================================== reference API
 
 
@@ -365,6 +423,10 @@ def query_min_distances(batch, obstacles: ObstacleVoxelSet, return_stats: bool =
     elif isinstance(batch, TrajectorySdf):
         occ, by_pos = obstacles.occupancy()
         out = batch.query_device(occ, by_pos)
+        d, link, voxel = (out["d"].cpu().numpy(), out["link"].cpu().numpy(), out["voxel"].cpu().numpy())
+    elif isinstance(batch, VoxelMajorSdf):
+        occ, _ = obstacles.occupancy()
+        out = batch.query_device(occ, obstacles.device_indices(), obstacles.n_occupied)
         d, link, voxel = (out["d"].cpu().numpy(), out["link"].cpu().numpy(), out["voxel"].cpu().numpy())
     else:
         t = N.torch()

@@ -681,3 +681,32 @@ def test_unstaged_shell_paths(L):
     assert np.abs(d[sub].astype(np.float64) - rd).max() <= D_TOL
     assert np.array_equal(link[sub], rl) and np.array_equal(voxel[sub], rv)
 
+
+@pytest.mark.parametrize("name", ["scene_c1", "scene_c2", "scene_arm7"])
+def test_voxel_major_mode(L, name):
+    """The paper's materialized mode, voxel-major: prepare once, then every
+    cycle's (d, link, voxel) equal the fused direct query bit for bit (and so
+    the reference gather + Appendix-B argmin), over several clouds."""
+    from paper_2309_12543_b200 import scenarios as S
+
+    g = golden(name)
+    robot, grid, sdfs, window = _scene(L, g)
+    traj = L.TrajectorySdf.from_configs(robot, g["q"], sdfs, grid, window)
+    dense = traj.materialize()
+    assert np.array_equal(dense.values, traj.values)  # the field is the assembled batch
+    clouds = [g["points"], S.human_cloud(5000, seed=3), np.zeros((0, 3)), S.crowd_cloud(4, 5000, seed=4)]
+    for pts in clouds:
+        obs = L.voxelize_pointcloud(pts, grid)
+        want = L.query_min_distances(traj, obs, return_argmin=True)
+        got = L.query_min_distances(dense, obs, return_argmin=True)
+        for a, b in zip(want, got):
+            assert np.array_equal(a, b)
+    # unsorted list with duplicates: first occurrence in the list
+    obs = L.voxelize_pointcloud(g["points"], grid)
+    idx = np.concatenate([obs.indices[::-1], obs.indices[:7]])
+    part = L.ObstacleVoxelSet(indices=idx, grid=grid, n_points=len(idx), n_dropped=0)
+    want = L.query_min_distances(traj, part, return_argmin=True)
+    got = L.query_min_distances(dense, part, return_argmin=True)
+    for a, b in zip(want, got):
+        assert np.array_equal(a, b)
+
