@@ -100,33 +100,44 @@ __global__ void materialize_vm_kernel(const __grid_constant__ VmParams p) {
 // over the CTAs along y; one 64-bit atomic per (configuration, CTA).
 constexpr int VM_THREADS = 512;
 constexpr int VM_BATCH = 16;
+constexpr int VM_STAGE = 256;  // voxel indices staged per CTA round
 
 __global__ void __launch_bounds__(VM_THREADS)
 query_vm_kernel(const float* __restrict__ field, int64_t C, lsdf_env_grid env, const int32_t* __restrict__ indices,
                 const int32_t* __restrict__ counters, int64_t n_list, unsigned long long* keys) {
-    __shared__ int64_t s_lin[VM_BATCH];
+    __shared__ int64_t s_lin[VM_STAGE];
     const int64_t c = (int64_t)blockIdx.x * VM_THREADS + threadIdx.x;
     const int n_occ = n_list >= 0 ? (int)n_list : counters[0];
     uint64_t best = ~0ull;  // (orderable value, list position): lexicographic = first occurrence
-    for (int b0 = blockIdx.y * VM_BATCH; b0 < n_occ; b0 += gridDim.y * VM_BATCH) {
+    // this CTA's voxels: batches b0 = blockIdx.y * VM_BATCH + k * stride; their
+    // indices are staged first (one round trip), then all row loads stream
+    const int stride = gridDim.y * VM_BATCH;
+    for (int k0 = 0;; k0 += VM_STAGE / VM_BATCH) {
+        const int first = blockIdx.y * VM_BATCH + k0 * stride;
+        if (first >= n_occ) break;
         __syncthreads();
-        if (threadIdx.x < VM_BATCH) {
-            const int r = b0 + threadIdx.x;
-            s_lin[threadIdx.x] = r < n_occ ? ((int64_t)__ldg(indices + 3 * r) * env.dims[1] +
-                                              __ldg(indices + 3 * r + 1)) * env.dims[2] + __ldg(indices + 3 * r + 2)
-                                           : -1;
+        for (int i = threadIdx.x; i < VM_STAGE; i += VM_THREADS) {
+            const int r = first + (i / VM_BATCH) * stride + (i % VM_BATCH);
+            s_lin[i] = r < n_occ ? ((int64_t)__ldg(indices + 3 * r) * env.dims[1] + __ldg(indices + 3 * r + 1)) *
+                                       env.dims[2] + __ldg(indices + 3 * r + 2)
+                                 : -1;
         }
         __syncthreads();
-        float v[VM_BATCH];
+        for (int bb = 0; bb < VM_STAGE / VM_BATCH; ++bb) {
+            const int b0 = first + bb * stride;
+            if (b0 >= n_occ) break;
+            float v[VM_BATCH];
 #pragma unroll
-        for (int j = 0; j < VM_BATCH; ++j) {
-            const int64_t lin = s_lin[j];
-            v[j] = (lin >= 0 && c < C) ? __ldcs(field + lin * C + c) : INFINITY;
-        }
+            for (int j = 0; j < VM_BATCH; ++j) {
+                const int64_t lin = s_lin[bb * VM_BATCH + j];
+                v[j] = (lin >= 0 && c < C) ? __ldcs(field + lin * C + c) : INFINITY;
+            }
 #pragma unroll
-        for (int j = 0; j < VM_BATCH; ++j) {
-            const uint64_t key = s_lin[j] >= 0 ? ((uint64_t)orderable(v[j]) << 32) | (uint32_t)(b0 + j) : ~0ull;
-            best = key < best ? key : best;
+            for (int j = 0; j < VM_BATCH; ++j) {
+                const uint64_t key = s_lin[bb * VM_BATCH + j] >= 0
+                                         ? ((uint64_t)orderable(v[j]) << 32) | (uint32_t)(b0 + j) : ~0ull;
+                best = key < best ? key : best;
+            }
         }
     }
     if (c < C && best != ~0ull) atomicMax(keys + c, ~best);  // the workspace holds complements (zero = empty)
