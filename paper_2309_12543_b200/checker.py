@@ -330,3 +330,88 @@ class CheckerPipeline:
                 chk = s["chk"]
                 chk._raise_flags(chk.host_inputs()[0], flags)
         return d.copy(), link.copy(), voxel.copy()
+
+
+class MaterializedChecker:
+    """The paper's two-phase use for a FIXED trajectory:
+    the robot SDF is prepared once as a voxel-major field (``VoxelMajorSdf``),
+    then every control cycle is one CUDA graph — voxelize the frame (read
+    zero-copy from pinned memory, with the sorted occupied list) and one
+    coalesced gather + the exact argmin-link pass, results written back to
+    pinned memory.  Same (d, link, voxel) as DistanceChecker on the same
+    trajectory (tests/test_gpu_parity.py::test_materialized_checker).
+    """
+
+    def __init__(self, robot, sdfs, grid, window, configs, *, d_far_global=None):
+        from .query import TrajectorySdf
+
+        self.grid = grid
+        self.traj = TrajectorySdf.from_configs(robot, configs, sdfs, grid, getattr(window, "window", window),
+                                               d_far_global)
+        self.field = self.traj.materialize()
+        self._graph = None
+
+    def prepare(self, n_points: int, points_dtype=np.float32, use_graph: bool = True):
+        t = N.torch()
+        pdt = np.dtype(points_dtype)
+        if pdt not in (np.float32, np.float64):
+            raise ValidationError(f"points must be float32 or float64, got {pdt}")
+        tdt = t.float32 if pdt == np.float32 else t.float64
+        C_ = self.traj.n_configs
+        self._n, self._pdt = int(n_points), pdt
+        pin = dict(pin_memory=True)
+        self.p_host = t.full((self._n, 3), float("nan"), dtype=tdt, **pin)
+        self.out_host = {"d": t.zeros((C_,), dtype=t.float32, **pin), "link": t.zeros((C_,), dtype=t.int32, **pin),
+                         "voxel": t.zeros((C_,), dtype=t.int32, **pin)}
+        self._p_ptr = N.mapped_pointer(self.p_host)
+        self._outs = {k: v for k, v in self.out_host.items()}
+        self.occ = occupancy_workspace(self.grid)
+        self.idx = N.empty((self.grid.n_voxels, 3), t.int32)
+        self._env = ctypes.byref(self.grid.c_struct())
+        self._d = N.empty((C_,), t.float32)
+        self._l = N.empty((C_,), t.int32)
+        self._v = N.empty((C_,), t.int32)
+        t.cuda.synchronize()
+        if use_graph:
+            s = t.cuda.Stream()
+            s.wait_stream(t.cuda.current_stream())
+            with t.cuda.stream(s):
+                for _ in range(2):
+                    self._run()
+            t.cuda.current_stream().wait_stream(s)
+            t.cuda.synchronize()
+            self._graph = t.cuda.CUDAGraph()
+            with t.cuda.graph(self._graph):
+                self._run()
+            t.cuda.synchronize()
+        return self
+
+    def _run(self):
+        t = N.torch()
+        N.call("lsdf_voxelize", self._p_ptr, int(self._pdt == np.float32), self._n, self._env, N.ptr(self.occ),
+               N.ptr(self.idx), t.cuda.current_stream().cuda_stream)
+        out = {"d": self._d, "link": self._l, "voxel": self._v}
+        self.field.query_device(self.occ, self.idx, -1, outputs=out)
+        for k in ("d", "link", "voxel"):
+            self.out_host[k].copy_(out[k], non_blocking=True)
+
+    def host_points(self):
+        """The pinned (n_points, 3) buffer a producer may fill in place."""
+        return self.p_host.numpy()
+
+    def query(self, points=None):
+        """One cycle from host points; returns numpy (d, link, voxel)."""
+        t = N.torch()
+        if points is not None:
+            p = np.asarray(points).reshape(-1, 3)
+            if len(p) > self._n:
+                raise ValidationError(f"{len(p)} points exceed the prepared capacity {self._n}")
+            host = self.p_host.numpy()
+            host[: len(p)] = p
+            host[len(p):] = np.nan
+        if self._graph is not None:
+            self._graph.replay()
+        else:
+            self._run()
+        t.cuda.current_stream().synchronize()
+        return tuple(self.out_host[k].numpy().copy() for k in ("d", "link", "voxel"))

@@ -710,3 +710,21 @@ def test_voxel_major_mode(L, name):
     for a, b in zip(want, got):
         assert np.array_equal(a, b)
 
+
+def test_materialized_checker(L):
+    """MaterializedChecker (prepare once, graph per cycle) == DistanceChecker, cycle by cycle."""
+    from paper_2309_12543_b200 import scenarios as S
+
+    g = golden("scene_c2")
+    robot, grid, sdfs, window = _scene(L, g)
+    q = g["q"]
+    mat = L.MaterializedChecker(robot, sdfs, grid, window, q).prepare(30_000, np.float32)
+    chk = L.DistanceChecker(robot, sdfs, grid, window).prepare(len(q), 30_000, np.float32)
+    for k, (_, pts) in enumerate(S.moving_human_frames(12, 30_000, seed=2)):
+        if k % 3:
+            continue
+        want = chk.query(q, pts.astype(np.float32))
+        got = mat.query(pts.astype(np.float32))
+        for a, b in zip(want, got):
+            assert np.array_equal(a, b)
+
