@@ -365,10 +365,17 @@ int lsdf_mesh_points(const double* tri_dev, int32_t n_tri, int32_t is_signed,
  * of 32 keeps every row 128-B aligned: the write-bound kernel then stores
  * whole L2 lines, 2.2x faster at W = 128 than the packed n_out stride).
  * hidden H <= 64.  Layer 2 runs on tcgen05 tensor cores (kind::tf32, 3xTF32
- * split) when use_tensor_cores != 0. */
+ * split) when use_tensor_cores != 0; it reads W2 split and swizzled into its
+ * operand layout: pass w2_packed_dev = lsdf_mlp_pack(W2) (the caller keeps it
+ * and re-packs when W2 changes) or NULL to pack into a temporary per call. */
 int lsdf_mlp_predict(const float* w1_dev, const float* b1_dev, const float* w2_dev,
-                     const float* b2_dev, int32_t H, int64_t n_out, const double* R_dev,
-                     int64_t B, float* y_dev, int64_t ldy, int32_t use_tensor_cores, void* stream);
+                     const float* w2_packed_dev, const float* b2_dev, int32_t H, int64_t n_out,
+                     const double* R_dev, int64_t B, float* y_dev, int64_t ldy,
+                     int32_t use_tensor_cores, void* stream);
+
+/* The tensor-core operand layout of W2 (H, n_out): bytes and fill. */
+int64_t lsdf_mlp_packed_bytes(int32_t H, int64_t n_out);
+int lsdf_mlp_pack(const float* w2_dev, int32_t H, int64_t n_out, float* packed_dev, void* stream);
 
 #ifdef __cplusplus
 }

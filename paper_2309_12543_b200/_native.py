@@ -95,7 +95,9 @@ _SIGS = {
     "lsdf_primitive_points": [_I32, C.POINTER(_D), _P, _I64, _P, _P],
     "lsdf_build_mesh": [_P, _I32, _I32, C.POINTER(_D), C.POINTER(_D), C.POINTER(_I32), _P, _P],
     "lsdf_mesh_points": [_P, _I32, _I32, _P, _I64, _P, _P],
-    "lsdf_mlp_predict": [_P, _P, _P, _P, _I32, _I64, _P, _I64, _P, _I64, _I32, _P],
+    "lsdf_mlp_predict": [_P, _P, _P, _P, _P, _I32, _I64, _P, _I64, _P, _I64, _I32, _P],
+    "lsdf_mlp_packed_bytes": [_I32, _I64],
+    "lsdf_mlp_pack": [_P, _I32, _I64, _P, _P],
     "lsdf_host_device_pointer": [_P, C.POINTER(C.c_void_p)],
 }
 

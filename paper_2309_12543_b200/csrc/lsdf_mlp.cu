@@ -51,18 +51,30 @@ __global__ void __launch_bounds__(COLS) mlp_cuda_core_kernel(const float* __rest
 
 }  // namespace
 
-int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const float* b2, int32_t H,
-                        int64_t n_out, const double* R, int64_t B, float* y, int64_t ldy, cudaStream_t s);
+int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const float* w2_packed, const float* b2,
+                        int32_t H, int64_t n_out, const double* R, int64_t B, float* y, int64_t ldy, cudaStream_t s);
+int64_t lsdf_mlp_packed_bytes_tc(int32_t H, int64_t n_out);
+int lsdf_mlp_pack_tc(const float* w2, int32_t H, int64_t n_out, float* packed, cudaStream_t s);
 
-extern "C" int lsdf_mlp_predict(const float* w1_dev, const float* b1_dev, const float* w2_dev, const float* b2_dev,
-                                int32_t H, int64_t n_out, const double* R_dev, int64_t B, float* y_dev,
-                                int64_t ldy, int32_t use_tensor_cores, void* stream) {
+extern "C" int64_t lsdf_mlp_packed_bytes(int32_t H, int64_t n_out) { return lsdf_mlp_packed_bytes_tc(H, n_out); }
+
+extern "C" int lsdf_mlp_pack(const float* w2_dev, int32_t H, int64_t n_out, float* packed_dev, void* stream) {
+    if (H < 1 || H > 64) return fail(LSDF_ERR_UNSUPPORTED, "TinyMlp hidden width %d outside 1..64", H);
+    if (n_out <= 0) return LSDF_OK;
+    return lsdf_mlp_pack_tc(w2_dev, H, n_out, packed_dev, (cudaStream_t)stream);
+}
+
+extern "C" int lsdf_mlp_predict(const float* w1_dev, const float* b1_dev, const float* w2_dev,
+                                const float* w2_packed_dev, const float* b2_dev, int32_t H, int64_t n_out,
+                                const double* R_dev, int64_t B, float* y_dev, int64_t ldy, int32_t use_tensor_cores,
+                                void* stream) {
     if (H < 1 || H > 64) return fail(LSDF_ERR_UNSUPPORTED, "TinyMlp hidden width %d outside 1..64", H);
     if (ldy < n_out) return fail(LSDF_ERR_VALIDATION, "TinyMlp: row stride %lld < %lld outputs", (long long)ldy,
                                  (long long)n_out);
     if (B <= 0 || n_out <= 0) return LSDF_OK;
-    if (use_tensor_cores) return lsdf_mlp_predict_tc(w1_dev, b1_dev, w2_dev, b2_dev, H, n_out, R_dev, B, y_dev, ldy,
-                                                     (cudaStream_t)stream);
+    if (use_tensor_cores)
+        return lsdf_mlp_predict_tc(w1_dev, b1_dev, w2_dev, w2_packed_dev, b2_dev, H, n_out, R_dev, B, y_dev, ldy,
+                                   (cudaStream_t)stream);
     dim3 grid((unsigned)((n_out + COLS - 1) / COLS), (unsigned)((B + ROWS - 1) / ROWS));
     mlp_cuda_core_kernel<<<grid, COLS, 0, (cudaStream_t)stream>>>(w1_dev, b1_dev, w2_dev, b2_dev, H, n_out, R_dev, B,
                                                                    y_dev, ldy);

@@ -318,36 +318,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(const __grid_cons
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * TN));
 }
 
-struct PackCache {
-    const float* w2 = nullptr;
-    int64_t N = 0;
-    int H = 0;
-    float* hi = nullptr;
-    float* lo = nullptr;
-};
-PackCache g_pack;
-
 }  // namespace
 
-// Pre-split / pre-swizzle W2 once per weight buffer (cached by pointer+shape).
-int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const float* b2, int32_t H, int64_t n_out,
-                        const double* R, int64_t B, float* y, int64_t ldy, cudaStream_t s) {
+// Packed W2^T (hi | lo TF32 halves, swizzled output tiles): bytes and fill.
+int64_t lsdf_mlp_packed_bytes_tc(int32_t H, int64_t n_out) {
+    const int kblocks = (H + 31) / 32;
+    const int64_t n_tiles = (n_out + TM - 1) / TM;
+    return 2 * n_tiles * kblocks * TM * 32 * (int64_t)sizeof(float);
+}
+
+int lsdf_mlp_pack_tc(const float* w2, int32_t H, int64_t n_out, float* packed, cudaStream_t s) {
+    using namespace lsdf;
+    const int kblocks = (H + 31) / 32;
+    const int64_t n_tiles = (n_out + TM - 1) / TM;
+    float* hi = packed;
+    float* lo = packed + n_tiles * kblocks * TM * 32;
+    pack_w2_kernel<<<148 * 8, 256, 0, s>>>(w2, H, n_out, kblocks, n_tiles, hi, lo);
+    return check_launch("pack_w2_kernel");
+}
+
+// w2_packed: lsdf_mlp_pack_tc output for these weights (kept by the caller
+// and re-packed whenever W2 changes), or null to pack into a temporary.
+int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const float* w2_packed, const float* b2,
+                        int32_t H, int64_t n_out, const double* R, int64_t B, float* y, int64_t ldy, cudaStream_t s) {
     using namespace lsdf;
     if (H > 64) return fail(LSDF_ERR_UNSUPPORTED, "tcgen05 TinyMlp supports hidden <= 64");
     const int kblocks = (H + 31) / 32;
     const int64_t n_tiles = (n_out + TM - 1) / TM;
-    if (g_pack.w2 != w2 || g_pack.N != n_out || g_pack.H != H) {
-        if (g_pack.hi) cudaFreeAsync(g_pack.hi, s);
-        if (g_pack.lo) cudaFreeAsync(g_pack.lo, s);
-        const size_t bytes = (size_t)n_tiles * kblocks * TM * 32 * sizeof(float);
-        LSDF_TRY(check_cuda(cudaMallocAsync((void**)&g_pack.hi, bytes, s), "mlp pack alloc"));
-        LSDF_TRY(check_cuda(cudaMallocAsync((void**)&g_pack.lo, bytes, s), "mlp pack alloc"));
-        pack_w2_kernel<<<148 * 8, 256, 0, s>>>(w2, H, n_out, kblocks, n_tiles, g_pack.hi, g_pack.lo);
-        LSDF_TRY(check_launch("pack_w2_kernel"));
-        g_pack.w2 = w2;
-        g_pack.N = n_out;
-        g_pack.H = H;
+    float* tmp = nullptr;
+    if (w2_packed == nullptr) {
+        LSDF_TRY(check_cuda(cudaMallocAsync((void**)&tmp, (size_t)lsdf_mlp_packed_bytes_tc(H, n_out), s),
+                            "mlp pack alloc"));
+        LSDF_TRY(lsdf_mlp_pack_tc(w2, H, n_out, tmp, s));
+        w2_packed = tmp;
     }
+    const float* w2_hi = w2_packed;
+    const float* w2_lo = w2_packed + n_tiles * kblocks * TM * 32;
     const int64_t r_tiles = (B + TN - 1) / TN;
     const size_t h_bytes = (size_t)r_tiles * kblocks * TN * 32 * sizeof(float);
     float *a_hi = nullptr, *a_lo = nullptr;
@@ -358,8 +364,8 @@ int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const
     MlpTcParams p{};
     p.h_hi = a_hi;
     p.h_lo = a_lo;
-    p.w2t_hi = g_pack.hi;
-    p.w2t_lo = g_pack.lo;
+    p.w2t_hi = w2_hi;
+    p.w2t_lo = w2_lo;
     p.b2 = b2;
     p.y = y;
     p.ldy = ldy;
@@ -381,6 +387,7 @@ int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const
     LSDF_TRY(check_launch("mlp_tc_kernel"));
     cudaFreeAsync(a_hi, s);
     cudaFreeAsync(a_lo, s);
+    if (tmp) cudaFreeAsync(tmp, s);
     return LSDF_OK;
 
 }

@@ -604,8 +604,8 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
                 attr = true;
             }
             // residency cache: (device, by_position, smem bytes) -> CTAs per SM
-            static int c_dev = -1, c_bp = -1, c_sm = 148, c_per = 1;
-            static size_t c_smem = 0;
+            thread_local int c_dev = -1, c_bp = -1, c_sm = 148, c_per = 1;
+            thread_local size_t c_smem = 0;
             int dev = 0;
             cudaGetDevice(&dev);
             if (dev != c_dev || (int)by_position != c_bp || smem_s != c_smem) {

@@ -569,6 +569,12 @@ def test_mlp_tensor_cores(L):
     b = big.predict_device(Rb, use_tensor_cores=False).cpu().numpy()
     scale = np.abs(b).max()
     assert np.abs(a - b).max() <= 1e-6 * max(1.0, scale) * 8
+    # new weights (same buffer shapes, possibly the same addresses): the packed copy follows
+    big.w2 = np.random.default_rng(9).normal(0, 0.3, size=big.w2.shape).astype(np.float32)
+    big._dev = None
+    a2 = big.predict_device(Rb, use_tensor_cores=True).cpu().numpy()
+    b2 = big.predict_device(Rb, use_tensor_cores=False).cpu().numpy()
+    assert np.abs(a2 - b2).max() <= 1e-6 * max(1.0, np.abs(b2).max()) * 8
     # row stride: packed, padded (the default allocation) and odd strides agree bit for bit;
     # 300 rotations = one full and one partial 256-rotation tile
     n = 3 * 2103
