@@ -300,7 +300,7 @@ def run_ours(args, rank, world, dist, sampler):
     achieved = alg_bytes / (q_ms / 1e3) / 1e9
     traffic = None
     tf = REPO / "profiles" / "query_traffic.json"
-    if tf.exists():
+    if tf.exists() and world == 1:  # the ncu capture is of the single-GPU launch
         try:
             traffic = json.loads(tf.read_text()).get(args.workload)
         except (ValueError, OSError):
@@ -508,12 +508,14 @@ def main():
         return
     import torch
 
-    torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
+    torch.cuda.set_device(_env_int("LOCAL_RANK", 0) % max(1, torch.cuda.device_count()))
     dist = None
     if world > 1:
         import torch.distributed as tdist
 
-        tdist.init_process_group("nccl")
+        # LSDF_BENCH_BACKEND=gloo: functional check of the multi-rank path on
+        # one GPU (numbers meaningless); the driver's runs use NCCL
+        tdist.init_process_group(os.environ.get("LSDF_BENCH_BACKEND", "nccl"))
         dist = tdist
     import paper_2309_12543_b200 as L
 
