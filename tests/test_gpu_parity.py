@@ -734,3 +734,33 @@ def test_materialized_checker(L):
         for a, b in zip(want, got):
             assert np.array_equal(a, b)
 
+
+@pytest.mark.parametrize("C", [64, 9000])
+def test_mixed_link_grids(L, C):
+    """Links baked at different resolutions (several launch groups, each with
+    its own task counter) and an anisotropic environment grid: direct ==
+    dense gather bit for bit, at a latency-sized and a throughput-sized batch."""
+    from paper_2309_12543_b200 import scenarios as S
+
+    doc = S.ARM6G
+    robot = L.RobotModel.from_dict(doc)
+    grid = L.EnvGrid([1.0, 0.8, 0.9], 0.04)
+    e_r = 0.32
+    res = [0.02, 0.01, 0.02, 0.04, 0.01, 0.02]
+    sdfs = [L.build_link_sdf(robot.links[i].geometry, e_r, r, link_id=i) for i, r in zip(robot.geometry_links, res)]
+    window = L.WindowGeometry.build(e_r, grid)
+    q = S.random_configs(doc, C, seed=12)
+    pts = S.human_cloud(30_000, seed=12)
+    traj = L.TrajectorySdf.from_configs(robot, q, sdfs, grid, window)
+    obs = L.voxelize_pointcloud(pts, grid)
+    d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
+    sub = slice(0, min(C, 2000))
+    part = L.TrajectorySdf.from_configs(robot, q[sub], sdfs, grid, window)
+    dense = L.RobotSdfBatch(part.device_values(), grid, part.d_far_global)
+    d2, _, v2 = L.query_min_distances(dense, obs, return_argmin=True)
+    assert np.array_equal(d[sub], d2) and np.array_equal(voxel[sub], v2)
+    pl = part.per_link_min_distances(obs)
+    for c in range(0, len(d2), 37):
+        if link[c] >= 0:
+            assert pl[c, link[c]] == d[c] and np.all(pl[c, :link[c]] > d[c])
+
