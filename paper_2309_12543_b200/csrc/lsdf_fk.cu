@@ -23,6 +23,7 @@ struct FkParams {
     const double* limits;
     lsdf_env_grid env;
     int32_t W[3];
+    double rinv[3];  // RN(1 / env resolution)
     double* R_all;
     double* T_all;
     double* R_geo;
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
         for (int e = 0; e < 9; ++e) p.R_geo[o * 9 + e] = w[e];
         int32_t anc[3];
         double del[3], T[3] = {w[9], w[10], w[11]};
-        if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del)) atomicAdd(&p.flags[1], 1);
+        if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del, p.rinv)) atomicAdd(&p.flags[1], 1);
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             p.dt_geo[o * 3 + k] = del[k];
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __gr
                 for (int e = 0; e < 9; ++e) oR[o * 9 + e] = R[e];
                 int32_t anc[3];
                 double del[3];
-                if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del))
+                if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del, p.rinv))
                     atomicAdd(&p.flags[1], 1);
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
@@ -338,7 +339,10 @@ extern "C" int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_
     p.C = C;
     p.q = q_dev;
     p.limits = limits_dev;
-    if (env) p.env = *env;
+    if (env) {
+        p.env = *env;
+        for (int a = 0; a < 3; ++a) p.rinv[a] = 1.0 / env->resolution[a];
+    }
     if (W) {
         p.W[0] = W[0];
         p.W[1] = W[1];

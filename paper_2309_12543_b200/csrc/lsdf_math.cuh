@@ -72,15 +72,27 @@ LSDF_HD void rodrigues(const double* skew, const double* outer, double c, double
     }
 }
 
+// x / r correctly rounded from rinv = RN(1 / r) without a division:
+// q0 = RN(x rinv), the exact residual x - q0 r by FMA, one correction step
+// (Markstein; also checked on 3.2e8 random operands,
+// tests/test_hostcheck.py::test_division_recipe).  Normal operands only.
+LSDF_HD double div_rn(double x, double r, double rinv) {
+    const double q0 = DMUL(x, rinv);
+    return DFMA(DFMA(-q0, r, x), rinv, q0);
+}
+
 // ---------------------------------------------------------------- alignment
 // placement.py:60-99 for one position. Returns true when the window overlaps.
+// rinv (optional): RN(1 / res) per axis, so the floor quotient needs no division.
 LSDF_HD bool align_one(const double* pos, const double* ext, const double* res,
-                       const int32_t* dims, const int32_t* W, int32_t* anchor, double* delta) {
+                       const int32_t* dims, const int32_t* W, int32_t* anchor, double* delta,
+                       const double* rinv = nullptr) {
     const double eps = 2.220446049250313e-16;  // np.finfo(np.float64).eps
     bool overlap = true;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        double jf = floor(DDIV(DADD(pos[a], ext[a]), res[a]));
+        const double x = DADD(pos[a], ext[a]);
+        double jf = floor(rinv ? div_rn(x, res[a], rinv[a]) : DDIV(x, res[a]));
         int64_t j = (int64_t)jf;
         // centers: -e + (j + 0.5) * r   (grids.py:80-83)
         double cen = DADD(-ext[a], DMUL(DADD((double)j, 0.5), res[a]));
@@ -99,8 +111,11 @@ LSDF_HD bool align_one(const double* pos, const double* ext, const double* res,
 }
 
 // dt_inv_k = -((dt0/e)*R0k + (dt1/e)*R1k + (dt2/e)*R2k)   (placement.py:165)
-LSDF_HD void shift_inverse(const double* R, const double* dt, double e_r, double* out) {
-    const double a0 = DDIV(dt[0], e_r), a1 = DDIV(dt[1], e_r), a2 = DDIV(dt[2], e_r);
+// e_rinv (optional, > 0): RN(1 / e_r), so the three quotients need no division.
+LSDF_HD void shift_inverse(const double* R, const double* dt, double e_r, double* out, double e_rinv = 0.0) {
+    const double a0 = e_rinv > 0.0 ? div_rn(dt[0], e_r, e_rinv) : DDIV(dt[0], e_r);
+    const double a1 = e_rinv > 0.0 ? div_rn(dt[1], e_r, e_rinv) : DDIV(dt[1], e_r);
+    const double a2 = e_rinv > 0.0 ? div_rn(dt[2], e_r, e_rinv) : DDIV(dt[2], e_r);
 #pragma unroll
     for (int k = 0; k < 3; ++k)
         out[k] = -DADD(DADD(DMUL(a0, R[k]), DMUL(a1, R[3 + k])), DMUL(a2, R[6 + k]));

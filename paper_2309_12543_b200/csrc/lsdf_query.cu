@@ -50,7 +50,7 @@ struct QueryParams {
     int32_t n_geo, split;
     int32_t W[3];
     int32_t full_window;  // iterate the whole window, masking per cell (d_far_l < clamp)
-    double e_r;
+    double e_r, e_rinv;  // window extent and RN(1 / e_r)
     const double* P;
     int32_t Wmax, by_position;
     const int16_t* zrange;
@@ -273,7 +273,7 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, uint32_t t, Sh
     for (int e = 0; e < 9; ++e) R[e] = __ldg(p.R + o * 9 + e);
 #pragma unroll
     for (int e = 0; e < 3; ++e) dt[e] = __ldg(p.dt + o * 3 + e);
-    shift_inverse(R, dt, p.e_r, dtinv);
+    shift_inverse(R, dt, p.e_r, dtinv, p.e_rinv);
     // |dt| rounded up (dt is the residual of T against its voxel centre)
     const float dtn = (float)(sqrt(dt[0] * dt[0] + dt[1] * dt[1] + dt[2] * dt[2]) * (1.0 + 1e-6) + 1e-12);
 #pragma unroll
@@ -534,6 +534,7 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     }
     p.full_window = full;
     p.e_r = window->e_r;
+    p.e_rinv = 1.0 / window->e_r;
     p.shell_cells = window->shell_cells_dev;
     p.shell_radius = window->shell_radius_dev;
     p.n_shell = window->n_masked;

@@ -62,6 +62,28 @@ int hc_align(const double* T, int64_t n, const lsdf_env_grid* env, const int32_t
     return bad;
 }
 
+// the same with the reciprocal-multiply quotient the FK kernels use
+int hc_align_rinv(const double* T, int64_t n, const lsdf_env_grid* env, const int32_t* W, int32_t* anchor,
+                  double* dt) {
+    const double rinv[3] = {1.0 / env->resolution[0], 1.0 / env->resolution[1], 1.0 / env->resolution[2]};
+    int bad = 0;
+    for (int64_t i = 0; i < n; ++i)
+        bad += !align_one(T + 3 * i, env->extent, env->resolution, env->dims, W, anchor + 3 * i, dt + 3 * i, rinv);
+    return bad;
+}
+
+// shift_inverse with and without the reciprocal (n rotations): the max |difference| (expect 0)
+double hc_shift_diff(const double* R, const double* dt, int64_t n, double e_r) {
+    double worst = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double a[3], b[3];
+        shift_inverse(R + 9 * i, dt + 3 * i, e_r, a);
+        shift_inverse(R + 9 * i, dt + 3 * i, e_r, b, 1.0 / e_r);
+        for (int k = 0; k < 3; ++k) worst = std::fmax(worst, std::fabs(a[k] - b[k]) + (a[k] != b[k] ? 1.0 : 0.0));
+    }
+    return worst;
+}
+
 // Same per-cell math as place_windows_kernel: all W^3 cells of one (R, dt).
 void hc_window(const double* R, const double* dt, const float* grid, const int32_t* gdims, const double* gext,
                const double* gres, float d_far, const double* P, int Wmax, const int32_t* W, const uint8_t* mask,

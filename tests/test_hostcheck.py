@@ -77,6 +77,20 @@ def test_alignment_recipe(hc, name):
     bad = hc.hc_align(P(T), ctypes.c_int64(len(T)), ctypes.byref(env), W, P(anchor), P(dt))
     assert bad == 0
     assert np.array_equal(anchor.reshape(g["anchors"].shape), g["anchors"])
+    # the reciprocal-multiply quotient (the FK kernels) gives the same bits
+    anchor2, dt2 = np.zeros_like(anchor), np.zeros_like(dt)
+    assert hc.hc_align_rinv(P(T), ctypes.c_int64(len(T)), ctypes.byref(env), W, P(anchor2), P(dt2)) == 0
+    assert np.array_equal(anchor2, anchor) and np.array_equal(dt2, dt)
+
+
+def test_shift_inverse_reciprocal_recipe(hc):
+    rng = np.random.default_rng(3)
+    n = 200_000
+    R = np.ascontiguousarray(rng.normal(size=(n, 9)))
+    dt = np.ascontiguousarray(rng.uniform(-0.05, 0.05, size=(n, 3)))
+    hc.hc_shift_diff.restype = ctypes.c_double
+    for e_r in (0.32, 0.3, 0.64, 0.17, 1.0 / 3.0):
+        assert hc.hc_shift_diff(P(R), P(dt), ctypes.c_int64(n), ctypes.c_double(e_r)) == 0.0
 
 
 def test_window_recipe_bit_exact(hc):
