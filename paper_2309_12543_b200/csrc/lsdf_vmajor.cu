@@ -108,7 +108,10 @@ query_vm_kernel(const float* __restrict__ field, int64_t C, lsdf_env_grid env, c
     __shared__ int64_t s_lin[VM_STAGE];
     const int64_t c = (int64_t)blockIdx.x * VM_THREADS + threadIdx.x;
     const int n_occ = n_list >= 0 ? (int)n_list : counters[0];
-    uint64_t best = ~0ull;  // (orderable value, list position): lexicographic = first occurrence
+    // each thread visits its voxels in increasing list position, so a strict
+    // "<" keeps the first occurrence (and -0 == +0); the key is formed once
+    float bestv = INFINITY;
+    int bestr = -1;
     // this CTA's voxels: batches b0 = blockIdx.y * VM_BATCH + k * stride; their
     // indices are staged first (one round trip), then all row loads stream
     const int stride = gridDim.y * VM_BATCH;
@@ -134,13 +137,14 @@ query_vm_kernel(const float* __restrict__ field, int64_t C, lsdf_env_grid env, c
             }
 #pragma unroll
             for (int j = 0; j < VM_BATCH; ++j) {
-                const uint64_t key = s_lin[bb * VM_BATCH + j] >= 0
-                                         ? ((uint64_t)orderable(v[j]) << 32) | (uint32_t)(b0 + j) : ~0ull;
-                best = key < best ? key : best;
+                const bool better = v[j] < bestv;  // INFINITY padding never wins
+                bestv = better ? v[j] : bestv;
+                bestr = better ? b0 + j : bestr;
             }
         }
     }
-    if (c < C && best != ~0ull) atomicMax(keys + c, ~best);  // the workspace holds complements (zero = empty)
+    if (c < C && bestr >= 0)
+        atomicMax(keys + c, ~(((unsigned long long)orderable(bestv) << 32) | (uint32_t)bestr));  // the workspace holds complements (zero = empty)
 }
 
 struct LinkParams {
