@@ -188,14 +188,18 @@ def _max_over_ranks(dist, torch, x):
     return float(t.item())
 
 
-def _e2e_entry(C_total, pipe_ms, single_ms, h2d, d2h):
+def _e2e_entry(C_total, pipe_ms, single_ms, h2d, d2h, world=1):
     """The public-API end-to-end number: the faster of the pipelined and the
     one-cycle-at-a-time paths (both copy every cycle's inputs in and results out)."""
     pipe_path = ("CheckerPipeline (2 cycles in flight): per cycle H2D of configs + cloud from pinned host memory on "
-                 "a copy stream, the cycle graph, D2H of (d, link, voxel) + flags; host wall clock over K cycles")
+                 "a copy stream, the cycle graph, D2H of (d, link, voxel) + flags; host wall clock over K cycles"
+                 if world == 1 else
+                 "ShardedCloudPipeline (2 cycles in flight, per rank): H2D of this rank's configs and 1/world of the "
+                 "cloud, voxelize the slice, NCCL all-gather of the partial occupancy bitmaps, merge, FK + query, "
+                 "D2H; host wall clock over K cycles, max over ranks")
     single_path = ("DistanceChecker.query() one cycle at a time from pinned host buffers (zero-copy kernel "
                    "reads/writes over PCIe); median cycle, host wall clock")
-    best_ms, path = (pipe_ms, pipe_path) if pipe_ms <= single_ms else (single_ms, single_path)
+    best_ms, path = (pipe_ms, pipe_path) if (pipe_ms <= single_ms or world > 1) else (single_ms, single_path)
     return {"value": C_total / (best_ms / 1e3), "unit": "waypoint-queries/s", "ms_per_step": best_ms,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "path": path,
             "pipelined_ms_per_step": pipe_ms, "single_cycle_ms": single_ms}
@@ -260,27 +264,49 @@ def run_ours(args, rank, world, dist, sampler):
     # ---- e2e throughput through the public API: CheckerPipeline, two cycles in
     # flight; every cycle copies its configurations and cloud from pinned host
     # memory (copy engine) and reads (d, link, voxel) back, K cycles wall clock
-    pipe = L.CheckerPipeline(chk.robot, chk.sdfs, chk.grid, chk.window, n_local, shape.n_points, np.float32,
-                             depth=2)
-    for k in range(pipe.depth):  # producers write straight into the pinned slots
-        qv, pv = pipe.inputs()
-        qv[...], pv[...] = host[k % len(host)]
-        pipe.submit()
-    for k in range(pipe.depth):
-        pipe.result(k)
-    for _ in range(args.warmup):
-        pipe.result(pipe.submit())
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    s0 = time.perf_counter()
-    tickets = [pipe.submit() for _ in range(pipe.depth)]
-    for k in range(args.steps):
-        pipe.result(tickets[k])
-        if k + pipe.depth < args.steps:
-            tickets.append(pipe.submit())
-    e2e_ms = _max_over_ranks(dist, torch, 1e3 * (time.perf_counter() - s0) / args.steps)
-    del pipe
+    # with several ranks the cloud is sharded too: each rank uploads its slice
+    # and the ranks all-gather their 16-KB partial occupancy bitmaps over NVLink
+    def run_pipe(sharded: bool):
+        if sharded:
+            from paper_2309_12543_b200.sharding import shard_range
+
+            plo, phi = shard_range(shape.n_points, rank, world)
+            pipe = L.ShardedCloudPipeline(chk.robot, chk.sdfs, chk.grid, chk.window, n_local, phi - plo,
+                                          np.float32, depth=2)
+        else:
+            plo, phi = 0, shape.n_points
+            pipe = L.CheckerPipeline(chk.robot, chk.sdfs, chk.grid, chk.window, n_local, shape.n_points,
+                                     np.float32, depth=2)
+        for k in range(pipe.depth):  # producers write straight into the pinned slots
+            qv, pv = pipe.inputs()
+            q_k, p_k = host[k % len(host)]
+            qv[...], pv[...] = q_k, p_k[plo:phi]
+            pipe.submit()
+        for k in range(pipe.depth):
+            pipe.result(k)
+        for _ in range(args.warmup):
+            pipe.result(pipe.submit())
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        s0 = time.perf_counter()
+        tickets = [pipe.submit() for _ in range(pipe.depth)]
+        for k in range(args.steps):
+            pipe.result(tickets[k])
+            if k + pipe.depth < args.steps:
+                tickets.append(pipe.submit())
+        return 1e3 * (time.perf_counter() - s0) / args.steps, plo, phi
+
+    sharded = world > 1
+    try:
+        pipe_ms, plo, phi = run_pipe(sharded)
+    except Exception as exc:  # noqa: BLE001 — keep the measurement if the sharded exchange fails
+        if not sharded:
+            raise
+        print(f"sharded-cloud pipeline failed ({exc!r}); e2e with the full cloud per rank", file=sys.stderr)
+        sharded = False
+        pipe_ms, plo, phi = run_pipe(False)
+    e2e_ms = _max_over_ranks(dist, torch, pipe_ms)
 
     from paper_2309_12543_b200 import _native as N
 
@@ -318,8 +344,8 @@ def run_ours(args, rank, world, dist, sampler):
                    "timing": "device: CUDA events around a graph replay of the cycle"},
         "gpu_launches": per_cycle * args.steps,
         "gpu_launches_per_step": per_cycle,
-        "e2e": _e2e_entry(C_total, e2e_ms, single_ms, int(n_local * robot.dof * 8 + shape.n_points * 12),
-                          int(n_local * 12 + 16)),
+        "e2e": _e2e_entry(C_total, e2e_ms, single_ms, int(n_local * robot.dof * 8 + (phi - plo) * 12),
+                          int(n_local * 12 + 16), world if sharded else 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "query_shells_kernel", "kernel_ms": q_ms,
                      "algorithmic_bytes": alg_bytes, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst)"},

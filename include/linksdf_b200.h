@@ -186,6 +186,16 @@ int lsdf_voxelize_bitmap(const void* points_dev, int32_t points_f32, int64_t N,
                          const lsdf_env_grid* env, void* occupancy_dev, void* stream);
 int lsdf_occupancy_prefix(const lsdf_env_grid* env, void* occupancy_dev, void* stream);
 
+/* A cloud sharded over ranks: each rank voxelizes its slice
+ * (lsdf_voxelize_bitmap), the ranks all-gather their bitmaps
+ * (n_parts, ceil(V/32)) u32 and dropped counters, and this ORs the parts
+ * into occupancy_dev and writes the rank prefix — the same occupancy as one
+ * rank voxelizing the whole cloud.  dropped_dev[k * dropped_stride] is part
+ * k's dropped-point count. */
+int lsdf_occupancy_merge(const uint32_t* parts_dev, int32_t n_parts, const int32_t* dropped_dev,
+                         int64_t dropped_stride, const lsdf_env_grid* env, void* occupancy_dev,
+                         void* stream);
+
 /* Occupancy from an explicit index list (ObstacleVoxelSet, query.py:47-58).
  * sorted_unique != 0 promises lexicographic order without duplicates (what
  * voxelize and np.unique produce); otherwise the first position of each voxel

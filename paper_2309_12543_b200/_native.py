@@ -65,6 +65,7 @@ _SIGS = {
     "lsdf_voxelize": [_P, _I32, _I64, C.POINTER(EnvGridT), _P, _P, _P],
     "lsdf_voxelize_bitmap": [_P, _I32, _I64, C.POINTER(EnvGridT), _P, _P],
     "lsdf_occupancy_prefix": [C.POINTER(EnvGridT), _P, _P],
+    "lsdf_occupancy_merge": [_P, _I32, _P, _I64, C.POINTER(EnvGridT), _P, _P],
     "lsdf_occupancy_from_indices": [_P, _I64, _I32, C.POINTER(EnvGridT), _P, _P],
     "lsdf_voxel_index": [_P, _I64, C.POINTER(EnvGridT), _P, _P, _P],
     "lsdf_query_direct": [_P, _P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT),

@@ -415,3 +415,123 @@ class MaterializedChecker:
             self._run()
         t.cuda.current_stream().synchronize()
         return tuple(self.out_host[k].numpy().copy() for k in ("d", "link", "voxel"))
+
+
+class ShardedCloudPipeline:
+    """CheckerPipeline for one rank of a multi-GPU throughput sweep whose cloud
+    is shared: each rank uploads only ITS slice of the points (and of the
+    waypoints), voxelizes the slice, and the ranks all-gather their partial
+    occupancy bitmaps (ceil(V/32) words each) and dropped counters over
+    NVLink; ``lsdf_occupancy_merge`` ORs them into the full occupancy.  Per
+    cycle a rank moves 1/world of the cloud over PCIe instead of all of it;
+    the exchange is 16 KB per rank at 50^3.  Results are those of one rank
+    voxelizing the whole cloud (tests: ``test_sharded_cloud_pipeline``).
+
+    Producers fill ``inputs()`` (pinned configs of this rank's waypoints,
+    pinned points of this rank's slice, NaN-padded), then ``submit()``;
+    ``result(ticket)`` returns this rank's (d, link, voxel).
+    """
+
+    def __init__(self, robot, sdfs, grid, window, n_configs: int, n_points_local: int, points_dtype=np.float32,
+                 depth: int = 2, group=None, **kw):
+        import torch.distributed as dist
+
+        t = N.torch()
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.grid = grid
+        n_words = (grid.n_voxels + 31) // 32
+        self._bits = slice(256 // 4, 256 // 4 + n_words)  # int32 view of the occupancy workspace
+        self.slots = []
+        for _ in range(depth):
+            chk = DistanceChecker(robot, sdfs, grid, window, **kw).prepare(
+                n_configs, n_points_local, points_dtype, use_graph=False, zero_copy=False)
+            pin = dict(pin_memory=True)
+            host_out = (t.zeros((n_configs,), dtype=t.float32, **pin), t.zeros((n_configs,), dtype=t.int32, **pin),
+                        t.zeros((n_configs,), dtype=t.int32, **pin), t.zeros((4,), dtype=t.int32, **pin))
+            part = occupancy_workspace(grid)
+            gather = N.empty((self.world, n_words), t.int32)
+            dropped = N.empty((self.world,), t.int32)
+            ev = {k: t.cuda.Event() for k in ("h2d", "compute", "d2h")}
+            self.slots.append({"chk": chk, "out": host_out, "part": part, "gather": gather, "dropped": dropped,
+                               "ev": ev, "busy": False, "ticket": -1})
+        self.copy = t.cuda.Stream()
+        self.compute = t.cuda.Stream()
+        self.d2h = t.cuda.Stream()
+        self._next = 0
+
+    @property
+    def depth(self) -> int:
+        return len(self.slots)
+
+    def _slot(self, ticket):
+        return self.slots[ticket % len(self.slots)]
+
+    def inputs(self):
+        s = self._slot(self._next)
+        if s["busy"]:
+            self.result(s["ticket"])
+        return s["chk"].host_inputs()
+
+    def _all_gather(self, out, inp):
+        import torch.distributed as dist
+
+        try:
+            dist.all_gather_into_tensor(out, inp, group=self.group)
+        except (RuntimeError, NotImplementedError):  # backends without the flat form (gloo)
+            dist.all_gather(list(out.unbind(0)), inp, group=self.group)
+
+    def submit(self) -> int:
+        t = N.torch()
+        ticket = self._next
+        s = self._slot(ticket)
+        if s["busy"]:
+            self.result(s["ticket"])
+        chk, ev = s["chk"], s["ev"]
+        C_, P, pdt = chk._shape
+        with t.cuda.stream(self.copy):
+            self.copy.wait_event(ev["compute"])
+            chk.q_dev.copy_(chk.q_host, non_blocking=True)
+            chk.p_dev.copy_(chk.p_host, non_blocking=True)
+            ev["h2d"].record(self.copy)
+        with t.cuda.stream(self.compute):
+            self.compute.wait_event(ev["h2d"])
+            self.compute.wait_event(ev["d2h"])
+            cs = self.compute.cuda_stream
+            N.call("lsdf_fk_align", chk._chain, chk.robot.n_links, len(chk.sdfs), N.ptr(chk.q_dev), C_,
+                   chk.robot.dof, N.ptr(chk.limits), chk._env, chk._W, None, None, N.ptr(chk.R_geo),
+                   N.ptr(chk.dt_geo), N.ptr(chk.anchor_geo), N.ptr(chk.flags), cs)
+            part = s["part"].view(t.int32)
+            N.call("lsdf_voxelize_bitmap", N.ptr(chk.p_dev), int(pdt == np.float32), P, chk._env, s["part"], cs)
+            self._all_gather(s["gather"], part[self._bits])
+            self._all_gather(s["dropped"], part[1:2])  # counters[1]: dropped points of the slice
+            N.call("lsdf_occupancy_merge", s["gather"], self.world, s["dropped"], 1, chk._env, N.ptr(chk.ws), cs)
+            tr = chk.traj
+            N.call("lsdf_query_direct", N.ptr(chk.R_geo), N.ptr(chk.dt_geo), N.ptr(chk.anchor_geo), C_, tr.n_links,
+                   tr._table, ctypes.byref(chk._wstruct), chk._env, N.ptr(chk.ws), 0, chk.d_far_global,
+                   N.ptr(chk.qws), N.ptr(chk.d_dev), N.ptr(chk.link_dev), N.ptr(chk.voxel_dev), None, cs)
+            ev["compute"].record(self.compute)
+        d, link, voxel, flags = s["out"]
+        with t.cuda.stream(self.d2h):
+            self.d2h.wait_event(ev["compute"])
+            d.copy_(chk.d_dev, non_blocking=True)
+            link.copy_(chk.link_dev, non_blocking=True)
+            voxel.copy_(chk.voxel_dev, non_blocking=True)
+            flags.copy_(chk.flags, non_blocking=True)
+            ev["d2h"].record(self.d2h)
+        s["busy"], s["ticket"] = True, ticket
+        self._next += 1
+        return ticket
+
+    def result(self, ticket: int):
+        s = self._slot(ticket)
+        if s["ticket"] != ticket:
+            raise ValidationError(f"cycle {ticket} is no longer held (pipeline depth {self.depth})")
+        s["ev"]["d2h"].synchronize()
+        d, link, voxel, flags = (a.numpy() for a in s["out"])
+        if s["busy"]:
+            s["busy"] = False
+            if flags[0] or flags[1]:
+                chk = s["chk"]
+                chk._raise_flags(chk.host_inputs()[0], flags)
+        return d.copy(), link.copy(), voxel.copy()

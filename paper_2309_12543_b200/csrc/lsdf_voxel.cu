@@ -118,6 +118,23 @@ voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, do
     }
 }
 
+// OR of n_parts partial bitmaps (n_parts, n_words) into the occupancy bitmap;
+// thread 0 also sums the parts' dropped-point counters.
+__global__ void merge_bitmaps_kernel(const uint32_t* __restrict__ parts, int32_t n_parts, int64_t n_words,
+                                     const int32_t* __restrict__ dropped, int64_t dropped_stride, uint32_t* bitmap,
+                                     int32_t* counters) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (int k = 0; k < n_parts; ++k) v |= __ldg(parts + k * n_words + w);
+        bitmap[w] = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        int32_t total = 0;
+        for (int k = 0; k < n_parts; ++k) total += dropped[k * dropped_stride];
+        counters[1] = total;
+    }
+}
+
 __global__ void __launch_bounds__(SCAN_THREADS) prefix_only_kernel(const uint32_t* bitmap, int64_t n_words,
                                                                     int32_t* prefix, int32_t* counters) {
     prefix_scan_block(bitmap, n_words, prefix, counters);
@@ -235,6 +252,19 @@ extern "C" int lsdf_voxelize_bitmap(const void* points_dev, int32_t points_f32, 
 extern "C" int lsdf_occupancy_prefix(const lsdf_env_grid* env, void* occupancy_dev, void* stream) {
     Occupancy o = carve_occupancy(occupancy_dev, *env);
     prefix_only_kernel<<<1, SCAN_THREADS, 0, (cudaStream_t)stream>>>(o.bitmap, o.n_words, o.prefix, o.counters);
+    return check_launch("prefix_only_kernel");
+}
+
+extern "C" int lsdf_occupancy_merge(const uint32_t* parts_dev, int32_t n_parts, const int32_t* dropped_dev,
+                                    int64_t dropped_stride, const lsdf_env_grid* env, void* occupancy_dev,
+                                    void* stream) {
+    if (n_parts < 1) return fail(LSDF_ERR_VALIDATION, "occupancy merge: %d parts", n_parts);
+    cudaStream_t s = (cudaStream_t)stream;
+    Occupancy o = carve_occupancy(occupancy_dev, *env);
+    merge_bitmaps_kernel<<<grid_for(o.n_words, 256), 256, 0, s>>>(parts_dev, n_parts, o.n_words, dropped_dev,
+                                                                   dropped_stride, o.bitmap, o.counters);
+    LSDF_TRY(check_launch("merge_bitmaps_kernel"));
+    prefix_only_kernel<<<1, SCAN_THREADS, 0, s>>>(o.bitmap, o.n_words, o.prefix, o.counters);
     return check_launch("prefix_only_kernel");
 }
 

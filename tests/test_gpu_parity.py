@@ -764,3 +764,59 @@ def test_mixed_link_grids(L, C):
         if link[c] >= 0:
             assert pl[c, link[c]] == d[c] and np.all(pl[c, :link[c]] > d[c])
 
+
+
+def _sharded_worker(rank, world, port, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    # gloo: several ranks share the one GPU of this box (a functional check of
+    # the exchange; production runs one rank per GPU over NCCL)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2309_12543_b200 as L
+    from paper_2309_12543_b200 import scenarios as S
+    from paper_2309_12543_b200.sharding import shard_range
+
+    g = golden("scene_c2")
+    robot, grid, sdfs, window = _scene(L, g)
+    q = S.random_configs(_doc(g), 64, seed=5)
+    pts = np.concatenate([S.human_cloud(40_000, seed=5), np.float64([[5.0, 0, 0], [np.nan, 0, 0]])]).astype(np.float32)
+    lo, hi = shard_range(len(pts), rank, world)
+    ql, qh = shard_range(len(q), rank, world)
+    pipe = L.ShardedCloudPipeline(robot, sdfs, grid, window, qh - ql, hi - lo, np.float32, depth=2)
+    results = []
+    for k in range(3):
+        qv, pv = pipe.inputs()
+        qv[...] = q[ql:qh]
+        pv[...] = pts[lo:hi]
+        results.append(pipe.result(pipe.submit()))
+    chk = L.DistanceChecker(robot, sdfs, grid, window).prepare(qh - ql, len(pts), np.float32)
+    want = chk.query(q[ql:qh], pts)
+    out.put((rank, all(all(np.array_equal(a, b) for a, b in zip(r, want)) for r in results)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_cloud_pipeline(L):
+    """Each of 2 ranks uploads half of the cloud; the bitmap all-gather + OR
+    merge reproduces one rank voxelizing everything (dropped points too)."""
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == {0: True, 1: True}
