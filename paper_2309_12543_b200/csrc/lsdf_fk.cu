@@ -33,7 +33,7 @@ struct FkParams {
 };
 
 constexpr int FK_THREADS = 128;
-constexpr int64_t FK_SERIAL_MIN = 4096;
+constexpr int64_t FK_SERIAL_MIN = 6144;  // measured crossover (tools/_fk_sweep.py): 12.5 vs 13.9 us at 4096, 16.7 vs 14.6 at 8192
 #ifndef FK_STAGE_OUTPUTS
 #define FK_STAGE_OUTPUTS 1
 #endif  // configurations from which one thread per configuration wins
