@@ -450,7 +450,7 @@ def test_config2_full_size_properties(L):
 
 
 def test_config4_shape_large_batch(L):
-    """Config-4 shape (arm7g, crowd, 64^3), 6,000 waypoints: the whole batch ==
+    """Config-4 shape (arm7g, crowd, 64^3), 8,000 waypoints: the whole batch ==
     the same waypoints in chunks (dynamic task fetch and grab sizes differ) ==
     the oracle on a subset; the graph checker agrees bit for bit."""
     from oracle import linksdf_oracle as O
@@ -462,18 +462,18 @@ def test_config4_shape_large_batch(L):
     sdfs = [L.build_link_sdf(robot.links[i].geometry, shape.link_extent, shape.link_res, link_id=i)
             for i in robot.geometry_links]
     window = L.WindowGeometry.build(shape.link_extent, grid)
-    C = 6000
+    C = 8000  # >= the FK thread-per-configuration threshold; the 2,000 chunks use the 3-phase kernel
     q = S.random_configs(shape.robot, C, seed=3)
     pts = S.cloud_for(shape, seed=3)[:300_000].astype(np.float32)
     obs = L.voxelize_pointcloud(pts, grid)
     traj = L.TrajectorySdf.from_configs(robot, q, sdfs, grid, window)
     d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
-    parts = [L.query_min_distances(L.TrajectorySdf.from_configs(robot, q[a:a + 1500], sdfs, grid, window), obs,
-                                   return_argmin=True) for a in range(0, C, 1500)]
+    parts = [L.query_min_distances(L.TrajectorySdf.from_configs(robot, q[a:a + 2000], sdfs, grid, window), obs,
+                                   return_argmin=True) for a in range(0, C, 2000)]
     assert np.array_equal(np.concatenate([p[0] for p in parts]), d)
     assert np.array_equal(np.concatenate([p[1] for p in parts]), link)
     assert np.array_equal(np.concatenate([p[2] for p in parts]), voxel)
-    sub = np.arange(0, C, 750)
+    sub = np.arange(0, C, 1000)
     grids = [s.values for s in sdfs]
     rd, rl, rv = O.run_pipeline(shape.robot, q[sub], pts, shape.grid_extent, shape.grid_res,
                                 shape.link_extent, grids, [shape.link_res] * len(grids))
