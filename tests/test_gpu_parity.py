@@ -820,3 +820,23 @@ def test_sharded_cloud_pipeline(L):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res == {0: True, 1: True}
+
+
+def test_clamp_above_link_far_values(L):
+    """d_far_global above the links' own far value (the masked window cells
+    then count, query.py:82-83): the full-window kernel path, direct == dense
+    gather bit for bit, per-link minima included."""
+    g = golden("scene_c1")
+    robot, grid, sdfs, window = _scene(L, g)
+    clamp = 0.45
+    assert all(s.d_far < clamp for s in sdfs)
+    traj = L.TrajectorySdf.from_configs(robot, g["q"], sdfs, grid, window, d_far_global=clamp)
+    obs = L.voxelize_pointcloud(g["points"], grid)
+    d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
+    dense = L.RobotSdfBatch(traj.device_values(), grid, clamp)
+    d2, _, v2 = L.query_min_distances(dense, obs, return_argmin=True)
+    assert np.array_equal(d, d2) and np.array_equal(voxel, v2)
+    assert np.any(d > max(s.d_far for s in sdfs) - 1e-6) or np.all(d < clamp)
+    vm = traj.materialize()
+    for a, b in zip(L.query_min_distances(vm, obs, return_argmin=True), (d, link, voxel)):
+        assert np.array_equal(a, b)
