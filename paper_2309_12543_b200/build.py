@@ -76,5 +76,24 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+DEMO_SRC = PKG.parent / "tests" / "native" / "abi_demo.c"
+DEMO = OUT_DIR / "abi_demo"
+
+
+def build_demo(force: bool = False) -> Path:
+    """The plain-C ABI client (tests/native/abi_demo.c), linked against the library."""
+    lib = build()
+    if DEMO.exists() and not force and DEMO.stat().st_mtime >= max(DEMO_SRC.stat().st_mtime, lib.stat().st_mtime):
+        return DEMO
+    nvcc = _nvcc()
+    cmd = [nvcc, "-O2", "-x", "c", str(DEMO_SRC), "-I", str(INCLUDE), "-L", str(OUT_DIR), "-llinksdf_b200",
+           "-Xlinker", "-rpath=$ORIGIN", "-o", str(DEMO)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"abi_demo build failed:\n{r.stdout}\n{r.stderr}")
+    return DEMO
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build_demo(force="--force" in sys.argv))

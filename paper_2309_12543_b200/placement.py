@@ -158,11 +158,14 @@ class WindowGeometry:
     def matches_link(self, sdf: LinkSdf) -> bool:
         return bool(np.all(np.abs(sdf.extent - self.extent) <= 1e-9 * self.extent))
 
-    def device_tables(self):
-        """Upload (once) the P tables, column z-ranges and mask bits; returns (struct, tensors)."""
-        if self._tables is not None:
-            return self._tables
-        t = N.torch()
+    def host_tables(self) -> dict:
+        """The ``lsdf_window`` tables as host arrays (what ``device_tables`` uploads).
+
+        P (3, Wmax) f64 normalized offsets; zrange (W1*W0, 2) i16 or None when a
+        column's kept cells are not one z interval; mask_bits u32; shell_cells
+        u32 / shell_radius f32 (kept cells by distance from the window centre,
+        radius rounded down); kept_cells i32 (x-fastest order).
+        """
         W = [int(d) for d in self.dims]
         if max(W) > 256:
             raise ValidationError(f"window width {W} exceeds the supported 256 cells")
@@ -183,19 +186,6 @@ class WindowGeometry:
                 if len(zs):
                     zr[my, mx] = (zs[0], zs[-1] + 1)
                     interval &= bool(len(zs) == zs[-1] + 1 - zs[0])
-        dev = {
-            "P": N.to_device(P, t.float64),
-            "mask_bits": N.to_device(words.view(np.int32), t.int32),
-            "zrange": N.to_device(zr.reshape(-1, 2), t.int16) if interval else None,
-        }
-        s = N.WindowT()
-        s.W[:] = W
-        s.n_masked = self.n_masked
-        s.e_r = float(self.extent)
-        s.P_dev = N.ptr(dev["P"])
-        s.Wmax = Wmax
-        s.zrange_dev = N.ptr(dev["zrange"])
-        s.mask_bits_dev = N.ptr(dev["mask_bits"])
         # kept cells sorted by distance from the window centre (shell order)
         off = _axis_offsets(self.extent, self.grid, False)
         mxs, mys, mzs = np.nonzero(self.mask)
@@ -204,10 +194,33 @@ class WindowGeometry:
         packed = (mxs | (mys << 8) | (mzs << 16)).astype(np.uint32)[order]
         radius = np.nextafter(dist[order].astype(np.float32), np.float32(-np.inf))  # rounded down
         radius = np.minimum(radius, dist[order]).astype(np.float32)
-        # kept cells in x-fastest order (the provider's point order)
-        dev["kept_cells"] = N.to_device(np.nonzero(self.mask.ravel(order="F"))[0].astype(np.int32), t.int32)
-        dev["shell_cells"] = N.to_device(packed.view(np.int32), t.int32)
-        dev["shell_radius"] = N.to_device(radius, t.float32)
+        return {"W": W, "Wmax": Wmax, "n_masked": self.n_masked, "e_r": float(self.extent), "P": P,
+                "zrange": zr.reshape(-1, 2) if interval else None, "mask_bits": words,
+                "shell_cells": packed, "shell_radius": radius,
+                "kept_cells": np.nonzero(mask_f)[0].astype(np.int32)}
+
+    def device_tables(self):
+        """Upload (once) the host tables; returns (``lsdf_window`` struct, tensors)."""
+        if self._tables is not None:
+            return self._tables
+        t = N.torch()
+        h = self.host_tables()
+        dev = {
+            "P": N.to_device(h["P"], t.float64),
+            "mask_bits": N.to_device(h["mask_bits"].view(np.int32), t.int32),
+            "zrange": N.to_device(h["zrange"], t.int16) if h["zrange"] is not None else None,
+            "kept_cells": N.to_device(h["kept_cells"], t.int32),
+            "shell_cells": N.to_device(h["shell_cells"].view(np.int32), t.int32),
+            "shell_radius": N.to_device(h["shell_radius"], t.float32),
+        }
+        s = N.WindowT()
+        s.W[:] = h["W"]
+        s.n_masked = h["n_masked"]
+        s.e_r = h["e_r"]
+        s.P_dev = N.ptr(dev["P"])
+        s.Wmax = h["Wmax"]
+        s.zrange_dev = N.ptr(dev["zrange"])
+        s.mask_bits_dev = N.ptr(dev["mask_bits"])
         s.shell_cells_dev = N.ptr(dev["shell_cells"])
         s.shell_radius_dev = N.ptr(dev["shell_radius"])
         self._tables = (s, dev)

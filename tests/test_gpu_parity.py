@@ -840,3 +840,31 @@ def test_clamp_above_link_far_values(L):
     vm = traj.materialize()
     for a, b in zip(L.query_min_distances(vm, obs, return_argmin=True), (d, link, voxel)):
         assert np.array_equal(a, b)
+
+
+# ----------------------------------------------------------------------------- plain-C client
+
+
+@pytest.mark.parametrize("name", ["scene_c2", "scene_arm7"])
+def test_c_abi_client(L, name, tmp_path):
+    """tests/native/abi_demo.c (C99 + CUDA runtime, no Python in the process) runs FK -> voxelize ->
+    fused query through the C ABI; repeated cycles reuse the workspace.  Same answers as the goldens,
+    bit-identical to the Python facade."""
+    import subprocess
+
+    from paper_2309_12543_b200.build import build_demo
+    from tests.native.abi_scene import read_result, write_scene
+
+    g = golden(name)
+    robot, grid, sdfs, window = _scene(L, g)
+    scene, out = tmp_path / "scene.bin", tmp_path / "out.bin"
+    write_scene(scene, robot, sdfs, grid, window, g["q"], g["points"], repeat=3)
+    r = subprocess.run([str(build_demo()), str(scene), str(out)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "kernels enqueued" in r.stdout
+    d, link, voxel, flags = read_result(out, len(g["q"]))
+    assert flags.tolist() == [0, 0]
+    assert np.abs(d.astype(np.float64) - g["d"]).max() <= D_TOL
+    assert np.array_equal(link, g["link"]) and np.array_equal(voxel, g["voxel"])
+    d_py, link_py, voxel_py = L.query_trajectory(robot, g["q"], sdfs, grid, window, g["points"])
+    assert np.array_equal(d, d_py) and np.array_equal(link, link_py) and np.array_equal(voxel, voxel_py)

@@ -102,3 +102,34 @@ def test_validation_errors_host_side():
     g = L.EnvGrid(1.0, 0.1)
     with pytest.raises(L.ValidationError):
         L.assemble_robot_sdfs([], g, 10_000_000, 0.5, max_bytes=1 << 20)
+
+
+def test_c_abi_client_builds_and_fails_loudly(tmp_path):
+    """The plain-C client (tests/native/abi_demo.c) links against the library alone, reads a scene
+    written from the host recipes, and without a GPU exits non-zero with a CUDA error (no CPU path)."""
+    import subprocess
+
+    import torch
+
+    import paper_2309_12543_b200 as L
+    from paper_2309_12543_b200 import scenarios as S
+    from paper_2309_12543_b200.build import build_demo
+    from tests.native.abi_scene import write_scene
+
+    exe = build_demo()
+    robot = L.RobotModel.from_dict(S.ARM7G)
+    grid = L.EnvGrid(1.0, 0.04)
+    ax = -0.32 + (np.arange(16) + 0.5) * 0.04
+    X, Y, Z = np.meshgrid(ax, ax, ax, indexing="ij")
+    sdfs = [L.LinkSdf(0.32, 0.04, np.sqrt(X * X + Y * Y + Z * Z) - 0.05, link_id=i) for i in robot.geometry_links]
+    window = L.WindowGeometry.build(0.32, grid)
+    q = np.zeros((8, robot.dof))
+    scene = tmp_path / "scene.bin"
+    write_scene(scene, robot, sdfs, grid, window, q, np.zeros((5, 3), np.float32))
+    raw = scene.read_bytes()
+    assert raw[:8] == b"LSDFABI1"
+    assert int.from_bytes(raw[8:16], "little") == 32  # header section
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: tests/test_gpu_parity.py::test_c_abi_client covers the run")
+    r = subprocess.run([str(exe), str(scene), str(tmp_path / "out.bin")], capture_output=True, text=True, timeout=60)
+    assert r.returncode != 0 and "cuda" in r.stderr.lower()
