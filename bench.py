@@ -162,14 +162,24 @@ class L2Flush:
         self.buf.zero_()
 
 
+SPIN_CYCLES = 200_000  # ~0.1 ms GPU spin: longer than the host needs to enqueue one step
+
+
 def _time_steps(torch, fn, steps, flush, before=None):
-    """Per-step device times (ms), CUDA events on the launching stream, L2 flushed before each."""
+    """Per-step device times (ms), CUDA events on the launching stream, L2 flushed before each.
+
+    A short GPU spin sits between the flush and the start event, so the host
+    has enqueued the step before the start event fires: the interval is the
+    step's device execution, not the host's launch latency (which the e2e
+    numbers include).
+    """
     stream = torch.cuda.current_stream()
     marks = []
     for k in range(steps):
         if before is not None:
             before(k)
         flush()
+        torch.cuda._sleep(SPIN_CYCLES)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -341,7 +351,8 @@ def run_ours(args, rank, world, dist, sampler):
                    "waypoints": C_total, "points": shape.n_points, "occupied_voxels": n_occ,
                    "parallelism": f"waypoint shards x{world}",
                    "l2": "flushed (256 MiB write) before every timed step",
-                   "timing": "device: CUDA events around a graph replay of the cycle"},
+                   "timing": "device: CUDA events around a graph replay of the cycle, enqueued behind a GPU spin "
+                             "(host launch latency excluded; e2e includes it)"},
         "gpu_launches": per_cycle * args.steps,
         "gpu_launches_per_step": per_cycle,
         "e2e": _e2e_entry(C_total, e2e_ms, single_ms, int(n_local * robot.dof * 8 + (phi - plo) * 12),

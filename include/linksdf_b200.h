@@ -26,6 +26,7 @@
 #ifndef LINKSDF_B200_H
 #define LINKSDF_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -140,6 +141,15 @@ uint64_t lsdf_launch_count(void);
 /* Device address of page-locked (mapped) host memory: lets the real-time
  * path read its inputs and write its results over PCIe without staging. */
 int lsdf_host_device_pointer(void* host, void** dev);
+
+/* Reserve up to `bytes` of L2 as the persisting set-aside on the current
+ * device (clamped to cudaDevAttrMaxPersistingL2CacheSize; never shrinks) and
+ * report what was granted.  The fused query then marks the link grids it
+ * reads persisting (an access-policy window over their span, hit ratio =
+ * granted / span), so grids stay in L2 between control cycles while other
+ * work streams through the cache (north_star: "grids pinned in L2").  Call
+ * it outside stream capture; without it the query runs with normal caching. */
+int lsdf_l2_reserve(size_t bytes, size_t* granted);
 
 /* ---- stage 1: forward kinematics + alignment --------------------------- */
 

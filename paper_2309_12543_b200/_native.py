@@ -100,6 +100,7 @@ _SIGS = {
     "lsdf_mlp_packed_bytes": [_I32, _I64],
     "lsdf_mlp_pack": [_P, _I32, _I64, _P, _P],
     "lsdf_host_device_pointer": [_P, C.POINTER(C.c_void_p)],
+    "lsdf_l2_reserve": [C.c_size_t, C.POINTER(C.c_size_t)],
 }
 
 EXPORTS = tuple(_SIGS) + ("lsdf_version", "lsdf_last_error", "lsdf_launch_count")
@@ -243,3 +244,10 @@ def f64s(v, n: int) -> C.Array:
     vals = [float(x) for x in np.ravel(v)]
     arr[: len(vals)] = vals
     return arr
+
+
+def l2_reserve(nbytes: int) -> int:
+    """Persisting-L2 set-aside on the current device (lsdf_l2_reserve); returns the bytes granted."""
+    got = C.c_size_t(0)
+    call("lsdf_l2_reserve", int(nbytes), C.byref(got))
+    return int(got.value)

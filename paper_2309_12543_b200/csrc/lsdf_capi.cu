@@ -26,3 +26,29 @@ extern "C" int lsdf_host_device_pointer(void* host, void** dev) {
     }
     return LSDF_OK;
 }
+
+// Persisting-L2 set-aside (bytes granted per device), read by the query
+// launches that attach an access-policy window over the link grids.
+namespace lsdf {
+size_t& l2_persist_bytes(int dev) {
+    static size_t granted[64] = {0};
+    return granted[dev & 63];
+}
+}  // namespace lsdf
+
+extern "C" int lsdf_l2_reserve(size_t bytes, size_t* granted) {
+    int dev = 0;
+    LSDF_TRY(lsdf::check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+    int max_persist = 0;
+    LSDF_TRY(lsdf::check_cuda(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev),
+                              "cudaDevAttrMaxPersistingL2CacheSize"));
+    size_t want = bytes < (size_t)max_persist ? bytes : (size_t)max_persist;
+    // the set-aside only grows: several trajectories may share the device
+    if (want < lsdf::l2_persist_bytes(dev)) want = lsdf::l2_persist_bytes(dev);
+    LSDF_TRY(lsdf::check_cuda(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want), "persisting L2 limit"));
+    size_t got = 0;
+    LSDF_TRY(lsdf::check_cuda(cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize), "persisting L2 limit"));
+    lsdf::l2_persist_bytes(dev) = got;
+    if (granted) *granted = got;
+    return LSDF_OK;
+}

@@ -14,6 +14,7 @@ namespace lsdf {
 
 std::string& last_error();
 std::atomic<uint64_t>& launch_counter();
+size_t& l2_persist_bytes(int dev);
 
 inline int fail(int code, const char* fmt, ...) {
     char buf[512];

@@ -625,12 +625,53 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
             const int64_t n_tasks = C * split * n_group;
             int64_t grab = n_tasks / (resident * WARPS * 16);
             grab = grab < 1 ? 1 : (grab > GRAB_MAX ? GRAB_MAX : grab);
+            // grids pinned in L2: an access-policy window over the span of
+            // this group's packed grids (contiguous when TrajectorySdf packed
+            // them into one arena), persisting within the set-aside that
+            // lsdf_l2_reserve granted; the attribute is captured into graphs
+            cudaLaunchAttribute attr_l2[1];
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(32 * WARPS);
+            cfg.dynamicSmemBytes = smem_s;
+            cfg.stream = s;
+            cfg.attrs = attr_l2;
+            cfg.numAttrs = 0;
+            const size_t persist = l2_persist_bytes(dev);
+            if (persist > 0) {
+                uintptr_t lo = UINTPTR_MAX, hi = 0;
+                for (int k = 0; k < n_group; ++k) {
+                    const lsdf_link_grid& g = grids[p.group[k]];
+                    const uintptr_t a = (uintptr_t)g.packed_dev;
+                    const uintptr_t b = a + (uintptr_t)(g.dims[0] - 1) * (g.dims[1] - 1) * (g.dims[2] - 1) * 32;
+                    lo = a < lo ? a : lo;
+                    hi = b > hi ? b : hi;
+                }
+                thread_local int w_dev = -1, w_max = 0;
+                if (w_dev != dev) {
+                    cudaDeviceGetAttribute(&w_max, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+                    w_dev = dev;
+                }
+                const size_t span = hi - lo;
+                if (span > 0 && span <= (size_t)w_max) {
+                    attr_l2[0].id = cudaLaunchAttributeAccessPolicyWindow;
+                    attr_l2[0].val.accessPolicyWindow.base_ptr = (void*)lo;
+                    attr_l2[0].val.accessPolicyWindow.num_bytes = span;
+                    attr_l2[0].val.accessPolicyWindow.hitRatio = span <= persist ? 1.0f : (float)persist / span;
+                    attr_l2[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                    attr_l2[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                    cfg.numAttrs = 1;
+                }
+            }
+            const int ig = (int)grab;
+            cudaError_t le;
             if (by_position)
-                query_shells_kernel<true><<<grid, 32 * WARPS, smem_s, s>>>(p, n_group, n_launch, (int)grab,
-                                                                          stage_shell, stage_bits, o.n_words);
+                le = cudaLaunchKernelEx(&cfg, query_shells_kernel<true>, p, n_group, n_launch, ig, stage_shell,
+                                        stage_bits, o.n_words);
             else
-                query_shells_kernel<false><<<grid, 32 * WARPS, smem_s, s>>>(p, n_group, n_launch, (int)grab,
-                                                                           stage_shell, stage_bits, o.n_words);
+                le = cudaLaunchKernelEx(&cfg, query_shells_kernel<false>, p, n_group, n_launch, ig, stage_shell,
+                                        stage_bits, o.n_words);
+            if (le != cudaSuccess) return fail(LSDF_ERR_CUDA, "query_shells_kernel: %s", cudaGetErrorString(le));
             ++n_launch;
         } else if (full) {
             if (by_position)

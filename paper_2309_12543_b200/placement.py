@@ -247,11 +247,29 @@ class ExactTransformProvider:
         return grid_transform_exact(rotations, delta_t, self.window.extent, self.window.masked_points)
 
 
-def link_grid_table(sdfs: Sequence[LinkSdf], packed: bool = False):
+def link_grid_table(sdfs: Sequence[LinkSdf], packed: bool = False, packed_ptrs=None):
     table = (N.LinkGridT * len(sdfs))()
     for i, s in enumerate(sdfs):
         table[i] = s.c_struct(packed)
+        if packed_ptrs is not None:
+            table[i].packed_dev = packed_ptrs[i]
     return table
+
+
+def packed_arena(sdfs: Sequence[LinkSdf]):
+    """One contiguous device copy of the links' packed-corner grids and each link's address in it.
+
+    Contiguity lets the query mark every grid it reads persisting in L2 with
+    a single access-policy window (lsdf_l2_reserve).
+    """
+    t = N.torch()
+    parts = [s.packed_values() for s in sdfs]
+    arena = t.cat(parts) if len(parts) > 1 else parts[0].clone()
+    ptrs, off = [], 0
+    for part in parts:
+        ptrs.append(N.ptr(arena) + off * 4)
+        off += int(part.numel())
+    return arena, ptrs
 
 
 def _check_links(sdfs, window: WindowGeometry):

@@ -22,6 +22,7 @@ the gather query run as CUDA kernels too.
 from __future__ import annotations
 
 import ctypes
+import os
 import struct
 from dataclasses import dataclass
 from pathlib import Path
@@ -178,8 +179,8 @@ class TrajectorySdf:
     """
 
     def __init__(self, sdfs, grid: EnvGrid, window, R_dev, dt_dev, anchor_dev, d_far_global=None,
-                 flags=None):
-        from .placement import _check_links, link_grid_table
+                 flags=None, pin_l2: bool | None = None):
+        from .placement import _check_links, link_grid_table, packed_arena
 
         _check_links(sdfs, window)
         self.sdfs = list(sdfs)
@@ -189,7 +190,12 @@ class TrajectorySdf:
         self.dt = dt_dev
         self.anchor = anchor_dev
         self.d_far_global = float(min(s.d_far for s in sdfs) if d_far_global is None else d_far_global)
-        self._table = link_grid_table(self.sdfs, packed=True)
+        # the packed grids in one arena, pinned in L2 (persisting set-aside)
+        self._arena, ptrs = packed_arena(self.sdfs)
+        self._table = link_grid_table(self.sdfs, packed=True, packed_ptrs=ptrs)
+        if pin_l2 is None:  # LSDF_L2_PIN=0 turns the set-aside off (A/B measurements)
+            pin_l2 = os.environ.get("LSDF_L2_PIN", "1") != "0"
+        self.l2_pinned_bytes = N.l2_reserve(self._arena.numel() * 4) if pin_l2 else 0
         self._ws = None
         self._dense = None
         self._flags = flags

@@ -241,6 +241,26 @@ def test_direct_query_stage_isolated(L, name):
     assert np.array_equal(traj.per_link_min_distances(obs), g["per_link"])
 
 
+def test_grids_pinned_in_l2(L):
+    """The packed grids live in one arena marked persisting in L2; results equal the unpinned query's."""
+    g = golden("scene_c2")
+    robot, grid, sdfs, window = _scene(L, g)
+    gl = g["geometry_links"]
+    poses = L.LinkPoseBatch(rotations=g["R"][:, gl], translations=g["T"][:, gl])
+    traj = L.TrajectorySdf.from_poses(sdfs, poses, grid, L.ExactTransformProvider(window))
+    assert traj.l2_pinned_bytes > 0
+    base = traj._arena.data_ptr()
+    sizes = [s.packed_values().numel() * 4 for s in sdfs]
+    assert [traj._table[i].packed_dev for i in range(len(sdfs))] == [base + sum(sizes[:i]) for i in range(len(sdfs))]
+    plain = L.TrajectorySdf(sdfs, grid, window, traj.R, traj.dt, traj.anchor, pin_l2=False)
+    obs = L.voxelize_pointcloud(g["points"], grid)
+    a = L.query_min_distances(traj, obs, return_argmin=True)
+    b = L.query_min_distances(plain, obs, return_argmin=True)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a[0], g["d"]) and np.array_equal(a[1], g["link"]) and np.array_equal(a[2], g["voxel"])
+
+
 @pytest.mark.parametrize("name", ["scene_c1", "scene_c2", "scene_arm7"])
 def test_full_pipeline_from_configs(L, name):
     g = golden(name)

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--device-only", action="store_true", help="inputs staged in HBM (the bench's value path)")
+    ap.add_argument("--flush", action="store_true", help="write 256 MiB (evicts L2) before every step")
     args = ap.parse_args()
     import torch
 
@@ -37,7 +38,10 @@ def main():
     if args.device_only:
         chk.q_dev.copy_(torch.from_numpy(q).cuda())
         chk.p_dev.copy_(torch.from_numpy(pts).cuda())
+        junk = torch.empty(64 << 20, dtype=torch.float32, device="cuda") if args.flush else None
         for _ in range(args.steps):
+            if junk is not None:
+                junk.fill_(1.0)
             chk.launch(device_only=True)
         torch.cuda.synchronize()
         d, link = chk.d_dev.cpu().numpy(), chk.link_dev.cpu().numpy()
