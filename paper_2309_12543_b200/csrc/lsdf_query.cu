@@ -63,6 +63,9 @@ struct QueryParams {
     uint32_t* counters;          // [LSDF_MAX_LINKS] shell-scan work counters (zero between launches)
     unsigned long long* keys;    // C: ~best key (atomicMax of the complement, zero = empty)
     uint32_t* perlink;           // C x n_geo: ~orderable(min value)
+    uint32_t* link_hist;         // [LSDF_MAX_LINKS] argmin-link counts of the previous cycle (link order)
+    uint32_t* exit_count;        // CTAs of the shell scan that have finished (last one resets link_hist)
+    int32_t track_order;         // finalize accumulates link_hist (the shell scan consumes and resets it)
     float* d_out;
     int32_t* link_out;
     int32_t* voxel_out;
@@ -72,7 +75,8 @@ struct QueryParams {
 constexpr int WARPS = 8;
 constexpr int QCAP = 32 * 16 + 32;  // queue entries per warp: <= 16 bits per lane per round
 
-__device__ __forceinline__ void finalize(const QueryParams& p, int64_t c) {
+// Returns the argmin link (-1 when clamped).
+__device__ __forceinline__ int finalize(const QueryParams& p, int64_t c) {
     const uint64_t k = ~(uint64_t)p.keys[c];
     p.keys[c] = 0ull;  // leave the workspace zeroed for the next launch
     if (p.per_link != nullptr) {
@@ -88,12 +92,13 @@ __device__ __forceinline__ void finalize(const QueryParams& p, int64_t c) {
         p.d_out[c] = p.clamp;
         p.link_out[c] = -1;
         p.voxel_out[c] = -1;
-        return;
+        return -1;
     }
     const uint32_t lo = (uint32_t)k;
     const uint32_t pos = lo / (uint32_t)p.n_geo;
+    const int link = (int)(lo % (uint32_t)p.n_geo);
     p.d_out[c] = from_orderable(hi);
-    p.link_out[c] = (int32_t)(lo % (uint32_t)p.n_geo);
+    p.link_out[c] = link;
     if (p.by_position) {
         p.voxel_out[c] = (int32_t)pos;
     } else {  // rank of the winning voxel in np.unique order
@@ -101,6 +106,7 @@ __device__ __forceinline__ void finalize(const QueryParams& p, int64_t c) {
         const uint32_t below = b ? (p.bitmap[w] & ((1u << b) - 1u)) : 0u;
         p.voxel_out[c] = p.prefix[w] + __popc(below);
     }
+    return link;
 }
 
 template <bool FULL, bool BY_POS>
@@ -262,9 +268,9 @@ struct __align__(16) ShellSetup {
     int32_t pad_;
 };
 
-__device__ __forceinline__ void shell_setup(const QueryParams& p, uint32_t t, ShellSetup& s) {
+__device__ __forceinline__ void shell_setup(const QueryParams& p, const int* order, uint32_t t, ShellSetup& s) {
     const uint32_t per_link = (uint32_t)(p.C * p.split);
-    const int l = p.group[t / per_link];
+    const int l = order[t / per_link];
     const uint32_t r = t % per_link;
     const int64_t c = p.split == 1 ? r : r / p.split;
     const int64_t o = c * p.n_geo + l;
@@ -418,8 +424,10 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
 template <bool BY_POS>
 __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __grid_constant__ QueryParams p,
                                                                   int n_group, int launch, int grab,
-                                                                  int stage_shell, int stage_bits, int64_t n_words) {
+                                                                  int stage_shell, int stage_bits, int64_t n_words,
+                                                                  int last_launch) {
     extern __shared__ double s_dyn[];
+    __shared__ int s_order[LSDF_MAX_LINKS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* sP = s_dyn;
     float* sPf = (float*)(sP + 3 * p.Wmax);
@@ -439,6 +447,16 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
         }
     if (stage_bits)
         for (int64_t i = threadIdx.x; i < n_words; i += blockDim.x) s_bits[i] = __ldcg(p.bitmap + i);
+    if (threadIdx.x < 32) {  // links by decreasing argmin count of the previous cycle (ties keep p.group order)
+        const int k = threadIdx.x;
+        const uint32_t mine = (k < n_group && p.track_order) ? __ldcg(p.link_hist + p.group[k]) : 0u;
+        int rank = 0;
+        for (int j = 0; j < n_group; ++j) {
+            const uint32_t other = __shfl_sync(FULL_MASK, mine, j);
+            rank += (other > mine) | ((other == mine) & (j < k));
+        }
+        if (k < n_group) s_order[rank] = p.group[k];
+    }
     __syncthreads();
     ShellView sv;
     sv.cells = stage_shell ? s_cells : p.shell_cells;
@@ -460,22 +478,45 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
         base = __shfl_sync(FULL_MASK, base, 0);
         if (base >= n_tasks) break;
         const uint32_t cnt = min((uint32_t)grab, n_tasks - base);
-        if ((uint32_t)lane < cnt) shell_setup(p, base + lane, s_setup[warp][lane]);
+        if ((uint32_t)lane < cnt) shell_setup(p, s_order, base + lane, s_setup[warp][lane]);
         __syncwarp();
         for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS>(p, sv, queue, s_setup[warp][j], lane);
         __syncwarp();
     }
+    // the last CTA of the last launch clears the counts this cycle's finalize refills
+    if (p.track_order) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(p.exit_count, 1u) == gridDim.x - 1) {
+                *p.exit_count = 0u;
+                if (last_launch)
+                    for (int k = 0; k < LSDF_MAX_LINKS; ++k) p.link_hist[k] = 0u;
+            }
+        }
+    }
 }
 
 // (d, link, voxel) per configuration from the reduced keys; resets the slots.
+// Also counts the argmin links (block histogram, then one atomic per link):
+// the next shell scan processes the links most often closest first, so the
+// per-configuration threshold they publish lets the other links stop early.
 __global__ void finalize_kernel(const __grid_constant__ QueryParams p) {
+    __shared__ uint32_t hist[LSDF_MAX_LINKS];
+    if (threadIdx.x < LSDF_MAX_LINKS) hist[threadIdx.x] = 0;
+    __syncthreads();
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c < LSDF_MAX_LINKS) p.counters[c] = 0;  // shell-scan work counters
-    if (c < p.C) finalize(p, c);
+    const int link = c < p.C ? finalize(p, c) : -1;
+    if (p.track_order) {
+        if (link >= 0) atomicAdd(hist + link, 1u);
+        __syncthreads();
+        if (threadIdx.x < p.n_geo && hist[threadIdx.x]) atomicAdd(p.link_hist + threadIdx.x, hist[threadIdx.x]);
+    }
 }
 
 inline int64_t ws_bytes(int64_t C, int32_t n_geo) {
-    return align256(C * 4) + align256(C * 8) + align256(C * n_geo * 4);
+    return align256(C * 4) + align256(C * 8) + align256(C * n_geo * 4) + 256;
 }
 
 }  // namespace
@@ -520,6 +561,9 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     p.C = C;
     p.n_geo = n_geo;
     const bool shells = !full && window->shell_cells_dev != nullptr && window->shell_radius_dev != nullptr;
+    // the link order matters when links share a threshold and the batch is
+    // larger than one wave of tasks (small batches run all links at once)
+    p.track_order = shells && per_link_dev == nullptr && C * n_geo >= SEG_FILTER_MIN_TASKS;
     // the column scan needs enough warps in flight for small batches; the
     // shell scan stops early, so one warp per (configuration, link) is best
     const int64_t target = 148LL * 64;
@@ -557,6 +601,9 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     p.keys = (unsigned long long*)w;
     w += align256(C * 8);
     p.perlink = (uint32_t*)w;
+    w += align256(C * n_geo * 4);
+    p.link_hist = (uint32_t*)w;                    // LSDF_MAX_LINKS counts
+    p.exit_count = (uint32_t*)w + LSDF_MAX_LINKS;
     p.d_out = d_dev;
     p.link_out = link_dev;
     p.voxel_out = voxel_dev;
@@ -565,6 +612,19 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     const int64_t blocks_per_link = (C * split + WARPS - 1) / WARPS;
     cudaStream_t s = (cudaStream_t)stream;
     // one launch per group of links with identical grid geometry (normally one)
+    auto same_geom = [&](int a_, int b_) {
+        bool same = true;
+        for (int a = 0; a < 3; ++a)
+            same &= grids[a_].dims[a] == grids[b_].dims[a] && grids[a_].extent[a] == grids[b_].extent[a] &&
+                    grids[a_].resolution[a] == grids[b_].resolution[a];
+        return same;
+    };
+    int n_groups_total = 0;
+    for (int l = 0; l < n_geo; ++l) {
+        bool first = true;
+        for (int k = 0; k < l && first; ++k) first = !same_geom(k, l);
+        n_groups_total += first;
+    }
     bool done[LSDF_MAX_LINKS] = {false};
     int n_launch = 0;
     for (int l0 = 0; l0 < n_geo && (stages & STAGE_SCAN); ++l0) {
@@ -664,13 +724,14 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
                 }
             }
             const int ig = (int)grab;
+            const int last = n_launch + 1 == n_groups_total;
             cudaError_t le;
             if (by_position)
                 le = cudaLaunchKernelEx(&cfg, query_shells_kernel<true>, p, n_group, n_launch, ig, stage_shell,
-                                        stage_bits, o.n_words);
+                                        stage_bits, o.n_words, last);
             else
                 le = cudaLaunchKernelEx(&cfg, query_shells_kernel<false>, p, n_group, n_launch, ig, stage_shell,
-                                        stage_bits, o.n_words);
+                                        stage_bits, o.n_words, last);
             if (le != cudaSuccess) return fail(LSDF_ERR_CUDA, "query_shells_kernel: %s", cudaGetErrorString(le));
             ++n_launch;
         } else if (full) {

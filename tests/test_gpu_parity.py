@@ -503,6 +503,18 @@ def test_config4_shape_large_batch(L):
     for _ in range(2):
         dc, lc, vc = chk.query(q, pts)
         assert np.array_equal(dc, d) and np.array_equal(lc, link) and np.array_equal(vc, voxel)
+    # the scan orders the links by the previous cycle's argmin counts (kept in
+    # the query workspace); any order must give the same answer: force some
+    a256 = lambda n: (n + 255) // 256 * 256  # noqa: E731
+    G = len(sdfs)
+    import torch
+
+    hist = chk.qws[a256(C * 4) + a256(C * 8) + a256(C * G * 4):][: 4 * G].view(torch.int32)
+    assert int(hist.sum().item()) == int((link >= 0).sum())  # the last cycle's argmin counts
+    for counts in (np.arange(G)[::-1], np.arange(G), np.roll(np.arange(G), 3), np.zeros(G)):
+        hist.copy_(torch.from_numpy(counts.astype(np.int32) * 100))
+        dc, lc, vc = chk.query(q, pts)
+        assert np.array_equal(dc, d) and np.array_equal(lc, link) and np.array_equal(vc, voxel)
 
 
 @pytest.mark.parametrize("seed", [0, 1])
