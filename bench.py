@@ -334,13 +334,16 @@ def run_ours(args, rank, world, dist, sampler):
     alg_bytes = 4.0 * n_occ * n_local
     peak, peak_kind = _peaks()
     achieved = alg_bytes / (q_ms / 1e3) / 1e9
-    traffic = None
+    traffic = warp_inst = None
     tf = REPO / "profiles" / "query_traffic.json"
     if tf.exists() and world == 1:  # the ncu capture is of the single-GPU launch
         try:
-            traffic = json.loads(tf.read_text()).get(args.workload)
+            counters = json.loads(tf.read_text())
+            traffic = counters.get(args.workload)
+            warp_inst = counters.get(f"{args.workload}_warp_inst")
         except (ValueError, OSError):
             traffic = None
+    clocks = sampler.summary(t0 - 0.2, t1 + 0.2) if sampler else None
     out = {
         "metric": METRIC, "value": value, "unit": "waypoint-queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -360,8 +363,19 @@ def run_ours(args, rank, world, dist, sampler):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "query_shells_kernel", "kernel_ms": q_ms,
                      "algorithmic_bytes": alg_bytes, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst)"},
-        "clocks": sampler.summary(t0 - 0.2, t1 + 0.2) if sampler else None,
+        "clocks": clocks,
     }
+    if warp_inst:
+        # the kernel is issue-bound: its instruction stream against
+        # one warp instruction per SM sub-partition per cycle at the sampled clock
+        mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+        peak_i = 148 * 4 * mhz * 1e6 / 1e9
+        ach_i = warp_inst / (q_ms / 1e3) / 1e9
+        out["roofline_issue"] = {"bound": "issue", "achieved": ach_i, "peak": peak_i, "unit": "G warp-inst/s",
+                                 "frac": ach_i / peak_i, "warp_inst_per_launch": warp_inst,
+                                 "source": "smsp__inst_executed.sum of one ncu --set full capture of this launch "
+                                           "(profiles/query_traffic.json) / the live kernel time; peak = 148 SMs x 4 "
+                                           "SMSPs x 1 inst/cycle x the sampled SM clock"}
     return out
 
 

@@ -243,6 +243,26 @@ constexpr int QCAP_SHELL = 64;
 constexpr int SHELL_STAGE_MAX = 4096;   // kept cells staged in shared memory (W <= 20)
 constexpr int BITMAP_STAGE_MAX = 8192;  // occupancy words staged in shared memory (<= 262k voxels)
 
+__device__ __forceinline__ void* align16_ptr(void* q) {
+    return (void*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// Block-cooperative asynchronous global -> shared copy of nbytes (a multiple
+// of 4): 16-B chunks when both sides are 16-B aligned, 4-B copies otherwise.
+__device__ __forceinline__ void stage_async(void* dst, const void* src, size_t nbytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    const char* g = (const char*)src;
+    size_t head = 0;
+    if ((((uintptr_t)src | (uintptr_t)d) & 15) == 0) {
+        head = nbytes & ~(size_t)15;
+        for (size_t o = (size_t)threadIdx.x * 16; o < head; o += (size_t)blockDim.x * 16)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + (uint32_t)o), "l"(g + o));
+    }
+    for (size_t o = head + (size_t)threadIdx.x * 4; o < nbytes; o += (size_t)blockDim.x * 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d + (uint32_t)o), "l"(g + o));
+}
+
 struct ShellView {
     const uint32_t* cells;   // shell-ordered kept cells (shared or global)
     const float* radius;
@@ -268,9 +288,8 @@ struct __align__(16) ShellSetup {
     int32_t pad_;
 };
 
-__device__ __forceinline__ void shell_setup(const QueryParams& p, const int* order, uint32_t t, ShellSetup& s) {
+__device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_t t, ShellSetup& s) {
     const uint32_t per_link = (uint32_t)(p.C * p.split);
-    const int l = order[t / per_link];
     const uint32_t r = t % per_link;
     const int64_t c = p.split == 1 ? r : r / p.split;
     const int64_t o = c * p.n_geo + l;
@@ -427,36 +446,68 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
                                                                   int stage_shell, int stage_bits, int64_t n_words,
                                                                   int last_launch) {
     extern __shared__ double s_dyn[];
-    __shared__ int s_order[LSDF_MAX_LINKS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* sP = s_dyn;
     float* sPf = (float*)(sP + 3 * p.Wmax);
     uint32_t* s_queue = (uint32_t*)(sPf + 3 * p.Wmax + (p.Wmax & 1) * 3);  // keep 8-B alignment
-    uint32_t* s_cells = s_queue + WARPS * QCAP_SHELL;
-    float* s_radius = (float*)(s_cells + (stage_shell ? p.n_shell : 0));
-    uint32_t* s_bits = (uint32_t*)(s_radius + (stage_shell ? p.n_shell : 0));
+    // staged tables start on 16-B boundaries (cp.async 16-B chunks)
+    uint32_t* s_cells = (uint32_t*)align16_ptr(s_queue + WARPS * QCAP_SHELL);
+    float* s_radius = (float*)align16_ptr(s_cells + (stage_shell ? p.n_shell : 0));
+    uint32_t* s_bits = (uint32_t*)align16_ptr(s_radius + (stage_shell ? p.n_shell : 0));
     __shared__ ShellSetup s_setup[WARPS][GRAB_MAX];
-    for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) {
-        sP[i] = p.P[i];
-        sPf[i] = (float)p.P[i];
+    // Stage the shell list and the occupancy bitmap with asynchronous copies
+    // (all in flight at once), and fetch + set up the first tasks while they
+    // land: the latency path pays one memory round trip here, not one per
+    // loop iteration.
+    if (stage_shell) {
+        stage_async(s_cells, p.shell_cells, (size_t)p.n_shell * 4);
+        stage_async(s_radius, p.shell_radius, (size_t)p.n_shell * 4);
     }
-    if (stage_shell)
-        for (int i = threadIdx.x; i < p.n_shell; i += blockDim.x) {
-            s_cells[i] = __ldg(p.shell_cells + i);
-            s_radius[i] = __ldg(p.shell_radius + i);
-        }
-    if (stage_bits)
-        for (int64_t i = threadIdx.x; i < n_words; i += blockDim.x) s_bits[i] = __ldcg(p.bitmap + i);
-    if (threadIdx.x < 32) {  // links by decreasing argmin count of the previous cycle (ties keep p.group order)
-        const int k = threadIdx.x;
+    if (stage_bits) stage_async(s_bits, p.bitmap, (size_t)n_words * 4);
+    cp_async_commit();
+    for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) {
+        const double v = p.P[i];
+        sP[i] = v;
+        sPf[i] = (float)v;
+    }
+    // link processing order (lane k holds the link of rank k): decreasing
+    // argmin count of the previous cycle, ties in p.group order
+    int order_lane;
+    {
+        const int k = lane;
         const uint32_t mine = (k < n_group && p.track_order) ? __ldcg(p.link_hist + p.group[k]) : 0u;
         int rank = 0;
         for (int j = 0; j < n_group; ++j) {
             const uint32_t other = __shfl_sync(FULL_MASK, mine, j);
             rank += (other > mine) | ((other == mine) & (j < k));
         }
-        if (k < n_group) s_order[rank] = p.group[k];
+        order_lane = k < n_group ? p.group[k] : 0;
+        int inv = 0;
+        for (int j = 0; j < n_group; ++j) {
+            const int rj = __shfl_sync(FULL_MASK, rank, j);
+            const int gj = __shfl_sync(FULL_MASK, order_lane, j);
+            inv = rj == k ? gj : inv;
+        }
+        order_lane = inv;
     }
+    // dynamic task fetch: task durations vary by orders of magnitude (early
+    // stop), so each warp takes `grab` tasks at a time from a global counter
+    // (reset by finalize_kernel).  Task order is link-major, so consecutive
+    // tasks share the link grid.
+    // The per-task constants of a grab are computed lane-parallel (lane j
+    // for task base + j) into shared memory.
+    const uint32_t n_tasks = (uint32_t)(p.C * p.split) * (uint32_t)n_group;
+    const uint32_t per_link = (uint32_t)(p.C * p.split);
+    __shared__ int s_order[WARPS][LSDF_MAX_LINKS];
+    if (lane < n_group) s_order[warp][lane] = order_lane;
+    __syncwarp();
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(p.counters + launch, (uint32_t)grab);
+    base = __shfl_sync(FULL_MASK, base, 0);
+    if (base < n_tasks && (uint32_t)lane < min((uint32_t)grab, n_tasks - base))
+        shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane]);
+    __syncwarp();
+    cp_async_wait_all();
     __syncthreads();
     ShellView sv;
     sv.cells = stage_shell ? s_cells : p.shell_cells;
@@ -465,20 +516,15 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     sv.P = sP;
     sv.Pf = sPf;
     uint32_t* queue = s_queue + warp * QCAP_SHELL;
-    // dynamic task fetch: task durations vary by orders of magnitude (early
-    // stop), so each warp takes `grab` tasks at a time from a global counter
-    // (reset by finalize_kernel).  Task order is link-major, so consecutive
-    // tasks share the link grid.
-    // The per-task constants of a grab are computed lane-parallel (lane j
-    // for task base + j) into shared memory.
-    const uint32_t n_tasks = (uint32_t)(p.C * p.split) * (uint32_t)n_group;
-    for (;;) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(p.counters + launch, (uint32_t)grab);
-        base = __shfl_sync(FULL_MASK, base, 0);
+    for (bool first = true;; first = false) {
+        if (!first) {
+            if (lane == 0) base = atomicAdd(p.counters + launch, (uint32_t)grab);
+            base = __shfl_sync(FULL_MASK, base, 0);
+        }
         if (base >= n_tasks) break;
         const uint32_t cnt = min((uint32_t)grab, n_tasks - base);
-        if ((uint32_t)lane < cnt) shell_setup(p, s_order, base + lane, s_setup[warp][lane]);
+        if (!first && (uint32_t)lane < cnt)
+            shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane]);
         __syncwarp();
         for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS>(p, sv, queue, s_setup[warp][j], lane);
         __syncwarp();
@@ -657,7 +703,8 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
             const int stage_bits = o.n_words <= BITMAP_STAGE_MAX;
             const size_t smem_s = (size_t)3 * window->Wmax * (sizeof(double) + sizeof(float)) + 12 +
                                   (size_t)WARPS * QCAP_SHELL * 4 +
-                                  (stage_shell ? (size_t)p.n_shell * 8 : 0) + (stage_bits ? (size_t)o.n_words * 4 : 0);
+                                  (stage_shell ? (size_t)p.n_shell * 8 : 0) + (stage_bits ? (size_t)o.n_words * 4 : 0) +
+                                  48;  // 16-B alignment of the three staged tables
             static bool attr = false;
             if (!attr) {
                 cudaFuncSetAttribute(query_shells_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);

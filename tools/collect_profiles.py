@@ -43,8 +43,10 @@ def main():
             return float(x.replace(",", "")) * scale
 
         traffic[w] = int(val("dram__bytes_read.sum") + val("dram__bytes_write.sum"))
+        traffic[f"{w}_warp_inst"] = int(val("smsp__inst_executed.sum"))
     traffic["_units"] = ("bytes per launch of query_shells_kernel: dram__bytes_read.sum + dram__bytes_write.sum from "
-                         f"one ncu --set full capture (profiles/{args.round}/ncu_summary.txt)")
+                         f"one ncu --set full capture (profiles/{args.round}/ncu_summary.txt); <w>_warp_inst: "
+                         "smsp__inst_executed.sum of the same launch")
     (REPO / "profiles" / "query_traffic.json").write_text(json.dumps(traffic))
     py = sys.executable
     lines = [f"# ncu summaries, round {args.round[1:]} (tools/refresh_profiles.sh; B200, --clock-control none)", "",
