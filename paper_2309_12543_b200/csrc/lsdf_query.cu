@@ -320,6 +320,13 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_
     s.az = __ldg(p.anchor + o * 3 + 2);
 }
 
+#ifdef LSDF_STATS  // instrumented build (tools/_stats.py): per-task scan counters
+__device__ unsigned long long g_stats[8];
+#define STAT(i, v) (sc[i] += (v))
+#else
+#define STAT(i, v) ((void)0)
+#endif
+
 // One warp, one (configuration c, link l, slice sidx) task.
 template <bool BY_POS>
 __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView& sv, uint32_t* queue,
@@ -377,8 +384,16 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
     const float4 sa = p.seg_a[l], su = p.seg_u[l];
     const float k_lo = sa.w, k_hi = p.seg_hi[l];
     const bool use_seg = p.seg_filter && k_lo >= 0.0f;
+#ifdef LSDF_STATS
+    unsigned long long sc[8] = {1, 0, 0, 0, 0, 0, 0, 0};
+#endif
     for (int k0 = sidx * 32; k0 < p.n_shell; k0 += 32 * p.split) {
-        if (sv.radius[k0] - slack > thresh) break;  // every later cell is farther
+        if (sv.radius[k0] - slack > thresh) {  // every later cell is farther
+            STAT(6, 1);
+            STAT(7, k0 == sidx * 32);
+            break;
+        }
+        STAT(1, 1);
         const int k = k0 + lane;
         bool occ = false;
         uint32_t cell = 0;
@@ -391,6 +406,13 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
                 occ = (sv.bits[lin >> 5] >> (lin & 31)) & 1u;
             }
         }
+#ifdef LSDF_STATS
+        {
+            const unsigned b0 = __ballot_sync(FULL_MASK, occ);
+            STAT(2, b0 != 0u);
+            STAT(3, __popc(b0));
+        }
+#endif
         if (use_seg && __any_sync(FULL_MASK, occ)) {
             float d2q = INFINITY;  // squared segment distance of a cell that stays queued
             if (occ) {
@@ -417,14 +439,23 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
         const unsigned ballot = __ballot_sync(FULL_MASK, occ);
         if (occ) queue[qlen + __popc(ballot & ((1u << lane) - 1u))] = cell;
         qlen += __popc(ballot);
+        STAT(4, __popc(ballot));
         __syncwarp();
         if (qlen >= 32) {
+            STAT(5, 1);
             evaluate(queue[qlen - 32 + lane], true);
             qlen -= 32;
         }
         __syncwarp();
     }
-    if (qlen > 0) evaluate(lane < qlen ? queue[lane] : 0u, lane < qlen);
+    if (qlen > 0) {
+        STAT(5, 1);
+        evaluate(lane < qlen ? queue[lane] : 0u, lane < qlen);
+    }
+#ifdef LSDF_STATS
+    if (lane == 0)
+        for (int i = 0; i < 8; ++i) atomicAdd(g_stats + i, sc[i]);
+#endif
 
     const uint32_t pos_key = bestpos == 0xffffffffu ? 0xffffffffu : bestpos * (uint32_t)p.n_geo + (uint32_t)l;
     uint64_t best = bestpos == 0xffffffffu ? ~0ull : (((uint64_t)orderable(bestv) << 32) | pos_key);
@@ -814,3 +845,14 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
 extern "C" int lsdf_query_direct(LSDF_QUERY_ARGS) { return query_impl(LSDF_QUERY_FWD, STAGE_SCAN | STAGE_FINALIZE); }
 extern "C" int lsdf_query_scan(LSDF_QUERY_ARGS) { return query_impl(LSDF_QUERY_FWD, STAGE_SCAN); }
 extern "C" int lsdf_query_finalize(LSDF_QUERY_ARGS) { return query_impl(LSDF_QUERY_FWD, STAGE_FINALIZE); }
+
+#ifdef LSDF_STATS
+extern "C" int lsdf_stats_read(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_stats, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_stats, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

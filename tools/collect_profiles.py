@@ -13,26 +13,14 @@ from pathlib import Path
 REPO = Path(__file__).resolve().parent.parent
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--round", default="r01")
-    args = ap.parse_args()
-    src = REPO / "gpurun_out" / "prof"
-    dst = REPO / "profiles" / args.round
-    dst.mkdir(parents=True, exist_ok=True)
-    for a, b in (("bench.json", "bench_config4_N1.json"), ("bench_config2.json", "bench_config2_N1.json"),
-                 ("bench_reference.json", "bench_reference_port.json")):
-        line = (src / a).read_text().strip().splitlines()[-1]
-        json.loads(line)
-        (dst / b).write_text(line + "\n")
-    for f in ("launches_config4.csv", "launches_config2.csv", "launches_bench.csv"):
-        shutil.copy(src / f, dst / f)
-    # per-launch DRAM traffic of the query kernel, read by bench.py's roofline
+def write_counters(src, out_path, rnd):
+    """Per-launch DRAM traffic and warp instructions of the query kernel (read by bench.py's rooflines)."""
+    import csv
+
     traffic = {}
     for w in ("config4", "config2"):
         out = subprocess.run(["ncu", "-i", str(src / f"shells_{w}.ncu-rep"), "--page", "raw", "--csv"],
                              capture_output=True, text=True).stdout.splitlines()
-        import csv
         rows = list(csv.reader(out))
         h, u, v = rows[0], rows[1], rows[2]
         d = dict(zip(h, zip(u, v)))
@@ -45,9 +33,31 @@ def main():
         traffic[w] = int(val("dram__bytes_read.sum") + val("dram__bytes_write.sum"))
         traffic[f"{w}_warp_inst"] = int(val("smsp__inst_executed.sum"))
     traffic["_units"] = ("bytes per launch of query_shells_kernel: dram__bytes_read.sum + dram__bytes_write.sum from "
-                         f"one ncu --set full capture (profiles/{args.round}/ncu_summary.txt); <w>_warp_inst: "
+                         f"one ncu --set full capture (profiles/{rnd}/ncu_summary.txt); <w>_warp_inst: "
                          "smsp__inst_executed.sum of the same launch")
-    (REPO / "profiles" / "query_traffic.json").write_text(json.dumps(traffic))
+    Path(out_path).write_text(json.dumps(traffic))
+    return traffic
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--round", default="r01")
+    ap.add_argument("--counters-only", metavar="OUT", help="write the query counters JSON to OUT and stop")
+    args = ap.parse_args()
+    src = REPO / "gpurun_out" / "prof"
+    if args.counters_only:
+        print(write_counters(src, args.counters_only, args.round))
+        return
+    dst = REPO / "profiles" / args.round
+    dst.mkdir(parents=True, exist_ok=True)
+    for a, b in (("bench.json", "bench_config4_N1.json"), ("bench_config2.json", "bench_config2_N1.json"),
+                 ("bench_reference.json", "bench_reference_port.json")):
+        line = (src / a).read_text().strip().splitlines()[-1]
+        json.loads(line)
+        (dst / b).write_text(line + "\n")
+    for f in ("launches_config4.csv", "launches_config2.csv", "launches_bench.csv"):
+        shutil.copy(src / f, dst / f)
+    traffic = write_counters(src, REPO / "profiles" / "query_traffic.json", args.round)
     py = sys.executable
     lines = [f"# ncu summaries, round {args.round[1:]} (tools/refresh_profiles.sh; B200, --clock-control none)", "",
              "## launch lists (cold, serialised; the first 4 query launches of each process are the checker's "
