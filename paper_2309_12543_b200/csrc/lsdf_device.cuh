@@ -17,6 +17,14 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
     return v;
 }
 
+// Warp minimum of the 64-bit keys (hi << 32 | lo) with two 32-bit reductions:
+// the smallest hi, then the smallest lo among the lanes holding it.
+__device__ __forceinline__ uint64_t warp_min_key(uint32_t hi, uint32_t lo) {
+    const uint32_t h = __reduce_min_sync(FULL_MASK, hi);
+    const uint32_t l = __reduce_min_sync(FULL_MASK, hi == h ? lo : 0xffffffffu);
+    return ((uint64_t)h << 32) | l;
+}
+
 __device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULL_MASK, v, o));

@@ -327,21 +327,57 @@ __device__ unsigned long long g_stats[8];
 #define STAT(i, v) ((void)0)
 #endif
 
-// One warp, one (configuration c, link l, slice sidx) task.
+// One round of exact lookups over queue entries (cell | task slot << 24),
+// one per lane: each lane evaluates its entry with its task's constants
+// (shared memory), the entries of one task reduce together (match-any
+// groups: min value, then min position) into the configuration's key slot
+// and, when requested, the per-link slot.  Entries of several tasks of the
+// warp's grab can share a round, so a task's leftover lookups ride with the
+// next task's instead of costing a partial round each.  Returns the
+// orderable minimum over the entries of task slot `cur`.
+template <bool BY_POS>
+__device__ __forceinline__ uint32_t lookup_round(const QueryParams& p, const ShellView& sv,
+                                                 const ShellSetup* setups, uint32_t entry, bool valid, uint32_t cur,
+                                                 int lane) {
+    const uint32_t slot = valid ? entry >> 24 : 0xffu;
+    uint32_t ov = 0xffffffffu, pk = 0xffffffffu;
+    int64_t c = 0;
+    int l = 0;
+    if (valid) {
+        const ShellSetup& st = setups[slot];
+        l = st.l;
+        c = st.c;
+        const int Wm = p.Wmax, ny = p.dims[1], nz = p.dims[2];
+        const int mx = entry & 0xff, my = (entry >> 8) & 0xff, mz = (entry >> 16) & 0xff;
+        double pt[3];
+        window_point(sv.P[mx], sv.P[Wm + my], sv.P[2 * Wm + mz], st.R, st.dtinv, p.e_r, pt);
+        const float v = trilinear_geom(p.geom, p.cells[l], p.dfar[l], pt[0], pt[1], pt[2]);
+        const int lin = ((st.ax + mx) * ny + (st.ay + my)) * nz + (st.az + mz);
+        const uint32_t pos = BY_POS ? (uint32_t)__ldg(p.posgrid + lin) : (uint32_t)lin;
+        ov = orderable(v);
+        pk = pos * (uint32_t)p.n_geo + (uint32_t)l;
+    }
+    const unsigned grp = __match_any_sync(FULL_MASK, slot);
+    const uint32_t h = __reduce_min_sync(grp, ov);
+    const uint32_t lo = __reduce_min_sync(grp, ov == h ? pk : 0xffffffffu);
+    if (valid && lane == __ffs(grp) - 1) {
+        atomicMax(p.keys + c, ~(((unsigned long long)h << 32) | lo));
+        if (p.per_link != nullptr) atomicMax(p.perlink + c * p.n_geo + l, ~h);
+    }
+    return __reduce_min_sync(FULL_MASK, slot == cur ? ov : 0xffffffffu);
+}
+
+// One warp, one (configuration c, link l, slice sidx) task: the task in slot
+// `j` of the warp's grab.  Occupied candidate cells go to the warp's queue;
+// full rounds of 32 are looked up at once, a remainder stays queued for the
+// next task (the kernel flushes it after the grab).
 template <bool BY_POS>
 __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView& sv, uint32_t* queue,
-                                           const ShellSetup& st, int lane) {
+                                           const ShellSetup* setups, uint32_t j, int& qlen, int lane) {
+    const ShellSetup& st = setups[j];
     const int l = st.l;
     const int64_t c = st.c;
     const int sidx = st.sidx;
-    const float4* __restrict__ cells = p.cells[l];
-    const float far = p.dfar[l];
-    const int64_t o = c * p.n_geo + l;
-    double R[9], dtinv[3];
-#pragma unroll
-    for (int e = 0; e < 9; ++e) R[e] = st.R[e];
-#pragma unroll
-    for (int e = 0; e < 3; ++e) dtinv[e] = st.dtinv[e];
     const float slack = st.slack;
     const int ax = st.ax, ay = st.ay, az = st.az;
     const int Wm = p.Wmax;
@@ -349,32 +385,12 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
     const int lin0 = (ax * ny + ay) * nz + az;
     const bool share_cfg = p.per_link == nullptr;
 
-    float bestv = INFINITY;
-    uint32_t bestpos = 0xffffffffu;
     float thresh = p.clamp;  // values >= clamp never change the answer
     if (share_cfg) {  // best key any link of this configuration has published so far
         const uint64_t k = ~(uint64_t)__ldcg(p.keys + c);
         if (k != ~0ull) thresh = fminf(thresh, from_orderable((uint32_t)(k >> 32)));
     }
-    int qlen = 0, rounds = 0;
-    auto evaluate = [&](uint32_t cell, bool valid) {
-        if (valid) {
-            const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
-            double pt[3];
-            window_point(sv.P[mx], sv.P[Wm + my], sv.P[2 * Wm + mz], R, dtinv, p.e_r, pt);
-            const float v = trilinear_geom(p.geom, cells, far, pt[0], pt[1], pt[2]);
-            const int lin = lin0 + (mx * ny + my) * nz + mz;
-            const uint32_t pos = BY_POS ? (uint32_t)__ldg(p.posgrid + lin) : (uint32_t)lin;
-            const bool better = (v < bestv) | ((v == bestv) & (pos < bestpos));
-            bestv = better ? v : bestv;
-            bestpos = better ? pos : bestpos;
-        }
-        thresh = fminf(thresh, from_orderable(__reduce_min_sync(FULL_MASK, orderable(bestv))));
-        if (share_cfg && (++rounds & 3) == 0) {
-            const uint64_t k = ~(uint64_t)__ldcg(p.keys + c);
-            if (k != ~0ull) thresh = fminf(thresh, from_orderable((uint32_t)(k >> 32)));
-        }
-    };
+    int rounds = 0;
 
     // Segment bound (f32, conservative): d(p) - k_lo <= value(p) <= d(p) + k_hi
     // with d the distance to the link's axis segment.  An occupied cell whose
@@ -437,34 +453,26 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
             }
         }
         const unsigned ballot = __ballot_sync(FULL_MASK, occ);
-        if (occ) queue[qlen + __popc(ballot & ((1u << lane) - 1u))] = cell;
+        if (occ) queue[qlen + __popc(ballot & ((1u << lane) - 1u))] = cell | (j << 24);
         qlen += __popc(ballot);
         STAT(4, __popc(ballot));
         __syncwarp();
         if (qlen >= 32) {
             STAT(5, 1);
-            evaluate(queue[qlen - 32 + lane], true);
+            const uint32_t m = lookup_round<BY_POS>(p, sv, setups, queue[qlen - 32 + lane], true, j, lane);
+            if (m != 0xffffffffu) thresh = fminf(thresh, from_orderable(m));
+            if (share_cfg && (++rounds & 3) == 0) {
+                const uint64_t kk = ~(uint64_t)__ldcg(p.keys + c);
+                if (kk != ~0ull) thresh = fminf(thresh, from_orderable((uint32_t)(kk >> 32)));
+            }
             qlen -= 32;
         }
         __syncwarp();
-    }
-    if (qlen > 0) {
-        STAT(5, 1);
-        evaluate(lane < qlen ? queue[lane] : 0u, lane < qlen);
     }
 #ifdef LSDF_STATS
     if (lane == 0)
         for (int i = 0; i < 8; ++i) atomicAdd(g_stats + i, sc[i]);
 #endif
-
-    const uint32_t pos_key = bestpos == 0xffffffffu ? 0xffffffffu : bestpos * (uint32_t)p.n_geo + (uint32_t)l;
-    uint64_t best = bestpos == 0xffffffffu ? ~0ull : (((uint64_t)orderable(bestv) << 32) | pos_key);
-    best = warp_min_u64(best);
-    if (lane == 0) atomicMax(p.keys + c, (unsigned long long)~best);
-    if (p.per_link != nullptr) {
-        const uint32_t wm = __reduce_min_sync(FULL_MASK, orderable(bestv));
-        if (lane == 0) atomicMax(p.perlink + o, ~wm);
-    }
 }
 
 // Persistent over groups of 8 tasks (a group never mixes links).  The window
@@ -557,7 +565,10 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
         if (!first && (uint32_t)lane < cnt)
             shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane]);
         __syncwarp();
-        for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS>(p, sv, queue, s_setup[warp][j], lane);
+        int qlen = 0;
+        for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS>(p, sv, queue, s_setup[warp], j, qlen, lane);
+        if (qlen > 0)  // the grab's remaining lookups, before its setups are overwritten
+            lookup_round<BY_POS>(p, sv, s_setup[warp], lane < qlen ? queue[lane] : 0u, lane < qlen, 0xffu, lane);
         __syncwarp();
     }
     // the last CTA of the last launch clears the counts this cycle's finalize refills
