@@ -273,7 +273,7 @@ struct ShellView {
 
 // Per-task constants, computed by one lane per task (up to GRAB_MAX tasks at a
 // time) and read back from shared memory by the warp that scans the task.
-constexpr int GRAB_MAX = 8;
+constexpr int GRAB_MAX = 16;
 constexpr int64_t SEG_FILTER_MIN_TASKS = 148LL * 32 * 8;  // ~8 tasks per resident warp
 struct __align__(16) ShellSetup {
     double R[9];
@@ -772,7 +772,7 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
             const int64_t resident = (int64_t)n_sm * (per_sm < 1 ? 1 : per_sm);
             const unsigned grid = (unsigned)((int64_t)blocks < resident ? (int64_t)blocks : resident);
             const int64_t n_tasks = C * split * n_group;
-            int64_t grab = n_tasks / (resident * WARPS * 16);
+            int64_t grab = n_tasks / (resident * WARPS * 8);
             grab = grab < 1 ? 1 : (grab > GRAB_MAX ? GRAB_MAX : grab);
             // grids pinned in L2: an access-policy window over the span of
             // this group's packed grids (contiguous when TrajectorySdf packed
