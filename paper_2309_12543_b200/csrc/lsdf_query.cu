@@ -285,7 +285,7 @@ struct __align__(16) ShellSetup {
     int32_t c;       // configuration
     int32_t sidx;    // slice of the shell list
     int32_t ax, ay, az;
-    int32_t pad_;
+    float thresh0;   // starting threshold: min(clamp, the configuration's best key at setup time)
 };
 
 __device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_t t, ShellSetup& s) {
@@ -312,6 +312,12 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_
 #pragma unroll
     for (int k = 0; k < 3; ++k) s.b[k] = (float)(dtinv[k] * p.e_r - (double)a3[k]);
     s.slack = dtn + p.core[l];
+    float t0 = p.clamp;  // values >= clamp never change the answer
+    if (p.per_link == nullptr) {  // best key any link of this configuration has published so far (an upper
+        const uint64_t k = ~(uint64_t)__ldcg(p.keys + c);  // bound of the minimum, so an older read stays valid)
+        if (k != ~0ull) t0 = fminf(t0, from_orderable((uint32_t)(k >> 32)));
+    }
+    s.thresh0 = t0;
     s.l = l;
     s.c = (int32_t)c;
     s.sidx = p.split == 1 ? 0 : (int32_t)(r % p.split);
@@ -385,11 +391,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
     const int lin0 = (ax * ny + ay) * nz + az;
     const bool share_cfg = p.per_link == nullptr;
 
-    float thresh = p.clamp;  // values >= clamp never change the answer
-    if (share_cfg) {  // best key any link of this configuration has published so far
-        const uint64_t k = ~(uint64_t)__ldcg(p.keys + c);
-        if (k != ~0ull) thresh = fminf(thresh, from_orderable((uint32_t)(k >> 32)));
-    }
+    float thresh = st.thresh0;  // read at setup (lane-parallel for the grab): no load latency here
     int rounds = 0;
 
     // Segment bound (f32, conservative): d(p) - k_lo <= value(p) <= d(p) + k_hi
