@@ -76,7 +76,9 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
         if (L.kind == 1) {  // revolute: r_o @ rodrigues(q)   robot.py:331-334
             const double a = q[L.q_col];
             double M[9], rl[9];
-            rodrigues(L.skew, L.outer, cos(a), sin(a), M);
+            double sa, ca;
+            sincos(a, &sa, &ca);
+            rodrigues(L.skew, L.outer, ca, sa, M);
             mm33(L.joint_R, M, rl);
 #pragma unroll
             for (int e = 0; e < 9; ++e) loc[e] = rl[e];
@@ -208,13 +210,17 @@ __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __gr
         // a later non-adjacent child needs go to a per-thread local array
         double prev[12];
         double world[LSDF_MAX_LINKS][12];
+        // the joints' sines and cosines first: independent of the chain, so
+        // they overlap instead of sitting on its dependent path
+        double sn[LSDF_MAX_LINKS], cs[LSDF_MAX_LINKS];
+        for (int k2 = 0; k2 < p.n_links; ++k2)
+            if (s_links[k2].kind == 1) sincos(q[s_links[k2].q_col], &sn[k2], &cs[k2]);
         for (int k2 = 0; k2 < p.n_links; ++k2) {
             const lsdf_link& L = s_links[k2];
             double rl[9], tl[3];  // joint-local transform (phase 1)
             if (L.kind == 1) {    // revolute: r_o @ rodrigues(q)   robot.py:331-334
-                const double a = q[L.q_col];
                 double M[9];
-                rodrigues(L.skew, L.outer, cos(a), sin(a), M);
+                rodrigues(L.skew, L.outer, cs[k2], sn[k2], M);
                 mm33(L.joint_R, M, rl);
 #pragma unroll
                 for (int k = 0; k < 3; ++k) tl[k] = L.joint_t[k];
