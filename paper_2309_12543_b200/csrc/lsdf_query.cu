@@ -542,10 +542,10 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     __shared__ int s_order[WARPS][LSDF_MAX_LINKS];
     if (lane < n_group) s_order[warp][lane] = order_lane;
     __syncwarp();
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(p.counters + launch, (uint32_t)grab);
+    uint32_t base = 0, g = (uint32_t)grab;
+    if (lane == 0) base = atomicAdd(p.counters + launch, g);
     base = __shfl_sync(FULL_MASK, base, 0);
-    if (base < n_tasks && (uint32_t)lane < min((uint32_t)grab, n_tasks - base))
+    if (base < n_tasks && (uint32_t)lane < min(g, n_tasks - base))
         shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane]);
     __syncwarp();
     cp_async_wait_all();
@@ -557,16 +557,23 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     sv.P = sP;
     sv.Pf = sPf;
     uint32_t* queue = s_queue + warp * QCAP_SHELL;
+    // guided grab sizes: the grab shrinks as the remaining work does, so the
+    // last warps to finish carry at most a small grab (shorter tail)
+    const uint32_t warps_total = gridDim.x * WARPS;
     for (bool first = true;; first = false) {
         if (!first) {
-            if (lane == 0) base = atomicAdd(p.counters + launch, (uint32_t)grab);
+            if (lane == 0) base = atomicAdd(p.counters + launch, g);
             base = __shfl_sync(FULL_MASK, base, 0);
         }
         if (base >= n_tasks) break;
-        const uint32_t cnt = min((uint32_t)grab, n_tasks - base);
+        const uint32_t cnt = min(g, n_tasks - base);
         if (!first && (uint32_t)lane < cnt)
             shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane]);
         __syncwarp();
+        {
+            const uint32_t left = n_tasks - min(base + cnt, n_tasks);
+            g = max(1u, min((uint32_t)grab, left / (2 * warps_total)));
+        }
         int qlen = 0;
         for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS>(p, sv, queue, s_setup[warp], j, qlen, lane);
         if (qlen > 0)  // the grab's remaining lookups, before its setups are overwritten
