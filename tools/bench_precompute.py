@@ -26,7 +26,8 @@ REPO = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(REPO))
 
 
-def _time(torch, fn, reps=3, warm=1):
+def _time(torch, fn, reps=5, warm=3):
+    """Median device time (ms); several warm-ups so the SM clock has ramped up from idle first."""
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
@@ -81,7 +82,7 @@ def main():
         kernel_us[robot.links[i].name] = 1e3 / 20 * _time(torch, g.replay)
     ico = L.make_icosphere(0.08, subdivisions=3)
     assert len(ico.triangles) == 1280
-    ms_mesh = _time(torch, lambda: L.build_link_sdf(ico, e_r, r_r), reps=2)
+    ms_mesh = _time(torch, lambda: L.build_link_sdf(ico, e_r, r_r), reps=5)
     cells = 128 ** 3
     prim_ms = statistics.mean(builds.values())
     k_us = statistics.mean(kernel_us.values())
@@ -116,7 +117,7 @@ def main():
             N.call("lsdf_grid_transform_exact", N.ptr(Rd[s:s + ch]), N.ptr(dtd[s:s + ch]), ch, N.ptr(P), V, 0.64,
                    N.ptr(G), N.stream())
 
-    ms_exact = _time(torch, exact_all, reps=2)
+    ms_exact = _time(torch, exact_all, reps=5)
     del G
     model = L.TinyMlp.initial(V, hidden=32, seed=0)
     model.w2 = np.random.default_rng(1).normal(0, 0.05, size=model.w2.shape).astype(np.float32)
@@ -129,8 +130,8 @@ def main():
         for s in range(0, B, mch):
             model.predict_device(Rd[s:s + mch], use_tensor_cores=tc, out=Y)
 
-    ms_tc = _time(torch, lambda: mlp_all(True), reps=2)
-    ms_cc = _time(torch, lambda: mlp_all(False), reps=2)
+    ms_tc = _time(torch, lambda: mlp_all(True), reps=5)
+    ms_cc = _time(torch, lambda: mlp_all(False), reps=5)
     flops = 2.0 * B * (9 * 32 + 32 * 3 * V)
     out["transform"] = {
         "rotations": B, "V_mask": V, "W": int(window.dims[0]), "chunk_exact": ch, "chunk_mlp": mch,

@@ -57,6 +57,11 @@ def main():
         (dst / b).write_text(line + "\n")
     for f in ("launches_config4.csv", "launches_config2.csv", "launches_bench.csv"):
         shutil.copy(src / f, dst / f)
+    for a, b in (("config5_dynamic.json", "config5_dynamic.json"), ("vmajor_config2.json", "vmajor_config2.json"),
+                 ("vmajor_config5.json", "vmajor_config5.json"), ("config3_precompute.json", "config3_precompute.json"),
+                 ("scan_stats.txt", "scan_stats.txt")):
+        if (src / a).exists() and (src / a).stat().st_size > 0:
+            shutil.copy(src / a, dst / b)
     traffic = write_counters(src, REPO / "profiles" / "query_traffic.json", args.round)
     py = sys.executable
     lines = [f"# ncu summaries, round {args.round[1:]} (tools/refresh_profiles.sh; B200, --clock-control none)", "",
