@@ -133,3 +133,41 @@ def test_c_abi_client_builds_and_fails_loudly(tmp_path):
         pytest.skip("GPU present: tests/test_gpu_parity.py::test_c_abi_client covers the run")
     r = subprocess.run([str(exe), str(scene), str(tmp_path / "out.bin")], capture_output=True, text=True, timeout=60)
     assert r.returncode != 0 and "cuda" in r.stderr.lower()
+
+
+def test_scan_bounds_hold_on_random_grids():
+    """The early-stop and segment bounds the shell scan relies on (LinkSdf.core_radius,
+    LinkSdf.segment_bound: lower bounds by convexity, upper bound + |h|/2) hold for
+    trilinear samples of noisy and exact grids, checked with the oracle's trilinear."""
+    from oracle import linksdf_oracle as O
+    from paper_2309_12543_b200.grids import LinkSdf, interpolation_spread
+
+    rng = np.random.default_rng(5)
+    # the spread itself: sum_i w_i |v_i - p| <= |h| / 2 over random cell fractions and anisotropic h
+    h = np.array([0.01, 0.02, 0.015])
+    f = rng.random((20000, 3))
+    corners = np.array([[i, j, k] for k in (0, 1) for j in (0, 1) for i in (0, 1)], dtype=np.float64)
+    w = np.prod(np.where(corners[None], f[:, None], 1.0 - f[:, None]), axis=-1)
+    dist = np.linalg.norm((corners[None] - f[:, None]) * h, axis=-1)
+    assert (w * dist).sum(axis=1).max() <= interpolation_spread(h) * (1 + 1e-12)
+    for shape_kind, noise in (("capsule", 0.004), ("sphere", 0.004), ("capsule", 0.0)):
+        e_r, r_r = 0.16, 0.01
+        c = -e_r + (np.arange(32) + 0.5) * r_r
+        X, Y, Z = np.meshgrid(c, c, c, indexing="ij")
+        if shape_kind == "capsule":
+            t = np.clip(Z, -0.05, 0.05)
+            base = np.sqrt(X * X + Y * Y + (Z - t) ** 2) - 0.04
+        else:
+            base = np.sqrt(X * X + Y * Y + Z * Z) - 0.05
+        # noise 0: an exact distance grid, where the interpolation term of the upper bound is tight
+        vals = (base + rng.normal(0, noise, base.shape)).astype(np.float32)
+        sdf = LinkSdf(e_r, r_r, vals, link_id=0)
+        kappa = sdf.core_radius()
+        a, u, length, k_lo, k_hi = sdf.segment_bound()
+        pts = rng.uniform(c[0], c[-1], size=(40000, 3))
+        v = O.trilinear(sdf.values, e_r, r_r, pts).astype(np.float64)
+        assert np.all(v >= np.linalg.norm(pts, axis=1) - kappa)
+        a, u = np.asarray(a), np.asarray(u)
+        tt = np.clip((pts - a) @ u, 0.0, length)
+        d = np.linalg.norm(pts - a - tt[:, None] * u, axis=1)
+        assert np.all(v >= d - k_lo) and np.all(v <= d + k_hi)
