@@ -38,6 +38,7 @@ struct QueryParams {
     float4 seg_u[LSDF_MAX_LINKS];           // (u.xyz, length)
     float seg_hi[LSDF_MAX_LINKS];           // kappa_hi
     int32_t seg_filter;                     // apply the segment bound (throughput-sized batches)
+    int32_t round_min;                      // queued cells that trigger a lookup round (<= 32)
     const uint32_t* shell_cells;            // kept window cells sorted by distance from the centre
     const float* shell_radius;              // their distance (m), rounded down
     int32_t n_shell;
@@ -459,15 +460,17 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
         qlen += __popc(ballot);
         STAT(4, __popc(ballot));
         __syncwarp();
-        if (qlen >= 32) {
+        if (qlen >= p.round_min) {
             STAT(5, 1);
-            const uint32_t m = lookup_round<BY_POS>(p, sv, setups, queue[qlen - 32 + lane], true, j, lane);
+            const int n = qlen < 32 ? qlen : 32;
+            const uint32_t m = lookup_round<BY_POS>(p, sv, setups, lane < n ? queue[qlen - n + lane] : 0u, lane < n,
+                                                    j, lane);
             if (m != 0xffffffffu) thresh = fminf(thresh, from_orderable(m));
             if (share_cfg && (++rounds & 3) == 0) {
                 const uint64_t kk = ~(uint64_t)__ldcg(p.keys + c);
                 if (kk != ~0ull) thresh = fminf(thresh, from_orderable((uint32_t)(kk >> 32)));
             }
-            qlen -= 32;
+            qlen -= n;
         }
         __syncwarp();
     }
@@ -682,6 +685,10 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     // the bound saves lookups but lengthens each warp's dependent chain: a
     // win when the GPU is full of tasks, a loss on the latency path
     p.seg_filter = C * n_geo >= SEG_FILTER_MIN_TASKS;
+    // latency-sized batches: a lookup round once 16 cells are queued, so the
+    // task's threshold drops (and its scan stops) sooner; throughput batches
+    // only run full rounds (issue-bound: a half round wastes lanes)
+    p.round_min = p.seg_filter ? 32 : 16;
     p.P = window->P_dev;
     p.Wmax = window->Wmax;
     p.by_position = by_position;
