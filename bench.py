@@ -202,10 +202,10 @@ def _max_over_ranks(dist, torch, x):
 def _e2e_entry(C_total, pipe_ms, single_ms, h2d, d2h, world=1):
     """The public-API end-to-end number: the faster of the pipelined and the
     one-cycle-at-a-time paths (both copy every cycle's inputs in and results out)."""
-    pipe_path = ("CheckerPipeline (2 cycles in flight): per cycle H2D of configs + cloud from pinned host memory on "
+    pipe_path = ("CheckerPipeline (3 cycles in flight): per cycle one H2D of configs + cloud from pinned host memory on "
                  "a copy stream, the cycle graph, D2H of (d, link, voxel) + flags; host wall clock over K cycles"
                  if world == 1 else
-                 "ShardedCloudPipeline (2 cycles in flight, per rank): H2D of this rank's configs and 1/world of the "
+                 "ShardedCloudPipeline (3 cycles in flight, per rank): H2D of this rank's configs and 1/world of the "
                  "cloud, voxelize the slice, NCCL all-gather of the partial occupancy bitmaps, merge, FK + query, "
                  "D2H; host wall clock over K cycles, max over ranks")
     single_path = ("DistanceChecker.query() one cycle at a time from pinned host buffers (zero-copy kernel "
@@ -283,11 +283,11 @@ def run_ours(args, rank, world, dist, sampler):
 
             plo, phi = shard_range(shape.n_points, rank, world)
             pipe = L.ShardedCloudPipeline(chk.robot, chk.sdfs, chk.grid, chk.window, n_local, phi - plo,
-                                          np.float32, depth=2)
+                                          np.float32, depth=3)
         else:
             plo, phi = 0, shape.n_points
             pipe = L.CheckerPipeline(chk.robot, chk.sdfs, chk.grid, chk.window, n_local, shape.n_points,
-                                     np.float32, depth=2)
+                                     np.float32, depth=3)
         for k in range(pipe.depth):  # producers write straight into the pinned slots
             qv, pv = pipe.inputs()
             q_k, p_k = host[k % len(host)]

@@ -51,7 +51,13 @@ class DistanceChecker:
 
     # ------------------------------------------------------------------ buffers
     def prepare(self, n_configs: int, n_points: int, points_dtype=np.float32, use_graph: bool = True,
-                zero_copy: bool = True):
+                zero_copy: bool = True, contiguous_inputs: bool = False):
+        """Size buffers for (n_configs, n_points) and capture the cycle graphs.
+
+        contiguous_inputs: configurations and cloud share one pinned host
+        buffer and one device buffer (``in_host`` / ``in_dev``), so a pipeline
+        moves a cycle's inputs with a single copy-engine transfer.
+        """
         t = N.torch()
         dev = N.device()
         pdt = np.dtype(points_dtype)
@@ -63,16 +69,33 @@ class DistanceChecker:
         self._shape = (C_, P, pdt)
         pin = dict(pin_memory=True)
         # host side (page-locked)
-        self.q_host = t.zeros((C_, D), dtype=t.float64, **pin)
-        self.p_host = t.full((P, 3), float("nan"), dtype=tdt, **pin)
+        if contiguous_inputs:  # [configs f64 | pad to 256 B | points]: one transfer per cycle
+            q_bytes = (C_ * D * 8 + 255) // 256 * 256
+            nbytes = q_bytes + P * 3 * pdt.itemsize
+            self.in_host = t.empty((nbytes,), dtype=t.uint8, **pin)
+            self.in_dev = t.empty((nbytes,), dtype=t.uint8, device=dev)
+            self.q_host = self.in_host[: C_ * D * 8].view(t.float64).view(C_, D)
+            self.p_host = self.in_host[q_bytes:].view(tdt).view(P, 3)
+            self.q_host.zero_()
+            self.p_host.fill_(float("nan"))
+        else:
+            self.in_host = self.in_dev = None
+            self.q_host = t.zeros((C_, D), dtype=t.float64, **pin)
+            self.p_host = t.full((P, 3), float("nan"), dtype=tdt, **pin)
         self.d_host = t.zeros((C_,), dtype=t.float32, **pin)
         self.link_host = t.zeros((C_,), dtype=t.int32, **pin)
         self.voxel_host = t.zeros((C_,), dtype=t.int32, **pin)
         self.flags_host = t.zeros((4,), dtype=t.int32, **pin)
         self._np = {k: getattr(self, k + "_host").numpy() for k in ("q", "p", "d", "link", "voxel", "flags")}
         # device side
-        self.q_dev = t.zeros((C_, D), dtype=t.float64, device=dev)
-        self.p_dev = t.full((P, 3), float("nan"), dtype=tdt, device=dev)
+        if contiguous_inputs:
+            self.q_dev = self.in_dev[: C_ * D * 8].view(t.float64).view(C_, D)
+            self.p_dev = self.in_dev[q_bytes:].view(tdt).view(P, 3)
+            self.q_dev.zero_()
+            self.p_dev.fill_(float("nan"))
+        else:
+            self.q_dev = t.zeros((C_, D), dtype=t.float64, device=dev)
+            self.p_dev = t.full((P, 3), float("nan"), dtype=tdt, device=dev)
         self.R_geo = t.zeros((C_, G, 3, 3), dtype=t.float64, device=dev)
         self.dt_geo = t.zeros((C_, G, 3), dtype=t.float64, device=dev)
         self.anchor_geo = t.zeros((C_, G, 3), dtype=t.int32, device=dev)
@@ -251,7 +274,7 @@ class CheckerPipeline:
         self.slots = []
         for _ in range(depth):
             chk = DistanceChecker(robot, sdfs, grid, window, **kw).prepare(n_configs, n_points, points_dtype,
-                                                                           zero_copy=False)
+                                                                           zero_copy=False, contiguous_inputs=True)
             pin = dict(pin_memory=True)
             host_out = (t.zeros((n_configs,), dtype=t.float32, **pin), t.zeros((n_configs,), dtype=t.int32, **pin),
                         t.zeros((n_configs,), dtype=t.int32, **pin), t.zeros((4,), dtype=t.int32, **pin))
@@ -297,8 +320,7 @@ class CheckerPipeline:
         ev = s["ev"]
         with t.cuda.stream(self.copy):
             self.copy.wait_event(ev["compute"])  # the slot's device inputs are free again
-            chk.q_dev.copy_(chk.q_host, non_blocking=True)
-            chk.p_dev.copy_(chk.p_host, non_blocking=True)
+            chk.in_dev.copy_(chk.in_host, non_blocking=True)  # configurations + cloud, one transfer
             ev["h2d"].record(self.copy)
         with t.cuda.stream(self.compute):
             self.compute.wait_event(ev["h2d"])
