@@ -46,32 +46,53 @@ __host__ __device__ inline int64_t n_vox(const lsdf_env_grid& e) { return (int64
 struct Occupancy {
     int32_t* counters;  // [0] n_occupied, [1] n_dropped, [2] block ticket, [3] spare
     uint32_t* bitmap;
+    uint32_t* bricks;   // per (bx, by) column of 4^3-voxel bricks: bit bz set when the brick is occupied
     int32_t* prefix;    // exclusive popcount prefix per word
     int32_t* posgrid;   // first position in an explicit index list (general path)
     int64_t n_words;
+    int32_t nbx, nby, nbz;
+    bool bricks_ok;     // nbz <= 32: every producer of the bitmap also maintains the brick columns
 };
+
+constexpr int BRICK_LOG2 = 2;  // 4^3 voxels per brick
 
 inline int64_t align256(int64_t b) { return (b + 255) / 256 * 256; }
 
+inline int64_t brick_columns(const lsdf_env_grid& env) {
+    return (int64_t)((env.dims[0] + 3) >> BRICK_LOG2) * ((env.dims[1] + 3) >> BRICK_LOG2);
+}
+
+// [counters 256 B | bitmap | brick columns | prefix | position grid]
 inline Occupancy carve_occupancy(void* base, const lsdf_env_grid& env) {
     Occupancy o;
     const int64_t V = n_vox(env);
     o.n_words = (V + 31) / 32;
+    o.nbx = (env.dims[0] + 3) >> BRICK_LOG2;
+    o.nby = (env.dims[1] + 3) >> BRICK_LOG2;
+    o.nbz = (env.dims[2] + 3) >> BRICK_LOG2;
+    o.bricks_ok = o.nbz <= 32;
     char* p = (char*)base;
     o.counters = (int32_t*)p;
     p += 256;
     o.bitmap = (uint32_t*)p;
     p += align256(o.n_words * 4);
+    o.bricks = (uint32_t*)p;
+    p += align256(brick_columns(env) * 4);
     o.prefix = (int32_t*)p;
     p += align256(o.n_words * 4);
     o.posgrid = (int32_t*)p;
     return o;
 }
 
+// bytes a producer clears before scattering: counters, bitmap, brick columns
+inline int64_t occupancy_clear_bytes(const Occupancy& o) {
+    return 256 + align256(o.n_words * 4) + (int64_t)o.nbx * o.nby * 4;
+}
+
 inline int64_t occupancy_bytes(const lsdf_env_grid& env) {
     const int64_t V = n_vox(env);
     const int64_t w = (V + 31) / 32;
-    return 256 + 2 * align256(w * 4) + align256(V * 4);
+    return 256 + 2 * align256(w * 4) + align256(brick_columns(env) * 4) + align256(V * 4);
 }
 
 // ------------------------------------------------------------------ link grid views

@@ -39,6 +39,8 @@ struct QueryParams {
     float seg_hi[LSDF_MAX_LINKS];           // kappa_hi
     int32_t seg_filter;                     // apply the segment bound (throughput-sized batches)
     int32_t round_min;                      // queued cells that trigger a lookup round (<= 32)
+    const uint32_t* bricks;                 // occupancy brick columns (4^3 voxels), or null: no box test
+    int32_t nby_brick;                      // brick columns per x row
     const uint32_t* shell_cells;            // kept window cells sorted by distance from the centre
     const float* shell_radius;              // their distance (m), rounded down
     int32_t n_shell;
@@ -268,6 +270,7 @@ struct ShellView {
     const uint32_t* cells;   // shell-ordered kept cells (shared or global)
     const float* radius;
     const uint32_t* bits;    // occupancy bitmap (shared or global)
+    const uint32_t* bricks;  // brick columns (shared), or null
     const double* P;         // window offsets (shared)
     const float* Pf;         // the same in f32 (shared), for the segment bound
 };
@@ -378,7 +381,7 @@ __device__ __forceinline__ uint32_t lookup_round(const QueryParams& p, const She
 // `j` of the warp's grab.  Occupied candidate cells go to the warp's queue;
 // full rounds of 32 are looked up at once, a remainder stays queued for the
 // next task (the kernel flushes it after the grab).
-template <bool BY_POS>
+template <bool BY_POS, bool BRICKS>
 __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView& sv, uint32_t* queue,
                                            const ShellSetup* setups, uint32_t j, int& qlen, int lane) {
     const ShellSetup& st = setups[j];
@@ -392,6 +395,22 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
     const int lin0 = (ax * ny + ay) * nz + az;
     const bool share_cfg = p.per_link == nullptr;
 
+    if (BRICKS) {  // nothing occupied in the window's box: the task has nothing to look up
+        const int x0 = max(ax, 0), x1 = min(ax + p.W[0], nx) - 1;
+        const int y0 = max(ay, 0), y1 = min(ay + p.W[1], ny) - 1;
+        const int z0 = max(az, 0), z1 = min(az + p.W[2], nz) - 1;
+        bool hit = false;
+        if (x0 <= x1 && y0 <= y1 && z0 <= z1) {
+            const int bx0 = x0 >> BRICK_LOG2, by0 = y0 >> BRICK_LOG2, nbyr = (y1 >> BRICK_LOG2) - by0 + 1;
+            const int ncol = ((x1 >> BRICK_LOG2) - bx0 + 1) * nbyr;
+            const uint32_t zmask = (2u << (z1 >> BRICK_LOG2)) - (1u << (z0 >> BRICK_LOG2));
+            for (int i = lane; i < ncol; i += 32) {
+                const int bx = bx0 + i / nbyr, by = by0 + i % nbyr;
+                hit |= (sv.bricks[bx * p.nby_brick + by] & zmask) != 0u;
+            }
+        }
+        if (!__any_sync(FULL_MASK, hit)) return;
+    }
     float thresh = st.thresh0;  // read at setup (lane-parallel for the grab): no load latency here
     int rounds = 0;
 
@@ -484,7 +503,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
 // offsets, the shell-ordered cell list and the occupancy bitmap are staged in
 // shared memory once per CTA when they fit, so the per-chunk loads of the
 // scan are shared-memory loads.
-template <bool BY_POS>
+template <bool BY_POS, bool BRICKS>
 __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __grid_constant__ QueryParams p,
                                                                   int n_group, int launch, int grab,
                                                                   int stage_shell, int stage_bits, int64_t n_words,
@@ -498,6 +517,8 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     uint32_t* s_cells = (uint32_t*)align16_ptr(s_queue + WARPS * QCAP_SHELL);
     float* s_radius = (float*)align16_ptr(s_cells + (stage_shell ? p.n_shell : 0));
     uint32_t* s_bits = (uint32_t*)align16_ptr(s_radius + (stage_shell ? p.n_shell : 0));
+    uint32_t* s_bricks = (uint32_t*)align16_ptr(s_bits + (stage_bits ? n_words : 0));
+    const int n_cols = BRICKS ? (int)(((p.dims[0] + 3) >> BRICK_LOG2) * p.nby_brick) : 0;
     __shared__ ShellSetup s_setup[WARPS][GRAB_MAX];
     // Stage the shell list and the occupancy bitmap with asynchronous copies
     // (all in flight at once), and fetch + set up the first tasks while they
@@ -508,6 +529,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
         stage_async(s_radius, p.shell_radius, (size_t)p.n_shell * 4);
     }
     if (stage_bits) stage_async(s_bits, p.bitmap, (size_t)n_words * 4);
+    if (n_cols) stage_async(s_bricks, p.bricks, (size_t)n_cols * 4);
     cp_async_commit();
     for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) {
         const double v = p.P[i];
@@ -557,6 +579,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     sv.cells = stage_shell ? s_cells : p.shell_cells;
     sv.radius = stage_shell ? s_radius : p.shell_radius;
     sv.bits = stage_bits ? s_bits : p.bitmap;
+    sv.bricks = n_cols ? s_bricks : nullptr;
     sv.P = sP;
     sv.Pf = sPf;
     uint32_t* queue = s_queue + warp * QCAP_SHELL;
@@ -578,7 +601,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
             g = max(1u, min((uint32_t)grab, left / (2 * warps_total)));
         }
         int qlen = 0;
-        for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS>(p, sv, queue, s_setup[warp], j, qlen, lane);
+        for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS, BRICKS>(p, sv, queue, s_setup[warp], j, qlen, lane);
         if (qlen > 0)  // the grab's remaining lookups, before its setups are overwritten
             lookup_round<BY_POS>(p, sv, s_setup[warp], lane < qlen ? queue[lane] : 0u, lane < qlen, 0xffu, lane);
         __syncwarp();
@@ -697,6 +720,10 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     p.clamp = clamp;
     Occupancy o = carve_occupancy(const_cast<void*>(occupancy_dev), *env);
     p.bitmap = o.bitmap;
+    // the brick box test: latency-sized batches (sparse or far obstacles leave
+    // whole windows empty); dense throughput batches would only pay for it
+    p.bricks = (o.bricks_ok && !p.seg_filter) ? o.bricks : nullptr;
+    p.nby_brick = o.nby;
     p.prefix = o.prefix;
     p.posgrid = o.posgrid;
     char* w = (char*)workspace_dev;
@@ -762,26 +789,29 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
             const size_t smem_s = (size_t)3 * window->Wmax * (sizeof(double) + sizeof(float)) + 12 +
                                   (size_t)WARPS * QCAP_SHELL * 4 +
                                   (stage_shell ? (size_t)p.n_shell * 8 : 0) + (stage_bits ? (size_t)o.n_words * 4 : 0) +
-                                  48;  // 16-B alignment of the three staged tables
+                                  (p.bricks != nullptr ? (size_t)o.nbx * o.nby * 4 : 0) +
+                                  64;  // 16-B alignment of the four staged tables
+            using ShellsKernel = void (*)(QueryParams, int, int, int, int, int, int64_t, int);
+            static const ShellsKernel kernels[4] = {query_shells_kernel<false, false>, query_shells_kernel<false, true>,
+                                                    query_shells_kernel<true, false>, query_shells_kernel<true, true>};
             static bool attr = false;
             if (!attr) {
-                cudaFuncSetAttribute(query_shells_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-                cudaFuncSetAttribute(query_shells_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+                for (ShellsKernel k : kernels)
+                    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
                 attr = true;
             }
-            // residency cache: (device, by_position, smem bytes) -> CTAs per SM
+            const int variant = (by_position ? 2 : 0) + (p.bricks != nullptr ? 1 : 0);
+            const ShellsKernel kern = kernels[variant];
+            // residency cache: (device, variant, smem bytes) -> CTAs per SM
             thread_local int c_dev = -1, c_bp = -1, c_sm = 148, c_per = 1;
             thread_local size_t c_smem = 0;
             int dev = 0;
             cudaGetDevice(&dev);
-            if (dev != c_dev || (int)by_position != c_bp || smem_s != c_smem) {
+            if (dev != c_dev || variant != c_bp || smem_s != c_smem) {
                 cudaDeviceGetAttribute(&c_sm, cudaDevAttrMultiProcessorCount, dev);
-                if (by_position)
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per, query_shells_kernel<true>, 32 * WARPS, smem_s);
-                else
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per, query_shells_kernel<false>, 32 * WARPS, smem_s);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per, kern, 32 * WARPS, smem_s);
                 c_dev = dev;
-                c_bp = by_position;
+                c_bp = variant;
                 c_smem = smem_s;
             }
             const int per_sm = c_per, n_sm = c_sm;
@@ -830,13 +860,8 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
             }
             const int ig = (int)grab;
             const int last = n_launch + 1 == n_groups_total;
-            cudaError_t le;
-            if (by_position)
-                le = cudaLaunchKernelEx(&cfg, query_shells_kernel<true>, p, n_group, n_launch, ig, stage_shell,
-                                        stage_bits, o.n_words, last);
-            else
-                le = cudaLaunchKernelEx(&cfg, query_shells_kernel<false>, p, n_group, n_launch, ig, stage_shell,
-                                        stage_bits, o.n_words, last);
+            const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, p, n_group, n_launch, ig, stage_shell, stage_bits,
+                                                      o.n_words, last);
             if (le != cudaSuccess) return fail(LSDF_ERR_CUDA, "query_shells_kernel: %s", cudaGetErrorString(le));
             ++n_launch;
         } else if (full) {

@@ -71,10 +71,12 @@ __device__ __forceinline__ int voxel_floor(double p, double e, double r, double 
 template <typename T, bool PRIVATE>
 __global__ void __launch_bounds__(SCATTER_THREADS)
 voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, double rx, double ry, double rz,
-                     uint32_t* bitmap, int32_t* counters, int64_t n_words) {
+                     uint32_t* bitmap, int32_t* counters, int64_t n_words, uint32_t* bricks, int32_t nby,
+                     int32_t n_cols) {
     extern __shared__ uint32_t s_bits[];
+    uint32_t* s_bricks = s_bits + n_words;  // brick columns (PRIVATE)
     if (PRIVATE) {
-        for (int64_t w = threadIdx.x; w < n_words; w += blockDim.x) s_bits[w] = 0u;
+        for (int64_t w = threadIdx.x; w < n_words + n_cols; w += blockDim.x) s_bits[w] = 0u;
         __syncthreads();
     }
     // grid-stride: a persistent grid of a few CTAs per SM amortises the
@@ -98,10 +100,15 @@ voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, do
                 iz = iz > env.dims[2] - 1 ? env.dims[2] - 1 : iz;
                 const uint32_t lin = ((uint32_t)ix * (uint32_t)env.dims[1] + (uint32_t)iy) * (uint32_t)env.dims[2] +
                                      (uint32_t)iz;
-                if (PRIVATE)
+                const int col = (ix >> BRICK_LOG2) * nby + (iy >> BRICK_LOG2);
+                const uint32_t zb = 1u << (iz >> BRICK_LOG2);
+                if (PRIVATE) {
                     atomicOr(s_bits + (lin >> 5), 1u << (lin & 31));
-                else
+                    if (n_cols) atomicOr(s_bricks + col, zb);
+                } else {
                     atomicOr(bitmap + (lin >> 5), 1u << (lin & 31));
+                    if (n_cols) atomicOr(bricks + col, zb);
+                }
             } else {
                 dropped = true;
             }
@@ -115,18 +122,30 @@ voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, do
             const uint32_t v = s_bits[w];
             if (v) atomicOr(bitmap + w, v);
         }
+        for (int w = threadIdx.x; w < n_cols; w += blockDim.x) {
+            const uint32_t v = s_bricks[w];
+            if (v) atomicOr(bricks + w, v);
+        }
     }
+}
+
+// brick column bit of an occupied voxel (linear C-order index)
+__device__ __forceinline__ void mark_brick(uint32_t* bricks, const lsdf_env_grid& env, int32_t nby, int64_t lin) {
+    const int64_t nyz = (int64_t)env.dims[1] * env.dims[2];
+    const int ix = (int)(lin / nyz), iy = (int)((lin / env.dims[2]) % env.dims[1]), iz = (int)(lin % env.dims[2]);
+    atomicOr(bricks + (ix >> BRICK_LOG2) * nby + (iy >> BRICK_LOG2), 1u << (iz >> BRICK_LOG2));
 }
 
 // OR of n_parts partial bitmaps (n_parts, n_words) into the occupancy bitmap;
 // thread 0 also sums the parts' dropped-point counters.
 __global__ void merge_bitmaps_kernel(const uint32_t* __restrict__ parts, int32_t n_parts, int64_t n_words,
                                      const int32_t* __restrict__ dropped, int64_t dropped_stride, uint32_t* bitmap,
-                                     int32_t* counters) {
+                                     int32_t* counters, lsdf_env_grid env, uint32_t* bricks, int32_t nby) {
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += (int64_t)gridDim.x * blockDim.x) {
         uint32_t v = 0;
         for (int k = 0; k < n_parts; ++k) v |= __ldg(parts + k * n_words + w);
         bitmap[w] = v;
+        for (uint32_t b = v; bricks != nullptr && b; b &= b - 1) mark_brick(bricks, env, nby, w * 32 + __ffs(b) - 1);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         int32_t total = 0;
@@ -160,18 +179,20 @@ __global__ void voxel_compact_kernel(const uint32_t* __restrict__ bitmap, const 
 }
 
 __global__ void occ_from_indices_kernel(const int32_t* idx, int64_t N, lsdf_env_grid env, uint32_t* bitmap,
-                                        int32_t* posgrid, int mode) {
+                                        int32_t* posgrid, int mode, uint32_t* bricks, int32_t nby) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const int64_t lin = ((int64_t)idx[3 * i] * env.dims[1] + idx[3 * i + 1]) * env.dims[2] + idx[3 * i + 2];
     if (mode == 0) {  // sorted unique: position == list index == rank
         posgrid[lin] = (int32_t)i;
         atomicOr(bitmap + (lin >> 5), 1u << (lin & 31));
+        if (bricks != nullptr) mark_brick(bricks, env, nby, lin);
     } else if (mode == 1) {  // general, pass 1: reset touched entries
         posgrid[lin] = 0x7fffffff;
     } else {  // general, pass 2: first occurrence wins (numpy argmin semantics)
         atomicMin(posgrid + lin, (int32_t)i);
         atomicOr(bitmap + (lin >> 5), 1u << (lin & 31));
+        if (bricks != nullptr) mark_brick(bricks, env, nby, lin);
     }
 }
 
@@ -199,31 +220,32 @@ namespace {
 // memset + scatter: the bitmap (and the dropped-point counter) of a cloud
 int scatter_bitmap(const void* points_dev, int32_t points_f32, int64_t N, const lsdf_env_grid* env, Occupancy& o,
                    void* occupancy_dev, cudaStream_t s) {
-    LSDF_TRY(check_cuda(cudaMemsetAsync(occupancy_dev, 0, 256 + o.n_words * 4, s), "voxelize memset"));
+    LSDF_TRY(check_cuda(cudaMemsetAsync(occupancy_dev, 0, occupancy_clear_bytes(o), s), "voxelize memset"));
     if (N <= 0) return LSDF_OK;
+    const int32_t n_cols = o.bricks_ok ? o.nbx * o.nby : 0;
     const double rx = 1.0 / env->resolution[0], ry = 1.0 / env->resolution[1], rz = 1.0 / env->resolution[2];
     // CTA-private shared bitmaps (a dense blob costs one global atomic per
     // touched word per CTA; measured: global atomics straight away, or
     // smaller CTAs, are slower even at 100k points), grid-stride over at most
     // two CTAs per SM so large clouds amortise the clear and merge
-    const bool priv = o.n_words <= PRIVATE_WORDS_MAX;
+    const bool priv = o.n_words + n_cols <= PRIVATE_WORDS_MAX;
     const unsigned threads = SCATTER_THREADS;
     const unsigned blocks = grid_for(N, threads) < 148u * 2u ? grid_for(N, threads) : 148u * 2u;
-    const size_t smem = priv ? (size_t)o.n_words * 4 : 0;
+    const size_t smem = priv ? (size_t)(o.n_words + n_cols) * 4 : 0;
     if (points_f32) {
         if (priv)
             voxel_scatter_kernel<float, true><<<blocks, threads, smem, s>>>(
-                (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+                (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols);
         else
             voxel_scatter_kernel<float, false><<<blocks, threads, 0, s>>>(
-                (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+                (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols);
     } else {
         if (priv)
             voxel_scatter_kernel<double, true><<<blocks, threads, smem, s>>>(
-                (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+                (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols);
         else
             voxel_scatter_kernel<double, false><<<blocks, threads, 0, s>>>(
-                (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words);
+                (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols);
     }
     return check_launch("voxel_scatter_kernel");
 }
@@ -261,8 +283,11 @@ extern "C" int lsdf_occupancy_merge(const uint32_t* parts_dev, int32_t n_parts, 
     if (n_parts < 1) return fail(LSDF_ERR_VALIDATION, "occupancy merge: %d parts", n_parts);
     cudaStream_t s = (cudaStream_t)stream;
     Occupancy o = carve_occupancy(occupancy_dev, *env);
+    if (o.bricks_ok)
+        LSDF_TRY(check_cuda(cudaMemsetAsync(o.bricks, 0, (size_t)o.nbx * o.nby * 4, s), "brick columns memset"));
     merge_bitmaps_kernel<<<grid_for(o.n_words, 256), 256, 0, s>>>(parts_dev, n_parts, o.n_words, dropped_dev,
-                                                                   dropped_stride, o.bitmap, o.counters);
+                                                                   dropped_stride, o.bitmap, o.counters, *env,
+                                                                   o.bricks_ok ? o.bricks : nullptr, o.nby);
     LSDF_TRY(check_launch("merge_bitmaps_kernel"));
     prefix_only_kernel<<<1, SCAN_THREADS, 0, s>>>(o.bitmap, o.n_words, o.prefix, o.counters);
     return check_launch("prefix_only_kernel");
@@ -272,15 +297,16 @@ extern "C" int lsdf_occupancy_from_indices(const int32_t* indices_dev, int64_t N
                                            const lsdf_env_grid* env, void* occupancy_dev, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     Occupancy o = carve_occupancy(occupancy_dev, *env);
-    LSDF_TRY(check_cuda(cudaMemsetAsync(occupancy_dev, 0, 256 + o.n_words * 4, s), "occupancy memset"));
+    LSDF_TRY(check_cuda(cudaMemsetAsync(occupancy_dev, 0, occupancy_clear_bytes(o), s), "occupancy memset"));
+    uint32_t* bricks = o.bricks_ok ? o.bricks : nullptr;
     if (N > 0) {
         if (sorted_unique) {
-            occ_from_indices_kernel<<<grid_for(N, 256), 256, 0, s>>>(indices_dev, N, *env, o.bitmap, o.posgrid, 0);
+            occ_from_indices_kernel<<<grid_for(N, 256), 256, 0, s>>>(indices_dev, N, *env, o.bitmap, o.posgrid, 0, bricks, o.nby);
             LSDF_TRY(check_launch("occ_from_indices_kernel"));
         } else {
-            occ_from_indices_kernel<<<grid_for(N, 256), 256, 0, s>>>(indices_dev, N, *env, o.bitmap, o.posgrid, 1);
+            occ_from_indices_kernel<<<grid_for(N, 256), 256, 0, s>>>(indices_dev, N, *env, o.bitmap, o.posgrid, 1, bricks, o.nby);
             LSDF_TRY(check_launch("occ_from_indices_kernel"));
-            occ_from_indices_kernel<<<grid_for(N, 256), 256, 0, s>>>(indices_dev, N, *env, o.bitmap, o.posgrid, 2);
+            occ_from_indices_kernel<<<grid_for(N, 256), 256, 0, s>>>(indices_dev, N, *env, o.bitmap, o.posgrid, 2, bricks, o.nby);
             LSDF_TRY(check_launch("occ_from_indices_kernel"));
         }
     }

@@ -517,9 +517,10 @@ def test_config4_shape_large_batch(L):
         assert np.array_equal(dc, d) and np.array_equal(lc, link) and np.array_equal(vc, voxel)
 
 
-@pytest.mark.parametrize("seed", [0, 1])
-def test_direct_equals_dense_on_adversarial_grids(L, seed):
-    """Random (non-Lipschitz) grid values, random rotations, a dense cloud:
+@pytest.mark.parametrize("seed,cloud", [(0, "uniform"), (1, "uniform"), (2, "clusters"), (3, "clusters")])
+def test_direct_equals_dense_on_adversarial_grids(L, seed, cloud):
+    """Random (non-Lipschitz) grid values, random rotations, a dense cloud or a
+    few tight clusters (most windows empty: the brick box test skips them):
     the screened direct kernel must select exactly what the dense gather selects."""
     rng = np.random.default_rng(seed)
     grid = L.EnvGrid(1.0, 0.05)
@@ -535,7 +536,12 @@ def test_direct_equals_dense_on_adversarial_grids(L, seed):
     R = L.sample_rotations(rng, C * 3).reshape(C, 3, 3, 3)
     T = rng.uniform(-0.6, 0.6, size=(C, 3, 3))
     traj = L.TrajectorySdf.from_poses(sdfs, L.LinkPoseBatch(R, T), grid, L.ExactTransformProvider(window))
-    obs = L.voxelize_pointcloud(rng.uniform(-1, 1, size=(20_000, 3)), grid)
+    if cloud == "uniform":
+        pts = rng.uniform(-1, 1, size=(20_000, 3))
+    else:  # tight blobs, one on a brick boundary and one in a grid corner
+        centres = np.array([[0.2, -0.2, 0.2], [-0.8, 0.8, -0.8], [0.0, 0.0, 0.0], [0.95, 0.95, 0.95]])
+        pts = np.concatenate([c + rng.normal(0, 0.03, size=(100, 3)) for c in centres])
+    obs = L.voxelize_pointcloud(pts, grid)
     d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
     dense = L.RobotSdfBatch(traj.device_values(), grid, traj.d_far_global)
     d2, _, v2 = L.query_min_distances(dense, obs, return_argmin=True)
