@@ -168,6 +168,18 @@ int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_geo,
                   double* R_geo_dev, double* dt_geo_dev, int32_t* anchor_geo_dev,
                   int32_t* flags_dev, void* stream);
 
+/* lsdf_fk_align with the geometry outputs link-major: R_geo (n_geo, C, 9),
+ * dt_geo (n_geo, C, 3), anchor_geo (n_geo, C, 3).  A warp then writes each
+ * link's records of its 32 configurations as one contiguous run, which needs
+ * no per-configuration staging (large batches: 2x the resident warps).  Pass
+ * LSDF_QUERY_POSES_LINK_MAJOR to the query with these buffers. */
+int lsdf_fk_align_link_major(const lsdf_link* links, int32_t n_links, int32_t n_geo,
+                             const double* q_dev, int64_t C, int32_t D, const double* limits_dev,
+                             const lsdf_env_grid* env, const int32_t W[3],
+                             double* R_all_dev, double* T_all_dev,
+                             double* R_geo_dev, double* dt_geo_dev, int32_t* anchor_geo_dev,
+                             int32_t* flags_dev, void* stream);
+
 /* compute_alignment (placement.py:60-99) for n positions T (n, 3) fp64. */
 int lsdf_align(const double* T_dev, int64_t n, const lsdf_env_grid* env, const int32_t W[3],
                int32_t* anchor_dev, double* dt_dev, int32_t* flags_dev, void* stream);
@@ -228,11 +240,15 @@ int lsdf_voxel_index(const double* points_dev, int64_t N, const lsdf_env_grid* e
  * robot SDF (query.py:128-150).  Outputs d (C) f32, link (C) i32 and voxel (C)
  * i32 (position in the obstacle list; -1/-1 when d equals the clamp or the set
  * is empty).  per_link_dev (C, n_geo) f32 or NULL: per_link_min_distances
- * (query.py:153-176).  by_position != 0 selects the general (unsorted list)
- * tie rule; set it when the occupancy came from an unsorted index list.
+ * (query.py:153-176).  by_position is a flags word: LSDF_QUERY_BY_POSITION
+ * selects the general (unsorted list) tie rule (set it when the occupancy came
+ * from an unsorted index list); LSDF_QUERY_POSES_LINK_MAJOR reads the poses
+ * in the (n_geo, C, .) layout of lsdf_fk_align_link_major.
  * workspace_dev: lsdf_query_workspace_bytes(C, n_geo) bytes, zeroed once at
  * allocation; every launch leaves it zeroed again (the finalize pass of each
  * configuration resets its slots), so graph replays need no memset. */
+#define LSDF_QUERY_BY_POSITION 1
+#define LSDF_QUERY_POSES_LINK_MAJOR 2
 int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_dev,
                       const int32_t* anchor_geo_dev, int64_t C, int32_t n_geo,
                       const lsdf_link_grid* grids, const lsdf_window* window,

@@ -60,6 +60,8 @@ _F = C.c_float
 _SIGS = {
     "lsdf_fk_align": [C.POINTER(LinkT), _I32, _I32, _P, _I64, _I32, _P, C.POINTER(EnvGridT),
                       C.POINTER(_I32), _P, _P, _P, _P, _P, _P, _P],
+    "lsdf_fk_align_link_major": [C.POINTER(LinkT), _I32, _I32, _P, _I64, _I32, _P, C.POINTER(EnvGridT),
+                                 C.POINTER(_I32), _P, _P, _P, _P, _P, _P, _P],
     "lsdf_align": [_P, _I64, C.POINTER(EnvGridT), C.POINTER(_I32), _P, _P, _P, _P],
     "lsdf_occupancy_bytes": [C.POINTER(EnvGridT)],
     "lsdf_voxelize": [_P, _I32, _I64, C.POINTER(EnvGridT), _P, _P, _P],
@@ -102,6 +104,9 @@ _SIGS = {
     "lsdf_host_device_pointer": [_P, C.POINTER(C.c_void_p)],
     "lsdf_l2_reserve": [C.c_size_t, C.POINTER(C.c_size_t)],
 }
+
+QUERY_BY_POSITION = 1        # lsdf_query_* flags word (include/linksdf_b200.h)
+QUERY_POSES_LINK_MAJOR = 2
 
 EXPORTS = tuple(_SIGS) + ("lsdf_version", "lsdf_last_error", "lsdf_launch_count")
 

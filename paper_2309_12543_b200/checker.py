@@ -30,6 +30,10 @@ from . import _native as N
 from .errors import LimitViolationError, NoOverlapError, ValidationError
 from .query import TrajectorySdf, occupancy_workspace
 
+# batch size from which FK runs one thread per configuration (lsdf_fk.cu
+# FK_SERIAL_MIN) and the checker keeps its poses link-major
+LINK_MAJOR_MIN = 6144
+
 
 class DistanceChecker:
     def __init__(self, robot, sdfs, grid, window, *, d_far_global=None, check_limits: bool = True):
@@ -96,9 +100,19 @@ class DistanceChecker:
         else:
             self.q_dev = t.zeros((C_, D), dtype=t.float64, device=dev)
             self.p_dev = t.full((P, 3), float("nan"), dtype=tdt, device=dev)
-        self.R_geo = t.zeros((C_, G, 3, 3), dtype=t.float64, device=dev)
-        self.dt_geo = t.zeros((C_, G, 3), dtype=t.float64, device=dev)
-        self.anchor_geo = t.zeros((C_, G, 3), dtype=t.int32, device=dev)
+        # large batches keep the poses link-major ((G, C, .) storage, exposed as
+        # (C, G, .) views): FK then writes each link's records contiguously
+        self.link_major = C_ >= LINK_MAJOR_MIN
+        if self.link_major:
+            self.R_geo = t.zeros((G, C_, 3, 3), dtype=t.float64, device=dev).transpose(0, 1)
+            self.dt_geo = t.zeros((G, C_, 3), dtype=t.float64, device=dev).transpose(0, 1)
+            self.anchor_geo = t.zeros((G, C_, 3), dtype=t.int32, device=dev).transpose(0, 1)
+        else:
+            self.R_geo = t.zeros((C_, G, 3, 3), dtype=t.float64, device=dev)
+            self.dt_geo = t.zeros((C_, G, 3), dtype=t.float64, device=dev)
+            self.anchor_geo = t.zeros((C_, G, 3), dtype=t.int32, device=dev)
+        self._fk_entry = "lsdf_fk_align_link_major" if self.link_major else "lsdf_fk_align"
+        self._qflags = N.QUERY_POSES_LINK_MAJOR if self.link_major else 0
         self.flags = t.zeros((4,), dtype=t.int32, device=dev)
         self.limits = N.to_device(np.ascontiguousarray(self._limits), t.float64)
         self.d_dev = t.zeros((C_,), dtype=t.float32, device=dev)
@@ -106,7 +120,7 @@ class DistanceChecker:
         self.voxel_dev = t.zeros((C_,), dtype=t.int32, device=dev)
         self.ws = occupancy_workspace(self.grid)
         self.traj = TrajectorySdf(self.sdfs, self.grid, self.window, self.R_geo, self.dt_geo, self.anchor_geo,
-                                  self.d_far_global)
+                                  self.d_far_global, link_major=self.link_major)
         self.qws = t.zeros((int(N.lib().lsdf_query_workspace_bytes(C_, G)),), dtype=t.uint8, device=dev)
         self._wstruct, _ = self.window.device_tables()
         for sdf in self.sdfs:
@@ -149,7 +163,7 @@ class DistanceChecker:
             if staged:
                 self.q_dev.copy_(self.q_host, non_blocking=True)
             q_ptr = self._map["q"] if zc else N.ptr(self.q_dev)
-            N.call("lsdf_fk_align", self._chain, self.robot.n_links, len(self.sdfs), q_ptr, C_, self.robot.dof,
+            N.call(self._fk_entry, self._chain, self.robot.n_links, len(self.sdfs), q_ptr, C_, self.robot.dof,
                    N.ptr(self.limits), self._env, self._W, None, None, N.ptr(self.R_geo), N.ptr(self.dt_geo),
                    N.ptr(self.anchor_geo), N.ptr(self.flags), side.cuda_stream)
         if staged:
@@ -172,7 +186,7 @@ class DistanceChecker:
             outs = (N.ptr(self.d_dev), N.ptr(self.link_dev), N.ptr(self.voxel_dev))
         tr = self.traj
         args = (N.ptr(self.R_geo), N.ptr(self.dt_geo), N.ptr(self.anchor_geo), C_, tr.n_links, tr._table,
-                ctypes.byref(self._wstruct), self._env, N.ptr(self.ws), 0, self.d_far_global, N.ptr(self.qws),
+                ctypes.byref(self._wstruct), self._env, N.ptr(self.ws), self._qflags, self.d_far_global, N.ptr(self.qws),
                 outs[0], outs[1], outs[2], None, main.cuda_stream)
         N.call("lsdf_query_scan", *args)
         main.wait_stream(pre)
@@ -520,7 +534,7 @@ class ShardedCloudPipeline:
             self.compute.wait_event(ev["h2d"])
             self.compute.wait_event(ev["d2h"])
             cs = self.compute.cuda_stream
-            N.call("lsdf_fk_align", chk._chain, chk.robot.n_links, len(chk.sdfs), N.ptr(chk.q_dev), C_,
+            N.call(chk._fk_entry, chk._chain, chk.robot.n_links, len(chk.sdfs), N.ptr(chk.q_dev), C_,
                    chk.robot.dof, N.ptr(chk.limits), chk._env, chk._W, None, None, N.ptr(chk.R_geo),
                    N.ptr(chk.dt_geo), N.ptr(chk.anchor_geo), N.ptr(chk.flags), cs)
             part = s["part"].view(t.int32)
@@ -530,7 +544,7 @@ class ShardedCloudPipeline:
             N.call("lsdf_occupancy_merge", s["gather"], self.world, s["dropped"], 1, chk._env, N.ptr(chk.ws), cs)
             tr = chk.traj
             N.call("lsdf_query_direct", N.ptr(chk.R_geo), N.ptr(chk.dt_geo), N.ptr(chk.anchor_geo), C_, tr.n_links,
-                   tr._table, ctypes.byref(chk._wstruct), chk._env, N.ptr(chk.ws), 0, chk.d_far_global,
+                   tr._table, ctypes.byref(chk._wstruct), chk._env, N.ptr(chk.ws), chk._qflags, chk.d_far_global,
                    N.ptr(chk.qws), N.ptr(chk.d_dev), N.ptr(chk.link_dev), N.ptr(chk.voxel_dev), None, cs)
             ev["compute"].record(self.compute)
         d, link, voxel, flags = s["out"]

@@ -17,7 +17,8 @@ namespace {
 
 struct FkParams {
     lsdf_link links[LSDF_MAX_LINKS];
-    int32_t n_links, n_geo, D, pad_;
+    int32_t n_links, n_geo, D;
+    int32_t link_major;  // geometry outputs (n_geo, C, .) instead of (C, n_geo, .)
     int64_t C;
     const double* q;
     const double* limits;
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
         for (int k = 0; k < 3; ++k) dtt[k] = w[9 + k];
     }
     if (L.geom_slot >= 0 && p.R_geo != nullptr) {
-        const int64_t o = c * p.n_geo + L.geom_slot;
+        const int64_t o = p.link_major ? L.geom_slot * p.C + c : c * p.n_geo + L.geom_slot;
 #pragma unroll
         for (int e = 0; e < 9; ++e) p.R_geo[o * 9 + e] = w[e];
         int32_t anc[3];
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
 // kernel keeps small batches latency-short.
 constexpr int FKS_THREADS = 64;
 
-template <bool STAGE>
+template <bool STAGE, bool LM>
 __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __grid_constant__ FkParams p) {
     // every thread walks the same link at the same time: the chain table is
     // read straight from the kernel parameters (uniform constant-bank loads)
@@ -194,11 +195,19 @@ __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __gr
     double* sdt = sR + FKS_THREADS * G * 9;
     int32_t* sanc = (int32_t*)(sdt + FKS_THREADS * G * 3);
     const int64_t c0 = (int64_t)blockIdx.x * FKS_THREADS;
-    const int64_t c = c0 + threadIdx.x;
     const int nc = (int)(p.C - c0 < FKS_THREADS ? p.C - c0 : FKS_THREADS);
-    if (c < p.C) {
+    // LM: the warp writes each link's records of its 32 configurations as one
+    // contiguous run; lanes past the end walk the last configuration so the
+    // warp's control flow stays uniform, and write nothing
+    const int lane = threadIdx.x & 31;
+    const int64_t cw = c0 + (threadIdx.x & ~31);
+    if (LM && cw >= p.C) return;
+    const int nw = (int)(p.C - cw < 32 ? p.C - cw : 32);
+    const bool live = c0 + threadIdx.x < p.C;
+    const int64_t c = (LM && !live) ? p.C - 1 : c0 + threadIdx.x;
+    if (LM || live) {
         const double* q = p.q + c * p.D;
-        if (p.limits != nullptr) {  // robot.py:297-302
+        if (live && p.limits != nullptr) {  // robot.py:297-302
             int bad = 0;
             for (int j = 0; j < p.D; ++j) {
                 const double v = q[j];
@@ -275,7 +284,7 @@ __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __gr
                 for (int e = 0; e < 12; ++e) w[e] = prev[e];
             }
             // outputs + window alignment (phase 3)
-            if (p.R_all != nullptr) {
+            if (p.R_all != nullptr && live) {
                 double* dr = p.R_all + (c * p.n_links + k2) * 9;
                 double* dtt = p.T_all + (c * p.n_links + k2) * 3;
 #pragma unroll
@@ -283,7 +292,32 @@ __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __gr
 #pragma unroll
                 for (int k = 0; k < 3; ++k) dtt[k] = T[k];
             }
-            if (L.geom_slot >= 0 && (STAGE || p.R_geo != nullptr)) {
+            if constexpr (LM) if (L.geom_slot >= 0 && p.R_geo != nullptr) {
+                __shared__ double s_R[FKS_THREADS / 32][32 * 9];
+                __shared__ double s_dt[FKS_THREADS / 32][32 * 3];
+                __shared__ int32_t s_anc[FKS_THREADS / 32][32 * 3];
+                const int wi = threadIdx.x >> 5;
+                int32_t anc[3];
+                double del[3];
+                if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del, p.rinv) && live)
+                    atomicAdd(&p.flags[1], 1);
+#pragma unroll
+                for (int e = 0; e < 9; ++e) s_R[wi][lane * 9 + e] = R[e];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    s_dt[wi][lane * 3 + k] = del[k];
+                    s_anc[wi][lane * 3 + k] = anc[k];
+                }
+                __syncwarp();
+                const int64_t run = (int64_t)L.geom_slot * p.C + cw;  // first record of the warp's run
+                for (int i = lane; i < nw * 9; i += 32) p.R_geo[run * 9 + i] = s_R[wi][i];
+                for (int i = lane; i < nw * 3; i += 32) {
+                    p.dt_geo[run * 3 + i] = s_dt[wi][i];
+                    p.anchor_geo[run * 3 + i] = s_anc[wi][i];
+                }
+                __syncwarp();
+            }
+            if (!LM && L.geom_slot >= 0 && (STAGE || p.R_geo != nullptr)) {
                 const int64_t o = STAGE ? (int64_t)threadIdx.x * G + L.geom_slot : c * G + L.geom_slot;
                 double* oR = STAGE ? sR : p.R_geo;
                 double* odt = STAGE ? sdt : p.dt_geo;
@@ -302,7 +336,7 @@ __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __gr
             }
         }
     }
-    if (!STAGE) return;
+    if (!STAGE || LM) return;
     __syncthreads();
     if (p.R_geo == nullptr) return;
     // this CTA's configurations are contiguous in every output
@@ -330,10 +364,11 @@ __global__ void align_kernel(const double* T, int64_t n, lsdf_env_grid env, int3
 
 }  // namespace
 
-extern "C" int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_geo, const double* q_dev, int64_t C,
-                             int32_t D, const double* limits_dev, const lsdf_env_grid* env, const int32_t W[3],
-                             double* R_all_dev, double* T_all_dev, double* R_geo_dev, double* dt_geo_dev,
-                             int32_t* anchor_geo_dev, int32_t* flags_dev, void* stream) {
+namespace {
+int fk_align_impl(const lsdf_link* links, int32_t n_links, int32_t n_geo, const double* q_dev, int64_t C, int32_t D,
+                  const double* limits_dev, const lsdf_env_grid* env, const int32_t W[3], double* R_all_dev,
+                  double* T_all_dev, double* R_geo_dev, double* dt_geo_dev, int32_t* anchor_geo_dev,
+                  int32_t* flags_dev, void* stream, bool link_major) {
     if (n_links < 1 || n_links > LSDF_MAX_LINKS || n_geo > LSDF_MAX_LINKS)
         return fail(LSDF_ERR_VALIDATION, "lsdf_fk_align: %d links outside 1..%d", n_links, LSDF_MAX_LINKS);
     if (C <= 0) return LSDF_OK;
@@ -341,6 +376,7 @@ extern "C" int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_
     for (int i = 0; i < n_links; ++i) p.links[i] = links[i];
     p.n_links = n_links;
     p.n_geo = n_geo;
+    p.link_major = link_major;
     p.D = D;
     p.C = C;
     p.q = q_dev;
@@ -366,25 +402,47 @@ extern "C" int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_
     const size_t smem = (size_t)2 * FK_THREADS * 12 * sizeof(double);  // local + world, cpb * lp slots each
     if (flags_dev != nullptr)
         LSDF_TRY(check_cuda(cudaMemsetAsync(flags_dev, 0, 2 * sizeof(int32_t), (cudaStream_t)stream), "fk flags memset"));
+    if (C >= FK_SERIAL_MIN && link_major) {
+        fk_align_serial_kernel<true, true><<<grid_for(C, FKS_THREADS), FKS_THREADS, 0, (cudaStream_t)stream>>>(p);
+        return check_launch("fk_align_serial_kernel");
+    }
     if (C >= FK_SERIAL_MIN) {
         if (FK_STAGE_OUTPUTS) {
             const size_t smem_s = (size_t)FKS_THREADS * n_geo * (12 * sizeof(double) + 3 * sizeof(int32_t));
             static bool attr = false;
             if (!attr) {
-                LSDF_TRY(check_cuda(cudaFuncSetAttribute(fk_align_serial_kernel<true>,
+                LSDF_TRY(check_cuda(cudaFuncSetAttribute(fk_align_serial_kernel<true, false>,
                                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024),
                                     "fk smem attribute"));
                 attr = true;
             }
-            fk_align_serial_kernel<true>
+            fk_align_serial_kernel<true, false>
                 <<<grid_for(C, FKS_THREADS), FKS_THREADS, smem_s, (cudaStream_t)stream>>>(p);
         } else {
-            fk_align_serial_kernel<false><<<grid_for(C, FKS_THREADS), FKS_THREADS, 0, (cudaStream_t)stream>>>(p);
+            fk_align_serial_kernel<false, false><<<grid_for(C, FKS_THREADS), FKS_THREADS, 0, (cudaStream_t)stream>>>(p);
         }
         return check_launch("fk_align_serial_kernel");
     }
     fk_align_kernel<<<grid_for(C, cpb), FK_THREADS, smem, (cudaStream_t)stream>>>(p, lp_log2);
     return check_launch("fk_align_kernel");
+}
+}  // namespace
+
+extern "C" int lsdf_fk_align(const lsdf_link* links, int32_t n_links, int32_t n_geo, const double* q_dev, int64_t C,
+                             int32_t D, const double* limits_dev, const lsdf_env_grid* env, const int32_t W[3],
+                             double* R_all_dev, double* T_all_dev, double* R_geo_dev, double* dt_geo_dev,
+                             int32_t* anchor_geo_dev, int32_t* flags_dev, void* stream) {
+    return fk_align_impl(links, n_links, n_geo, q_dev, C, D, limits_dev, env, W, R_all_dev, T_all_dev, R_geo_dev,
+                         dt_geo_dev, anchor_geo_dev, flags_dev, stream, false);
+}
+
+extern "C" int lsdf_fk_align_link_major(const lsdf_link* links, int32_t n_links, int32_t n_geo, const double* q_dev,
+                                        int64_t C, int32_t D, const double* limits_dev, const lsdf_env_grid* env,
+                                        const int32_t W[3], double* R_all_dev, double* T_all_dev, double* R_geo_dev,
+                                        double* dt_geo_dev, int32_t* anchor_geo_dev, int32_t* flags_dev,
+                                        void* stream) {
+    return fk_align_impl(links, n_links, n_geo, q_dev, C, D, limits_dev, env, W, R_all_dev, T_all_dev, R_geo_dev,
+                         dt_geo_dev, anchor_geo_dev, flags_dev, stream, true);
 }
 
 extern "C" int lsdf_align(const double* T_dev, int64_t n, const lsdf_env_grid* env, const int32_t W[3],

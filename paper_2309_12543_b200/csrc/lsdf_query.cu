@@ -56,6 +56,7 @@ struct QueryParams {
     double e_r, e_rinv;  // window extent and RN(1 / e_r)
     const double* P;
     int32_t Wmax, by_position;
+    int64_t pose_cs, pose_ls;  // pose record of (c, l) at c * pose_cs + l * pose_ls (config- or link-major)
     const int16_t* zrange;
     const uint32_t* mask_bits;
     int32_t dims[3];
@@ -130,12 +131,13 @@ __global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_c
     uint32_t* queue = s_queue + warp * QCAP;
     const float4* __restrict__ cells = p.cells[l];
     const float far = p.dfar[l];
-    const int64_t o = c * p.n_geo + l;
+    const int64_t o = c * p.n_geo + l;                  // per-link slot
+    const int64_t po = c * p.pose_cs + l * p.pose_ls;   // pose record
     double R[9], dtinv[3];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) R[e] = __ldg(p.R + o * 9 + e);
-    shift_inverse(R, p.dt + o * 3, p.e_r, dtinv);
-    const int ax = __ldg(p.anchor + o * 3), ay = __ldg(p.anchor + o * 3 + 1), az = __ldg(p.anchor + o * 3 + 2);
+    for (int e = 0; e < 9; ++e) R[e] = __ldg(p.R + po * 9 + e);
+    shift_inverse(R, p.dt + po * 3, p.e_r, dtinv);
+    const int ax = __ldg(p.anchor + po * 3), ay = __ldg(p.anchor + po * 3 + 1), az = __ldg(p.anchor + po * 3 + 2);
     const int W0 = p.W[0], W1 = p.W[1], W2 = p.W[2];
     const int ny = p.dims[1], nz = p.dims[2];
     const int n_cols = W0 * W1;
@@ -296,7 +298,7 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_
     const uint32_t per_link = (uint32_t)(p.C * p.split);
     const uint32_t r = t % per_link;
     const int64_t c = p.split == 1 ? r : r / p.split;
-    const int64_t o = c * p.n_geo + l;
+    const int64_t o = c * p.pose_cs + l * p.pose_ls;  // pose record
     double R[9], dtinv[3], dt[3];
 #pragma unroll
     for (int e = 0; e < 9; ++e) R[e] = __ldg(p.R + o * 9 + e);
@@ -714,7 +716,10 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     p.round_min = p.seg_filter ? 32 : 16;
     p.P = window->P_dev;
     p.Wmax = window->Wmax;
-    p.by_position = by_position;
+    p.by_position = by_position & LSDF_QUERY_BY_POSITION;
+    const bool link_major = (by_position & LSDF_QUERY_POSES_LINK_MAJOR) != 0;
+    p.pose_cs = link_major ? 1 : n_geo;
+    p.pose_ls = link_major ? C : 1;
     p.zrange = window->zrange_dev;
     p.mask_bits = window->mask_bits_dev;
     p.clamp = clamp;
@@ -800,7 +805,7 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
                     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
                 attr = true;
             }
-            const int variant = (by_position ? 2 : 0) + (p.bricks != nullptr ? 1 : 0);
+            const int variant = (p.by_position ? 2 : 0) + (p.bricks != nullptr ? 1 : 0);
             const ShellsKernel kern = kernels[variant];
             // residency cache: (device, variant, smem bytes) -> CTAs per SM
             thread_local int c_dev = -1, c_bp = -1, c_sm = 148, c_per = 1;
@@ -865,12 +870,12 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
             if (le != cudaSuccess) return fail(LSDF_ERR_CUDA, "query_shells_kernel: %s", cudaGetErrorString(le));
             ++n_launch;
         } else if (full) {
-            if (by_position)
+            if (p.by_position)
                 query_direct_kernel<true, true><<<blocks, 32 * WARPS, smem, s>>>(p, blocks_per_link);
             else
                 query_direct_kernel<true, false><<<blocks, 32 * WARPS, smem, s>>>(p, blocks_per_link);
         } else {
-            if (by_position)
+            if (p.by_position)
                 query_direct_kernel<false, true><<<blocks, 32 * WARPS, smem, s>>>(p, blocks_per_link);
             else
                 query_direct_kernel<false, false><<<blocks, 32 * WARPS, smem, s>>>(p, blocks_per_link);

@@ -179,7 +179,7 @@ class TrajectorySdf:
     """
 
     def __init__(self, sdfs, grid: EnvGrid, window, R_dev, dt_dev, anchor_dev, d_far_global=None,
-                 flags=None, pin_l2: bool | None = None):
+                 flags=None, pin_l2: bool | None = None, link_major: bool = False):
         from .placement import _check_links, link_grid_table, packed_arena
 
         _check_links(sdfs, window)
@@ -189,6 +189,10 @@ class TrajectorySdf:
         self.R = R_dev
         self.dt = dt_dev
         self.anchor = anchor_dev
+        # link-major storage ((L, C, .) buffers seen as (C, L, .) views, as the
+        # DistanceChecker keeps large batches): the fused query reads it in
+        # place, the other kernels get configuration-major copies
+        self.link_major = bool(link_major)
         self.d_far_global = float(min(s.d_far for s in sdfs) if d_far_global is None else d_far_global)
         # the packed grids in one arena, pinned in L2 (persisting set-aside)
         self._arena, ptrs = packed_arena(self.sdfs)
@@ -203,6 +207,12 @@ class TrajectorySdf:
     @property
     def n_configs(self) -> int:
         return int(self.R.shape[0])
+
+    def config_major(self):
+        """(R, dt, anchor) in the (C, L, .) layout the placement and materialization kernels read."""
+        if not self.link_major:
+            return self.R, self.dt, self.anchor
+        return self.R.contiguous(), self.dt.contiguous(), self.anchor.contiguous()
 
     @property
     def n_links(self) -> int:
@@ -260,7 +270,8 @@ class TrajectorySdf:
     def windows_device(self):
         from .placement import place_windows_device
 
-        return place_windows_device(self.sdfs, self.R, self.dt, self.window)
+        R, dt, _ = self.config_major()
+        return place_windows_device(self.sdfs, R, dt, self.window)
 
     def device_values(self, max_bytes: int = 1 << 36):
         if self._dense is None:
@@ -273,7 +284,7 @@ class TrajectorySdf:
             win = self.windows_device()
             cfg = t.arange(C_, device=win.device, dtype=t.int32).repeat_interleave(L)
             out = N.empty((C_,) + tuple(int(d) for d in self.grid.dims), t.float32)
-            N.call("lsdf_assemble", N.ptr(win), N.ptr(self.anchor), N.ptr(cfg), C_ * L, N.i32x3(self.window.dims),
+            N.call("lsdf_assemble", N.ptr(win), N.ptr(self.config_major()[2]), N.ptr(cfg), C_ * L, N.i32x3(self.window.dims),
                    ctypes.byref(self.grid.c_struct()), C_, self.d_far_global, N.ptr(out), N.stream())
             self._dense = out
         return self._dense
@@ -299,9 +310,10 @@ class TrajectorySdf:
         if self._ws is None:  # zeroed once; every launch leaves it zeroed again
             nbytes = int(N.lib().lsdf_query_workspace_bytes(C_, self.n_links))
             self._ws = N.zeros((nbytes,), t.uint8)
+        flags = (N.QUERY_BY_POSITION if by_position else 0) | (N.QUERY_POSES_LINK_MAJOR if self.link_major else 0)
         N.call("lsdf_query_direct", N.ptr(self.R), N.ptr(self.dt), N.ptr(self.anchor), C_, self.n_links,
                self._table, ctypes.byref(ws), ctypes.byref(self.grid.c_struct()), N.ptr(occupancy),
-               int(by_position), self.d_far_global, N.ptr(self._ws), N.ptr(out["d"]), N.ptr(out["link"]),
+               flags, self.d_far_global, N.ptr(self._ws), N.ptr(out["d"]), N.ptr(out["link"]),
                N.ptr(out["voxel"]), N.ptr(out.get("per_link")), N.stream())
         return out
 
@@ -327,7 +339,8 @@ class VoxelMajorSdf:
         C_ = traj.n_configs
         self.field = N.empty((self.grid.n_voxels, C_), t.float32)
         ws, _ = traj.window.device_tables()
-        N.call("lsdf_materialize_vm", N.ptr(traj.R), N.ptr(traj.dt), N.ptr(traj.anchor), C_, traj.n_links,
+        self._poses = R, dt, anchor = traj.config_major()  # the per-cycle link pass reads them too
+        N.call("lsdf_materialize_vm", N.ptr(R), N.ptr(dt), N.ptr(anchor), C_, traj.n_links,
                traj._table, ctypes.byref(ws), ctypes.byref(self.grid.c_struct()), self.d_far_global,
                self.field, N.stream())
         self._keys = N.zeros((C_,), t.int64)  # the kernels leave it zeroed
@@ -355,7 +368,8 @@ class VoxelMajorSdf:
             out["voxel"] = N.empty((C_,), t.int32)
         tr = self.traj
         ws, _ = tr.window.device_tables()
-        N.call("lsdf_query_vm", self.field, N.ptr(tr.R), N.ptr(tr.dt), N.ptr(tr.anchor), C_, tr.n_links, tr._table,
+        R, dt, anchor = self._poses
+        N.call("lsdf_query_vm", self.field, N.ptr(R), N.ptr(dt), N.ptr(anchor), C_, tr.n_links, tr._table,
                ctypes.byref(ws), ctypes.byref(self.grid.c_struct()), N.ptr(occupancy), N.ptr(indices_dev), int(n_list),
                self.d_far_global, self._keys, out["d"], out["link"], out["voxel"], N.stream())
         return out

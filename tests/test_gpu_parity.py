@@ -500,9 +500,13 @@ def test_config4_shape_large_batch(L):
     assert np.abs(d[sub].astype(np.float64) - rd).max() <= D_TOL
     assert np.array_equal(link[sub], rl) and np.array_equal(voxel[sub], rv)
     chk = L.DistanceChecker(robot, sdfs, grid, window).prepare(C, len(pts), np.float32)
+    assert chk.link_major  # large batches keep the poses link-major
     for _ in range(2):
         dc, lc, vc = chk.query(q, pts)
         assert np.array_equal(dc, d) and np.array_equal(lc, link) and np.array_equal(vc, voxel)
+    # the link-major poses (lsdf_fk_align_link_major) == the configuration-major ones, bit for bit
+    for a, b in zip(chk.traj.config_major(), (traj.R, traj.dt, traj.anchor)):
+        assert np.array_equal(a.reshape(C, len(sdfs), -1).cpu().numpy(), b.reshape(C, len(sdfs), -1).cpu().numpy())
     # the scan orders the links by the previous cycle's argmin counts (kept in
     # the query workspace); any order must give the same answer: force some
     a256 = lambda n: (n + 255) // 256 * 256  # noqa: E731

@@ -51,7 +51,7 @@ def main():
     def query():
         tr = chk.traj
         N.call("lsdf_query_direct", N.ptr(chk.R_geo), N.ptr(chk.dt_geo), N.ptr(chk.anchor_geo), C_, tr.n_links,
-               tr._table, ctypes.byref(chk._wstruct), env, N.ptr(chk.ws), 0, chk.d_far_global, N.ptr(chk.qws),
+               tr._table, ctypes.byref(chk._wstruct), env, N.ptr(chk.ws), chk._qflags, chk.d_far_global, N.ptr(chk.qws),
                N.ptr(chk.d_dev), N.ptr(chk.link_dev), N.ptr(chk.voxel_dev), None,
                torch.cuda.current_stream().cuda_stream)
 

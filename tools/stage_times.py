@@ -42,7 +42,7 @@ def main():
     env = ctypes.byref(grid.c_struct())
 
     def fk():
-        N.call("lsdf_fk_align", chk._chain, robot.n_links, len(sdfs), N.ptr(chk.q_dev), C_, robot.dof,
+        N.call(chk._fk_entry, chk._chain, robot.n_links, len(sdfs), N.ptr(chk.q_dev), C_, robot.dof,
                N.ptr(chk.limits), env, chk._W, None, None, N.ptr(chk.R_geo), N.ptr(chk.dt_geo), N.ptr(chk.anchor_geo),
                N.ptr(chk.flags), N.stream())
 
@@ -52,7 +52,7 @@ def main():
     def query():
         tr = chk.traj
         N.call("lsdf_query_direct", N.ptr(chk.R_geo), N.ptr(chk.dt_geo), N.ptr(chk.anchor_geo), C_, tr.n_links,
-               tr._table, ctypes.byref(chk._wstruct), env, N.ptr(chk.ws), 0, chk.d_far_global, N.ptr(chk.qws),
+               tr._table, ctypes.byref(chk._wstruct), env, N.ptr(chk.ws), chk._qflags, chk.d_far_global, N.ptr(chk.qws),
                N.ptr(chk.d_dev), N.ptr(chk.link_dev), N.ptr(chk.voxel_dev), None, N.stream())
 
     def graph():
