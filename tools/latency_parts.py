@@ -40,7 +40,7 @@ def main():
     s = torch.cuda.Stream()
 
     def fk():
-        N.call("lsdf_fk_align", chk._chain, robot.n_links, len(sdfs), N.ptr(chk.q_dev), C_, robot.dof,
+        N.call(chk._fk_entry, chk._chain, robot.n_links, len(sdfs), N.ptr(chk.q_dev), C_, robot.dof,
                N.ptr(chk.limits), env, chk._W, None, None, N.ptr(chk.R_geo), N.ptr(chk.dt_geo), N.ptr(chk.anchor_geo),
                N.ptr(chk.flags), torch.cuda.current_stream().cuda_stream)
 
