@@ -138,7 +138,10 @@ def load_library(path: Path | None = None):
                 f"linksdf-b200 CUDA extension not built ({p}); run "
                 "`python -m paper_2309_12543_b200.build` (nvcc, sm_100a)")
         lib = C.CDLL(str(p))
+        alternative = path is None and "LINKSDF_B200_LIB" in os.environ
         for name, argtypes in _SIGS.items():
+            if alternative and not hasattr(lib, name):  # an older build in an A/B run: skip newer entries
+                continue
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = C.c_int64 if name.endswith("_bytes") else C.c_int

@@ -103,8 +103,9 @@ voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, do
                 const int col = (ix >> BRICK_LOG2) * nby + (iy >> BRICK_LOG2);
                 const uint32_t zb = 1u << (iz >> BRICK_LOG2);
                 if (PRIVATE) {
-                    atomicOr(s_bits + (lin >> 5), 1u << (lin & 31));
-                    if (n_cols) atomicOr(s_bricks + col, zb);
+                    const uint32_t bit = 1u << (lin & 31);
+                    // a voxel marks its brick once per CTA (dense clouds repeat voxels)
+                    if (!(atomicOr(s_bits + (lin >> 5), bit) & bit) && n_cols) atomicOr(s_bricks + col, zb);
                 } else {
                     atomicOr(bitmap + (lin >> 5), 1u << (lin & 31));
                     if (n_cols) atomicOr(bricks + col, zb);
