@@ -910,3 +910,29 @@ def test_c_abi_client(L, name, tmp_path):
     assert np.array_equal(link, g["link"]) and np.array_equal(voxel, g["voxel"])
     d_py, link_py, voxel_py = L.query_trajectory(robot, g["q"], sdfs, grid, window, g["points"])
     assert np.array_equal(d, d_py) and np.array_equal(link, link_py) and np.array_equal(voxel, voxel_py)
+
+
+@pytest.mark.parametrize("C", [6161, 6145 + 64])
+def test_link_major_checker_ragged_batch(L, C):
+    """Link-major poses (lsdf_fk_align_link_major) with a batch that ends inside a
+    warp / CTA: the checker == the configuration-major fused query bit for bit."""
+    from paper_2309_12543_b200 import scenarios as S
+
+    shape = S.CONFIG4
+    robot = L.RobotModel.from_dict(shape.robot)
+    grid = L.EnvGrid(shape.grid_extent, shape.grid_res)
+    sdfs = [L.build_link_sdf(robot.links[i].geometry, shape.link_extent, shape.link_res, link_id=i)
+            for i in robot.geometry_links]
+    window = L.WindowGeometry.build(shape.link_extent, grid)
+    q = S.random_configs(shape.robot, C, seed=9)
+    pts = S.cloud_for(shape, seed=9)[:200_000].astype(np.float32)
+    traj = L.TrajectorySdf.from_configs(robot, q, sdfs, grid, window)
+    ref = L.query_min_distances(traj, L.voxelize_pointcloud(pts, grid), return_argmin=True)
+    chk = L.DistanceChecker(robot, sdfs, grid, window).prepare(C, len(pts), np.float32)
+    assert chk.link_major
+    for _ in range(2):
+        got = chk.query(q, pts)
+        for a, b in zip(got, ref):
+            assert np.array_equal(a, b)
+    for a, b in zip(chk.traj.config_major(), (traj.R, traj.dt, traj.anchor)):
+        assert np.array_equal(a.reshape(C, len(sdfs), -1).cpu().numpy(), b.reshape(C, len(sdfs), -1).cpu().numpy())
