@@ -808,7 +808,7 @@ def test_mixed_link_grids(L, C):
 
 
 
-def _sharded_worker(rank, world, port, out):
+def _sharded_worker(rank, world, port, out, n_configs=64):
     import os
 
     import torch
@@ -825,7 +825,7 @@ def _sharded_worker(rank, world, port, out):
 
     g = golden("scene_c2")
     robot, grid, sdfs, window = _scene(L, g)
-    q = S.random_configs(_doc(g), 64, seed=5)
+    q = S.random_configs(_doc(g), n_configs, seed=5)
     pts = np.concatenate([S.human_cloud(40_000, seed=5), np.float64([[5.0, 0, 0], [np.nan, 0, 0]])]).astype(np.float32)
     lo, hi = shard_range(len(pts), rank, world)
     ql, qh = shard_range(len(q), rank, world)
@@ -843,9 +843,11 @@ def _sharded_worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_sharded_cloud_pipeline(L):
+@pytest.mark.parametrize("n_configs", [64, 12_400])
+def test_sharded_cloud_pipeline(L, n_configs):
     """Each of 2 ranks uploads half of the cloud; the bitmap all-gather + OR
-    merge reproduces one rank voxelizing everything (dropped points too)."""
+    merge reproduces one rank voxelizing everything (dropped points too);
+    6,200 configurations per rank run the link-major pose path."""
     import multiprocessing as mp
     import socket
 
@@ -854,7 +856,7 @@ def test_sharded_cloud_pipeline(L):
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q, n_configs)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(2))
