@@ -171,3 +171,18 @@ def test_scan_bounds_hold_on_random_grids():
         tt = np.clip((pts - a) @ u, 0.0, length)
         d = np.linalg.norm(pts - a - tt[:, None] * u, axis=1)
         assert np.all(v >= d - k_lo) and np.all(v <= d + k_hi)
+
+
+def test_link_major_threshold_matches_fk_crossover():
+    """The checker keeps poses link-major from the batch size at which FK runs one
+    thread per configuration (the kernel whose writes the layout serves)."""
+    from paper_2309_12543_b200.checker import LINK_MAJOR_MIN
+
+    src = (REPO / "paper_2309_12543_b200" / "csrc" / "lsdf_fk.cu").read_text()
+    m = re.search(r"constexpr int64_t FK_SERIAL_MIN = (\d+);", src)
+    assert m and int(m.group(1)) == LINK_MAJOR_MIN
+    header = (REPO / "include" / "linksdf_b200.h").read_text()
+    from paper_2309_12543_b200 import _native as N
+
+    assert f"#define LSDF_QUERY_BY_POSITION {N.QUERY_BY_POSITION}" in header
+    assert f"#define LSDF_QUERY_POSES_LINK_MAJOR {N.QUERY_POSES_LINK_MAJOR}" in header
