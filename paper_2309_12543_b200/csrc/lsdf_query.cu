@@ -274,7 +274,6 @@ struct ShellView {
     const uint32_t* bits;    // occupancy bitmap (shared or global)
     const uint32_t* bricks;  // brick columns (shared), or null
     const double* P;         // window offsets (shared)
-    const float* Pf;         // the same in f32 (shared), for the segment bound
 };
 
 // Per-task constants, computed by one lane per task (up to GRAB_MAX tasks at a
@@ -313,10 +312,20 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_
     for (int e = 0; e < 3; ++e) s.dtinv[e] = dtinv[e];
     const float4 sa = p.seg_a[l];
     const float a3[3] = {sa.x, sa.y, sa.z};
+    // the window offsets are affine in the cell index, P_a[m] = P_a[0] + m s_a:
+    // fold them in, so the scan evaluates A' m + b' straight from the cell
+    // indices (no offset-table loads)
+    const int Wm = p.Wmax;
+    const double p0[3] = {__ldg(p.P), __ldg(p.P + Wm), __ldg(p.P + 2 * Wm)};
+    const double sc[3] = {__ldg(p.P + 1) - p0[0], __ldg(p.P + Wm + 1) - p0[1], __ldg(p.P + 2 * Wm + 1) - p0[2]};
 #pragma unroll
-    for (int e = 0; e < 9; ++e) s.A[e] = (float)(R[e] * p.e_r);
+    for (int a = 0; a < 3; ++a)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) s.b[k] = (float)(dtinv[k] * p.e_r - (double)a3[k]);
+        for (int k = 0; k < 3; ++k) s.A[3 * a + k] = (float)(R[3 * a + k] * p.e_r * sc[a]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        s.b[k] = (float)(dtinv[k] * p.e_r - (double)a3[k] +
+                         p.e_r * (R[k] * p0[0] + R[3 + k] * p0[1] + R[6 + k] * p0[2]));
     s.slack = dtn + p.core[l];
     float t0 = p.clamp;  // values >= clamp never change the answer
     if (p.per_link == nullptr) {  // best key any link of this configuration has published so far (an upper
@@ -457,7 +466,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
             float d2q = INFINITY;  // squared segment distance of a cell that stays queued
             if (occ) {
                 const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
-                const float px = sv.Pf[mx], py = sv.Pf[Wm + my], pz = sv.Pf[2 * Wm + mz];
+                const float px = (float)mx, py = (float)my, pz = (float)mz;  // offsets folded into A, b
                 float q[3];
 #pragma unroll
                 for (int e = 0; e < 3; ++e) q[e] = fmaf(pz, st.A[6 + e], fmaf(py, st.A[3 + e], fmaf(px, st.A[e], st.b[e])));
@@ -513,8 +522,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     extern __shared__ double s_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* sP = s_dyn;
-    float* sPf = (float*)(sP + 3 * p.Wmax);
-    uint32_t* s_queue = (uint32_t*)(sPf + 3 * p.Wmax + (p.Wmax & 1) * 3);  // keep 8-B alignment
+    uint32_t* s_queue = (uint32_t*)(sP + 3 * p.Wmax);
     // staged tables start on 16-B boundaries (cp.async 16-B chunks)
     uint32_t* s_cells = (uint32_t*)align16_ptr(s_queue + WARPS * QCAP_SHELL);
     float* s_radius = (float*)align16_ptr(s_cells + (stage_shell ? p.n_shell : 0));
@@ -533,11 +541,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     if (stage_bits) stage_async(s_bits, p.bitmap, (size_t)n_words * 4);
     if (n_cols) stage_async(s_bricks, p.bricks, (size_t)n_cols * 4);
     cp_async_commit();
-    for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) {
-        const double v = p.P[i];
-        sP[i] = v;
-        sPf[i] = (float)v;
-    }
+    for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) sP[i] = p.P[i];
     // link processing order (lane k holds the link of rank k): decreasing
     // argmin count of the previous cycle, ties in p.group order
     int order_lane;
@@ -583,7 +587,6 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     sv.bits = stage_bits ? s_bits : p.bitmap;
     sv.bricks = n_cols ? s_bricks : nullptr;
     sv.P = sP;
-    sv.Pf = sPf;
     uint32_t* queue = s_queue + warp * QCAP_SHELL;
     // guided grab sizes: the grab shrinks as the remaining work does, so the
     // last warps to finish carry at most a small grab (shorter tail)
@@ -791,7 +794,7 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
         if (shells) {
             const int stage_shell = p.n_shell <= SHELL_STAGE_MAX;
             const int stage_bits = o.n_words <= BITMAP_STAGE_MAX;
-            const size_t smem_s = (size_t)3 * window->Wmax * (sizeof(double) + sizeof(float)) + 12 +
+            const size_t smem_s = (size_t)3 * window->Wmax * sizeof(double) +
                                   (size_t)WARPS * QCAP_SHELL * 4 +
                                   (stage_shell ? (size_t)p.n_shell * 8 : 0) + (stage_bits ? (size_t)o.n_words * 4 : 0) +
                                   (p.bricks != nullptr ? (size_t)o.nbx * o.nby * 4 : 0) +
