@@ -128,7 +128,8 @@ typedef struct {
     const uint32_t* mask_bits_dev;
     /* window cells of the sphere mask sorted by distance from the window
      * centre: packed (mx | my << 8 | mz << 16) and the distance in metres
-     * (rounded down), n_masked entries each; NULL disables shell order */
+     * (rounded down), n_masked entries each, padded to a multiple of 32 with
+     * copies of the last entry; NULL disables shell order */
     const uint32_t* shell_cells_dev;
     const float* shell_radius_dev;
 } lsdf_window;

@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_c
 // stops.  Occupied cells are compacted with a ballot and evaluated 32 at a
 // time with the exact fp64 recipe, so the results are those of the full scan.
 constexpr int QCAP_SHELL = 64;
+__host__ __device__ __forceinline__ int shell_padded(int n) { return (n + 31) & ~31; }
 constexpr int SHELL_STAGE_MAX = 4096;   // kept cells staged in shared memory (W <= 20)
 constexpr int BITMAP_STAGE_MAX = 8192;  // occupancy words staged in shared memory (<= 262k voxels)
 
@@ -443,11 +444,10 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
             break;
         }
         STAT(1, 1);
-        const int k = k0 + lane;
+        // the shell list is padded to whole chunks with copies of its last cell
+        const uint32_t cell = sv.cells[k0 + lane];
         bool occ = false;
-        uint32_t cell = 0;
-        if (k < p.n_shell) {
-            cell = sv.cells[k];
+        {
             const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
             const int x = ax + mx, y = ay + my, z = az + mz;
             if (x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz) {
@@ -525,8 +525,8 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     uint32_t* s_queue = (uint32_t*)(sP + 3 * p.Wmax);
     // staged tables start on 16-B boundaries (cp.async 16-B chunks)
     uint32_t* s_cells = (uint32_t*)align16_ptr(s_queue + WARPS * QCAP_SHELL);
-    float* s_radius = (float*)align16_ptr(s_cells + (stage_shell ? p.n_shell : 0));
-    uint32_t* s_bits = (uint32_t*)align16_ptr(s_radius + (stage_shell ? p.n_shell : 0));
+    float* s_radius = (float*)align16_ptr(s_cells + (stage_shell ? shell_padded(p.n_shell) : 0));
+    uint32_t* s_bits = (uint32_t*)align16_ptr(s_radius + (stage_shell ? shell_padded(p.n_shell) : 0));
     uint32_t* s_bricks = (uint32_t*)align16_ptr(s_bits + (stage_bits ? n_words : 0));
     const int n_cols = BRICKS ? (int)(((p.dims[0] + 3) >> BRICK_LOG2) * p.nby_brick) : 0;
     __shared__ ShellSetup s_setup[WARPS][GRAB_MAX];
@@ -535,8 +535,8 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     // land: the latency path pays one memory round trip here, not one per
     // loop iteration.
     if (stage_shell) {
-        stage_async(s_cells, p.shell_cells, (size_t)p.n_shell * 4);
-        stage_async(s_radius, p.shell_radius, (size_t)p.n_shell * 4);
+        stage_async(s_cells, p.shell_cells, (size_t)shell_padded(p.n_shell) * 4);
+        stage_async(s_radius, p.shell_radius, (size_t)shell_padded(p.n_shell) * 4);
     }
     if (stage_bits) stage_async(s_bits, p.bitmap, (size_t)n_words * 4);
     if (n_cols) stage_async(s_bricks, p.bricks, (size_t)n_cols * 4);
@@ -796,7 +796,7 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
             const int stage_bits = o.n_words <= BITMAP_STAGE_MAX;
             const size_t smem_s = (size_t)3 * window->Wmax * sizeof(double) +
                                   (size_t)WARPS * QCAP_SHELL * 4 +
-                                  (stage_shell ? (size_t)p.n_shell * 8 : 0) + (stage_bits ? (size_t)o.n_words * 4 : 0) +
+                                  (stage_shell ? (size_t)shell_padded(p.n_shell) * 8 : 0) + (stage_bits ? (size_t)o.n_words * 4 : 0) +
                                   (p.bricks != nullptr ? (size_t)o.nbx * o.nby * 4 : 0) +
                                   64;  // 16-B alignment of the four staged tables
             using ShellsKernel = void (*)(QueryParams, int, int, int, int, int, int64_t, int);

@@ -164,7 +164,7 @@ class WindowGeometry:
         P (3, Wmax) f64 normalized offsets; zrange (W1*W0, 2) i16 or None when a
         column's kept cells are not one z interval; mask_bits u32; shell_cells
         u32 / shell_radius f32 (kept cells by distance from the window centre,
-        radius rounded down); kept_cells i32 (x-fastest order).
+        radius rounded down; padded to a multiple of 32 with the last cell); kept_cells i32 (x-fastest order).
         """
         W = [int(d) for d in self.dims]
         if max(W) > 256:
@@ -194,6 +194,12 @@ class WindowGeometry:
         packed = (mxs | (mys << 8) | (mzs << 16)).astype(np.uint32)[order]
         radius = np.nextafter(dist[order].astype(np.float32), np.float32(-np.inf))  # rounded down
         radius = np.minimum(radius, dist[order]).astype(np.float32)
+        # padded to whole 32-cell chunks with copies of the last cell: the scan
+        # needs no per-lane bound check, and a repeated cell changes no minimum
+        pad = -len(packed) % 32
+        if pad and len(packed):
+            packed = np.concatenate([packed, np.repeat(packed[-1:], pad)])
+            radius = np.concatenate([radius, np.repeat(radius[-1:], pad)])
         return {"W": W, "Wmax": Wmax, "n_masked": self.n_masked, "e_r": float(self.extent), "P": P,
                 "zrange": zr.reshape(-1, 2) if interval else None, "mask_bits": words,
                 "shell_cells": packed, "shell_radius": radius,
