@@ -449,8 +449,9 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
         bool occ = false;
         {
             const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
-            const int x = ax + mx, y = ay + my, z = az + mz;
-            if (x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz) {
+            // 0 <= x < nx as one unsigned compare per axis
+            const unsigned x = (unsigned)(ax + mx), y = (unsigned)(ay + my), z = (unsigned)(az + mz);
+            if ((x < (unsigned)nx) & (y < (unsigned)ny) & (z < (unsigned)nz)) {
                 const int lin = lin0 + (mx * ny + my) * nz + mz;
                 occ = (sv.bits[lin >> 5] >> (lin & 31)) & 1u;
             }
