@@ -463,7 +463,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
             STAT(3, __popc(b0));
         }
 #endif
-        if (use_seg && __any_sync(FULL_MASK, occ)) {
+        if (use_seg) {  // (dense clouds: some lane of a chunk is nearly always occupied)
             float d2q = INFINITY;  // squared segment distance of a cell that stays queued
             if (occ) {
                 const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
