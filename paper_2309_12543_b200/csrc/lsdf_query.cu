@@ -464,20 +464,18 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
         }
 #endif
         if (use_seg) {  // (dense clouds: some lane of a chunk is nearly always occupied)
-            float d2q = INFINITY;  // squared segment distance of a cell that stays queued
-            if (occ) {
-                const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
-                const float px = (float)mx, py = (float)my, pz = (float)mz;  // offsets folded into A, b
-                float q[3];
+            // every lane evaluates the bound (no divergent branch; most lanes are occupied)
+            const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
+            const float px = (float)mx, py = (float)my, pz = (float)mz;  // offsets folded into A, b
+            float q[3];
 #pragma unroll
-                for (int e = 0; e < 3; ++e) q[e] = fmaf(pz, st.A[6 + e], fmaf(py, st.A[3 + e], fmaf(px, st.A[e], st.b[e])));
-                const float t = fminf(fmaxf(fmaf(q[2], su.z, fmaf(q[1], su.y, q[0] * su.x)), 0.0f), su.w);
-                const float ex = fmaf(-t, su.x, q[0]), ey = fmaf(-t, su.y, q[1]), ez = fmaf(-t, su.z, q[2]);
-                const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
-                const float lim = thresh + k_lo;
-                occ = lim >= 0.0f && d2 <= lim * lim;
-                d2q = occ ? d2 : INFINITY;
-            }
+            for (int e = 0; e < 3; ++e) q[e] = fmaf(pz, st.A[6 + e], fmaf(py, st.A[3 + e], fmaf(px, st.A[e], st.b[e])));
+            const float t = fminf(fmaxf(fmaf(q[2], su.z, fmaf(q[1], su.y, q[0] * su.x)), 0.0f), su.w);
+            const float ex = fmaf(-t, su.x, q[0]), ey = fmaf(-t, su.y, q[1]), ez = fmaf(-t, su.z, q[2]);
+            const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+            const float lim = thresh + k_lo;
+            occ = occ && lim >= 0.0f && d2 <= lim * lim;
+            const float d2q = occ ? d2 : INFINITY;  // squared segment distance of a cell that stays queued
             // non-negative floats order like their bits: one integer min over the warp
             const uint32_t m = __reduce_min_sync(FULL_MASK, __float_as_uint(d2q));
             if (m < 0x7f800000u) {
