@@ -451,10 +451,10 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
             const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
             // 0 <= x < nx as one unsigned compare per axis
             const unsigned x = (unsigned)(ax + mx), y = (unsigned)(ay + my), z = (unsigned)(az + mz);
-            if ((x < (unsigned)nx) & (y < (unsigned)ny) & (z < (unsigned)nz)) {
-                const int lin = lin0 + (mx * ny + my) * nz + mz;
-                occ = (sv.bits[lin >> 5] >> (lin & 31)) & 1u;
-            }
+            // branch-free: cells outside the grid read word 0 and are masked out
+            const bool inb = (x < (unsigned)nx) & (y < (unsigned)ny) & (z < (unsigned)nz);
+            const int lin = inb ? lin0 + (mx * ny + my) * nz + mz : 0;
+            occ = inb & ((sv.bits[lin >> 5] >> (lin & 31)) & 1u);
         }
 #ifdef LSDF_STATS
         {
