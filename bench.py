@@ -2,7 +2,8 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One JSON line on rank 0.  A *step* is one pass of the hot path over one batch:
+One JSON line on rank 0.  ``--gpus N`` outside torchrun launches N ranks
+itself (torch.distributed.run on 127.0.0.1, one GPU per rank, NCCL).  A *step* is one pass of the hot path over one batch:
 FK + alignment for every waypoint, voxelization of the step's obstacle cloud,
 and the fused transform / trilinear / min / argmin query, producing
 (d, link, voxel) for every waypoint.
@@ -19,11 +20,14 @@ and the fused transform / trilinear / min / argmin query, producing
 * ``e2e`` — config 4 through the public API (DistanceChecker.query) from
   pinned host buffers: the kernels read the inputs and write the results
   across PCIe inside the timed region (host wall clock per step).
-* ``roofline`` — query_shells_kernel (the dominant kernel): algorithmic bytes
-  4 * N_occ per waypoint-query (the reference's gather) over
-  its event-timed duration, against MEASURED_PEAKS.json hbm_gbs.  The kernel
-  culls cells it can prove irrelevant, so frac > 1 means "faster than
-  gathering the dense robot SDF at HBM speed".
+* ``roofline`` — query_shells_kernel (the dominant kernel) against the bound
+  it actually meets, the SM issue rate: warp instructions per launch (live
+  ``ncu`` counter pass on this box during the run) over the event-timed launch
+  duration, against 148 SMs x 4 sub-partitions x 1 warp-instruction/cycle at
+  the sampled clock; ``traffic`` = DRAM bytes of the same launch.
+* ``work_avoided`` — the reference's dense gather (4 B per occupied voxel per
+  waypoint) at HBM peak vs the culled kernel's time: the
+  algorithmic ratio, not a roofline fraction.
 * ``cpu_baseline`` — the oracle port of the reference pipeline (numpy) on
   this host, bounded sample, rank 0 at N = 1.
 
@@ -335,15 +339,11 @@ def run_ours(args, rank, world, dist, sampler):
     alg_bytes = 4.0 * n_occ * n_local
     peak, peak_kind = _peaks()
     achieved = alg_bytes / (q_ms / 1e3) / 1e9
-    traffic = warp_inst = None
-    tf = REPO / "profiles" / "query_traffic.json"
-    if tf.exists() and world == 1:  # the ncu capture is of the single-GPU launch
-        try:
-            counters = json.loads(tf.read_text())
-            traffic = counters.get(args.workload)
-            warp_inst = counters.get(f"{args.workload}_warp_inst")
-        except (ValueError, OSError):
-            traffic = None
+    # live hardware counters of this very launch (ncu subprocess, one replayed
+    # launch of the same workload; never timed): warp instructions and DRAM bytes
+    counters = None
+    if rank == 0 and world == 1 and not args.no_counters:
+        counters = live_counters(args.workload)
     clocks = sampler.summary(t0 - 0.2, t1 + 0.2) if sampler else None
     out = {
         "metric": METRIC, "value": value, "unit": "waypoint-queries/s", "n_gpus": world, "steps": args.steps,
@@ -361,23 +361,95 @@ def run_ours(args, rank, world, dist, sampler):
         "gpu_launches_per_step": per_cycle,
         "e2e": _e2e_entry(C_total, e2e_ms, single_ms, int(n_local * robot.dof * 8 + (phi - plo) * 12),
                           int(n_local * 12 + 16), world if sharded else 1),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "query_shells_kernel", "kernel_ms": q_ms,
-                     "algorithmic_bytes": alg_bytes, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst)"},
+        # the dense gather the reference performs (4 B per occupied voxel per
+        # waypoint, query.py:146) at HBM speed, against the culled kernel: work
+        # avoided, not a roofline (the kernel never reads that field)
+        "work_avoided": {"dense_gather_bytes": alg_bytes, "dense_gather_ms_at_hbm_peak": alg_bytes / (peak * 1e9) * 1e3,
+                         "kernel_ms": q_ms, "ratio": (alg_bytes / (peak * 1e9) * 1e3) / q_ms,
+                         "peak_gbs": peak, "peak_kind": peak_kind},
         "clocks": clocks,
     }
-    if warp_inst:
-        # the kernel is issue-bound: its instruction stream against
-        # one warp instruction per SM sub-partition per cycle at the sampled clock
-        mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
-        peak_i = 148 * 4 * mhz * 1e6 / 1e9
-        ach_i = warp_inst / (q_ms / 1e3) / 1e9
-        out["roofline_issue"] = {"bound": "issue", "achieved": ach_i, "peak": peak_i, "unit": "G warp-inst/s",
-                                 "frac": ach_i / peak_i, "warp_inst_per_launch": warp_inst,
-                                 "source": "smsp__inst_executed.sum of one ncu --set full capture of this launch "
-                                           "(profiles/query_traffic.json) / the live kernel time; peak = 148 SMs x 4 "
-                                           "SMSPs x 1 inst/cycle x the sampled SM clock"}
+    # the bound the kernel meets: its warp-instruction stream
+    # against one warp instruction per SM sub-partition per cycle at the
+    # sampled clock; DRAM traffic of the same launch alongside
+    mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+    peak_i = 148 * 4 * mhz * 1e6 / 1e9
+    warp_inst = (counters or {}).get("warp_inst")
+    ach_i = warp_inst / (q_ms / 1e3) / 1e9 if warp_inst else None
+    out["roofline"] = {
+        "bound": "issue", "achieved": ach_i, "peak": peak_i, "unit": "G warp-inst/s",
+        "frac": ach_i / peak_i if ach_i else None,
+        "traffic": (counters or {}).get("dram_bytes"), "kernel": "query_shells_kernel", "kernel_ms": q_ms,
+        "warp_inst_per_launch": warp_inst,
+        "peak_kind": f"148 SMs x 4 SMSPs x 1 warp-inst/cycle x the sampled SM clock ({mhz:.0f} MHz)",
+        "source": (counters or {}).get("source", "counters not collected"),
+    }
     return out
+
+
+# ----------------------------------------------------------------------------- live counters
+
+
+_PROBE_METRICS = "smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"
+
+
+def probe_counters(args):
+    """The workload's cycle, untimed, for ncu to capture one query launch (--probe-counters)."""
+    import torch
+
+    import paper_2309_12543_b200 as L
+    from paper_2309_12543_b200 import scenarios as S
+
+    shape = _shape(args.workload)
+    _, chk = _checker(shape, shape.n_waypoints, L)
+    q = S.random_configs(shape.robot, shape.n_waypoints, seed=11)
+    chk.q_dev.copy_(torch.from_numpy(np.ascontiguousarray(q)))
+    chk.p_dev.copy_(torch.from_numpy(_cloud(shape, 11)))
+    for _ in range(3):  # warm cycles (the link order comes from the previous cycle)
+        chk.launch(device_only=True)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()  # ncu --profile-from-start off: only this cycle is profiled
+    chk.launch(device_only=True)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+
+
+def live_counters(workload: str, timeout: float = 240.0):
+    """smsp__inst_executed / DRAM bytes of one query_shells_kernel launch of this
+    workload, from ncu run on this box now (a launch replayed under the
+    profiler: counted, never timed)."""
+    import csv
+    import shutil
+    import tempfile
+
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not Path(ncu).exists():
+        return {"source": "ncu not found"}
+    with tempfile.TemporaryDirectory() as td:
+        log = Path(td) / "counters.csv"
+        cmd = [ncu, "--metrics", _PROBE_METRICS, "--clock-control", "none", "--print-units", "base", "--csv",
+               "--profile-from-start", "off", "-k", "regex:query_shells_kernel", "--launch-count", "1",
+               "--log-file", str(log), sys.executable, str(Path(__file__).resolve()), "--probe-counters",
+               "--workload", workload]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+        except subprocess.TimeoutExpired:
+            return {"source": f"ncu timed out after {timeout:.0f} s"}
+        if r.returncode != 0 or not log.exists():
+            return {"source": f"ncu failed (rc {r.returncode}): {(r.stderr or r.stdout)[-200:]}"}
+        rows = [row for row in csv.reader(log.read_text().splitlines()) if row]
+    try:
+        hi = next(i for i, row in enumerate(rows) if row[0] == "ID")
+    except StopIteration:
+        return {"source": "ncu wrote no metrics"}
+    h = rows[hi]
+    name_i, val_i = h.index("Metric Name"), h.index("Metric Value")
+    m = {row[name_i]: float(row[val_i].replace(",", "")) for row in rows[hi + 1:]}
+    return {"warp_inst": m.get("smsp__inst_executed.sum"),
+            "dram_bytes": (m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)) or None,
+            "ncu_duration_ns": m.get("gpu__time_duration.sum"),
+            "source": f"ncu --metrics {_PROBE_METRICS} on this box during this run: the scan of the 4th "
+                      f"{workload} cycle (replayed under the profiler, caches flushed; counted, not timed)"}
 
 
 def run_realtime(args, L):
@@ -511,7 +583,8 @@ def cpu_baseline(workload: str, budget_s: float = 15.0, sample: int = 64):
         pool.close()
     v = 1.0 / statistics.median(per_wp)
     return {"value": v, "unit": "waypoint-queries/s", "cores": pool.procs, "kind": "port",
-            "sample": pool.port.describe(len(per_wp), pool.procs)}
+            "sample": pool.port.describe(len(per_wp), pool.procs), "extrapolated": True,
+            "sample_waypoints_per_step": pool.procs * pool.port.sample}
 
 
 def run_reference(args, rank, world):
@@ -536,9 +609,45 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": shape.name, "waypoints": shape.n_waypoints, "points": shape.n_points},
+            "extrapolated": True,
+            "sample_waypoints_per_step": pool.procs * pool.port.sample,
+            "full_step_waypoints": shape.n_waypoints,
             "cpu_baseline": {"value": value, "unit": "waypoint-queries/s", "cores": pool.procs, "kind": "port",
-                             "sample": pool.port.describe(len(per_wp), pool.procs)},
+                             "sample": pool.port.describe(len(per_wp), pool.procs),
+                             "extrapolated": True},
             "e2e": {"value": value, "unit": "waypoint-queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _spawn_ranks(n: int) -> int:
+    """``--gpus N`` outside torchrun: launch N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1 and pass rank 0's line through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def run_dry(args, rank, world, dist):
+    """``--dry-run``: the multi-rank plumbing only (rendezvous, barrier,
+    max-over-ranks reduction, rank-0 print) with no GPU work — what the CPU
+    test of ``--gpus N`` exercises."""
+    import torch
+
+    per_rank_ms = 1.0 + rank  # stand-in step time: the max over ranks must be the last rank's
+    t = torch.tensor([per_rank_ms], dtype=torch.float64)
+    if dist is not None:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"metric": METRIC, "dry_run": True, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(t.item()), "backend": dist.get_backend() if dist is not None else None}
 
 
 def main():
@@ -549,8 +658,15 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["config4", "config2", "config1"], default="config4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-counters", action="store_true", help="skip the live ncu counter pass")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only, no GPU work")
+    ap.add_argument("--probe-counters", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.probe_counters:
+        return probe_counters(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(_spawn_ranks(args.gpus))
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     if args.impl == "reference":
@@ -560,15 +676,27 @@ def main():
         return
     import torch
 
-    torch.cuda.set_device(_env_int("LOCAL_RANK", 0) % max(1, torch.cuda.device_count()))
     dist = None
     if world > 1:
         import torch.distributed as tdist
 
-        # LSDF_BENCH_BACKEND=gloo: functional check of the multi-rank path on
-        # one GPU (numbers meaningless); the driver's runs use NCCL
-        tdist.init_process_group(os.environ.get("LSDF_BENCH_BACKEND", "nccl"))
+        # LSDF_BENCH_BACKEND=gloo: functional check of the multi-rank path
+        # (the CPU test's --dry-run, or one GPU: numbers meaningless); the
+        # driver's runs use NCCL, one GPU per rank
+        backend = os.environ.get("LSDF_BENCH_BACKEND", "gloo" if args.dry_run else "nccl")
+        if backend == "nccl":
+            torch.cuda.set_device(_env_int("LOCAL_RANK", 0) % max(1, torch.cuda.device_count()))
+        tdist.init_process_group(backend)
         dist = tdist
+    if args.dry_run:
+        out = run_dry(args, rank, world, dist)
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    torch.cuda.set_device(_env_int("LOCAL_RANK", 0) % max(1, torch.cuda.device_count()))
     import paper_2309_12543_b200 as L
 
     sampler = ClockSampler(torch.cuda.current_device()).start()

@@ -1,4 +1,8 @@
 // lsdf_capi.cu — library-wide state: thread-local error text, launch counter, version.
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "lsdf_common.cuh"
 
 namespace lsdf {
@@ -9,6 +13,27 @@ std::string& last_error() {
 std::atomic<uint64_t>& launch_counter() {
     static std::atomic<uint64_t> n{0};
     return n;
+}
+
+// Static + dynamic shared memory above 48 KB needs a per-function attribute,
+// and function attributes live in each device's context: track what was
+// granted per (device, kernel) so a process driving several GPUs raises it on
+// each (one attribute call per device and kernel, then a map lookup).
+int ensure_smem(const void* func, size_t bytes, const char* what) {
+    int dev = 0;
+    LSDF_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> granted;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& g = granted[{dev, func}];
+    if (bytes <= g) return LSDF_OK;
+    const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LSDF_ERR_UNSUPPORTED, "%s: %zu B of shared memory: %s", what, bytes, cudaGetErrorString(e));
+    }
+    g = bytes;
+    return LSDF_OK;
 }
 }  // namespace lsdf
 

@@ -15,6 +15,8 @@ namespace lsdf {
 std::string& last_error();
 std::atomic<uint64_t>& launch_counter();
 size_t& l2_persist_bytes(int dev);
+// raises the kernel's dynamic shared-memory limit to `bytes` on the current device (once per device)
+int ensure_smem(const void* func, size_t bytes, const char* what);
 
 inline int fail(int code, const char* fmt, ...) {
     char buf[512];

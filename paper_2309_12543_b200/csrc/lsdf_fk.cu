@@ -409,13 +409,7 @@ int fk_align_impl(const lsdf_link* links, int32_t n_links, int32_t n_geo, const 
     if (C >= FK_SERIAL_MIN) {
         if (FK_STAGE_OUTPUTS) {
             const size_t smem_s = (size_t)FKS_THREADS * n_geo * (12 * sizeof(double) + 3 * sizeof(int32_t));
-            static bool attr = false;
-            if (!attr) {
-                LSDF_TRY(check_cuda(cudaFuncSetAttribute(fk_align_serial_kernel<true, false>,
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024),
-                                    "fk smem attribute"));
-                attr = true;
-            }
+            LSDF_TRY(ensure_smem((const void*)fk_align_serial_kernel<true, false>, smem_s, "fk_align_serial_kernel"));
             fk_align_serial_kernel<true, false>
                 <<<grid_for(C, FKS_THREADS), FKS_THREADS, smem_s, (cudaStream_t)stream>>>(p);
         } else {

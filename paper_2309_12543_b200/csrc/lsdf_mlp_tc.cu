@@ -375,13 +375,8 @@ int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const
     p.r_tiles = r_tiles;
     p.kblocks = kblocks;
     const size_t smem = 1024 + (size_t)kblocks * (2 * KB_BYTES_A + 4 * KB_BYTES_B) + 128;
-    static bool attr = false;
-    if (!attr) {
-        LSDF_TRY(check_cuda(cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
-                            "mlp smem attribute"));
-        attr = true;
-    }
     if (smem > 227 * 1024) return fail(LSDF_ERR_UNSUPPORTED, "tcgen05 TinyMlp: hidden %d needs too much smem", H);
+    LSDF_TRY(ensure_smem((const void*)mlp_tc_kernel, smem, "mlp_tc_kernel"));
     const unsigned grid = (unsigned)(n_tiles < 148 ? n_tiles : 148);
     mlp_tc_kernel<<<grid, TC_THREADS, smem, s>>>(p);
     LSDF_TRY(check_launch("mlp_tc_kernel"));

@@ -35,11 +35,13 @@ struct QueryParams {
     float dfar[LSDF_MAX_LINKS];             // float32 link sentinel per link
     float core[LSDF_MAX_LINKS];             // value(p) >= |p| - core  (lsdf_link_grid.core_radius)
     float4 seg_a[LSDF_MAX_LINKS];           // segment bound: (a.xyz, kappa_lo); kappa_lo < 0 disables it
+    double hull;                            // ball around the link origin inside the grid's cell-centre hull
     float4 seg_u[LSDF_MAX_LINKS];           // (u.xyz, length)
     float seg_hi[LSDF_MAX_LINKS];           // kappa_hi
     int32_t seg_filter;                     // apply the segment bound (throughput-sized batches)
     int32_t round_min;                      // queued cells that trigger a lookup round (<= 32)
     const uint32_t* bricks;                 // occupancy brick columns (4^3 voxels), or null: no box test
+    int32_t stage_bricks;                   // brick columns copied to shared memory (else read from global)
     int32_t nby_brick;                      // brick columns per x row
     const uint32_t* shell_cells;            // kept window cells sorted by distance from the centre
     const float* shell_radius;              // their distance (m), rounded down
@@ -248,6 +250,7 @@ constexpr int QCAP_SHELL = 64;
 __host__ __device__ __forceinline__ int shell_padded(int n) { return (n + 31) & ~31; }
 constexpr int SHELL_STAGE_MAX = 4096;   // kept cells staged in shared memory (W <= 20)
 constexpr int BITMAP_STAGE_MAX = 8192;  // occupancy words staged in shared memory (<= 262k voxels)
+constexpr int BRICK_STAGE_MAX = 4096;   // brick columns staged in shared memory (16 KB: x, y <= 256 voxels)
 
 __device__ __forceinline__ void* align16_ptr(void* q) {
     return (void*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
@@ -287,6 +290,7 @@ struct __align__(16) ShellSetup {
     float A[9];  // f32 link-frame point of window offset P minus the segment origin:
     float b[3];  //   p_k - a_k = Px A[k] + Py A[3+k] + Pz A[6+k] + b[k]
     float slack;     // |dt| (rounded up) + core radius of the link
+    float hull_lim;  // cells with shell radius <= hull_lim map inside the link grid's cell-centre hull
     int32_t l;       // geometry link
     int32_t c;       // configuration
     int32_t sidx;    // slice of the shell list
@@ -328,6 +332,10 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_
         s.b[k] = (float)(dtinv[k] * p.e_r - (double)a3[k] +
                          p.e_r * (R[k] * p0[0] + R[3 + k] * p0[1] + R[6 + k] * p0[2]));
     s.slack = dtn + p.core[l];
+    // |link-frame point| <= rho + |dt|: a cell with rho <= hull - |dt| samples
+    // inside the hull of the grid's cell centres, where the segment's upper
+    // bound holds (outside it the sample is the link's far value)
+    s.hull_lim = (float)(p.hull - (double)dtn) * (1.0f - 0x1p-20f) - 1e-6f;
     float t0 = p.clamp;  // values >= clamp never change the answer
     if (p.per_link == nullptr) {  // best key any link of this configuration has published so far (an upper
         const uint64_t k = ~(uint64_t)__ldcg(p.keys + c);  // bound of the minimum, so an older read stays valid)
@@ -434,6 +442,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
     const float4 sa = p.seg_a[l], su = p.seg_u[l];
     const float k_lo = sa.w, k_hi = p.seg_hi[l];
     const bool use_seg = p.seg_filter && k_lo >= 0.0f;
+    const float hull_lim = st.hull_lim;
 #ifdef LSDF_STATS
     unsigned long long sc[8] = {1, 0, 0, 0, 0, 0, 0, 0};
 #endif
@@ -478,7 +487,9 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
             const float d2q = occ ? d2 : INFINITY;  // squared segment distance of a cell that stays queued
             // non-negative floats order like their bits: one integer min over the warp
             const uint32_t m = __reduce_min_sync(FULL_MASK, __float_as_uint(d2q));
-            if (m < 0x7f800000u) {
+            // the upper bound d + k_hi holds only for samples inside the grid's
+            // cell-centre hull: chunks past the inscribed ball leave thresh alone
+            if (m < 0x7f800000u && sv.radius[k0 + 31] <= hull_lim) {
                 const float dm = __uint_as_float(m);
                 const float r = dm > 0.0f ? dm * rsqrtf(dm) : 0.0f;  // ~2^-22 relative: rounded up below
                 thresh = fminf(thresh, fmaf(r, 1.0f + 0x1p-18f, k_hi));
@@ -527,7 +538,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     float* s_radius = (float*)align16_ptr(s_cells + (stage_shell ? shell_padded(p.n_shell) : 0));
     uint32_t* s_bits = (uint32_t*)align16_ptr(s_radius + (stage_shell ? shell_padded(p.n_shell) : 0));
     uint32_t* s_bricks = (uint32_t*)align16_ptr(s_bits + (stage_bits ? n_words : 0));
-    const int n_cols = BRICKS ? (int)(((p.dims[0] + 3) >> BRICK_LOG2) * p.nby_brick) : 0;
+    const int n_cols = (BRICKS && p.stage_bricks) ? (int)(((p.dims[0] + 3) >> BRICK_LOG2) * p.nby_brick) : 0;
     __shared__ ShellSetup s_setup[WARPS][GRAB_MAX];
     // Stage the shell list and the occupancy bitmap with asynchronous copies
     // (all in flight at once), and fetch + set up the first tasks while they
@@ -584,7 +595,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     sv.cells = stage_shell ? s_cells : p.shell_cells;
     sv.radius = stage_shell ? s_radius : p.shell_radius;
     sv.bits = stage_bits ? s_bits : p.bitmap;
-    sv.bricks = n_cols ? s_bricks : nullptr;
+    sv.bricks = n_cols ? s_bricks : p.bricks;
     sv.P = sP;
     uint32_t* queue = s_queue + warp * QCAP_SHELL;
     // guided grab sizes: the grab shrinks as the remaining work does, so the
@@ -787,28 +798,30 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
             p.geom.topd[a] = (double)(g0.dims[a] - 2);
             p.geom.top[a] = g0.dims[a] - 2;
         }
+        {  // inscribed ball of the cell-centre hull [-e + r/2, e - r/2]^3, less a margin for rounding
+            double h = g0.extent[0] - 0.5 * g0.resolution[0];
+            for (int a = 1; a < 3; ++a) h = fmin(h, g0.extent[a] - 0.5 * g0.resolution[a]);
+            p.hull = h - 1e-5;
+        }
         p.geom.cx = g0.dims[0] - 1;
         p.geom.cy = g0.dims[1] - 1;
         const unsigned blocks = (unsigned)(blocks_per_link * n_group);
         if (shells) {
             const int stage_shell = p.n_shell <= SHELL_STAGE_MAX;
             const int stage_bits = o.n_words <= BITMAP_STAGE_MAX;
+            // brick columns in shared memory when they fit the budget, else read from L2
+            p.stage_bricks = p.bricks != nullptr && (int64_t)o.nbx * o.nby <= BRICK_STAGE_MAX;
             const size_t smem_s = (size_t)3 * window->Wmax * sizeof(double) +
                                   (size_t)WARPS * QCAP_SHELL * 4 +
                                   (stage_shell ? (size_t)shell_padded(p.n_shell) * 8 : 0) + (stage_bits ? (size_t)o.n_words * 4 : 0) +
-                                  (p.bricks != nullptr ? (size_t)o.nbx * o.nby * 4 : 0) +
+                                  (p.stage_bricks ? (size_t)o.nbx * o.nby * 4 : 0) +
                                   64;  // 16-B alignment of the four staged tables
             using ShellsKernel = void (*)(QueryParams, int, int, int, int, int, int64_t, int);
             static const ShellsKernel kernels[4] = {query_shells_kernel<false, false>, query_shells_kernel<false, true>,
                                                     query_shells_kernel<true, false>, query_shells_kernel<true, true>};
-            static bool attr = false;
-            if (!attr) {
-                for (ShellsKernel k : kernels)
-                    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-                attr = true;
-            }
             const int variant = (p.by_position ? 2 : 0) + (p.bricks != nullptr ? 1 : 0);
             const ShellsKernel kern = kernels[variant];
+            LSDF_TRY(ensure_smem((const void*)kern, smem_s, "query_shells_kernel"));
             // residency cache: (device, variant, smem bytes) -> CTAs per SM
             thread_local int c_dev = -1, c_bp = -1, c_sm = 148, c_per = 1;
             thread_local size_t c_smem = 0;

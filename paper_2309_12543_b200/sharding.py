@@ -90,13 +90,53 @@ def allreduce_min_keys(keys: np.ndarray, group=None, device=None) -> np.ndarray:
     return _from_signed(t.cpu().numpy())
 
 
+# ---- the same keys as torch tensors (device-resident on the NCCL path: no host round trip)
+
+_I64_MIN = -(1 << 63)
+_I64_MAX = (1 << 63) - 1
+
+
+def pack_keys_tensor(d, link, voxel, n_links: int, voxel_offset: int = 0):
+    """Torch form of :func:`pack_keys` in signed order (key ^ 2^63 as int64, for a MIN all-reduce).
+
+    d f32, link / voxel int32 tensors on any device; -1 links map to the largest key.
+    """
+    import torch
+
+    d = torch.where(d == 0, torch.zeros_like(d), d)  # -0.0 == +0.0
+    b = d.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    neg = (b & 0x80000000) != 0
+    ordr = torch.where(neg, (~b) & 0xFFFFFFFF, b | 0x80000000)
+    lo = (voxel.to(torch.int64) + voxel_offset) * n_links + link.to(torch.int64)
+    key = ((ordr << 32) | lo) ^ _I64_MIN  # u64 bits, flipped into signed order
+    return torch.where(link < 0, torch.full_like(key, _I64_MAX), key)
+
+
+def unpack_keys_tensor(keys, n_links: int, clamp: float):
+    """Inverse of :func:`pack_keys_tensor` -> (d f32, link i32, voxel i32) tensors, clamp rule applied."""
+    import torch
+
+    none = keys == _I64_MAX
+    u = keys ^ _I64_MIN
+    hi = (u >> 32) & 0xFFFFFFFF
+    lo = u & 0xFFFFFFFF
+    bits = torch.where((hi & 0x80000000) != 0, hi & 0x7FFFFFFF, (~hi) & 0xFFFFFFFF)
+    d = bits.to(torch.int32).view(torch.float32)  # low 32 bits reinterpret (two's complement wrap)
+    d = torch.where(none, torch.full_like(d, float(np.float32(clamp))), d)
+    link = torch.where(none, torch.full_like(lo, -1), lo % n_links).to(torch.int32)
+    voxel = torch.where(none, torch.full_like(lo, -1), lo // n_links).to(torch.int32)
+    return d, link, voxel
+
+
 def query_obstacle_sharded(traj, obstacles, group=None):
     """(d, link, voxel) over the full obstacle set, each rank evaluating its voxel slice.
 
     ``obstacles`` is the full (replicated) ObstacleVoxelSet; rank r keeps the
     occupied voxels of rank [lo, hi) in the sorted list, queries them on its
-    GPU, and the packed keys meet in one MIN all-reduce.
+    GPU, and the packed keys meet in one MIN all-reduce.  With NCCL the keys
+    are packed, reduced and unpacked on the device; only the result leaves it.
     """
+    import torch
     import torch.distributed as dist
 
     from .query import ObstacleVoxelSet, query_min_distances
@@ -105,35 +145,55 @@ def query_obstacle_sharded(traj, obstacles, group=None):
     lo, hi = shard_range(obstacles.n_occupied, rank, world)
     part = ObstacleVoxelSet(indices=obstacles.indices[lo:hi], grid=obstacles.grid, n_points=obstacles.n_points,
                             n_dropped=obstacles.n_dropped, _sorted_unique=True)
+    if dist.get_backend(group) == "nccl":
+        C_ = traj.n_configs
+        if part.n_occupied:
+            occ, by_pos = part.occupancy()
+            out = traj.query_device(occ, by_pos)
+            keys = pack_keys_tensor(out["d"], out["link"], out["voxel"], traj.n_links, voxel_offset=lo)
+        else:
+            keys = torch.full((C_,), _I64_MAX, dtype=torch.int64, device=torch.cuda.current_device())
+        dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group)
+        d, link, voxel = unpack_keys_tensor(keys, traj.n_links, traj.d_far_global)
+        return d.cpu().numpy(), link.cpu().numpy(), voxel.cpu().numpy()
     d, link, voxel = query_min_distances(traj, part, return_argmin=True)
     keys = pack_keys(d, link, voxel, traj.n_links, voxel_offset=lo)
-    dev = None
-    if dist.get_backend(group) == "nccl":
-        import torch
-
-        dev = torch.device("cuda", torch.cuda.current_device())
-    return unpack_keys(allreduce_min_keys(keys, group, dev), traj.n_links, traj.d_far_global)
+    return unpack_keys(allreduce_min_keys(keys, group), traj.n_links, traj.d_far_global)
 
 
 def gather_waypoint_results(d, link, voxel, group=None):
-    """All-gather the per-rank waypoint slices (variable lengths) into full arrays on every rank."""
+    """All-gather the per-rank waypoint slices (variable lengths) into full arrays on every rank.
+
+    Inputs are numpy arrays or tensors.  With NCCL every buffer lives on this
+    rank's GPU (NCCL cannot move host tensors); gloo gathers host tensors.
+    Returns numpy (d f32, link i32, voxel i32) in rank order.
+    """
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    n = torch.tensor([len(d)], dtype=torch.int64)
-    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" \
+        else torch.device("cpu")
+
+    def as_t(x, dtype):
+        return (x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))).to(dev, dtype)
+
+    d_t, l_t, v_t = as_t(d, torch.float32), as_t(link, torch.int32), as_t(voxel, torch.int32)
+    n = torch.tensor([d_t.shape[0]], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
-    m = int(max(s.item() for s in sizes))
-    packed = np.zeros((m, 3), dtype=np.float64)
-    packed[: len(d), 0] = d
-    packed[: len(d), 1] = link
-    packed[: len(d), 2] = voxel
-    mine = torch.from_numpy(packed)
-    parts = [torch.zeros_like(mine) for _ in range(world)]
+    sizes = [int(s.item()) for s in sizes]
+    m = max(sizes)
+    # one int32 block per rank: d bits, link, voxel (exact, 12 B per waypoint)
+    mine = torch.zeros((m, 3), dtype=torch.int32, device=dev)
+    mine[: d_t.shape[0], 0] = d_t.view(torch.int32)
+    mine[: d_t.shape[0], 1] = l_t
+    mine[: d_t.shape[0], 2] = v_t
+    parts = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(parts, mine, group=group)
-    rows = np.concatenate([p.numpy()[: int(s.item())] for p, s in zip(parts, sizes)])
-    return rows[:, 0].astype(np.float32), rows[:, 1].astype(np.int32), rows[:, 2].astype(np.int32)
+    rows = torch.cat([p[:s] for p, s in zip(parts, sizes)]).cpu()
+    return (rows[:, 0].contiguous().view(torch.float32).numpy(), rows[:, 1].numpy().astype(np.int32),
+            rows[:, 2].numpy().astype(np.int32))
 
 
 def build_link_sdfs_sharded(geometries, extent, resolution, group=None, build=None):

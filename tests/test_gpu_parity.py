@@ -560,10 +560,14 @@ def test_direct_equals_dense_on_adversarial_grids(L, seed, cloud):
             assert np.all(pl[c, : link[c]] > d[c]) or voxel[c] >= 0
 
 
-def test_segment_bound_exact_on_noisy_grids(L):
+@pytest.mark.parametrize("cloud", ["dense", "sparse"])
+def test_segment_bound_exact_on_noisy_grids(L, cloud):
     """Throughput-sized batch (segment bound active) on capsule-like grids
     with noise (the bound's kappas come from the values): direct == dense
-    gather, and == the same waypoints in small chunks (bound inactive)."""
+    gather, and == the same waypoints in small chunks (bound inactive).
+    The sparse cloud leaves a few occupied cells per window, many in the outer
+    shell past the link grid's cell-centre hull (sample = far value, above
+    the segment's upper bound): the threshold must not be lowered there."""
     rng = np.random.default_rng(11)
     grid = L.EnvGrid(1.0, 0.05)
     e_r, r_r = 0.3, 0.02
@@ -583,16 +587,99 @@ def test_segment_bound_exact_on_noisy_grids(L):
     poses = L.LinkPoseBatch(R, T)
     prov = L.ExactTransformProvider(window)
     traj = L.TrajectorySdf.from_poses(sdfs, poses, grid, prov)
-    obs = L.voxelize_pointcloud(rng.uniform(-1, 1, size=(20_000, 3)), grid)
+    obs = L.voxelize_pointcloud(rng.uniform(-1, 1, size=(20_000 if cloud == "dense" else 400, 3)), grid)
     d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
     dense = L.RobotSdfBatch(traj.device_values(), grid, traj.d_far_global)
     d2, _, v2 = L.query_min_distances(dense, obs, return_argmin=True)
     assert np.array_equal(d, d2) and np.array_equal(voxel, v2)
+    if cloud == "sparse":
+        assert np.mean(link >= 0) > 0.3  # most waypoints see an obstacle: the case is exercised
     for a in range(0, C, 2600):
         part = L.TrajectorySdf.from_poses(sdfs, L.LinkPoseBatch(R[a:a + 2600], T[a:a + 2600]), grid, prov)
         dc, lc, vc = L.query_min_distances(part, obs, return_argmin=True)
         assert np.array_equal(dc, d[a:a + 2600]) and np.array_equal(lc, link[a:a + 2600])
         assert np.array_equal(vc, voxel[a:a + 2600])
+
+
+def _hull_trap_scenes(n_scenes, seed=0):
+    """Poses where the shell scan's segment bound meets a window cell outside
+    the link grid's cell-centre hull (sample = far value, above the segment's
+    upper bound) BEFORE an in-hull cell holding the true minimum, which the
+    unguarded threshold update would then skip.  CPU search with
+    the oracle's trilinear; returns the link grid and, per scene, (R, dt, cells)."""
+    from oracle import linksdf_oracle as O
+    from paper_2309_12543_b200.placement import _axis_offsets
+
+    import paper_2309_12543_b200 as L
+
+    rng = np.random.default_rng(seed)
+    e_r, r_r = 0.3, 0.02
+    ax = -e_r + (np.arange(30) + 0.5) * r_r
+    X, Y, Z = np.meshgrid(ax, ax, ax, indexing="ij")
+    vals = (np.sqrt(X * X + Y * Y + (Z - np.clip(Z, -0.2, 0.2)) ** 2) - 0.02).astype(np.float32)  # long thin capsule
+    sdf = L.LinkSdf(e_r, r_r, vals, 0)
+    a, u, length, k_lo, k_hi = sdf.segment_bound()
+    a, u = np.asarray(a), np.asarray(u)
+    core = sdf.core_radius()
+    grid = L.EnvGrid(1.0, 0.05)
+    w = L.WindowGeometry.build(e_r, grid)
+    h = w.host_tables()
+    off = _axis_offsets(w.extent, w.grid, False)
+    cells = h["shell_cells"][: w.n_masked].astype(np.int64)
+    m = np.stack([cells & 0xFF, (cells >> 8) & 0xFF, (cells >> 16) & 0xFF], 1)
+    Pm = np.stack([off[0][m[:, 0]], off[1][m[:, 1]], off[2][m[:, 2]]], 1)
+    rad = h["shell_radius"][: w.n_masked]
+    hull, clamp = e_r - r_r / 2, np.float32(e_r)
+    chunk = np.arange(len(Pm)) // 32
+    scenes = []
+    while len(scenes) < n_scenes:
+        R = L.sample_rotations(rng, 1)[0]
+        dt = rng.uniform(-0.024, 0.024, 3)
+        p = (Pm - dt) @ R
+        v = O.trilinear(vals, e_r, r_r, p).astype(np.float64)
+        tt = np.clip((p - a) @ u, 0, length)
+        d = np.linalg.norm(p - a - tt[:, None] * u, axis=1)
+        outside = np.any(np.abs(p) > hull + 1e-3, axis=1)
+        for o in np.nonzero(outside)[0]:
+            th = min(clamp, d[o] + k_hi)
+            skipped = (d - k_lo > th) | (rad[chunk * 32] - (np.linalg.norm(dt) + core) > th)
+            cand = np.nonzero((chunk > chunk[o]) & ~outside & skipped & (v < clamp - 0.01))[0]
+            if d[o] - k_lo <= clamp and len(cand):
+                scenes.append((R, dt, m[o], m[cand[0]]))
+                break
+    return sdf, grid, w, scenes
+
+
+def test_segment_bound_guard_outside_hull(L):
+    """Throughput-sized batch whose windows hold exactly two occupied cells: one
+    past the link grid's cell-centre hull in an early shell chunk, one inside
+    it farther out with the true minimum.  The direct kernel (segment bound
+    on) must equal the dense gather and the same poses as a small batch."""
+    sdf, grid, window, scenes = _hull_trap_scenes(27)
+    W = int(window.dims[0])
+    env_c = lambda j: -1.0 + (np.asarray(j) + 0.5) * 0.05  # noqa: E731  voxel centres
+    Rs, Ts, pts = [], [], []
+    for k, (R, dt, co, ci) in enumerate(scenes):  # 27 disjoint windows on a 3 x 3 x 3 lattice of anchors
+        anchor = 13 * np.array([k % 3, (k // 3) % 3, k // 9])
+        Rs.append(R)
+        Ts.append(env_c(anchor + W // 2) + dt)
+        pts += [env_c(anchor + co), env_c(anchor + ci)]
+    Rs, Ts = np.asarray(Rs), np.asarray(Ts)
+    obs = L.voxelize_pointcloud(np.asarray(pts), grid)
+    assert obs.n_occupied == 2 * len(scenes)
+    prov = L.ExactTransformProvider(window)
+    small = L.TrajectorySdf.from_poses([sdf], L.LinkPoseBatch(Rs[:, None], Ts[:, None]), grid, prov)
+    d0, l0, v0 = L.query_min_distances(small, obs, return_argmin=True)
+    dense = L.RobotSdfBatch(small.device_values(), grid, small.d_far_global)
+    d1, _, v1 = L.query_min_distances(dense, obs, return_argmin=True)
+    assert np.array_equal(d0, d1) and np.array_equal(v0, v1)
+    assert np.all(l0 == 0) and np.all(d0 < np.float32(0.3))  # every trap has its in-hull minimum
+    reps = 40_000 // len(scenes) + 1  # > 37,888 tasks: the segment bound is on
+    big = L.TrajectorySdf.from_poses([sdf], L.LinkPoseBatch(np.tile(Rs, (reps, 1, 1))[:, None],
+                                                            np.tile(Ts, (reps, 1))[:, None]), grid, prov)
+    d, link, voxel = L.query_min_distances(big, obs, return_argmin=True)
+    assert np.array_equal(d, np.tile(d0, reps)) and np.array_equal(link, np.tile(l0, reps))
+    assert np.array_equal(voxel, np.tile(v0, reps))
 
 
 def test_mlp_tensor_cores(L):

@@ -167,10 +167,29 @@ def test_scan_bounds_hold_on_random_grids():
         pts = rng.uniform(c[0], c[-1], size=(40000, 3))
         v = O.trilinear(sdf.values, e_r, r_r, pts).astype(np.float64)
         assert np.all(v >= np.linalg.norm(pts, axis=1) - kappa)
-        a, u = np.asarray(a), np.asarray(u)
-        tt = np.clip((pts - a) @ u, 0.0, length)
-        d = np.linalg.norm(pts - a - tt[:, None] * u, axis=1)
+        a, u_seg = np.asarray(a), np.asarray(u)
+        tt = np.clip((pts - a) @ u_seg, 0.0, length)
+        d = np.linalg.norm(pts - a - tt[:, None] * u_seg, axis=1)
         assert np.all(v >= d - k_lo) and np.all(v <= d + k_hi)
+        # Window cells reach |p| <= e_r + |dt|, past the hull of the cell centres,
+        # where the sample is the far value: the lower bounds still hold as
+        # min(bound, d_far) (values >= the clamp never change a minimum), but
+        # the upper bound holds only inside the hull -- the kernel applies it to
+        # chunks whose shell radius + |dt| stays in the inscribed ball.
+        hull = e_r - r_r / 2
+        u = rng.normal(size=(60000, 3))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        pts = u * (e_r + 0.04) * np.cbrt(rng.random((60000, 1)))
+        v = O.trilinear(sdf.values, e_r, r_r, pts).astype(np.float64)
+        rad = np.linalg.norm(pts, axis=1)
+        tt = np.clip((pts - a) @ u_seg, 0.0, length)
+        d = np.linalg.norm(pts - a - tt[:, None] * u_seg, axis=1)
+        assert np.all(v >= np.minimum(rad - kappa, sdf.d_far))
+        assert np.all(v >= np.minimum(d - k_lo, sdf.d_far))
+        ball = rad <= hull - 1e-5
+        assert np.all(v[ball] <= d[ball] + k_hi)
+        outside = np.any(np.abs(pts) > hull, axis=1)
+        assert np.any(v[outside] > d[outside] + k_hi)  # why the guard exists (not vacuous)
 
 
 def test_link_major_threshold_matches_fk_crossover():

@@ -55,6 +55,13 @@ def _worker(rank, world, port, vals, clamp, out):
     d, link, voxel = _shard_result(vals, lo, hi, clamp)
     keys = S.pack_keys(d, link, voxel, L, voxel_offset=lo)
     red = S.unpack_keys(S.allreduce_min_keys(keys), L, clamp)
+    # the tensor form the NCCL path runs on the device (here: gloo on host tensors)
+    import torch
+
+    kt = S.pack_keys_tensor(torch.from_numpy(d), torch.from_numpy(link), torch.from_numpy(voxel), L, voxel_offset=lo)
+    dist.all_reduce(kt, op=dist.ReduceOp.MIN)
+    red_t = tuple(x.numpy() for x in S.unpack_keys_tensor(kt, L, clamp))
+    assert all(np.array_equal(a, b) for a, b in zip(red, red_t))
     wl, wh = S.shard_range(C, rank, world)
     gd, gl, gv = S.gather_waypoint_results(red[0][wl:wh], red[1][wl:wh], red[2][wl:wh])
     if rank == 0:
@@ -102,6 +109,21 @@ def test_key_round_trip_and_order():
     assert np.all(d2[link >= 0] == d[link >= 0]) and d2[4] == np.float32(0.3)
     order = np.argsort(S._to_signed(k), kind="stable")
     assert list(order[:2]) == [1, 2]  # -0.2 first, then 0.0 (rank 11, link 2) before -0.0 (rank 11, link 3)
+
+
+def test_key_tensor_form_matches_numpy():
+    import torch
+
+    rng = np.random.default_rng(3)
+    d = np.concatenate([np.float32([0.0, -0.0, 0.3, -1e-30, 1e-30]), rng.normal(0, 0.2, 200).astype(np.float32)])
+    link = rng.integers(-1, 7, len(d)).astype(np.int32)
+    voxel = np.where(link < 0, -1, rng.integers(0, 50000, len(d))).astype(np.int32)
+    k_np = S._to_signed(S.pack_keys(d, link, voxel, 7, voxel_offset=123))
+    k_t = S.pack_keys_tensor(torch.from_numpy(d), torch.from_numpy(link), torch.from_numpy(voxel), 7, 123)
+    assert np.array_equal(k_t.numpy(), k_np)
+    got = [x.numpy() for x in S.unpack_keys_tensor(k_t, 7, 0.3)]
+    want = S.unpack_keys(S._from_signed(k_np), 7, 0.3)
+    assert all(np.array_equal(a, b) for a, b in zip(got, want))
 
 
 def test_shard_ranges_cover():
