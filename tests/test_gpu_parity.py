@@ -358,6 +358,8 @@ def test_stream_min_distances(L):
     frames = [(float(i), g["points"]) for i in range(3)] + [(3.0, np.empty((0, 3)))]
     rows = list(L.stream_min_distances(traj, frames))
     assert all(np.array_equal(r[1], rows[0][1]) for r in rows[:3])
+    assert np.abs(rows[0][1].astype(np.float64) - g["d"]).max() <= D_TOL  # the reference's query (query.py:294-306)
+    assert [r[0] for r in rows] == [0.0, 1.0, 2.0, 3.0]
     assert np.all(rows[3][1] == np.float32(traj.d_far_global))
 
 

@@ -135,3 +135,39 @@ def test_voxelize_known_answers():
     assert len(idx) == 1 and drop == 2 and list(idx[0]) == [10, 10, 10]
     idx, _, drop = O.voxelize(np.float64([[1.0, 0, 0], [-1.0, 0, 0]]), env)
     assert drop == 1 and list(idx[0]) == [0, 10, 10]
+
+
+# ----------------------------------------------------------------------------- round-2 fixtures: the benchmarked inputs
+
+
+def _bench_grids(shape):
+    chain = O.chain_from_doc(shape.robot)
+    return [O.build_grid(chain[i]["geometry"], shape.link_extent, shape.link_res) for i in O.geometry_links(chain)]
+
+
+def test_oracle_on_bench_config2_seed21():
+    """The oracle reproduces the reference on bench.py's own config-2 input (seed 21, 500 waypoints)."""
+    from paper_2309_12543_b200 import scenarios as S
+
+    g = golden("bench_c2")
+    shape = S.CONFIG2
+    q = S.random_configs(shape.robot, shape.n_waypoints, seed=21)
+    pts = S.cloud_for(shape, 21).astype(np.float32)
+    assert np.array_equal(np.float64([q.sum(), np.abs(q).sum(), q.size]), g["s21_q_digest"])
+    d, link, voxel = O.run_pipeline(shape.robot, q, pts, shape.grid_extent, shape.grid_res, shape.link_extent,
+                                    _bench_grids(shape), [shape.link_res] * 6)
+    assert np.array_equal(d, g["s21_d"]) and np.array_equal(link, g["s21_link"])
+    assert np.array_equal(voxel, g["s21_voxel"])
+
+
+def test_oracle_builds_at_128():
+    """Config 3 (i): an arm6g capsule at 128^3 and the 1,280-triangle icosphere (strided cells)."""
+    from paper_2309_12543_b200 import scenarios as S
+
+    g = golden("builds128")
+    geo = next(lk for lk in S.ARM6G["links"] if lk["name"] == "l2")["geometry"]
+    flat = O.build_grid(geo, 0.64, 0.01).ravel(order="F")
+    assert np.array_equal(flat[g["prim_l2_idx"]], g["prim_l2"])
+    ijk = np.stack(np.unravel_index(g["mesh_idx"][::10], (128, 128, 128), order="F"), axis=1)
+    got = O.mesh_sdf(g["mesh_V"], g["mesh_F"], -0.64 + (ijk + 0.5) * 0.01, signed=True).astype(np.float32)
+    assert np.array_equal(got, g["mesh"][::10])
