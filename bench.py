@@ -339,6 +339,11 @@ def run_ours(args, rank, world, dist, sampler):
     alg_bytes = 4.0 * n_occ * n_local
     peak, peak_kind = _peaks()
     achieved = alg_bytes / (q_ms / 1e3) / 1e9
+    # robustness: the same 65,536-waypoint cycle against clouds that leave
+    # most windows empty (the scan must not fall back to scanning every cell)
+    variants = None
+    if rank == 0 and world == 1:
+        variants = run_cloud_variants(torch, chk, host[0][0], shape, flush)
     # live hardware counters of this very launch (ncu subprocess, one replayed
     # launch of the same workload; never timed): warp instructions and DRAM bytes
     counters = None
@@ -369,6 +374,8 @@ def run_ours(args, rank, world, dist, sampler):
                          "peak_gbs": peak, "peak_kind": peak_kind},
         "clocks": clocks,
     }
+    if variants is not None:
+        out["cloud_variants"] = variants
     # the bound the kernel meets: its warp-instruction stream
     # against one warp instruction per SM sub-partition per cycle at the
     # sampled clock; DRAM traffic of the same launch alongside
@@ -384,6 +391,31 @@ def run_ours(args, rank, world, dist, sampler):
         "peak_kind": f"148 SMs x 4 SMSPs x 1 warp-inst/cycle x the sampled SM clock ({mhz:.0f} MHz)",
         "source": (counters or {}).get("source", "counters not collected"),
     }
+    return out
+
+
+def run_cloud_variants(torch, chk, q, shape, flush, reps: int = 20):
+    """Device cycle of the config-4 batch against an empty, a corner-packed
+    ("far") and a sparse uniform cloud next to the crowd (L2 flushed, median)."""
+    from paper_2309_12543_b200 import scenarios as S
+
+    n = shape.n_points
+    clouds = {
+        "crowd": _cloud(shape, 11),
+        "empty": np.full((n, 3), np.nan, np.float32),
+        "far_corners": S.far_crowd_cloud(n, 11).astype(np.float32),
+        "sparse_2k": np.concatenate([S.sparse_cloud(2000, 11), np.full((n - 2000, 3), np.nan)]).astype(np.float32),
+    }
+    chk.q_dev.copy_(torch.from_numpy(q))
+    out = {}
+    for name, pts in clouds.items():
+        chk.p_dev.copy_(torch.from_numpy(pts))
+        step = lambda: chk.launch(device_only=True)  # noqa: E731
+        _time_steps(torch, step, 3, flush)
+        ms = statistics.median(_time_steps(torch, step, reps, flush))
+        n_occ = int(chk.ws[:4].view(torch.int32).item())
+        out[name] = {"occupied_voxels": n_occ, "ms_per_step": ms,
+                     "waypoint_queries_per_s": shape.n_waypoints / (ms / 1e3)}
     return out
 
 

@@ -42,6 +42,9 @@ struct QueryParams {
     int32_t round_min;                      // queued cells that trigger a lookup round (<= 32)
     const uint32_t* bricks;                 // occupancy brick columns (4^3 voxels), or null: no box test
     int32_t stage_bricks;                   // brick columns copied to shared memory (else read from global)
+    int32_t dilate;                         // > 0: empty-neighbourhood test at setup, dilation radius in bricks
+    const uint32_t* brick_cols;             // the occupancy brick columns (input of the dilation)
+    int32_t nbx_brick, nbz_brick;           // brick grid (x columns, z bits)
     int32_t nby_brick;                      // brick columns per x row
     const uint32_t* shell_cells;            // kept window cells sorted by distance from the centre
     const float* shell_radius;              // their distance (m), rounded down
@@ -298,7 +301,41 @@ struct __align__(16) ShellSetup {
     float thresh0;   // starting threshold: min(clamp, the configuration's best key at setup time)
 };
 
-__device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_t t, ShellSetup& s) {
+// Dilated brick occupancy (throughput batches): a (bx, by) column word whose
+// bit bz is set when some occupied brick lies within `dilate` bricks of
+// (bx, by, bz) in every axis.  A window [j - W/2, j + W/2) stays within
+// (W/2 + 3) / 4 bricks of its centre brick j / 4, so a clear bit at the centre
+// brick proves the window holds no occupied voxel.  Built per CTA in shared
+// memory (separable: z by shifts, then y, then x); `tmp` is scratch.
+constexpr int DILATE_MAX_COLS = 1024;  // 2 x 4 KB of shared memory (x, y <= 128 voxels)
+__device__ void build_dilated(const QueryParams& p, uint32_t* dil, uint32_t* tmp) {
+    const int nbx = p.nbx_brick, nby = p.nby_brick, r = p.dilate, n = nbx * nby;
+    const uint32_t zmask = p.nbz_brick >= 32 ? 0xffffffffu : ((1u << p.nbz_brick) - 1u);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t w = __ldg(p.brick_cols + i);
+        uint32_t d = w;
+        for (int k = 1; k <= r; ++k) d |= (w << k) | (w >> k);
+        dil[i] = d & zmask;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int bx = i / nby, by = i - bx * nby;
+        uint32_t d = 0;
+        for (int y = max(by - r, 0); y <= min(by + r, nby - 1); ++y) d |= dil[bx * nby + y];
+        tmp[i] = d;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int bx = i / nby, by = i - bx * nby;
+        uint32_t d = 0;
+        for (int x = max(bx - r, 0); x <= min(bx + r, nbx - 1); ++x) d |= tmp[x * nby + by];
+        dil[i] = d;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_t t, ShellSetup& s,
+                                            const uint32_t* dil) {
     const uint32_t per_link = (uint32_t)(p.C * p.split);
     const uint32_t r = t % per_link;
     const int64_t c = p.split == 1 ? r : r / p.split;
@@ -348,6 +385,14 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_
     s.ax = __ldg(p.anchor + o * 3);
     s.ay = __ldg(p.anchor + o * 3 + 1);
     s.az = __ldg(p.anchor + o * 3 + 2);
+    if (dil != nullptr) {  // nothing occupied near the window: the task stops at its first chunk
+        const unsigned bx = (unsigned)(s.ax + p.W[0] / 2) >> BRICK_LOG2, by = (unsigned)(s.ay + p.W[1] / 2) >> BRICK_LOG2;
+        const unsigned bz = (unsigned)(s.az + p.W[2] / 2) >> BRICK_LOG2;
+        // (a centre outside the grid -- negative coordinates wrap to large -- keeps the scan)
+        if (bx < (unsigned)p.nbx_brick && by < (unsigned)p.nby_brick && bz < (unsigned)p.nbz_brick &&
+            ((dil[bx * p.nby_brick + by] >> bz) & 1u) == 0u)
+            s.thresh0 = -INFINITY;
+    }
 }
 
 #ifdef LSDF_STATS  // instrumented build (tools/_stats.py): per-task scan counters
@@ -539,6 +584,8 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     uint32_t* s_bits = (uint32_t*)align16_ptr(s_radius + (stage_shell ? shell_padded(p.n_shell) : 0));
     uint32_t* s_bricks = (uint32_t*)align16_ptr(s_bits + (stage_bits ? n_words : 0));
     const int n_cols = (BRICKS && p.stage_bricks) ? (int)(((p.dims[0] + 3) >> BRICK_LOG2) * p.nby_brick) : 0;
+    uint32_t* s_dil = s_bricks;  // throughput variant: the dilated map (and its scratch) in place of the columns
+    const bool dilate = !BRICKS && p.dilate > 0;
     __shared__ ShellSetup s_setup[WARPS][GRAB_MAX];
     // Stage the shell list and the occupancy bitmap with asynchronous copies
     // (all in flight at once), and fetch + set up the first tasks while they
@@ -552,6 +599,8 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     if (n_cols) stage_async(s_bricks, p.bricks, (size_t)n_cols * 4);
     cp_async_commit();
     for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) sP[i] = p.P[i];
+    if (dilate) build_dilated(p, s_dil, s_dil + p.nbx_brick * p.nby_brick);
+    const uint32_t* dil = dilate ? s_dil : nullptr;
     // link processing order (lane k holds the link of rank k): decreasing
     // argmin count of the previous cycle, ties in p.group order
     int order_lane;
@@ -587,7 +636,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     if (lane == 0) base = atomicAdd(p.counters + launch, g);
     base = __shfl_sync(FULL_MASK, base, 0);
     if (base < n_tasks && (uint32_t)lane < min(g, n_tasks - base))
-        shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane]);
+        shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane], dil);
     __syncwarp();
     cp_async_wait_all();
     __syncthreads();
@@ -609,7 +658,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
         if (base >= n_tasks) break;
         const uint32_t cnt = min(g, n_tasks - base);
         if (!first && (uint32_t)lane < cnt)
-            shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane]);
+            shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane], dil);
         __syncwarp();
         {
             const uint32_t left = n_tasks - min(base + cnt, n_tasks);
@@ -742,6 +791,10 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     // whole windows empty); dense throughput batches would only pay for it
     p.bricks = (o.bricks_ok && !p.seg_filter) ? o.bricks : nullptr;
     p.nby_brick = o.nby;
+    p.brick_cols = o.bricks;
+    p.nbx_brick = o.nbx;
+    p.nbz_brick = o.nbz;
+    p.dilate = 0;
     p.prefix = o.prefix;
     p.posgrid = o.posgrid;
     char* w = (char*)workspace_dev;
@@ -811,10 +864,14 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
             const int stage_bits = o.n_words <= BITMAP_STAGE_MAX;
             // brick columns in shared memory when they fit the budget, else read from L2
             p.stage_bricks = p.bricks != nullptr && (int64_t)o.nbx * o.nby <= BRICK_STAGE_MAX;
+            // throughput batches: the dilated brick map (one bit test per task at setup)
+            p.dilate = (p.bricks == nullptr && o.bricks_ok && (int64_t)o.nbx * o.nby <= DILATE_MAX_COLS)
+                           ? (window->Wmax / 2 + 3) >> BRICK_LOG2 : 0;
             const size_t smem_s = (size_t)3 * window->Wmax * sizeof(double) +
                                   (size_t)WARPS * QCAP_SHELL * 4 +
                                   (stage_shell ? (size_t)shell_padded(p.n_shell) * 8 : 0) + (stage_bits ? (size_t)o.n_words * 4 : 0) +
                                   (p.stage_bricks ? (size_t)o.nbx * o.nby * 4 : 0) +
+                                  (p.dilate ? (size_t)o.nbx * o.nby * 8 : 0) +
                                   64;  // 16-B alignment of the four staged tables
             using ShellsKernel = void (*)(QueryParams, int, int, int, int, int, int64_t, int);
             static const ShellsKernel kernels[4] = {query_shells_kernel<false, false>, query_shells_kernel<false, true>,

@@ -140,6 +140,19 @@ def crowd_cloud(n_humans: int, per_human: int, seed: int) -> np.ndarray:
     return np.concatenate(parts, axis=0)
 
 
+def far_crowd_cloud(n_points: int, seed: int) -> np.ndarray:
+    """Config-4 robustness variant: the crowd's points packed into the eight
+    corners of the grid (|x|, |y|, |z| in [0.8, 1)), out of most windows' reach."""
+    rng = np.random.default_rng(seed)
+    corner = rng.choice([-1.0, 1.0], size=(n_points, 3))
+    return corner * rng.uniform(0.8, 1.0, size=(n_points, 3))
+
+
+def sparse_cloud(n_points: int, seed: int) -> np.ndarray:
+    """Config-4 robustness variant: a few uniform points over the grid (most windows empty or nearly)."""
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n_points, 3))
+
+
 def moving_human_frames(n_frames: int = 100, n_points: int = 30_000, seed: int = 0,
                         start_x: float = 1.4, speed: float = 1.6, dt: float = 0.008):
     """[(timestamp_ms, points)] for a blob approaching the base along -x."""

@@ -161,3 +161,41 @@ def test_mlp_w128_tensor_cores_vs_cuda_cores(L):
     want = O.mlp_predict(model.w1, model.b1, model.w2[:, cols], model.b2[cols], R[:8]).reshape(8, -1)
     got = y_tc[:8].cpu().numpy()[:, cols]
     assert np.abs(got - want).max() <= 1e-5 * max(1.0, np.abs(want).max())
+
+
+@pytest.mark.parametrize("cloud", ["far_corners", "sparse_2k", "blobs", "empty"])
+def test_config4_sparse_clouds_vs_dense(L, cloud):
+    """The throughput batch (65,536 waypoints, segment bound and dilated-brick
+    skip on) against clouds that leave most windows empty: == the dense gather
+    on slices, and empty clouds give the clamp everywhere."""
+    from paper_2309_12543_b200 import scenarios as S
+
+    shape = S.CONFIG4
+    robot, grid, sdfs, window = _setup(L, shape)
+    q = S.random_configs(shape.robot, shape.n_waypoints, seed=5)
+    rng = np.random.default_rng(5)
+    if cloud == "far_corners":
+        pts = S.far_crowd_cloud(200_000, 5)
+    elif cloud == "sparse_2k":
+        pts = S.sparse_cloud(2000, 5)
+    elif cloud == "blobs":  # tight blobs: on brick boundaries, in a grid corner, near the base
+        centres = np.array([[0.28, -0.28, 0.36], [-0.96, 0.96, -0.96], [0.12, 0.0, 0.44], [0.6, 0.6, -0.2]])
+        pts = np.concatenate([c + rng.normal(0, 0.02, size=(300, 3)) for c in centres])
+    else:
+        pts = np.empty((0, 3))
+    chk = L.DistanceChecker(robot, sdfs, grid, window).prepare(shape.n_waypoints, max(len(pts), 1), np.float32)
+    d, link, voxel = _device_cycle(chk, q, np.asarray(pts, np.float32).reshape(-1, 3) if len(pts)
+                                   else np.full((1, 3), np.nan, np.float32))
+    if cloud == "empty":
+        assert np.all(d == np.float32(chk.d_far_global)) and np.all(link == -1) and np.all(voxel == -1)
+        return
+    obs = L.voxelize_pointcloud(pts, grid)
+    for a in (0, 40_000):
+        part = L.TrajectorySdf.from_configs(robot, q[a:a + 2000], sdfs, grid, window)
+        dense = L.RobotSdfBatch(part.device_values(), grid, part.d_far_global)
+        dd, _, vd = L.query_min_distances(dense, obs, return_argmin=True)
+        assert np.array_equal(dd, d[a:a + 2000]) and np.array_equal(vd, voxel[a:a + 2000])
+        _, lp, _ = L.query_min_distances(part, obs, return_argmin=True)
+        assert np.array_equal(lp, link[a:a + 2000])
+    if cloud != "far_corners":
+        assert np.any(link >= 0)  # some windows do see an obstacle
