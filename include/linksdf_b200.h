@@ -181,6 +181,21 @@ int lsdf_fk_align_link_major(const lsdf_link* links, int32_t n_links, int32_t n_
                              double* R_geo_dev, double* dt_geo_dev, int32_t* anchor_geo_dev,
                              int32_t* flags_dev, void* stream);
 
+/* lsdf_fk_align / lsdf_fk_align_link_major with an options word:
+ * LSDF_FK_LINK_MAJOR selects the link-major geometry outputs;
+ * LSDF_FK_FLAGS_SELF_RESET: flags_dev holds 8 int32, zeroed once at
+ * allocation; the kernel counts into [2..3] and its last CTA publishes
+ * [0..1] and re-zeroes [2..4] — no reset launch before each call (one graph
+ * node less per control cycle: DistanceChecker). */
+#define LSDF_FK_LINK_MAJOR 1
+#define LSDF_FK_FLAGS_SELF_RESET 2
+int lsdf_fk_align_ex(const lsdf_link* links, int32_t n_links, int32_t n_geo,
+                     const double* q_dev, int64_t C, int32_t D, const double* limits_dev,
+                     const lsdf_env_grid* env, const int32_t W[3],
+                     double* R_all_dev, double* T_all_dev,
+                     double* R_geo_dev, double* dt_geo_dev, int32_t* anchor_geo_dev,
+                     int32_t* flags_dev, int32_t options, void* stream);
+
 /* compute_alignment (placement.py:60-99) for n positions T (n, 3) fp64. */
 int lsdf_align(const double* T_dev, int64_t n, const lsdf_env_grid* env, const int32_t W[3],
                int32_t* anchor_dev, double* dt_dev, int32_t* flags_dev, void* stream);

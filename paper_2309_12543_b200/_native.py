@@ -62,6 +62,8 @@ _SIGS = {
                       C.POINTER(_I32), _P, _P, _P, _P, _P, _P, _P],
     "lsdf_fk_align_link_major": [C.POINTER(LinkT), _I32, _I32, _P, _I64, _I32, _P, C.POINTER(EnvGridT),
                                  C.POINTER(_I32), _P, _P, _P, _P, _P, _P, _P],
+    "lsdf_fk_align_ex": [C.POINTER(LinkT), _I32, _I32, _P, _I64, _I32, _P, C.POINTER(EnvGridT),
+                         C.POINTER(_I32), _P, _P, _P, _P, _P, _P, _I32, _P],
     "lsdf_align": [_P, _I64, C.POINTER(EnvGridT), C.POINTER(_I32), _P, _P, _P, _P],
     "lsdf_occupancy_bytes": [C.POINTER(EnvGridT)],
     "lsdf_voxelize": [_P, _I32, _I64, C.POINTER(EnvGridT), _P, _P, _P],
@@ -107,6 +109,8 @@ _SIGS = {
 
 QUERY_BY_POSITION = 1        # lsdf_query_* flags word (include/linksdf_b200.h)
 QUERY_POSES_LINK_MAJOR = 2
+FK_LINK_MAJOR = 1            # lsdf_fk_align_ex options
+FK_FLAGS_SELF_RESET = 2
 
 EXPORTS = tuple(_SIGS) + ("lsdf_version", "lsdf_last_error", "lsdf_launch_count")
 

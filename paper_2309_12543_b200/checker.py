@@ -112,8 +112,11 @@ class DistanceChecker:
             self.dt_geo = t.zeros((C_, G, 3), dtype=t.float64, device=dev)
             self.anchor_geo = t.zeros((C_, G, 3), dtype=t.int32, device=dev)
         self._fk_entry = "lsdf_fk_align_link_major" if self.link_major else "lsdf_fk_align"
+        # self-resetting FK flags: no reset node ahead of FK on the cycle's critical branch
+        self._fk_opts = (N.FK_LINK_MAJOR if self.link_major else 0) | N.FK_FLAGS_SELF_RESET
         self._qflags = N.QUERY_POSES_LINK_MAJOR if self.link_major else 0
-        self.flags = t.zeros((4,), dtype=t.int32, device=dev)
+        # FK flags: [0..1] published per cycle, [2..4] the kernel's self-resetting counters
+        self.flags = t.zeros((8,), dtype=t.int32, device=dev)
         self.limits = N.to_device(np.ascontiguousarray(self._limits), t.float64)
         self.d_dev = t.zeros((C_,), dtype=t.float32, device=dev)
         self.link_dev = t.zeros((C_,), dtype=t.int32, device=dev)
@@ -163,9 +166,9 @@ class DistanceChecker:
             if staged:
                 self.q_dev.copy_(self.q_host, non_blocking=True)
             q_ptr = self._map["q"] if zc else N.ptr(self.q_dev)
-            N.call(self._fk_entry, self._chain, self.robot.n_links, len(self.sdfs), q_ptr, C_, self.robot.dof,
+            N.call("lsdf_fk_align_ex", self._chain, self.robot.n_links, len(self.sdfs), q_ptr, C_, self.robot.dof,
                    N.ptr(self.limits), self._env, self._W, None, None, N.ptr(self.R_geo), N.ptr(self.dt_geo),
-                   N.ptr(self.anchor_geo), N.ptr(self.flags), side.cuda_stream)
+                   N.ptr(self.anchor_geo), N.ptr(self.flags), self._fk_opts, side.cuda_stream)
         if staged:
             self.p_dev.copy_(self.p_host, non_blocking=True)
         p_ptr = self._map["p"] if zc else N.ptr(self.p_dev)
@@ -179,14 +182,15 @@ class DistanceChecker:
         main.wait_stream(side)
         if e2e:
             with t.cuda.stream(side):  # 16 B of flags back to the host, off the critical path
-                self.flags_host.copy_(self.flags, non_blocking=True)
+                self.flags_host.copy_(self.flags[:4], non_blocking=True)
         if zc:
             outs = (self._map["d"], self._map["link"], self._map["voxel"])
         else:
             outs = (N.ptr(self.d_dev), N.ptr(self.link_dev), N.ptr(self.voxel_dev))
         tr = self.traj
         args = (N.ptr(self.R_geo), N.ptr(self.dt_geo), N.ptr(self.anchor_geo), C_, tr.n_links, tr._table,
-                ctypes.byref(self._wstruct), self._env, N.ptr(self.ws), self._qflags, self.d_far_global, N.ptr(self.qws),
+                ctypes.byref(self._wstruct), self._env, N.ptr(self.ws), self._qflags,
+                self.d_far_global, N.ptr(self.qws),
                 outs[0], outs[1], outs[2], None, main.cuda_stream)
         N.call("lsdf_query_scan", *args)
         main.wait_stream(pre)
@@ -347,7 +351,7 @@ class CheckerPipeline:
             d.copy_(chk.d_dev, non_blocking=True)
             link.copy_(chk.link_dev, non_blocking=True)
             voxel.copy_(chk.voxel_dev, non_blocking=True)
-            flags.copy_(chk.flags, non_blocking=True)
+            flags.copy_(chk.flags[:4], non_blocking=True)
             ev["d2h"].record(self.d2h)
         s["busy"], s["ticket"] = True, ticket
         self._next += 1
@@ -553,7 +557,7 @@ class ShardedCloudPipeline:
             d.copy_(chk.d_dev, non_blocking=True)
             link.copy_(chk.link_dev, non_blocking=True)
             voxel.copy_(chk.voxel_dev, non_blocking=True)
-            flags.copy_(chk.flags, non_blocking=True)
+            flags.copy_(chk.flags[:4], non_blocking=True)
             ev["d2h"].record(self.d2h)
         s["busy"], s["ticket"] = True, ticket
         self._next += 1

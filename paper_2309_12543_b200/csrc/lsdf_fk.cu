@@ -31,7 +31,24 @@ struct FkParams {
     double* dt_geo;
     int32_t* anchor_geo;
     int32_t* flags;
+    int32_t* acc;        // where the kernels count (flags, or flags + 2 when self-resetting)
+    uint32_t* ticket;    // self-resetting flags: CTAs done (the last one publishes and re-zeroes), or null
 };
+
+// Self-resetting flags (LSDF_FK_FLAGS_SELF_RESET): every CTA counts into
+// acc = flags + 2; the last CTA to finish publishes flags[0..1] and re-zeroes
+// acc and the ticket, so a captured cycle needs no memset node.
+__device__ __forceinline__ void fk_epilogue(const FkParams& p, bool counted) {
+    if (p.ticket == nullptr) return;
+    if (counted) __threadfence();  // (only a thread that counted something needs its atomics ordered)
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(p.ticket, 1u) == gridDim.x - 1) {
+        __threadfence();
+        p.flags[0] = atomicExch(p.acc, 0);
+        p.flags[1] = atomicExch(p.acc + 1, 0);
+        *p.ticket = 0u;
+    }
+}
 
 constexpr int FK_THREADS = 128;
 constexpr int64_t FK_SERIAL_MIN = 6144;  // measured crossover (tools/_fk_sweep.py): 12.5 vs 13.9 us at 4096, 16.7 vs 14.6 at 8192
@@ -45,7 +62,8 @@ constexpr int64_t FK_SERIAL_MIN = 6144;  // measured crossover (tools/_fk_sweep.
 //      (sin/cos, Rodrigues, r_o @ r_motion) — independent work, in parallel;
 //   2. one thread per configuration: the parents-first chain (matmuls only);
 //   3. one thread per (configuration, link): outputs + window alignment.
-__global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_constant__ FkParams p, int lp_log2) {
+__device__ __forceinline__ bool fk_align_body(const FkParams& p, int lp_log2) {
+    bool counted = false;
     extern __shared__ double s_fk[];
     // the chain table in shared memory: lanes of a warp read different links,
     // which the constant cache would serialize
@@ -70,7 +88,10 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
             const double v = q[j];
             bad += (v < p.limits[2 * j] || v > p.limits[2 * j + 1]);
         }
-        if (bad) atomicAdd(&p.flags[0], bad);
+        if (bad) {
+            atomicAdd(&p.acc[0], bad);
+            counted = true;
+        }
     }
     if (active) {
         const lsdf_link& L = s_links[li];
@@ -139,7 +160,7 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
         }
     }
     __syncthreads();
-    if (!active) return;
+    if (!active) return counted;
     const double* w = world + ((size_t)cl * lp + li) * 12;
     const lsdf_link& L = s_links[li];
     if (p.R_all != nullptr) {
@@ -156,13 +177,17 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
         for (int e = 0; e < 9; ++e) p.R_geo[o * 9 + e] = w[e];
         int32_t anc[3];
         double del[3], T[3] = {w[9], w[10], w[11]};
-        if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del, p.rinv)) atomicAdd(&p.flags[1], 1);
+        if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del, p.rinv)) {
+                    atomicAdd(&p.acc[1], 1);
+                    counted = true;
+                }
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             p.dt_geo[o * 3 + k] = del[k];
             p.anchor_geo[o * 3 + k] = anc[k];
         }
     }
+    return counted;
 }
 
 // Large batches: one thread per configuration walks the whole chain with the
@@ -175,7 +200,8 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
 constexpr int FKS_THREADS = 64;
 
 template <bool STAGE, bool LM>
-__global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __grid_constant__ FkParams p) {
+__device__ __forceinline__ bool fk_serial_body(const FkParams& p) {
+    bool counted = false;
     // every thread walks the same link at the same time: the chain table is
     // read straight from the kernel parameters (uniform constant-bank loads)
     const lsdf_link* s_links = p.links;
@@ -201,7 +227,7 @@ __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __gr
     // warp's control flow stays uniform, and write nothing
     const int lane = threadIdx.x & 31;
     const int64_t cw = c0 + (threadIdx.x & ~31);
-    if (LM && cw >= p.C) return;
+    if (LM && cw >= p.C) return counted;
     const int nw = (int)(p.C - cw < 32 ? p.C - cw : 32);
     const bool live = c0 + threadIdx.x < p.C;
     const int64_t c = (LM && !live) ? p.C - 1 : c0 + threadIdx.x;
@@ -213,7 +239,10 @@ __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __gr
                 const double v = q[j];
                 bad += (v < p.limits[2 * j] || v > p.limits[2 * j + 1]);
             }
-            if (bad) atomicAdd(&p.flags[0], bad);
+            if (bad) {
+            atomicAdd(&p.acc[0], bad);
+            counted = true;
+        }
         }
         // world pose of the previous link in registers (serial chains); poses
         // a later non-adjacent child needs go to a per-thread local array
@@ -300,7 +329,10 @@ __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __gr
                 int32_t anc[3];
                 double del[3];
                 if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del, p.rinv) && live)
-                    atomicAdd(&p.flags[1], 1);
+                    {
+                    atomicAdd(&p.acc[1], 1);
+                    counted = true;
+                }
 #pragma unroll
                 for (int e = 0; e < 9; ++e) s_R[wi][lane * 9 + e] = R[e];
 #pragma unroll
@@ -327,7 +359,10 @@ __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __gr
                 int32_t anc[3];
                 double del[3];
                 if (!align_one(T, p.env.extent, p.env.resolution, p.env.dims, p.W, anc, del, p.rinv))
-                    atomicAdd(&p.flags[1], 1);
+                    {
+                    atomicAdd(&p.acc[1], 1);
+                    counted = true;
+                }
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
                     odt[o * 3 + k] = del[k];
@@ -336,15 +371,27 @@ __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __gr
             }
         }
     }
-    if (!STAGE || LM) return;
+    if (!STAGE || LM) return counted;
     __syncthreads();
-    if (p.R_geo == nullptr) return;
+    if (p.R_geo == nullptr) return counted;
     // this CTA's configurations are contiguous in every output
     for (int i = threadIdx.x; i < nc * G * 9; i += FKS_THREADS) p.R_geo[c0 * G * 9 + i] = sR[i];
     for (int i = threadIdx.x; i < nc * G * 3; i += FKS_THREADS) {
         p.dt_geo[c0 * G * 3 + i] = sdt[i];
         p.anchor_geo[c0 * G * 3 + i] = sanc[i];
     }
+    return counted;
+}
+
+__global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_constant__ FkParams p, int lp_log2) {
+    const bool counted = fk_align_body(p, lp_log2);
+    fk_epilogue(p, counted);
+}
+
+template <bool STAGE, bool LM>
+__global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __grid_constant__ FkParams p) {
+    const bool counted = fk_serial_body<STAGE, LM>(p);
+    fk_epilogue(p, counted);
 }
 
 __global__ void align_kernel(const double* T, int64_t n, lsdf_env_grid env, int32_t W0, int32_t W1, int32_t W2,
@@ -368,7 +415,7 @@ namespace {
 int fk_align_impl(const lsdf_link* links, int32_t n_links, int32_t n_geo, const double* q_dev, int64_t C, int32_t D,
                   const double* limits_dev, const lsdf_env_grid* env, const int32_t W[3], double* R_all_dev,
                   double* T_all_dev, double* R_geo_dev, double* dt_geo_dev, int32_t* anchor_geo_dev,
-                  int32_t* flags_dev, void* stream, bool link_major) {
+                  int32_t* flags_dev, void* stream, bool link_major, bool flags_self_reset=false) {
     if (n_links < 1 || n_links > LSDF_MAX_LINKS || n_geo > LSDF_MAX_LINKS)
         return fail(LSDF_ERR_VALIDATION, "lsdf_fk_align: %d links outside 1..%d", n_links, LSDF_MAX_LINKS);
     if (C <= 0) return LSDF_OK;
@@ -396,11 +443,14 @@ int fk_align_impl(const lsdf_link* links, int32_t n_links, int32_t n_geo, const 
     p.dt_geo = dt_geo_dev;
     p.anchor_geo = anchor_geo_dev;
     p.flags = flags_dev;
+    p.acc = flags_self_reset ? flags_dev + 2 : flags_dev;
+    p.ticket = flags_self_reset ? (uint32_t*)(flags_dev + 4) : nullptr;
     int lp_log2 = 0;
     while ((1 << lp_log2) < n_links) ++lp_log2;
     const int cpb = FK_THREADS >> lp_log2;
     const size_t smem = (size_t)2 * FK_THREADS * 12 * sizeof(double);  // local + world, cpb * lp slots each
-    if (flags_dev != nullptr)
+    if (flags_self_reset && flags_dev == nullptr) return fail(LSDF_ERR_VALIDATION, "fk: self-resetting flags need a buffer");
+    if (flags_dev != nullptr && !flags_self_reset)
         LSDF_TRY(check_cuda(cudaMemsetAsync(flags_dev, 0, 2 * sizeof(int32_t), (cudaStream_t)stream), "fk flags memset"));
     if (C >= FK_SERIAL_MIN && link_major) {
         fk_align_serial_kernel<true, true><<<grid_for(C, FKS_THREADS), FKS_THREADS, 0, (cudaStream_t)stream>>>(p);
@@ -437,6 +487,15 @@ extern "C" int lsdf_fk_align_link_major(const lsdf_link* links, int32_t n_links,
                                         void* stream) {
     return fk_align_impl(links, n_links, n_geo, q_dev, C, D, limits_dev, env, W, R_all_dev, T_all_dev, R_geo_dev,
                          dt_geo_dev, anchor_geo_dev, flags_dev, stream, true);
+}
+
+extern "C" int lsdf_fk_align_ex(const lsdf_link* links, int32_t n_links, int32_t n_geo, const double* q_dev, int64_t C,
+                                int32_t D, const double* limits_dev, const lsdf_env_grid* env, const int32_t W[3],
+                                double* R_all_dev, double* T_all_dev, double* R_geo_dev, double* dt_geo_dev,
+                                int32_t* anchor_geo_dev, int32_t* flags_dev, int32_t options, void* stream) {
+    return fk_align_impl(links, n_links, n_geo, q_dev, C, D, limits_dev, env, W, R_all_dev, T_all_dev, R_geo_dev,
+                         dt_geo_dev, anchor_geo_dev, flags_dev, stream, (options & LSDF_FK_LINK_MAJOR) != 0,
+                         (options & LSDF_FK_FLAGS_SELF_RESET) != 0);
 }
 
 extern "C" int lsdf_align(const double* T_dev, int64_t n, const lsdf_env_grid* env, const int32_t W[3],

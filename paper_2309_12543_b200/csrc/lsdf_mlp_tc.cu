@@ -24,7 +24,10 @@
 // lane quarter, one per rotation half) drain it with tcgen05.ld and store.
 // 3xTF32 keeps ~fp32 accuracy, inside the 1e-5 (normalized) contract; the
 // CUDA-core kernel (lsdf_mlp.cu) stays the bit-reproducing path.
+#include "lsdf_async.cuh"
 #include "lsdf_common.cuh"
+
+using namespace lsdf;
 
 namespace {
 
@@ -33,7 +36,6 @@ constexpr int TN = 256;   // rotations per tile (tcgen05 N)
 constexpr int KB_BYTES_A = TM * 128;  // one 32-wide k-block of A (W2^T): 128 rows x 128 B
 constexpr int KB_BYTES_B = TN * 128;  // one 32-wide k-block of B (h): 256 rows x 128 B
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // byte offset of element (row, k) inside a K-major, 128B-swizzled k-block
 __host__ __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t k) {
@@ -44,35 +46,6 @@ __device__ __forceinline__ float tf32_rna(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-// Bounded wait: a lost arrival traps (a kernel error) instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    for (uint32_t spin = 0; spin < (1u << 26); ++spin) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (done) return;
-    }
-    __trap();
-}
-
-__device__ __forceinline__ void bulk_copy(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                     smem_u32(smem_dst)),
-                 "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
 }
 
 // tcgen05 shared-memory matrix descriptor: K-major, 128-byte swizzle,

@@ -23,6 +23,9 @@
 // query_direct_kernel (fallback when a link's far value is below the clamp or
 // the mask has no column intervals): walks the window's (x, y) columns over
 // the kept z-interval of each, with `split` column slices per (c, l).
+#include <cstdlib>
+
+#include "lsdf_async.cuh"
 #include "lsdf_device.cuh"
 
 using namespace lsdf;
@@ -258,23 +261,6 @@ constexpr int BRICK_STAGE_MAX = 4096;   // brick columns staged in shared memory
 __device__ __forceinline__ void* align16_ptr(void* q) {
     return (void*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-// Block-cooperative asynchronous global -> shared copy of nbytes (a multiple
-// of 4): 16-B chunks when both sides are 16-B aligned, 4-B copies otherwise.
-__device__ __forceinline__ void stage_async(void* dst, const void* src, size_t nbytes) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-    const char* g = (const char*)src;
-    size_t head = 0;
-    if ((((uintptr_t)src | (uintptr_t)d) & 15) == 0) {
-        head = nbytes & ~(size_t)15;
-        for (size_t o = (size_t)threadIdx.x * 16; o < head; o += (size_t)blockDim.x * 16)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + (uint32_t)o), "l"(g + o));
-    }
-    for (size_t o = head + (size_t)threadIdx.x * 4; o < nbytes; o += (size_t)blockDim.x * 4)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d + (uint32_t)o), "l"(g + o));
-}
-
 struct ShellView {
     const uint32_t* cells;   // shell-ordered kept cells (shared or global)
     const float* radius;
@@ -352,27 +338,29 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_
     for (int e = 0; e < 9; ++e) s.R[e] = R[e];
 #pragma unroll
     for (int e = 0; e < 3; ++e) s.dtinv[e] = dtinv[e];
-    const float4 sa = p.seg_a[l];
-    const float a3[3] = {sa.x, sa.y, sa.z};
-    // the window offsets are affine in the cell index, P_a[m] = P_a[0] + m s_a:
-    // fold them in, so the scan evaluates A' m + b' straight from the cell
-    // indices (no offset-table loads)
-    const int Wm = p.Wmax;
-    const double p0[3] = {__ldg(p.P), __ldg(p.P + Wm), __ldg(p.P + 2 * Wm)};
-    const double sc[3] = {__ldg(p.P + 1) - p0[0], __ldg(p.P + Wm + 1) - p0[1], __ldg(p.P + 2 * Wm + 1) - p0[2]};
+    if (p.seg_filter) {  // segment-bound constants (throughput batches only)
+        const float4 sa = p.seg_a[l];
+        const float a3[3] = {sa.x, sa.y, sa.z};
+        // the window offsets are affine in the cell index, P_a[m] = P_a[0] + m s_a:
+        // fold them in, so the scan evaluates A' m + b' straight from the cell
+        // indices (no offset-table loads)
+        const int Wm = p.Wmax;
+        const double p0[3] = {__ldg(p.P), __ldg(p.P + Wm), __ldg(p.P + 2 * Wm)};
+        const double sc[3] = {__ldg(p.P + 1) - p0[0], __ldg(p.P + Wm + 1) - p0[1], __ldg(p.P + 2 * Wm + 1) - p0[2]};
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+        for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) s.A[3 * a + k] = (float)(R[3 * a + k] * p.e_r * sc[a]);
+            for (int k = 0; k < 3; ++k) s.A[3 * a + k] = (float)(R[3 * a + k] * p.e_r * sc[a]);
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
-        s.b[k] = (float)(dtinv[k] * p.e_r - (double)a3[k] +
-                         p.e_r * (R[k] * p0[0] + R[3 + k] * p0[1] + R[6 + k] * p0[2]));
+        for (int k = 0; k < 3; ++k)
+            s.b[k] = (float)(dtinv[k] * p.e_r - (double)a3[k] +
+                             p.e_r * (R[k] * p0[0] + R[3 + k] * p0[1] + R[6 + k] * p0[2]));
+        // |link-frame point| <= rho + |dt|: a cell with rho <= hull - |dt| samples
+        // inside the hull of the grid's cell centres, where the segment's upper
+        // bound holds (outside it the sample is the link's far value)
+        s.hull_lim = (float)(p.hull - (double)dtn) * (1.0f - 0x1p-20f) - 1e-6f;
+    }
     s.slack = dtn + p.core[l];
-    // |link-frame point| <= rho + |dt|: a cell with rho <= hull - |dt| samples
-    // inside the hull of the grid's cell centres, where the segment's upper
-    // bound holds (outside it the sample is the link's far value)
-    s.hull_lim = (float)(p.hull - (double)dtn) * (1.0f - 0x1p-20f) - 1e-6f;
     float t0 = p.clamp;  // values >= clamp never change the answer
     if (p.per_link == nullptr) {  // best key any link of this configuration has published so far (an upper
         const uint64_t k = ~(uint64_t)__ldcg(p.keys + c);  // bound of the minimum, so an older read stays valid)
@@ -469,8 +457,10 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
             const int bx0 = x0 >> BRICK_LOG2, by0 = y0 >> BRICK_LOG2, nbyr = (y1 >> BRICK_LOG2) - by0 + 1;
             const int ncol = ((x1 >> BRICK_LOG2) - bx0 + 1) * nbyr;
             const uint32_t zmask = (2u << (z1 >> BRICK_LOG2)) - (1u << (z0 >> BRICK_LOG2));
+            const float rinv_y = 1.0f / (float)nbyr;
             for (int i = lane; i < ncol; i += 32) {
-                const int bx = bx0 + i / nbyr, by = by0 + i % nbyr;
+                const int qx = __float2int_rz(((float)i + 0.5f) * rinv_y);  // i / nbyr (small integers: exact)
+                const int bx = bx0 + qx, by = by0 + (i - qx * nbyr);
                 hit |= (sv.bricks[bx * p.nby_brick + by] & zmask) != 0u;
             }
         }
@@ -582,7 +572,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     uint32_t* s_cells = (uint32_t*)align16_ptr(s_queue + WARPS * QCAP_SHELL);
     float* s_radius = (float*)align16_ptr(s_cells + (stage_shell ? shell_padded(p.n_shell) : 0));
     uint32_t* s_bits = (uint32_t*)align16_ptr(s_radius + (stage_shell ? shell_padded(p.n_shell) : 0));
-    uint32_t* s_bricks = (uint32_t*)align16_ptr(s_bits + (stage_bits ? n_words : 0));
+    uint32_t* s_bricks = (uint32_t*)align16_ptr(s_bits + (stage_bits ? (n_words + 3) & ~3 : 0));
     const int n_cols = (BRICKS && p.stage_bricks) ? (int)(((p.dims[0] + 3) >> BRICK_LOG2) * p.nby_brick) : 0;
     uint32_t* s_dil = s_bricks;  // throughput variant: the dilated map (and its scratch) in place of the columns
     const bool dilate = !BRICKS && p.dilate > 0;
@@ -591,28 +581,37 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     // (all in flight at once), and fetch + set up the first tasks while they
     // land: the latency path pays one memory round trip here, not one per
     // loop iteration.
-    if (stage_shell) {
-        stage_async(s_cells, p.shell_cells, (size_t)shell_padded(p.n_shell) * 4);
-        stage_async(s_radius, p.shell_radius, (size_t)shell_padded(p.n_shell) * 4);
+    // one thread issues a bulk copy per table (cp.async.bulk, completing on an
+    // mbarrier); sizes round up to 16 B inside the padded source allocations
+    __shared__ uint64_t s_bar;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        const uint32_t b_shell = stage_shell ? (uint32_t)shell_padded(p.n_shell) * 4u : 0u;
+        const uint32_t b_bits = stage_bits ? ((uint32_t)n_words * 4u + 15u) & ~15u : 0u;
+        const uint32_t b_cols = ((uint32_t)n_cols * 4u + 15u) & ~15u;
+        mbar_expect_tx(&s_bar, 2u * b_shell + b_bits + b_cols);
+        if (b_shell) {
+            bulk_copy(s_cells, p.shell_cells, b_shell, &s_bar);
+            bulk_copy(s_radius, p.shell_radius, b_shell, &s_bar);
+        }
+        if (b_bits) bulk_copy(s_bits, p.bitmap, b_bits, &s_bar);
+        if (b_cols) bulk_copy(s_bricks, p.bricks, b_cols, &s_bar);
     }
-    if (stage_bits) stage_async(s_bits, p.bitmap, (size_t)n_words * 4);
-    if (n_cols) stage_async(s_bricks, p.bricks, (size_t)n_cols * 4);
-    cp_async_commit();
     for (int i = threadIdx.x; i < 3 * p.Wmax; i += blockDim.x) sP[i] = p.P[i];
     if (dilate) build_dilated(p, s_dil, s_dil + p.nbx_brick * p.nby_brick);
     const uint32_t* dil = dilate ? s_dil : nullptr;
     // link processing order (lane k holds the link of rank k): decreasing
     // argmin count of the previous cycle, ties in p.group order
-    int order_lane;
-    {
+    int order_lane = lane < n_group ? p.group[lane] : 0;
+    if (p.track_order) {
         const int k = lane;
-        const uint32_t mine = (k < n_group && p.track_order) ? __ldcg(p.link_hist + p.group[k]) : 0u;
+        const uint32_t mine = k < n_group ? __ldcg(p.link_hist + p.group[k]) : 0u;
         int rank = 0;
         for (int j = 0; j < n_group; ++j) {
             const uint32_t other = __shfl_sync(FULL_MASK, mine, j);
             rank += (other > mine) | ((other == mine) & (j < k));
         }
-        order_lane = k < n_group ? p.group[k] : 0;
         int inv = 0;
         for (int j = 0; j < n_group; ++j) {
             const int rj = __shfl_sync(FULL_MASK, rank, j);
@@ -632,14 +631,18 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     __shared__ int s_order[WARPS][LSDF_MAX_LINKS];
     if (lane < n_group) s_order[warp][lane] = order_lane;
     __syncwarp();
+    // the first grab of every warp is static (warp w takes tasks [w g, w g + g)):
+    // thousands of warps starting at once would otherwise serialise on the
+    // counter's L2 atomic unit; later grabs come from the counter, offset past
+    // the static range
     uint32_t base = 0, g = (uint32_t)grab;
-    if (lane == 0) base = atomicAdd(p.counters + launch, g);
-    base = __shfl_sync(FULL_MASK, base, 0);
+    const uint32_t static_total = gridDim.x * WARPS * g;
+    base = (blockIdx.x * WARPS + warp) * g;
     if (base < n_tasks && (uint32_t)lane < min(g, n_tasks - base))
         shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane], dil);
     __syncwarp();
-    cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();  // (the barrier's init is visible to every thread from here)
+    mbar_wait(&s_bar, 0);
     ShellView sv;
     sv.cells = stage_shell ? s_cells : p.shell_cells;
     sv.radius = stage_shell ? s_radius : p.shell_radius;
@@ -652,7 +655,7 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     const uint32_t warps_total = gridDim.x * WARPS;
     for (bool first = true;; first = false) {
         if (!first) {
-            if (lane == 0) base = atomicAdd(p.counters + launch, g);
+            if (lane == 0) base = static_total + atomicAdd(p.counters + launch, g);
             base = __shfl_sync(FULL_MASK, base, 0);
         }
         if (base >= n_tasks) break;
@@ -714,6 +717,13 @@ namespace {
 
 constexpr int STAGE_SCAN = 1, STAGE_FINALIZE = 2;
 
+// Tuning overrides for A/B sweeps on the GPU box (tools/cycle_parts.py):
+// LSDF_TUNE_<NAME>=<int>, read once per process; unset = the built-in choice.
+int tune(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return (v != nullptr && *v) ? atoi(v) : dflt;
+}
+
 int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t* anchor_geo_dev, int64_t C,
                int32_t n_geo, const lsdf_link_grid* grids, const lsdf_window* window, const lsdf_env_grid* env,
                const void* occupancy_dev, int32_t by_position, double d_far_global, void* workspace_dev, float* d_dev,
@@ -757,6 +767,8 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     // shells: about one resident wave (148 SMs x 32 warps) in flight for small batches
     int64_t split = shells ? (148LL * 32 + C * n_geo - 1) / (C * n_geo) : (target + C * n_geo - 1) / (C * n_geo);
     split = split < 1 ? 1 : (split > (shells ? 4 : 8) ? (shells ? 4 : 8) : split);
+    static const int t_split = tune("LSDF_TUNE_SPLIT", 0);
+    if (t_split > 0 && shells) split = t_split;
     p.split = (int32_t)split;
     p.n_tasks = C * n_geo * split;
     for (int a = 0; a < 3; ++a) {
@@ -775,7 +787,8 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     // latency-sized batches: a lookup round once 16 cells are queued, so the
     // task's threshold drops (and its scan stops) sooner; throughput batches
     // only run full rounds (issue-bound: a half round wastes lanes)
-    p.round_min = p.seg_filter ? 32 : 16;
+    static const int t_round = tune("LSDF_TUNE_ROUND_MIN", 0);
+    p.round_min = t_round > 0 ? t_round : (p.seg_filter ? 32 : 16);
     p.P = window->P_dev;
     p.Wmax = window->Wmax;
     p.by_position = by_position & LSDF_QUERY_BY_POSITION;
@@ -789,7 +802,8 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     p.bitmap = o.bitmap;
     // the brick box test: latency-sized batches (sparse or far obstacles leave
     // whole windows empty); dense throughput batches would only pay for it
-    p.bricks = (o.bricks_ok && !p.seg_filter) ? o.bricks : nullptr;
+    static const int t_bricks = tune("LSDF_TUNE_BRICKS", 1);
+    p.bricks = (o.bricks_ok && !p.seg_filter && t_bricks) ? o.bricks : nullptr;
     p.nby_brick = o.nby;
     p.brick_cols = o.bricks;
     p.nbx_brick = o.nbx;
@@ -806,6 +820,7 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     w += align256(C * n_geo * 4);
     p.link_hist = (uint32_t*)w;                    // LSDF_MAX_LINKS counts
     p.exit_count = (uint32_t*)w + LSDF_MAX_LINKS;
+
     p.d_out = d_dev;
     p.link_out = link_dev;
     p.voxel_out = voxel_dev;
@@ -860,8 +875,9 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
         p.geom.cy = g0.dims[1] - 1;
         const unsigned blocks = (unsigned)(blocks_per_link * n_group);
         if (shells) {
-            const int stage_shell = p.n_shell <= SHELL_STAGE_MAX;
-            const int stage_bits = o.n_words <= BITMAP_STAGE_MAX;
+            static const int t_stage = tune("LSDF_TUNE_STAGE", 3);  // bit 0: shell list, bit 1: bitmap
+            const int stage_shell = (t_stage & 1) && p.n_shell <= SHELL_STAGE_MAX;
+            const int stage_bits = (t_stage & 2) && o.n_words <= BITMAP_STAGE_MAX;
             // brick columns in shared memory when they fit the budget, else read from L2
             p.stage_bricks = p.bricks != nullptr && (int64_t)o.nbx * o.nby <= BRICK_STAGE_MAX;
             // throughput batches: the dilated brick map (one bit test per task at setup)
@@ -872,7 +888,7 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
                                   (stage_shell ? (size_t)shell_padded(p.n_shell) * 8 : 0) + (stage_bits ? (size_t)o.n_words * 4 : 0) +
                                   (p.stage_bricks ? (size_t)o.nbx * o.nby * 4 : 0) +
                                   (p.dilate ? (size_t)o.nbx * o.nby * 8 : 0) +
-                                  64;  // 16-B alignment of the four staged tables
+                                  96;  // 16-B alignment and 16-B rounding of the staged tables
             using ShellsKernel = void (*)(QueryParams, int, int, int, int, int, int64_t, int);
             static const ShellsKernel kernels[4] = {query_shells_kernel<false, false>, query_shells_kernel<false, true>,
                                                     query_shells_kernel<true, false>, query_shells_kernel<true, true>};
@@ -897,6 +913,8 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
             const int64_t n_tasks = C * split * n_group;
             int64_t grab = n_tasks / (resident * WARPS * 8);
             grab = grab < 1 ? 1 : (grab > GRAB_MAX ? GRAB_MAX : grab);
+            static const int t_grab = tune("LSDF_TUNE_GRAB", 0);
+            if (t_grab > 0) grab = t_grab < GRAB_MAX ? t_grab : GRAB_MAX;
             // grids pinned in L2: an access-policy window over the span of
             // this group's packed grids (contiguous when TrajectorySdf packed
             // them into one arena), persisting within the set-aside that

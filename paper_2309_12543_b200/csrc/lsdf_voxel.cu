@@ -8,6 +8,7 @@
 // voxel_compact_kernel: optional, one thread per voxel, writes the sorted
 //   index list (the ObstacleVoxelSet.indices the API returns) and posgrid.
 #include <cub/block/block_scan.cuh>
+#include <cstdlib>
 
 #include "lsdf_device.cuh"
 
@@ -72,7 +73,7 @@ template <typename T, bool PRIVATE>
 __global__ void __launch_bounds__(SCATTER_THREADS)
 voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, double rx, double ry, double rz,
                      uint32_t* bitmap, int32_t* counters, int64_t n_words, uint32_t* bricks, int32_t nby,
-                     int32_t n_cols) {
+                     int32_t n_cols, int32_t use_vec) {
     extern __shared__ uint32_t s_bits[];
     uint32_t* s_bricks = s_bits + n_words;  // brick columns (PRIVATE)
     if (PRIVATE) {
@@ -80,13 +81,41 @@ voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, do
         __syncthreads();
     }
     // grid-stride: a persistent grid of a few CTAs per SM amortises the
-    // private bitmap's clear and merge over many points
+    // private bitmap's clear and merge over many points.  f32 clouds: each
+    // thread takes VEC = 4 consecutive points per step as three 16-B loads
+    // (48 B, coalesced across the warp) when the buffer is 16-B aligned.
+    constexpr int VEC = sizeof(T) == 4 ? 4 : 1;
+    const bool vec = VEC > 1 && use_vec;
+    const int per = vec ? VEC : 1;
     int dropped_count = 0;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < N; i0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = i0 + threadIdx.x;
+    for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x) * per; i0 < N; i0 += (int64_t)gridDim.x * blockDim.x * per) {
+      const int64_t ib = i0 + (int64_t)threadIdx.x * per;
+      float buf[12];
+      if (vec && ib + VEC <= N) {
+          const float4* src = (const float4*)(pts + 3 * ib);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+              const float4 v = __ldcs(src + k);  // streamed once: evict-first
+              buf[4 * k] = v.x;
+              buf[4 * k + 1] = v.y;
+              buf[4 * k + 2] = v.z;
+              buf[4 * k + 3] = v.w;
+          }
+      }
+      for (int u = 0; u < per; ++u) {
+        const int64_t i = ib + u;
         bool dropped = false;
         if (i < N) {
-            const double x = (double)pts[3 * i], y = (double)pts[3 * i + 1], z = (double)pts[3 * i + 2];
+            double x, y, z;
+            if (vec && ib + VEC <= N) {
+                x = (double)buf[3 * u];
+                y = (double)buf[3 * u + 1];
+                z = (double)buf[3 * u + 2];
+            } else {
+                x = (double)pts[3 * i];
+                y = (double)pts[3 * i + 1];
+                z = (double)pts[3 * i + 2];
+            }
             const double ex = env.extent[0], ey = env.extent[1], ez = env.extent[2];
             // query.py:112: keep -e <= p < e on every axis (NaN fails the test -> dropped)
             const bool inside = (x >= -ex) && (x < ex) && (y >= -ey) && (y < ey) && (z >= -ez) && (z < ez);
@@ -115,6 +144,7 @@ voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, do
             }
         }
         dropped_count += __popc(__ballot_sync(FULL_MASK, dropped));
+      }
     }
     if ((threadIdx.x & 31) == 0 && dropped_count) atomicAdd(&counters[1], dropped_count);
     if (PRIVATE) {
@@ -231,22 +261,28 @@ int scatter_bitmap(const void* points_dev, int32_t points_f32, int64_t N, const 
     // two CTAs per SM so large clouds amortise the clear and merge
     const bool priv = o.n_words + n_cols <= PRIVATE_WORDS_MAX;
     const unsigned threads = SCATTER_THREADS;
-    const unsigned blocks = grid_for(N, threads) < 148u * 2u ? grid_for(N, threads) : 148u * 2u;
+    // 4 points per thread (float4 loads) only when that still fills the GPU:
+    // small clouds keep one point per thread (more CTAs in flight)
+    static const int t_vec = [] { const char* v = getenv("LSDF_TUNE_VOXVEC"); return v && *v ? atoi(v) : -1; }();
+    const bool want_vec = t_vec >= 0 ? t_vec != 0 : N >= 148LL * 2 * SCATTER_THREADS * 2;
+    const int64_t per_thread = (want_vec && points_f32 && (((uintptr_t)points_dev) & 15) == 0) ? 4 : 1;
+    const unsigned want = grid_for((N + per_thread - 1) / per_thread, threads);
+    const unsigned blocks = want < 148u * 2u ? want : 148u * 2u;
     const size_t smem = priv ? (size_t)(o.n_words + n_cols) * 4 : 0;
     if (points_f32) {
         if (priv)
             voxel_scatter_kernel<float, true><<<blocks, threads, smem, s>>>(
-                (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols);
+                (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols, (int)(per_thread > 1));
         else
             voxel_scatter_kernel<float, false><<<blocks, threads, 0, s>>>(
-                (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols);
+                (const float*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols, (int)(per_thread > 1));
     } else {
         if (priv)
             voxel_scatter_kernel<double, true><<<blocks, threads, smem, s>>>(
-                (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols);
+                (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols, (int)(per_thread > 1));
         else
             voxel_scatter_kernel<double, false><<<blocks, threads, 0, s>>>(
-                (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols);
+                (const double*)points_dev, N, *env, rx, ry, rz, o.bitmap, o.counters, o.n_words, o.bricks, o.nby, n_cols, (int)(per_thread > 1));
     }
     return check_launch("voxel_scatter_kernel");
 }

@@ -1,15 +1,17 @@
 """Per-source-line instruction and stall-sample shares of one ncu report (first kernel).
 
-    python tools/ncu_lines.py report.ncu-rep [top]
+    python tools/ncu_lines.py report.ncu-rep [top] [kernel-regex]
 """
 import csv
 import subprocess
 import sys
 
 
-def main(path, top=30):
-    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                         capture_output=True, text=True).stdout
+def main(path, top=30, kernel=None):
+    cmd = ["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if kernel:
+        cmd += ["--kernel-name", f"regex:{kernel}"]
+    out = subprocess.run(cmd, capture_output=True, text=True).stdout
     cur, hdr, rows = None, None, []
     for r in csv.reader(out.splitlines()):
         if r and r[0] == "File Path":
@@ -29,4 +31,4 @@ def main(path, top=30):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30, sys.argv[3] if len(sys.argv) > 3 else None)

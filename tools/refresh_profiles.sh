@@ -19,7 +19,7 @@ python bench.py --workload config2 --no-cpu-baseline > $O/bench_config2.json 2> 
 # launch list of the bench command (cold, serialised: shares, not absolutes)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_bench.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_bench.log 2>&1
-python tools/_stats.py config2 config4 > $O/scan_stats.txt 2>&1
+python tools/scan_stats.py config2 config4 > $O/scan_stats.txt 2>&1
 echo done
 # secondary workloads (configs 3 and 5, materialized mode) for DESIGN §6
 python tools/bench_dynamic.py > $O/config5_dynamic.json 2> $O/config5_dynamic.err

@@ -1,7 +1,7 @@
 """Scan statistics from the instrumented build (-DLSDF_STATS): per-task chunks, occupied cells, lookups.
 
-    python tools/_stats.py build          # here: builds _ab/libS.so
-    python tools/_stats.py config4 ...    # on the GPU box
+    python tools/scan_stats.py build          # here: builds _ab/libS.so
+    python tools/scan_stats.py config4 ...    # on the GPU box
 """
 import ctypes
 import os
