@@ -59,6 +59,10 @@ struct QueryParams {
     int64_t C;
     int64_t n_tasks;
     int32_t n_geo, split;
+    int32_t split_log2;          // split is a power of two on the shell path
+    uint32_t pl_mul;             // t / (C * split) as a multiply-high (Granlund-Montgomery), see fast_div
+    int32_t pl_shift;
+    int32_t static_sched;        // latency batches: warp w takes tasks w, w + W, ... (no task counter)
     int32_t W[3];
     int32_t full_window;  // iterate the whole window, masking per cell (d_far_l < clamp)
     double e_r, e_rinv;  // window extent and RN(1 / e_r)
@@ -320,11 +324,22 @@ __device__ void build_dilated(const QueryParams& p, uint32_t* dil, uint32_t* tmp
     __syncthreads();
 }
 
-__device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_t t, ShellSetup& s,
+// n / d for 32-bit n and a launch-constant d: q = (hi + ((n - hi) >> 1)) >> (sh - 1),
+// hi = umulhi(m, n), m = floor(2^32 (2^sh - d) / d) + 1, sh = ceil(log2 d) (d > 1);
+// d == 1 is encoded as sh == 0.
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t m, int sh) {
+    if (sh == 0) return n;
+    const uint32_t hi = __umulhi(m, n);
+    return (hi + ((n - hi) >> 1)) >> (sh - 1);
+}
+
+__device__ __forceinline__ void shell_setup(const QueryParams& p, const int* order, uint32_t t, ShellSetup& s,
                                             const uint32_t* dil) {
     const uint32_t per_link = (uint32_t)(p.C * p.split);
-    const uint32_t r = t % per_link;
-    const int64_t c = p.split == 1 ? r : r / p.split;
+    const uint32_t li = fast_div(t, p.pl_mul, p.pl_shift);  // rank of the task's link in the launch order
+    const int l = order[li];
+    const uint32_t r = t - li * per_link;
+    const int64_t c = r >> p.split_log2;
     const int64_t o = c * p.pose_cs + l * p.pose_ls;  // pose record
     double R[9], dtinv[3], dt[3];
 #pragma unroll
@@ -332,8 +347,10 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_
 #pragma unroll
     for (int e = 0; e < 3; ++e) dt[e] = __ldg(p.dt + o * 3 + e);
     shift_inverse(R, dt, p.e_r, dtinv, p.e_rinv);
-    // |dt| rounded up (dt is the residual of T against its voxel centre)
-    const float dtn = (float)(sqrt(dt[0] * dt[0] + dt[1] * dt[1] + dt[2] * dt[2]) * (1.0 + 1e-6) + 1e-12);
+    // |dt| rounded up (dt is the residual of T against its voxel centre): an
+    // f32 square root rounded up of the fp64 square sum rounded up, plus margin
+    const float dtn = __fsqrt_ru(__double2float_ru(dt[0] * dt[0] + dt[1] * dt[1] + dt[2] * dt[2])) * (1.0f + 1e-6f) +
+                      1e-12f;
 #pragma unroll
     for (int e = 0; e < 9; ++e) s.R[e] = R[e];
 #pragma unroll
@@ -369,7 +386,7 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_
     s.thresh0 = t0;
     s.l = l;
     s.c = (int32_t)c;
-    s.sidx = p.split == 1 ? 0 : (int32_t)(r % p.split);
+    s.sidx = (int32_t)(r & (uint32_t)(p.split - 1));
     s.ax = __ldg(p.anchor + o * 3);
     s.ay = __ldg(p.anchor + o * 3 + 1);
     s.az = __ldg(p.anchor + o * 3 + 2);
@@ -383,7 +400,19 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, int l, uint32_
     }
 }
 
-#ifdef LSDF_STATS  // instrumented build (tools/_stats.py): per-task scan counters
+#ifdef LSDF_TIMING  // instrumented build (tools/scan_timing.py): globaltimer stamps per warp / grab / task
+__device__ unsigned long long g_tim[16];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TIM(i, v) atomicAdd(g_tim + (i), (unsigned long long)(v))
+#else
+#define TIM(i, v) ((void)0)
+#endif
+
+#ifdef LSDF_STATS  // instrumented build (tools/scan_stats.py): per-task scan counters
 __device__ unsigned long long g_stats[8];
 #define STAT(i, v) (sc[i] += (v))
 #else
@@ -566,6 +595,10 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
                                                                   int last_launch) {
     extern __shared__ double s_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef LSDF_TIMING
+    const unsigned long long t_entry = gtime();
+    if (lane == 0) atomicMin(g_tim + 0, t_entry);
+#endif
     double* sP = s_dyn;
     uint32_t* s_queue = (uint32_t*)(sP + 3 * p.Wmax);
     // staged tables start on 16-B boundaries (cp.async 16-B chunks)
@@ -627,7 +660,6 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     // The per-task constants of a grab are computed lane-parallel (lane j
     // for task base + j) into shared memory.
     const uint32_t n_tasks = (uint32_t)(p.C * p.split) * (uint32_t)n_group;
-    const uint32_t per_link = (uint32_t)(p.C * p.split);
     __shared__ int s_order[WARPS][LSDF_MAX_LINKS];
     if (lane < n_group) s_order[warp][lane] = order_lane;
     __syncwarp();
@@ -639,10 +671,17 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     const uint32_t static_total = gridDim.x * WARPS * g;
     base = (blockIdx.x * WARPS + warp) * g;
     if (base < n_tasks && (uint32_t)lane < min(g, n_tasks - base))
-        shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane], dil);
+        shell_setup(p, s_order[warp], base + lane, s_setup[warp][lane], dil);
     __syncwarp();
     __syncthreads();  // (the barrier's init is visible to every thread from here)
     mbar_wait(&s_bar, 0);
+#ifdef LSDF_TIMING
+    const unsigned long long t_staged = gtime();
+    if (lane == 0) {
+        TIM(1, t_staged - t_entry);  // prologue incl. the first grab's setup
+        TIM(2, 1);                   // warps
+    }
+#endif
     ShellView sv;
     sv.cells = stage_shell ? s_cells : p.shell_cells;
     sv.radius = stage_shell ? s_radius : p.shell_radius;
@@ -655,24 +694,54 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     const uint32_t warps_total = gridDim.x * WARPS;
     for (bool first = true;; first = false) {
         if (!first) {
-            if (lane == 0) base = static_total + atomicAdd(p.counters + launch, g);
-            base = __shfl_sync(FULL_MASK, base, 0);
+            if (p.static_sched) {  // (g == 1) warp w's tasks are w, w + W, w + 2W, ...
+                base += warps_total;
+            } else {
+                if (lane == 0) base = static_total + atomicAdd(p.counters + launch, g);
+                base = __shfl_sync(FULL_MASK, base, 0);
+            }
         }
         if (base >= n_tasks) break;
         const uint32_t cnt = min(g, n_tasks - base);
+#ifdef LSDF_TIMING
+        const unsigned long long t_g0 = gtime();
+#endif
         if (!first && (uint32_t)lane < cnt)
-            shell_setup(p, s_order[warp][(base + lane) / per_link], base + lane, s_setup[warp][lane], dil);
+            shell_setup(p, s_order[warp], base + lane, s_setup[warp][lane], dil);
         __syncwarp();
-        {
+#ifdef LSDF_TIMING
+        const unsigned long long t_g1 = gtime();
+        if (lane == 0) {
+            TIM(3, t_g1 - t_g0);  // setup (later grabs)
+            TIM(4, 1);            // grabs
+            TIM(5, cnt);          // tasks
+        }
+#endif
+        if (grab > 1) {
             const uint32_t left = n_tasks - min(base + cnt, n_tasks);
             g = max(1u, min((uint32_t)grab, left / (2 * warps_total)));
         }
         int qlen = 0;
         for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS, BRICKS>(p, sv, queue, s_setup[warp], j, qlen, lane);
+#ifdef LSDF_TIMING
+        const unsigned long long t_g2 = gtime();
+        if (lane == 0) TIM(6, t_g2 - t_g1);  // scans of the grab's tasks
+#endif
         if (qlen > 0)  // the grab's remaining lookups, before its setups are overwritten
             lookup_round<BY_POS>(p, sv, s_setup[warp], lane < qlen ? queue[lane] : 0u, lane < qlen, 0xffu, lane);
         __syncwarp();
+#ifdef LSDF_TIMING
+        if (lane == 0) TIM(7, gtime() - t_g2);  // flush rounds
+#endif
     }
+#ifdef LSDF_TIMING
+    if (lane == 0) {
+        const unsigned long long t_end = gtime();
+        atomicMax(g_tim + 8, t_end);
+        TIM(9, t_end - t_entry);  // warp lifetime
+        TIM(10, t_end - t_staged);
+    }
+#endif
     // the last CTA of the last launch clears the counts this cycle's finalize refills
     if (p.track_order) {
         __syncthreads();
@@ -769,8 +838,17 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     split = split < 1 ? 1 : (split > (shells ? 4 : 8) ? (shells ? 4 : 8) : split);
     static const int t_split = tune("LSDF_TUNE_SPLIT", 0);
     if (t_split > 0 && shells) split = t_split;
+    if (shells) split = split >= 4 ? 4 : (split >= 2 ? 2 : 1);  // a power of two: shifts in the task decode
+    p.split_log2 = split == 4 ? 2 : (split == 2 ? 1 : 0);
     p.split = (int32_t)split;
     p.n_tasks = C * n_geo * split;
+    {  // magic numbers of t / (C * split)
+        const uint64_t d = (uint64_t)C * split;
+        int sh = 0;
+        while ((1ull << sh) < d) ++sh;
+        p.pl_shift = sh;
+        p.pl_mul = sh == 0 ? 0u : (uint32_t)(((1ull << 32) * ((1ull << sh) - d)) / d + 1);
+    }
     for (int a = 0; a < 3; ++a) {
         p.W[a] = window->W[a];
         p.dims[a] = env->dims[a];
@@ -915,6 +993,11 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
             grab = grab < 1 ? 1 : (grab > GRAB_MAX ? GRAB_MAX : grab);
             static const int t_grab = tune("LSDF_TUNE_GRAB", 0);
             if (t_grab > 0) grab = t_grab < GRAB_MAX ? t_grab : GRAB_MAX;
+            // latency batches (one task per grab, a few tasks per warp): a static
+            // round-robin schedule, no task counter for thousands of warps to
+            // serialise on
+            static const int t_static = tune("LSDF_TUNE_STATIC", 0);
+            p.static_sched = t_static && grab == 1 && n_tasks <= 4 * resident * WARPS;
             // grids pinned in L2: an access-policy window over the span of
             // this group's packed grids (contiguous when TrajectorySdf packed
             // them into one arena), persisting within the set-aside that
@@ -992,6 +1075,18 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
 extern "C" int lsdf_query_direct(LSDF_QUERY_ARGS) { return query_impl(LSDF_QUERY_FWD, STAGE_SCAN | STAGE_FINALIZE); }
 extern "C" int lsdf_query_scan(LSDF_QUERY_ARGS) { return query_impl(LSDF_QUERY_FWD, STAGE_SCAN); }
 extern "C" int lsdf_query_finalize(LSDF_QUERY_ARGS) { return query_impl(LSDF_QUERY_FWD, STAGE_FINALIZE); }
+
+#ifdef LSDF_TIMING
+extern "C" int lsdf_timing_read(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_tim, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {0};
+        z[0] = ~0ull;
+        cudaMemcpyToSymbol(g_tim, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 #ifdef LSDF_STATS
 extern "C" int lsdf_stats_read(unsigned long long* out, int reset) {
