@@ -520,11 +520,58 @@ def run_realtime(args, L):
     torch.cuda.synchronize()
     n_occ = int(chk.ws[:4].view(torch.int32).item())
     pct = lambda a, p: float(np.percentile(np.asarray(a) * 1e3, p))  # noqa: E731  ms -> µs
+    sphere = sphere_comparison(torch, L, shape, inputs[0], flush)
     return {"workload": f"{shape.name}: arm6g 500 waypoints vs 100k pts, 64^3, W=16", "occupied_voxels": n_occ,
             "device_p50_us": pct(devt, 50), "device_p99_us": pct(devt, 99),
             "e2e_p50_us": pct(e2e, 50), "e2e_p99_us": pct(e2e, 99), "samples": n,
             "waypoint_queries_per_s_device": 500 / (statistics.mean(devt) / 1e3),
-            "paper_gpu_ms_per_trajectory": 0.391}
+            "paper_gpu_ms_per_trajectory": 0.391,
+            "sphere_baseline": sphere}
+
+
+# covering spheres of the arm6g links (tests/golden/make_golden_r2.py ARM6G_SPHERES)
+_ARM6G_SPHERES = {
+    "l1": [{"center": [0, 0, z], "radius": 0.07} for z in (-0.06, 0.0, 0.06)],
+    "l2": [{"center": [0, 0, z], "radius": 0.06} for z in (-0.08, 0.0, 0.08)],
+    "l3": [{"center": [0, 0, z], "radius": 0.05} for z in (-0.07, 0.0, 0.07)],
+    "l4": [{"center": [0, 0, z], "radius": 0.045} for z in (-0.05, 0.0, 0.05)],
+    "l5": [{"center": [0, 0, 0], "radius": 0.0755}],
+    "l6": [{"center": [0, 0, 0], "radius": 0.05}],
+}
+
+
+def sphere_comparison(torch, L, shape, inp, flush, reps: int = 50):
+    """The paper's comparison (Table: 5.47 ms sphere model vs
+    0.391 ms per trajectory): the covering-sphere checker (query.py:254-291,
+    every sphere x every occupied voxel, fp64) on the same 500 waypoints and
+    cloud, device time per trajectory with poses and voxels resident."""
+    import copy
+    import ctypes
+
+    from paper_2309_12543_b200 import _native as N
+
+    doc = copy.deepcopy(shape.robot)
+    doc["spheres"] = _ARM6G_SPHERES
+    robot = L.RobotModel.from_dict(doc)
+    grid = L.EnvGrid(shape.grid_extent, shape.grid_res)
+    q, pts = inp
+    poses = L.forward_kinematics_batch(robot, L.ConfigBatch(q))
+    obs = L.voxelize_pointcloud(pts, grid)
+    sph = L.SphereRobotModel.from_robot(robot)
+    R = torch.from_numpy(np.ascontiguousarray(poses.rotations)).cuda()
+    T = torch.from_numpy(np.ascontiguousarray(poses.translations)).cuda()
+    sl = torch.from_numpy(sph.link_indices.astype(np.int32)).cuda()
+    sc = torch.from_numpy(np.ascontiguousarray(sph.centers)).cuda()
+    sr = torch.from_numpy(np.ascontiguousarray(sph.radii)).cuda()
+    out = torch.empty((len(q),), dtype=torch.float64, device="cuda")
+    idx = obs.device_indices()
+    env = ctypes.byref(grid.c_struct())
+    call = lambda: N.call("lsdf_sphere_baseline", R, T, len(q), poses.n_links, sl, sc, sr, sph.n_spheres,  # noqa: E731
+                          idx, obs.n_occupied, env, out, N.stream())
+    _time_steps(torch, call, 3, flush)
+    ts = _time_steps(torch, call, reps, flush)
+    return {"spheres": sph.n_spheres, "occupied_voxels": obs.n_occupied, "device_p50_us": float(np.median(ts) * 1e3),
+            "distance_evals": int(len(q) * sph.n_spheres * obs.n_occupied), "paper_sphere_ms_per_trajectory": 5.47}
 
 
 # ----------------------------------------------------------------------------- CPU (oracle port)

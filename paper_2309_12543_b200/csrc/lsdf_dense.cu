@@ -163,9 +163,17 @@ __global__ void per_link_fields_kernel(const float* __restrict__ windows, const 
     }
 }
 
-__global__ void sphere_baseline_kernel(const double* __restrict__ R, const double* __restrict__ T, int32_t L,
-                                       const int32_t* sl, const double* sc, const double* sr, int32_t S,
-                                       const int32_t* __restrict__ idx, int64_t N, lsdf_env_grid env, double* out) {
+// One CTA per configuration.  min over voxels n and spheres s of
+// sqrt(|c_s - x_n|^2) - r_s equals min over s of (sqrt(min_n |c_s - x_n|^2) - r_s)
+// exactly (the correctly rounded sqrt and the subtraction are monotone), so a
+// thread keeps one running squared minimum per sphere (MAXS registers) and
+// takes S square roots at the end instead of one per (sphere, voxel).
+template <int MAXS>
+__global__ void __launch_bounds__(256) sphere_baseline_kernel(const double* __restrict__ R, const double* __restrict__ T,
+                                                              int32_t L, const int32_t* sl, const double* sc,
+                                                              const double* sr, int32_t S,
+                                                              const int32_t* __restrict__ idx, int64_t N,
+                                                              lsdf_env_grid env, double* out) {
     extern __shared__ double s_w[];  // S x 4: world centre + radius
     __shared__ double s_min[32];
     const int64_t c = blockIdx.x;
@@ -178,15 +186,42 @@ __global__ void sphere_baseline_kernel(const double* __restrict__ R, const doubl
     }
     __syncthreads();
     double m = INFINITY;
-    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
-        double x[3];
-        for (int k = 0; k < 3; ++k)
-            x[k] = DADD(-env.extent[k], DMUL(DADD((double)idx[3 * i + k], 0.5), env.resolution[k]));
-        for (int s = 0; s < S; ++s) {
-            const double d0 = DSUB(s_w[4 * s], x[0]), d1 = DSUB(s_w[4 * s + 1], x[1]),
-                         d2 = DSUB(s_w[4 * s + 2], x[2]);
-            const double d = DSUB(DSQRT(dot3(d0, d1, d2, d0, d1, d2)), s_w[4 * s + 3]);
-            m = d < m ? d : m;
+    if (MAXS > 0) {
+        double m2[MAXS > 0 ? MAXS : 1];
+#pragma unroll
+        for (int s = 0; s < MAXS; ++s) m2[s] = INFINITY;
+        for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+            double x[3];
+            for (int k = 0; k < 3; ++k)
+                x[k] = DADD(-env.extent[k], DMUL(DADD((double)__ldg(idx + 3 * i + k), 0.5), env.resolution[k]));
+#pragma unroll
+            for (int s = 0; s < MAXS; ++s) {
+                if (s < S) {
+                    const double d0 = DSUB(s_w[4 * s], x[0]), d1 = DSUB(s_w[4 * s + 1], x[1]),
+                                 d2 = DSUB(s_w[4 * s + 2], x[2]);
+                    const double q = dot3(d0, d1, d2, d0, d1, d2);
+                    m2[s] = q < m2[s] ? q : m2[s];
+                }
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < MAXS; ++s) {
+            if (s < S) {
+                const double d = DSUB(DSQRT(m2[s]), s_w[4 * s + 3]);
+                m = d < m ? d : m;
+            }
+        }
+    } else {
+        for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+            double x[3];
+            for (int k = 0; k < 3; ++k)
+                x[k] = DADD(-env.extent[k], DMUL(DADD((double)idx[3 * i + k], 0.5), env.resolution[k]));
+            for (int s = 0; s < S; ++s) {
+                const double d0 = DSUB(s_w[4 * s], x[0]), d1 = DSUB(s_w[4 * s + 1], x[1]),
+                             d2 = DSUB(s_w[4 * s + 2], x[2]);
+                const double d = DSUB(DSQRT(dot3(d0, d1, d2, d0, d1, d2)), s_w[4 * s + 3]);
+                m = d < m ? d : m;
+            }
         }
     }
 #pragma unroll
@@ -370,9 +405,11 @@ extern "C" int lsdf_sphere_baseline(const double* R_all_dev, const double* T_all
                                     const lsdf_env_grid* env, double* out_dev, void* stream) {
     if (C <= 0) return LSDF_OK;
     if (S <= 0 || S > 4096) return fail(LSDF_ERR_VALIDATION, "sphere model with %d spheres", S);
-    sphere_baseline_kernel<<<(unsigned)C, 256, (size_t)S * 4 * sizeof(double), (cudaStream_t)stream>>>(
-        R_all_dev, T_all_dev, L, sphere_link_dev, sphere_center_dev, sphere_radius_dev, S, indices_dev, N, *env,
-        out_dev);
+    const size_t smem = (size_t)S * 4 * sizeof(double);
+    auto kern = S <= 8 ? sphere_baseline_kernel<8> : (S <= 24 ? sphere_baseline_kernel<24> : sphere_baseline_kernel<0>);
+    LSDF_TRY(ensure_smem((const void*)kern, smem, "sphere_baseline_kernel"));
+    kern<<<(unsigned)C, 256, smem, (cudaStream_t)stream>>>(R_all_dev, T_all_dev, L, sphere_link_dev, sphere_center_dev,
+                                                         sphere_radius_dev, S, indices_dev, N, *env, out_dev);
     return check_launch("sphere_baseline_kernel");
 }
 

@@ -13,6 +13,8 @@
   a strided subset of cells (every 97th x-fastest cell for primitives, 3,000
   seeded cells for the mesh, where each cell costs 1,280 triangle tests) plus
   the full-grid f64 sums of the primitives.
+* ``sphere_c2.npz`` — the covering-sphere comparator (query.py:254-291) on
+  config 2's seed-21 input, arm6g with 18 covering spheres.
 
 Inputs are regenerated from ``paper_2309_12543_b200.scenarios`` (seeded numpy);
 the fixtures store checksums of them so drift fails loudly.
@@ -105,11 +107,43 @@ def builds128():
     return out
 
 
+ARM6G_SPHERES = {  # covering spheres of the arm6g primitives: capsules by 3 spheres on the axis, box by 1, sphere itself
+    "l1": [{"center": [0, 0, z], "radius": 0.07} for z in (-0.06, 0.0, 0.06)],
+    "l2": [{"center": [0, 0, z], "radius": 0.06} for z in (-0.08, 0.0, 0.08)],
+    "l3": [{"center": [0, 0, z], "radius": 0.05} for z in (-0.07, 0.0, 0.07)],
+    "l4": [{"center": [0, 0, z], "radius": 0.045} for z in (-0.05, 0.0, 0.05)],
+    "l5": [{"center": [0, 0, 0], "radius": 0.0755}],
+    "l6": [{"center": [0, 0, 0], "radius": 0.05}],
+}
+
+
+def sphere_baseline():
+    """sphere_baseline_distances (query.py:254-291) on config 2's seed-21 input:
+    arm6g with covering spheres, 500 waypoints, the 100k-point human."""
+    import json
+
+    shape = S.CONFIG2
+    doc = json.loads(json.dumps(shape.robot))
+    doc["spheres"] = ARM6G_SPHERES
+    robot = MG._robot(doc)
+    grid = ref.EnvGrid(shape.grid_extent, shape.grid_res)
+    q = S.random_configs(shape.robot, shape.n_waypoints, seed=21)
+    pts = S.cloud_for(shape, 21).astype(np.float32)
+    poses = ref.forward_kinematics_batch(robot, ref.ConfigBatch(q))
+    obs = ref.voxelize_pointcloud(pts, grid)
+    spheres = ref.SphereRobotModel.from_robot(robot)
+    d, st = ref.sphere_baseline_distances(spheres, poses, obs, grid, return_stats=True)
+    print(f"sphere baseline: {spheres.n_spheres} spheres, {st['distance_evals']} distance evaluations")
+    return {"robot_json": np.frombuffer(json.dumps(doc).encode(), dtype=np.uint8), "d": d,
+            "evals": np.int64(st["distance_evals"]), "q_digest": _digest(q), "pts_digest": _digest(pts)}
+
+
 def main():
+    np.savez_compressed(HERE / "sphere_c2.npz", **sphere_baseline())
     np.savez_compressed(HERE / "builds128.npz", **builds128())
     np.savez_compressed(HERE / "bench_c4.npz", **bench_c4())
     np.savez_compressed(HERE / "bench_c2.npz", **bench_c2())
-    for n in ("builds128", "bench_c4", "bench_c2"):
+    for n in ("sphere_c2", "builds128", "bench_c4", "bench_c2"):
         p = HERE / f"{n}.npz"
         print(f"{p.name}: {p.stat().st_size / 1024:.0f} KiB")
 

@@ -199,3 +199,25 @@ def test_config4_sparse_clouds_vs_dense(L, cloud):
         assert np.array_equal(lp, link[a:a + 2000])
     if cloud != "far_corners":
         assert np.any(link >= 0)  # some windows do see an obstacle
+
+
+def test_sphere_baseline_vs_reference(L):
+    """The covering-sphere comparator (query.py:254-291) on config 2's seed-21
+    input against the reference's own output (tests/golden/sphere_c2.npz)."""
+    import json
+
+    from paper_2309_12543_b200 import scenarios as S
+
+    g = golden("sphere_c2")
+    shape = S.CONFIG2
+    robot = L.RobotModel.from_dict(json.loads(bytes(g["robot_json"]).decode()))
+    grid = L.EnvGrid(shape.grid_extent, shape.grid_res)
+    q = S.random_configs(shape.robot, shape.n_waypoints, seed=21)
+    pts = S.cloud_for(shape, 21).astype(np.float32)
+    assert np.array_equal(_digest(q), g["q_digest"]) and np.array_equal(_digest(pts), g["pts_digest"])
+    poses = L.forward_kinematics_batch(robot, L.ConfigBatch(q))
+    obs = L.voxelize_pointcloud(pts, grid)
+    spheres = L.SphereRobotModel.from_robot(robot)
+    d, st = L.sphere_baseline_distances(spheres, poses, obs, grid, return_stats=True)
+    assert st["distance_evals"] == int(g["evals"])
+    assert np.abs(d - g["d"]).max() <= 1e-12
