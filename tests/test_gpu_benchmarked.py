@@ -221,3 +221,42 @@ def test_sphere_baseline_vs_reference(L):
     d, st = L.sphere_baseline_distances(spheres, poses, obs, grid, return_stats=True)
     assert st["distance_evals"] == int(g["evals"])
     assert np.abs(d - g["d"]).max() <= 1e-12
+
+
+def test_replay_end_to_end(L, tmp_path):
+    """Config 5 replay (bench.py:410-430): manifest + f32 frame files -> one
+    cycle per frame (direct and materialized) -> the distance CSV.  Both CSVs
+    equal the one written from stream_min_distances on the same trajectory,
+    and every frame matches the oracle on every 25th waypoint."""
+    from oracle import linksdf_oracle as O
+    from paper_2309_12543_b200 import scenarios as S
+
+    shape = S.CONFIG5
+    robot, grid, sdfs, window = _setup(L, shape)
+    frames = S.moving_human_frames(12, shape.n_points, seed=5, dt=0.05)  # walks into range within the replay
+    q = S.smooth_trajectory(shape.robot, shape.n_waypoints, seed=5)
+    lines = []
+    for k, (stamp, pts) in enumerate(frames):
+        L.query.write_pointcloud_frame(tmp_path / f"f{k:03d}.bin", pts)
+        lines.append(f"{stamp} f{k:03d}.bin")
+    (tmp_path / "manifest.txt").write_text("# timestamp_ms frame\n" + "\n".join(lines) + "\n")
+    out_d = L.run_replay(robot, sdfs, grid, window, q, tmp_path / "manifest.txt", tmp_path / "direct.csv")
+    out_m = L.run_replay(robot, sdfs, grid, window, q, tmp_path / "manifest.txt", tmp_path / "mat.csv",
+                         materialized=True)
+    assert out_d["frames"] == 12 and out_d["waypoints"] == shape.n_waypoints and out_d["min_distance_m"] < 0.32
+    traj = L.TrajectorySdf.from_configs(robot, q, sdfs, grid, window)
+    rows = list(L.stream_min_distances(traj, L.query.iter_cloud_frames(tmp_path / "manifest.txt")))
+    L.query.write_distance_csv(tmp_path / "stream.csv", rows, len(q))
+    ref_csv = (tmp_path / "stream.csv").read_text()
+    assert (tmp_path / "direct.csv").read_text() == ref_csv
+    assert (tmp_path / "mat.csv").read_text() == ref_csv
+    assert out_m["min_distance_m"] == out_d["min_distance_m"]
+    grids = [s.values for s in sdfs]
+    sub = np.arange(0, shape.n_waypoints, 25)
+    near = 0
+    for (stamp, d), (_, pts) in zip(rows, frames):
+        rd, rl, _ = O.run_pipeline(shape.robot, q[sub], pts.astype(np.float32).astype(np.float64), shape.grid_extent,
+                                   shape.grid_res, shape.link_extent, grids, [shape.link_res] * len(grids))
+        assert np.abs(d[sub].astype(np.float64) - rd).max() <= D_TOL
+        near += int((rl >= 0).any())
+    assert near >= 3  # the human does come into range

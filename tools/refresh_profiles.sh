@@ -22,7 +22,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-fil
 python tools/scan_stats.py config2 config4 > $O/scan_stats.txt 2>&1
 echo done
 # secondary workloads (configs 3 and 5, materialized mode) for DESIGN §6
-python tools/bench_dynamic.py > $O/config5_dynamic.json 2> $O/config5_dynamic.err
+
 python tools/bench_vmajor.py --workload config2 > $O/vmajor_config2.json 2> $O/vmajor.err
 python tools/bench_vmajor.py --workload config5 > $O/vmajor_config5.json 2>> $O/vmajor.err
 python tools/bench_precompute.py > $O/config3_precompute.json 2> $O/config3_precompute.err
