@@ -351,6 +351,15 @@ int lsdf_query_dense(const float* values_dev, int64_t C, const lsdf_env_grid* en
                      const int32_t* indices_dev, int64_t N, float* d_dev,
                      int32_t* argmin_dev, void* stream);
 
+/* Appendix-B argmin on placed windows (any transform provider): windows
+ * (C, n_links, W^3) f32 x-fastest with anchors (C, n_links, 3); given the
+ * dense query's d and first-occurrence argmin over the index list, link =
+ * the lowest link whose window value at that voxel equals d, voxel = the
+ * argmin; both -1 when d is not below clamp = float32(d_far_global). */
+int lsdf_link_at_voxel(const float* windows_dev, const int32_t* anchors_dev, int64_t C, int32_t n_links,
+                       const int32_t W[3], const int32_t* indices_dev, const int32_t* argmin_dev,
+                       const float* d_dev, float clamp, int32_t* link_dev, int32_t* voxel_dev, void* stream);
+
 /* per_link_min_distances (query.py:153-176) over explicit fields: for field f
  * (config configs[f], link links[f], window values (W^3, x-fastest), anchor)
  * out[c * n_links + l] = min(out, d_far_f, window values at occupied voxels).

@@ -92,6 +92,7 @@ _SIGS = {
     "lsdf_per_link_fields": [_P, _P, _P, _P, _P, _I64, C.POINTER(_I32), _I32, C.POINTER(EnvGridT),
                              _P, _P, _P],
     "lsdf_fill": [_P, _I64, _F, _P],
+    "lsdf_link_at_voxel": [_P, _P, _I64, _I32, C.POINTER(_I32), _P, _P, _P, _F, _P, _P, _P],
     "lsdf_sphere_baseline": [_P, _P, _I64, _I32, _P, _P, _P, _I32, _P, _I64, C.POINTER(EnvGridT),
                              _P, _P],
     "lsdf_trilinear": [C.POINTER(LinkGridT), _P, _I64, _D, _P, _P],

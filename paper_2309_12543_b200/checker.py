@@ -35,6 +35,18 @@ from .query import TrajectorySdf, occupancy_workspace
 LINK_MAJOR_MIN = 6144
 
 
+def _require_exact(window_or_provider, who: str):
+    """The fused real-time cycle evaluates the exact transform; refuse another
+    provider loudly instead of silently using its window with exact values."""
+    from .placement import ExactTransformProvider, WindowGeometry
+
+    if isinstance(window_or_provider, (WindowGeometry, ExactTransformProvider)):
+        return
+    raise ValidationError(f"{who} runs the exact transform (placement.py:148-169) in its fused cycle; for "
+                          f"{type(window_or_provider).__name__} use TrajectorySdf.from_poses(..., provider) or "
+                          f"MaterializedChecker(..., provider)")
+
+
 class DistanceChecker:
     def __init__(self, robot, sdfs, grid, window, *, d_far_global=None, check_limits: bool = True):
         from .placement import _check_links
@@ -44,6 +56,7 @@ class DistanceChecker:
         if len(self.sdfs) != len(robot.geometry_links):
             raise ValidationError(f"{len(self.sdfs)} SDFs for {len(robot.geometry_links)} geometry links")
         self.grid = grid
+        _require_exact(window, "DistanceChecker")
         self.window = getattr(window, "window", window)
         _check_links(self.sdfs, self.window)
         self.d_far_global = float(min(s.d_far for s in self.sdfs) if d_far_global is None else d_far_global)
@@ -383,12 +396,26 @@ class MaterializedChecker:
     """
 
     def __init__(self, robot, sdfs, grid, window, configs, *, d_far_global=None):
-        from .query import TrajectorySdf
+        """``window``: a WindowGeometry / ExactTransformProvider (the voxel-major
+        field, one CUDA graph per cycle), or another TransformProvider such as
+        NeuralTransformProvider — the trajectory's windows are then placed with
+        that provider once (PlacedTrajectorySdf) and each cycle is the dense
+        gather + Appendix-B link (not graph-captured: the occupied count sizes
+        the gather)."""
+        from .placement import ExactTransformProvider, WindowGeometry, place_windows_device
+        from .query import PlacedTrajectorySdf, TrajectorySdf
 
         self.grid = grid
-        self.traj = TrajectorySdf.from_configs(robot, configs, sdfs, grid, getattr(window, "window", window),
-                                               d_far_global)
-        self.field = self.traj.materialize()
+        geom = getattr(window, "window", window)
+        self.traj = TrajectorySdf.from_configs(robot, configs, sdfs, grid, geom, d_far_global)
+        self.provider = None if isinstance(window, (WindowGeometry, ExactTransformProvider)) else window
+        if self.provider is None:
+            self.field = self.traj.materialize()
+        else:
+            R, dt, anchor = self.traj.config_major()
+            win = place_windows_device(self.traj.sdfs, R, dt, geom, self.provider)
+            self.field = PlacedTrajectorySdf(self.traj.sdfs, grid, geom, win, anchor, self.traj.d_far_global,
+                                             self.provider)
         self._graph = None
 
     def prepare(self, n_points: int, points_dtype=np.float32, use_graph: bool = True):
@@ -403,6 +430,8 @@ class MaterializedChecker:
         self.p_host = t.full((self._n, 3), float("nan"), dtype=tdt, **pin)
         self.out_host = {"d": t.zeros((C_,), dtype=t.float32, **pin), "link": t.zeros((C_,), dtype=t.int32, **pin),
                          "voxel": t.zeros((C_,), dtype=t.int32, **pin)}
+        if self.provider is not None:  # placed windows: an un-captured cycle (see __init__)
+            return self
         self._p_ptr = N.mapped_pointer(self.p_host)
         self._outs = {k: v for k, v in self.out_host.items()}
         self.occ = occupancy_workspace(self.grid)
@@ -449,6 +478,11 @@ class MaterializedChecker:
             host = self.p_host.numpy()
             host[: len(p)] = p
             host[len(p):] = np.nan
+        if self.provider is not None:
+            from .query import query_min_distances, voxelize_pointcloud
+
+            obs = voxelize_pointcloud(self.p_host.to("cuda", non_blocking=True), self.grid)
+            return query_min_distances(self.field, obs, return_argmin=True)
         if self._graph is not None:
             self._graph.replay()
         else:

@@ -138,6 +138,34 @@ __global__ void query_dense_kernel(const float* __restrict__ values, int64_t V, 
     }
 }
 
+// SURVEY Appendix B on placed windows: the argmin link is the lowest link
+// whose window value at the winning voxel equals d (d == clamp: -1 / -1).
+__global__ void link_at_voxel_kernel(const float* __restrict__ windows, const int32_t* __restrict__ anchors,
+                                     int64_t C, int32_t L, int32_t W0, int32_t W1, int32_t W2,
+                                     const int32_t* __restrict__ idx, const int32_t* __restrict__ argmin,
+                                     const float* __restrict__ d, float clamp, int32_t* link, int32_t* voxel) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const float dc = d[c];
+    if (!(dc < clamp)) {  // query.py:142-144 + the clamp rule
+        link[c] = -1;
+        voxel[c] = -1;
+        return;
+    }
+    const int32_t pos = argmin[c];
+    const int vx = idx[3 * pos], vy = idx[3 * pos + 1], vz = idx[3 * pos + 2];
+    const int64_t n = (int64_t)W0 * W1 * W2;
+    int best = -1;
+    for (int l = 0; l < L && best < 0; ++l) {
+        const int32_t* a = anchors + (c * L + l) * 3;
+        const int rx = vx - a[0], ry = vy - a[1], rz = vz - a[2];
+        if (rx < 0 || ry < 0 || rz < 0 || rx >= W0 || ry >= W1 || rz >= W2) continue;
+        if (windows[(c * L + l) * n + rx + (int64_t)W0 * (ry + (int64_t)W1 * rz)] == dc) best = l;
+    }
+    link[c] = best;
+    voxel[c] = pos;
+}
+
 __global__ void per_link_fields_kernel(const float* __restrict__ windows, const int32_t* anchors,
                                        const int32_t* configs, const int32_t* links, const float* d_far,
                                        int32_t W0, int32_t W1, int32_t W2, int32_t n_links, lsdf_env_grid env,
@@ -385,6 +413,17 @@ extern "C" int lsdf_query_dense(const float* values_dev, int64_t C, const lsdf_e
     query_dense_kernel<<<(unsigned)C, 256, 0, (cudaStream_t)stream>>>(values_dev, n_vox(*env), *env, indices_dev, N,
                                                                        d_dev, argmin_dev);
     return check_launch("query_dense_kernel");
+}
+
+extern "C" int lsdf_link_at_voxel(const float* windows_dev, const int32_t* anchors_dev, int64_t C, int32_t n_links,
+                                  const int32_t W[3], const int32_t* indices_dev, const int32_t* argmin_dev,
+                                  const float* d_dev, float clamp, int32_t* link_dev, int32_t* voxel_dev,
+                                  void* stream) {
+    if (C <= 0) return LSDF_OK;
+    link_at_voxel_kernel<<<grid_for(C, 128), 128, 0, (cudaStream_t)stream>>>(
+        windows_dev, anchors_dev, C, n_links, W[0], W[1], W[2], indices_dev, argmin_dev, d_dev, clamp, link_dev,
+        voxel_dev);
+    return check_launch("link_at_voxel_kernel");
 }
 
 extern "C" int lsdf_per_link_fields(const float* windows_dev, const int32_t* anchors_dev, const int32_t* configs_dev,

@@ -219,11 +219,20 @@ class TrajectorySdf:
         return len(self.sdfs)
 
     @classmethod
-    def from_poses(cls, sdfs, poses, grid: EnvGrid, provider, d_far_global=None) -> "TrajectorySdf":
-        """From geometry-link poses (LinkPoseBatch, C x L) — placement.py:289-295 alignment on GPU."""
-        from .errors import NoOverlapError
-        from .placement import _align_device
+    def from_poses(cls, sdfs, poses, grid: EnvGrid, provider, d_far_global=None):
+        """From geometry-link poses (LinkPoseBatch, C x L) — placement.py:289-295 alignment on GPU.
 
+        The fused direct kernel evaluates the exact transform (placement.py:148-169).
+        Any other provider (NeuralTransformProvider, or a custom one) returns a
+        :class:`PlacedTrajectorySdf` instead: the windows are placed with that
+        provider's coordinates (placement.py:300-313) and queried by the dense
+        gather, as the reference does with it.
+        """
+        from .errors import NoOverlapError
+        from .placement import ExactTransformProvider, _align_device
+
+        if not isinstance(provider, ExactTransformProvider):
+            return PlacedTrajectorySdf.from_poses(sdfs, poses, grid, provider, d_far_global)
         window = provider.window
         t = N.torch()
         C_, L = poses.n_configs, poses.n_links
@@ -321,6 +330,112 @@ class TrajectorySdf:
         """(C, L) per-link minima (query.py:153-176) from the same fused kernel."""
         occ, by_pos = obstacles.occupancy()
         return self.query_device(occ, by_pos, per_link=True)["per_link"].cpu().numpy()
+
+
+class PlacedTrajectorySdf:
+    """RobotSdfBatch-compatible trajectory whose windows come from any
+    TransformProvider (placement.py:213-220) — in practice the neural one.
+
+    The windows of every (waypoint, link) are placed on the GPU with the
+    provider's coordinates (NeuralTransformProvider: TinyMlp on the tensor
+    cores, then the fp64 shift and trilinear sampling), min-merged into the
+    dense (C, nx, ny, nz) batch (query.py:61-103) once, and every query is the
+    dense gather (query.py:128-150) plus the Appendix-B argmin link read off
+    the windows at the winning voxel.  The fused shell scan is not used here:
+    its culling bounds are proven for the exact transform only.
+    """
+
+    def __init__(self, sdfs, grid: EnvGrid, window, windows_dev, anchors_dev, d_far_global, provider=None,
+                 max_bytes: int = 1 << 36):
+        self.sdfs = list(sdfs)
+        self.grid = grid
+        self.window = window
+        self.provider = provider
+        self.windows = windows_dev      # (C, L, W^3) f32, x-fastest cells, masked = link d_far
+        self.anchors = anchors_dev      # (C, L, 3) i32
+        self.d_far_global = float(d_far_global)
+        C_, L = int(windows_dev.shape[0]), int(windows_dev.shape[1])
+        need = C_ * grid.n_voxels * 4
+        if need > max_bytes:
+            raise ValidationError(f"dense robot SDF batch needs {need / 2**20:.0f} MiB, "
+                                  f"over the {max_bytes / 2**20:.0f} MiB budget")
+        t = N.torch()
+        cfg = t.arange(C_, device=windows_dev.device, dtype=t.int32).repeat_interleave(L)
+        self._dense = N.empty((C_,) + tuple(int(d) for d in grid.dims), t.float32)
+        N.call("lsdf_assemble", N.ptr(windows_dev), N.ptr(anchors_dev), N.ptr(cfg), C_ * L, N.i32x3(window.dims),
+               ctypes.byref(grid.c_struct()), C_, self.d_far_global, N.ptr(self._dense), N.stream())
+
+    @classmethod
+    def from_poses(cls, sdfs, poses, grid: EnvGrid, provider, d_far_global=None) -> "PlacedTrajectorySdf":
+        from .errors import NoOverlapError
+        from .placement import _align_device, _check_links, place_windows_device
+
+        window = provider.window
+        _check_links(sdfs, window)
+        t = N.torch()
+        C_, L = poses.n_configs, poses.n_links
+        if len(sdfs) != L:
+            raise ValidationError(f"{len(sdfs)} SDFs for {L} links")
+        R = N.to_device(np.ascontiguousarray(poses.rotations, dtype=np.float64), t.float64)
+        T = N.to_device(np.ascontiguousarray(np.asarray(poses.translations, np.float64).reshape(-1, 3)), t.float64)
+        anchor, dt, flags = _align_device(T, grid, window.dims)
+        if int(flags[1].item()):
+            raise NoOverlapError(f"{int(flags[1].item())} window(s) miss the grid entirely")
+        win = place_windows_device(sdfs, R, dt.reshape(C_, L, 3), window, provider)
+        d_far = float(min(s.d_far for s in sdfs) if d_far_global is None else d_far_global)
+        return cls(sdfs, grid, window, win, anchor.reshape(C_, L, 3), d_far, provider)
+
+    @property
+    def n_configs(self) -> int:
+        return int(self.windows.shape[0])
+
+    @property
+    def n_links(self) -> int:
+        return len(self.sdfs)
+
+    def device_values(self):
+        return self._dense
+
+    @property
+    def values(self) -> np.ndarray:
+        v = self._dense.cpu().numpy()
+        v.flags.writeable = False
+        return v
+
+    def query_device(self, indices_dev, n_occupied: int, outputs=None):
+        """(d, link, voxel) CUDA tensors for a sorted index list (the reference's gather + Appendix B)."""
+        t = N.torch()
+        C_ = self.n_configs
+        out = outputs if outputs is not None else {}
+        if "d" not in out:
+            out["d"] = N.empty((C_,), t.float32)
+            out["link"] = N.empty((C_,), t.int32)
+            out["voxel"] = N.empty((C_,), t.int32)
+        if "argmin" not in out:
+            out["argmin"] = N.empty((C_,), t.int32)
+        N.call("lsdf_query_dense", N.ptr(self._dense), C_, ctypes.byref(self.grid.c_struct()), N.ptr(indices_dev),
+               int(n_occupied), N.ptr(out["d"]), N.ptr(out["argmin"]), N.stream())
+        N.call("lsdf_link_at_voxel", N.ptr(self.windows), N.ptr(self.anchors), C_, self.n_links,
+               N.i32x3(self.window.dims), N.ptr(indices_dev), N.ptr(out["argmin"]), N.ptr(out["d"]),
+               float(np.float32(self.d_far_global)), N.ptr(out["link"]), N.ptr(out["voxel"]), N.stream())
+        return out
+
+    def per_link_min_distances(self, obstacles: "ObstacleVoxelSet") -> np.ndarray:
+        """(C, L) per-link minima (query.py:153-176) over the placed windows."""
+        t = N.torch()
+        C_, L = self.n_configs, self.n_links
+        out = N.empty((C_, L), t.float32)
+        N.call("lsdf_fill", N.ptr(out), out.numel(), float(np.float32(self.d_far_global)), N.stream())
+        if obstacles.n_occupied == 0:
+            return out.cpu().numpy()
+        occ, _ = obstacles.occupancy()
+        cfg = t.arange(C_, device=out.device, dtype=t.int32).repeat_interleave(L)
+        lnk = t.arange(L, device=out.device, dtype=t.int32).repeat(C_)
+        dfar = t.tensor([float(np.float32(s.d_far)) for s in self.sdfs], dtype=t.float32, device=out.device).repeat(C_)
+        N.call("lsdf_per_link_fields", N.ptr(self.windows), N.ptr(self.anchors), N.ptr(cfg), N.ptr(lnk), N.ptr(dfar),
+               C_ * L, N.i32x3(self.window.dims), L, ctypes.byref(obstacles.grid.c_struct()), N.ptr(occ), N.ptr(out),
+               N.stream())
+        return out.cpu().numpy()
 
 
 class VoxelMajorSdf:
@@ -443,6 +558,9 @@ def query_min_distances(batch, obstacles: ObstacleVoxelSet, return_stats: bool =
     elif isinstance(batch, TrajectorySdf):
         occ, by_pos = obstacles.occupancy()
         out = batch.query_device(occ, by_pos)
+        d, link, voxel = (out["d"].cpu().numpy(), out["link"].cpu().numpy(), out["voxel"].cpu().numpy())
+    elif isinstance(batch, PlacedTrajectorySdf):
+        out = batch.query_device(obstacles.device_indices(), obstacles.n_occupied)
         d, link, voxel = (out["d"].cpu().numpy(), out["link"].cpu().numpy(), out["voxel"].cpu().numpy())
     elif isinstance(batch, VoxelMajorSdf):
         occ, _ = obstacles.occupancy()

@@ -260,3 +260,88 @@ def test_replay_end_to_end(L, tmp_path):
         assert np.abs(d[sub].astype(np.float64) - rd).max() <= D_TOL
         near += int((rl >= 0).any())
     assert near >= 3  # the human does come into range
+
+
+def _linear_mlp(L, window, hidden=32):
+    """A TinyMlp that IS the exact transform up to f32 rounding: units 0-8 / 9-17
+    carry relu(+R) / relu(-R) (TinyMlp.initial), W2 maps them through the canonical
+    points (y_vk = sum_j P_vj R_jk, approx.py:123-130 with placement.py:164)."""
+    P = window.masked_points  # (V, 3)
+    V = len(P)
+    m = L.TinyMlp.initial(V, hidden=hidden, seed=0)
+    w2 = np.zeros((hidden, 3 * V), np.float32)
+    for j in range(3):
+        for k in range(3):
+            w2[3 * j + k, k::3] = P[:, j]
+            w2[9 + 3 * j + k, k::3] = -P[:, j]
+    return L.TinyMlp(m.w1, m.b1, w2, m.b2)
+
+
+def test_neural_provider_honoured(L):
+    """TrajectorySdf.from_poses with a NeuralTransformProvider places the windows
+    with the MLP (no silent exact fallback): == the reference pipeline on the same
+    windows (place_links_batch -> assemble -> gather), Appendix-B link on those
+    windows, close to the oracle's neural pipeline and to the exact path; the
+    MaterializedChecker honours the provider; DistanceChecker refuses it."""
+    from oracle import linksdf_oracle as O
+    from paper_2309_12543_b200 import scenarios as S
+
+    shape = S.CONFIG2
+    robot, grid, sdfs, window = _setup(L, shape)
+    model = _linear_mlp(L, window)
+    prov = L.NeuralTransformProvider(model, window)
+    q = S.random_configs(shape.robot, 160, seed=8)
+    pts = S.cloud_for(shape, 8)[:50_000]
+    poses_all = L.forward_kinematics_batch(robot, L.ConfigBatch(q))
+    gl = robot.geometry_links
+    poses = L.LinkPoseBatch(rotations=poses_all.rotations[:, gl], translations=poses_all.translations[:, gl])
+    obs = L.voxelize_pointcloud(pts, grid)
+    traj = L.TrajectorySdf.from_poses(sdfs, poses, grid, prov)
+    assert isinstance(traj, L.PlacedTrajectorySdf)
+    d, link, voxel = L.query_min_distances(traj, obs, return_argmin=True)
+    fields = list(L.place_links_batch(sdfs, poses, grid, prov))
+    batch = L.assemble_robot_sdfs(((c, f) for c, _, f in fields), grid, len(q), traj.d_far_global)
+    d2, _, v2 = L.query_min_distances(batch, obs, return_argmin=True)
+    assert np.array_equal(d, d2) and np.array_equal(voxel, v2)
+    win = {(c, li): f for c, li, f in fields}
+    for c in range(len(q)):
+        if link[c] < 0:
+            continue
+        v = obs.indices[voxel[c]]
+        vals = []
+        for li in range(len(gl)):
+            rel = v - win[(c, li)].anchor
+            inside = np.all(rel >= 0) and np.all(rel < window.dims)
+            vals.append(win[(c, li)].values[tuple(rel)] if inside else np.inf)
+        assert vals[link[c]] == d[c] and all(x != d[c] for x in vals[:link[c]])
+    # the exact path (the model is the exact product up to f32 rounding)
+    exact = L.TrajectorySdf.from_poses(sdfs, poses, grid, L.ExactTransformProvider(window))
+    de = L.query_min_distances(exact, obs)
+    assert np.abs(d.astype(np.float64) - de).max() <= 1e-5
+    # the oracle's neural pipeline on a few configurations
+    sub = np.arange(0, len(q), 20)
+    e_r, r_r = shape.link_extent, shape.link_res
+    env = O.Env(shape.grid_extent, shape.grid_res)
+    anchors, dts, _ = O.align(poses.translations[sub].reshape(-1, 3), env, e_r)
+    mask = O.window_mask(e_r, env).ravel(order="F")
+    W = int(window.dims[0])
+    wins = np.empty((len(sub), len(gl), W ** 3), np.float32)
+    for i, c in enumerate(sub):
+        for li in range(len(gl)):
+            G = O.mlp_transform(model.w1, model.b1, model.w2, model.b2, poses.rotations[c, li],
+                                dts[i * len(gl) + li], e_r)
+            blk = np.full(W ** 3, np.float32(sdfs[li].d_far), np.float32)
+            blk[mask] = O.trilinear(sdfs[li].values, e_r, r_r, (G * e_r).reshape(-1, 3))
+            wins[i, li] = blk
+    wins = wins.reshape(len(sub), len(gl), W, W, W).transpose(0, 1, 4, 3, 2)
+    ob = O.assemble(wins, anchors.reshape(len(sub), len(gl), 3), env, traj.d_far_global)
+    rd = O.query_min(ob, obs.indices, traj.d_far_global)
+    assert np.abs(d[sub].astype(np.float64) - rd).max() <= 1e-5
+    # MaterializedChecker with the provider; DistanceChecker refuses it
+    mat = L.MaterializedChecker(robot, sdfs, grid, prov, q).prepare(len(pts), np.float32)
+    dm, lm, vm = mat.query(pts.astype(np.float32))
+    dn, ln, vn = L.query_min_distances(L.TrajectorySdf.from_poses(sdfs, poses, grid, prov),
+                                       L.voxelize_pointcloud(pts.astype(np.float32), grid), return_argmin=True)
+    assert np.array_equal(dm, dn) and np.array_equal(lm, ln) and np.array_equal(vm, vn)
+    with pytest.raises(L.ValidationError):
+        L.DistanceChecker(robot, sdfs, grid, prov)
