@@ -434,6 +434,35 @@ int lsdf_mlp_predict(const float* w1_dev, const float* b1_dev, const float* w2_d
                      const double* R_dev, int64_t B, float* y_dev, int64_t ldy,
                      int32_t use_tensor_cores, void* stream);
 
+/* ---- TinyMlp training (approx.py:212-289) ------------------------------ */
+
+/* Parameters and Adam state of one TinyMlp in device memory (f32, row-major:
+ * w1 (9, H), b1 (H), w2 (H, n_out), b2 (n_out)), the canonical points (V, 3)
+ * f32 with n_out = 3V, the optimiser constants and a device step counter
+ * (int64, 0 before the first step; the bias corrections use step + 1). */
+typedef struct {
+    float *w1, *b1, *w2, *b2;
+    float *m_w1, *m_b1, *m_w2, *m_b2;
+    float *v_w1, *v_b1, *v_w2, *v_b2;
+    const float* points;
+    int32_t hidden;
+    int64_t n_out;
+    float lr, beta1, beta2, eps;
+    int64_t* step;
+} lsdf_tmlp_train;
+
+/* One optimisation step on B rotations R (B, 3, 3) fp64: forward, exact f32
+ * targets P R, L1 gradients and the Adam update of every parameter with the
+ * reference's f32 operation order.  B even, <= 128; hidden a multiple of 4,
+ * <= 32.  workspace: lsdf_tmlp_train_workspace_bytes(B, H). */
+int64_t lsdf_tmlp_train_workspace_bytes(int32_t B, int32_t H);
+int lsdf_tmlp_train_step(const lsdf_tmlp_train* state, const double* R_dev, int32_t B, void* workspace_dev,
+                         void* stream);
+
+/* n uniform random rotations (fp64, the quaternion recipe of approx.py:32-47)
+ * from the device Philox stream `seed`, rotation i at subsequence offset + i. */
+int lsdf_sample_rotations(uint64_t seed, uint64_t offset, int64_t n, double* R_dev, void* stream);
+
 /* The tensor-core operand layout of W2 (H, n_out): bytes and fill. */
 int64_t lsdf_mlp_packed_bytes(int32_t H, int64_t n_out);
 int lsdf_mlp_pack(const float* w2_dev, int32_t H, int64_t n_out, float* packed_dev, void* stream);

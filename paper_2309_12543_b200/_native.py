@@ -44,6 +44,13 @@ class LinkGridT(C.Structure):
                 ("seg_a", C.c_float * 3), ("seg_u", C.c_float * 3)]
 
 
+class TmlpTrainT(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("w1", "b1", "w2", "b2", "m_w1", "m_b1", "m_w2", "m_b2",
+                                         "v_w1", "v_b1", "v_w2", "v_b2", "points")] + [
+        ("hidden", C.c_int32), ("n_out", C.c_int64), ("lr", C.c_float), ("beta1", C.c_float),
+        ("beta2", C.c_float), ("eps", C.c_float), ("step", C.c_void_p)]
+
+
 class WindowT(C.Structure):
     _fields_ = [("W", C.c_int32 * 3), ("n_masked", C.c_int32), ("e_r", C.c_double),
                 ("P_dev", C.c_void_p), ("Wmax", C.c_int32), ("pad_", C.c_int32),
@@ -105,6 +112,9 @@ _SIGS = {
     "lsdf_mlp_packed_bytes": [_I32, _I64],
     "lsdf_mlp_pack": [_P, _I32, _I64, _P, _P],
     "lsdf_host_device_pointer": [_P, C.POINTER(C.c_void_p)],
+    "lsdf_tmlp_train_workspace_bytes": [_I32, _I32],
+    "lsdf_tmlp_train_step": [C.POINTER(TmlpTrainT), _P, _I32, _P, _P],
+    "lsdf_sample_rotations": [C.c_uint64, C.c_uint64, _I64, _P, _P],
     "lsdf_l2_reserve": [C.c_size_t, C.POINTER(C.c_size_t)],
 }
 

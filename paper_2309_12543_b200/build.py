@@ -24,7 +24,7 @@ LIB = OUT_DIR / "liblinksdf_b200.so"
 INCLUDE = PKG.parent / "include"
 
 SOURCES = ["lsdf_capi.cu", "lsdf_fk.cu", "lsdf_voxel.cu", "lsdf_query.cu", "lsdf_dense.cu", "lsdf_build.cu",
-           "lsdf_mlp.cu", "lsdf_mlp_tc.cu", "lsdf_vmajor.cu"]
+           "lsdf_mlp.cu", "lsdf_mlp_tc.cu", "lsdf_vmajor.cu", "lsdf_train.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -48,6 +48,8 @@ def main():
     ap.add_argument("--rotations", type=int, default=3000)
     ap.add_argument("--chunk", type=int, default=1000, help="rotations per exact-transform launch (fp64 G)")
     ap.add_argument("--mlp-chunk", type=int, default=3000, help="rotations per MLP launch (f32 y)")
+    ap.add_argument("--train", action="store_true", help="train a W=128 model first and time that one")
+    ap.add_argument("--train-steps", type=int, default=40_000)
     args = ap.parse_args()
     import torch
 
@@ -119,9 +121,28 @@ def main():
 
     ms_exact = _time(torch, exact_all, reps=5)
     del G
-    model = L.TinyMlp.initial(V, hidden=32, seed=0)
-    model.w2 = np.random.default_rng(1).normal(0, 0.05, size=model.w2.shape).astype(np.float32)
-    model._dev = None
+    training = None
+    if args.train:
+        # a real W = 128 model, trained here on the GPU (lsdf_train.cu; rotations
+        # drawn on the device), used for the MLP timing and its accuracy check
+        cfg = L.TrainingConfig(steps=args.train_steps, device_rng=True, val_size=2000)
+        t0 = time.perf_counter()
+        try:
+            model = L.train_approximator(window.masked_points, cfg)
+            converged = True
+        except L.NotConvergedError as exc:
+            model, converged = exc.model, False
+        training = {"converged": converged, "steps": model.steps_run, "seconds": time.perf_counter() - t0,
+                    "val_max_abs_error": model.validation_max_error,
+                    "val_mean_abs_error": model.validation_mean_error, "target_max_error": cfg.target_max_error,
+                    "history_tail": model.history[-3:],
+                    "note": "TrainingConfig defaults (hidden 32, batch 64, lr 1e-4, L1 + Adam, stop at half the target "
+                            "on the validation set), device-drawn rotations; 2,000 validation rotations"}
+        out["training"] = training
+    else:
+        model = L.TinyMlp.initial(V, hidden=32, seed=0)
+        model.w2 = np.random.default_rng(1).normal(0, 0.05, size=model.w2.shape).astype(np.float32)
+        model._dev = None
     mch = args.mlp_chunk
     # rows at a 32-float stride (128-B aligned, the layout predict_device allocates)
     Y = torch.empty((mch, (3 * V + 31) // 32 * 32), dtype=torch.float32, device="cuda")[:, :3 * V]
@@ -144,6 +165,7 @@ def main():
         "mlp_tcgen05_write_GBps": B * V * 12 / (ms_tc / 1e3) / 1e9,
         "mlp_tcgen05_frac_hbm_write": B * V * 12 / (ms_tc / 1e3) / 1e9 / hbm,
         "tf32_dense_peak_TFLOPs": tf32_peak,
+        "weights": "trained W=128 model (see training)" if training else "random W2 (no trained model)",
         "note": "the MLP costs 32 MACs per output coordinate vs 3 for the exact product; with both writing G the "
                 "MLP is output-write bound (12 B/point f32) and the exact transform writes 24 B/point (fp64)",
     }
