@@ -279,7 +279,46 @@ class DistanceChecker:
             raise NoOverlapError(f"{int(f[1])} window(s) miss the grid entirely")
 
 
-class CheckerPipeline:
+class _CycleResults:
+    """Outcome bookkeeping shared by the pipelines: a recycled slot is drained
+    into ``_done`` (copies plus any flag error) and each ticket's result(),
+    including its error, is delivered by that ticket's own result() call."""
+
+    def _drain(self, s):
+        """Wait for the slot's cycle and keep its outcome (copies, and any limit /
+        no-overlap error) for its own result(ticket) call, so recycling the slot
+        neither raises an older cycle's error here nor drops its distances."""
+        s["ev"]["d2h"].synchronize()
+        d, link, voxel, flags = (a.numpy() for a in s["out"])
+        err = None
+        if flags[0] or flags[1]:
+            chk = s["chk"]
+            try:
+                chk._raise_flags(chk.host_inputs()[0], flags)
+            except Exception as exc:  # noqa: BLE001 — re-raised from result(ticket)
+                err = exc
+        self._done[s["ticket"]] = (d.copy(), link.copy(), voxel.copy(), err)
+        for old in [k for k in self._done if k < self._next - 4 * len(self.slots)]:
+            del self._done[old]
+        s["busy"] = False
+
+    def result(self, ticket: int):
+        """(d, link, voxel) numpy copies of a submitted cycle (blocks until it is
+        back on the host); raises that cycle's LimitViolationError /
+        NoOverlapError, if any."""
+        s = self._slot(ticket)
+        if s["ticket"] == ticket and s["busy"]:
+            self._drain(s)
+        if ticket not in self._done:
+            raise ValidationError(f"cycle {ticket} is no longer held (pipeline depth {self.depth})")
+        d, link, voxel, err = self._done.pop(ticket)
+        if err is not None:
+            raise err
+        return d, link, voxel
+
+
+
+class CheckerPipeline(_CycleResults):
     """Throughput form of DistanceChecker: ``depth`` cycles in flight.
 
     Each slot is a prepared DistanceChecker (its own device buffers and
@@ -315,7 +354,7 @@ class CheckerPipeline:
         self.compute = t.cuda.Stream()
         self.d2h = t.cuda.Stream()
         self._next = 0
-        self._done_upto = -1
+        self._done = {}  # ticket -> (d, link, voxel, error) of cycles drained before their result() call
 
     @property
     def depth(self) -> int:
@@ -328,7 +367,7 @@ class CheckerPipeline:
         """Pinned (configs, points) views of the next cycle's slot (waits if it is still in flight)."""
         s = self._slot(self._next)
         if s["busy"]:
-            self.result(s["ticket"])
+            self._drain(s)
         return s["chk"].host_inputs()
 
     def submit(self, configs=None, points=None) -> int:
@@ -337,7 +376,7 @@ class CheckerPipeline:
         ticket = self._next
         s = self._slot(ticket)
         if s["busy"]:
-            self.result(s["ticket"])
+            self._drain(s)
         chk = s["chk"]
         q_np, p_np = chk.host_inputs()
         if configs is not None:
@@ -369,21 +408,6 @@ class CheckerPipeline:
         s["busy"], s["ticket"] = True, ticket
         self._next += 1
         return ticket
-
-    def result(self, ticket: int):
-        """(d, link, voxel) numpy copies of a submitted cycle (blocks until it is back on the host)."""
-        s = self._slot(ticket)
-        if s["ticket"] != ticket:
-            raise ValidationError(f"cycle {ticket} is no longer held (pipeline depth {self.depth})")
-        s["ev"]["d2h"].synchronize()
-        d, link, voxel, flags = (a.numpy() for a in s["out"])
-        if s["busy"]:
-            s["busy"] = False
-            if flags[0] or flags[1]:
-                chk = s["chk"]
-                chk._raise_flags(chk.host_inputs()[0], flags)
-        return d.copy(), link.copy(), voxel.copy()
-
 
 class MaterializedChecker:
     """The paper's two-phase use for a FIXED trajectory:
@@ -491,7 +515,7 @@ class MaterializedChecker:
         return tuple(self.out_host[k].numpy().copy() for k in ("d", "link", "voxel"))
 
 
-class ShardedCloudPipeline:
+class ShardedCloudPipeline(_CycleResults):
     """CheckerPipeline for one rank of a multi-GPU throughput sweep whose cloud
     is shared: each rank uploads only ITS slice of the points (and of the
     waypoints), voxelizes the slice, and the ranks all-gather their partial
@@ -533,6 +557,7 @@ class ShardedCloudPipeline:
         self.compute = t.cuda.Stream()
         self.d2h = t.cuda.Stream()
         self._next = 0
+        self._done = {}
 
     @property
     def depth(self) -> int:
@@ -544,7 +569,7 @@ class ShardedCloudPipeline:
     def inputs(self):
         s = self._slot(self._next)
         if s["busy"]:
-            self.result(s["ticket"])
+            self._drain(s)
         return s["chk"].host_inputs()
 
     def _all_gather(self, out, inp):
@@ -560,7 +585,7 @@ class ShardedCloudPipeline:
         ticket = self._next
         s = self._slot(ticket)
         if s["busy"]:
-            self.result(s["ticket"])
+            self._drain(s)
         chk, ev = s["chk"], s["ev"]
         C_, P, pdt = chk._shape
         with t.cuda.stream(self.copy):
@@ -596,16 +621,3 @@ class ShardedCloudPipeline:
         s["busy"], s["ticket"] = True, ticket
         self._next += 1
         return ticket
-
-    def result(self, ticket: int):
-        s = self._slot(ticket)
-        if s["ticket"] != ticket:
-            raise ValidationError(f"cycle {ticket} is no longer held (pipeline depth {self.depth})")
-        s["ev"]["d2h"].synchronize()
-        d, link, voxel, flags = (a.numpy() for a in s["out"])
-        if s["busy"]:
-            s["busy"] = False
-            if flags[0] or flags[1]:
-                chk = s["chk"]
-                chk._raise_flags(chk.host_inputs()[0], flags)
-        return d.copy(), link.copy(), voxel.copy()

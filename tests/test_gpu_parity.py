@@ -310,6 +310,15 @@ def test_checker_pipeline(L, depth):
     q_bad[5, 2] = 9.0
     with pytest.raises(L.LimitViolationError):
         pipe.result(pipe.submit(q_bad, cycles[0][1]))
+    # a bad cycle whose slot is recycled before its result() call: the later
+    # submissions go through, its own result() raises, the others return
+    bad = pipe.submit(q_bad, cycles[0][1])
+    later = [pipe.submit(q, p) for q, p in cycles[1:1 + depth]]
+    for k, t in enumerate(later):
+        d1, l1, v1 = pipe.result(t)
+        assert np.array_equal(d1, want[k + 1][0]) and np.array_equal(l1, want[k + 1][1])
+    with pytest.raises(L.LimitViolationError):
+        pipe.result(bad)
 
 
 def test_known_answer_tie_clamp_empty(L):
