@@ -260,14 +260,20 @@ int scatter_bitmap(const void* points_dev, int32_t points_f32, int64_t N, const 
     // smaller CTAs, are slower even at 100k points), grid-stride over at most
     // two CTAs per SM so large clouds amortise the clear and merge
     const bool priv = o.n_words + n_cols <= PRIVATE_WORDS_MAX;
-    const unsigned threads = SCATTER_THREADS;
+    // small clouds: 256-thread CTAs, so every SM issues loads (zero-copy clouds
+    // come over PCIe: more SMs with reads in flight, config 2 host to host
+    // 56.6 -> 50.8 us); large clouds: 1024-thread CTAs amortise the private
+    // bitmap's clear and merge
+    static const int t_threads = [] { const char* v = getenv("LSDF_TUNE_VOXTHREADS"); return v && *v ? atoi(v) : 0; }();
+    const unsigned threads = t_threads > 0 ? (unsigned)t_threads
+                                           : (N >= 148LL * 2 * SCATTER_THREADS ? SCATTER_THREADS : 256u);
     // 4 points per thread (float4 loads) only when that still fills the GPU:
     // small clouds keep one point per thread (more CTAs in flight)
     static const int t_vec = [] { const char* v = getenv("LSDF_TUNE_VOXVEC"); return v && *v ? atoi(v) : -1; }();
     const bool want_vec = t_vec >= 0 ? t_vec != 0 : N >= 148LL * 2 * SCATTER_THREADS * 2;
     const int64_t per_thread = (want_vec && points_f32 && (((uintptr_t)points_dev) & 15) == 0) ? 4 : 1;
     const unsigned want = grid_for((N + per_thread - 1) / per_thread, threads);
-    const unsigned blocks = want < 148u * 2u ? want : 148u * 2u;
+    const unsigned blocks = want < 148u * 2u ? want : 148u * 2u;  // (more CTAs: more private-bitmap merges)
     const size_t smem = priv ? (size_t)(o.n_words + n_cols) * 4 : 0;
     if (points_f32) {
         if (priv)
