@@ -20,6 +20,7 @@ struct PlaceParams {
     lsdf_link_grid grids[LSDF_MAX_LINKS];
     const double* R;
     const double* dt;
+    int64_t C;
     int32_t n_geo;
     int32_t W[3];
     double e_r;
@@ -29,12 +30,18 @@ struct PlaceParams {
     float* out;
 };
 
+// Blocks run link-major (block b: link b / C, configuration b % C), so the
+// windows of one link sample its grid back to back while it sits in L2; with
+// the packed-corner grid a lookup is one 32-B sector instead of eight
+// scattered 4-B loads (trilinear_packed: the same arithmetic, bit-exact).
 __global__ void place_windows_kernel(const __grid_constant__ PlaceParams p) {
-    const int64_t f = blockIdx.x;  // field = c * n_geo + l
-    const int l = (int)(f % p.n_geo);
+    const int l = (int)(blockIdx.x / p.C);
+    const int64_t f = (int64_t)(blockIdx.x % p.C) * p.n_geo + l;  // field = c * n_geo + l
     const lsdf_link_grid& G = p.grids[l];
     const GridView gv = view_of(G);
     const LdgLoad ld{G.values_dev};
+    const bool packed = G.packed_dev != nullptr;
+    const PackedGrid pg = packed_of(G);
     double R[9], dtinv[3];
 #pragma unroll
     for (int e = 0; e < 9; ++e) R[e] = p.R[f * 9 + e];
@@ -42,16 +49,22 @@ __global__ void place_windows_kernel(const __grid_constant__ PlaceParams p) {
     const int W0 = p.W[0], W1 = p.W[1];
     const int n = W0 * W1 * p.W[2];
     float* dst = p.out + f * (int64_t)n;
-    for (int cell = threadIdx.x; cell < n; cell += blockDim.x) {
+    // warps walk the window's x rows (my, mz), lanes the cells of a row: two
+    // divisions per row instead of per cell
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int row = warp; row < W1 * p.W[2]; row += nw) {
+      const int my = row % W1, mz = row / W1;
+      for (int mx = lane; mx < W0; mx += 32) {
+        const int cell = mx + W0 * row;
         const bool keep = (__ldg(p.mask_bits + (cell >> 5)) >> (cell & 31)) & 1u;
         float v = gv.d_far;  // masked cells carry the link sentinel (placement.py:305-308)
         if (keep) {
-            const int mx = cell % W0, my = (cell / W0) % W1, mz = cell / (W0 * W1);
             double pt[3];
             window_point(p.P[mx], p.P[p.Wmax + my], p.P[2 * p.Wmax + mz], R, dtinv, p.e_r, pt);
-            v = trilinear_at(gv, pt[0], pt[1], pt[2], ld);
+            v = packed ? trilinear_packed(pg, pt[0], pt[1], pt[2]) : trilinear_at(gv, pt[0], pt[1], pt[2], ld);
         }
         dst[cell] = v;
+      }
     }
 }
 
@@ -60,11 +73,13 @@ __global__ void place_windows_kernel(const __grid_constant__ PlaceParams p) {
 // dtinv) * e_r (approx.py:302-305 then placement.py:300-313).
 __global__ void place_windows_g_kernel(const __grid_constant__ PlaceParams p, const float* __restrict__ y,
                                        int64_t ldy, const int32_t* __restrict__ kept, int32_t n_kept) {
-    const int64_t f = blockIdx.y;  // field = c * n_geo + l
-    const int l = (int)(f % p.n_geo);
+    const int l = (int)(blockIdx.y / p.C);  // link-major, as place_windows_kernel
+    const int64_t f = (int64_t)(blockIdx.y % p.C) * p.n_geo + l;  // field = c * n_geo + l
     const lsdf_link_grid& G = p.grids[l];
     const GridView gv = view_of(G);
     const LdgLoad ld{G.values_dev};
+    const bool packed = G.packed_dev != nullptr;
+    const PackedGrid pg = packed_of(G);
     double R[9], dtinv[3];
 #pragma unroll
     for (int e = 0; e < 9; ++e) R[e] = p.R[f * 9 + e];
@@ -80,7 +95,8 @@ __global__ void place_windows_g_kernel(const __grid_constant__ PlaceParams p, co
         const double gx = DADD((double)__ldg(yf + 3 * k), dtinv[0]);
         const double gy = DADD((double)__ldg(yf + 3 * k + 1), dtinv[1]);
         const double gz = DADD((double)__ldg(yf + 3 * k + 2), dtinv[2]);
-        dst[__ldg(kept + k)] = trilinear_at(gv, DMUL(gx, p.e_r), DMUL(gy, p.e_r), DMUL(gz, p.e_r), ld);
+        const double px = DMUL(gx, p.e_r), py = DMUL(gy, p.e_r), pz = DMUL(gz, p.e_r);
+        dst[__ldg(kept + k)] = packed ? trilinear_packed(pg, px, py, pz) : trilinear_at(gv, px, py, pz, ld);
     }
 }
 
@@ -352,6 +368,7 @@ extern "C" int lsdf_place_windows(const double* R_geo_dev, const double* dt_geo_
     for (int l = 0; l < n_geo; ++l) p.grids[l] = grids[l];
     p.R = R_geo_dev;
     p.dt = dt_geo_dev;
+    p.C = C;
     p.n_geo = n_geo;
     for (int a = 0; a < 3; ++a) p.W[a] = window->W[a];
     p.e_r = window->e_r;
@@ -377,6 +394,7 @@ extern "C" int lsdf_place_windows_g(const float* g_dev, int64_t ldg, const int32
     for (int l = 0; l < n_geo; ++l) p.grids[l] = grids[l];
     p.R = R_geo_dev;
     p.dt = dt_geo_dev;
+    p.C = C;
     p.n_geo = n_geo;
     for (int a = 0; a < 3; ++a) p.W[a] = window->W[a];
     p.e_r = window->e_r;

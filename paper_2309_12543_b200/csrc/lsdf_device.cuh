@@ -128,6 +128,22 @@ struct PackedGrid {
     float d_far;
 };
 
+__device__ __forceinline__ PackedGrid packed_of(const lsdf_link_grid& g) {
+    PackedGrid q;
+    q.cells = (const float4*)g.packed_dev;
+    for (int a = 0; a < 3; ++a) {
+        q.ext[a] = g.extent[a];
+        q.res[a] = g.resolution[a];
+        q.rinv[a] = 1.0 / g.resolution[a];  // RN(1/r): the Markstein reciprocal
+        q.hi[a] = (double)(g.dims[a] - 1);
+        q.top[a] = g.dims[a] - 2;
+    }
+    q.cx = g.dims[0] - 1;
+    q.cy = g.dims[1] - 1;
+    q.d_far = g.d_far;
+    return q;
+}
+
 // u = (p + e) / r - 0.5 with the division done as q0 = x*rinv, corrected by
 // one FMA residual step: with rinv = RN(1/r) this yields the correctly
 // rounded quotient (Markstein's theorem; also checked on 3.2e8 random

@@ -292,7 +292,7 @@ def place_windows_device(sdfs, R_dev, dt_dev, window: WindowGeometry, provider=N
     out = N.empty((C_, L, window.n_cells), t.float32)
     if provider is None or isinstance(provider, ExactTransformProvider):
         ws, _ = window.device_tables()
-        N.call("lsdf_place_windows", N.ptr(R_dev), N.ptr(dt_dev), C_, L, link_grid_table(sdfs),
+        N.call("lsdf_place_windows", N.ptr(R_dev), N.ptr(dt_dev), C_, L, link_grid_table(sdfs, packed=True),
                ctypes.byref(ws), N.ptr(out), N.stream())
         return out
     ws, dev = window.device_tables()
@@ -305,7 +305,7 @@ def place_windows_device(sdfs, R_dev, dt_dev, window: WindowGeometry, provider=N
         y = provider.model.predict_device(R_flat, use_tensor_cores=provider.use_tensor_cores)
         N.call("lsdf_place_windows_g", y, int(y.stride(0)), dev["kept_cells"], window.n_masked, N.ptr(R_dev),
                N.ptr(dt_dev), C_, L,
-               link_grid_table(sdfs), ctypes.byref(ws), out, N.stream())
+               link_grid_table(sdfs, packed=True), ctypes.byref(ws), out, N.stream())
         return out
     # generic provider: its coordinates (host), our sampler (placement.py:300-313)
     mask_f = t.from_numpy(window.mask.ravel(order="F")).to(out.device)

@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=1000, help="rotations per exact-transform launch (fp64 G)")
     ap.add_argument("--mlp-chunk", type=int, default=3000, help="rotations per MLP launch (f32 y)")
     ap.add_argument("--train", action="store_true", help="train a W=128 model first and time that one")
+    ap.add_argument("--placement", action="store_true", help="also time exact vs neural placement of 500 x 6 windows")
     ap.add_argument("--train-steps", type=int, default=40_000)
     args = ap.parse_args()
     import torch
@@ -169,6 +170,33 @@ def main():
         "note": "the MLP costs 32 MACs per output coordinate vs 3 for the exact product; with both writing G the "
                 "MLP is output-write bound (12 B/point f32) and the exact transform writes 24 B/point (fp64)",
     }
+    # (iv) placement of 500 waypoints x 6 links at this window (placement.py:267-313):
+    # exact transform vs the (trained) TinyMlp provider, windows on the device
+    if args.placement:
+        from paper_2309_12543_b200.placement import place_windows_device
+
+        del Y
+        torch.cuda.empty_cache()
+        sdfs = [L.build_link_sdf(robot.links[i].geometry, e_r, r_r, link_id=i) for i in robot.geometry_links]
+        q = S.random_configs(S.ARM6G, 500, seed=3)
+        poses = L.forward_kinematics_batch(robot, L.ConfigBatch(q))
+        gl = robot.geometry_links
+        Rg = torch.from_numpy(np.ascontiguousarray(poses.rotations[:, gl])).cuda()
+        Tg = torch.from_numpy(np.ascontiguousarray(poses.translations[:, gl]).reshape(-1, 3)).cuda()
+        from paper_2309_12543_b200.placement import _align_device
+
+        _, dtg, _ = _align_device(Tg, grid, window.dims)
+        dtg = dtg.reshape(500, len(gl), 3)
+        prov_n = L.NeuralTransformProvider(model, window)
+        ms_place_exact = _time(torch, lambda: place_windows_device(sdfs, Rg, dtg, window), reps=3, warm=1)
+        torch.cuda.empty_cache()
+        ms_place_neural = _time(torch, lambda: place_windows_device(sdfs, Rg, dtg, window, prov_n), reps=3, warm=1)
+        out["placement"] = {"waypoints": 500, "links": len(gl), "windows": 500 * len(gl),
+                            "cells_per_window": int(window.n_cells), "kept_per_window": V,
+                            "exact_ms": ms_place_exact, "neural_ms": ms_place_neural,
+                            "window_bytes_written": 500 * len(gl) * int(window.n_cells) * 4,
+                            "note": "neural = TinyMlp on tcgen05 writing G (f32) + provider-coordinate sampler reading "
+                                    "it back; exact = fused fp64 transform + sampler"}
     if args.cpu:
         from oracle import linksdf_oracle as O
 
