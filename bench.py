@@ -347,7 +347,7 @@ def run_ours(args, rank, world, dist, sampler):
     # live hardware counters of this very launch (ncu subprocess, one replayed
     # launch of the same workload; never timed): warp instructions and DRAM bytes
     counters = None
-    if rank == 0 and world == 1 and not args.no_counters:
+    if rank == 0 and not args.no_counters:  # (N > 1: rank 0's GPU, after the timed region)
         counters = live_counters(args.workload)
     clocks = sampler.summary(t0 - 0.2, t1 + 0.2) if sampler else None
     out = {
