@@ -449,6 +449,8 @@ typedef struct {
     int64_t n_out;
     float lr, beta1, beta2, eps;
     int64_t* step;
+    int64_t ld_w2;   /* row pitch (elements) of w2, m_w2, v_w2; 0 = n_out.  A multiple of 4 lets the
+                      * tensor-core step move its tiles with 16-B copies */
 } lsdf_tmlp_train;
 
 /* One optimisation step on B rotations R (B, 3, 3) fp64: forward, exact f32

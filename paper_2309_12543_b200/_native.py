@@ -48,7 +48,7 @@ class TmlpTrainT(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("w1", "b1", "w2", "b2", "m_w1", "m_b1", "m_w2", "m_b2",
                                          "v_w1", "v_b1", "v_w2", "v_b2", "points")] + [
         ("hidden", C.c_int32), ("n_out", C.c_int64), ("lr", C.c_float), ("beta1", C.c_float),
-        ("beta2", C.c_float), ("eps", C.c_float), ("step", C.c_void_p)]
+        ("beta2", C.c_float), ("eps", C.c_float), ("step", C.c_void_p), ("ld_w2", C.c_int64)]
 
 
 class WindowT(C.Structure):

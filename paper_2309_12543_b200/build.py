@@ -39,7 +39,7 @@ def _nvcc() -> str:
 
 def _digest() -> str:
     h = hashlib.sha256()
-    for name in SOURCES + ["lsdf_math.cuh", "lsdf_common.cuh", "lsdf_device.cuh", "lsdf_async.cuh"]:
+    for name in SOURCES + ["lsdf_math.cuh", "lsdf_common.cuh", "lsdf_device.cuh", "lsdf_async.cuh", "lsdf_tc.cuh"]:
         h.update((CSRC / name).read_bytes())
     h.update((INCLUDE / "linksdf_b200.h").read_bytes())
     h.update(" ".join(ARCH + FLAGS).encode())

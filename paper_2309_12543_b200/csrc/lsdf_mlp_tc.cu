@@ -25,6 +25,7 @@
 // 3xTF32 keeps ~fp32 accuracy, inside the 1e-5 (normalized) contract; the
 // CUDA-core kernel (lsdf_mlp.cu) stays the bit-reproducing path.
 #include "lsdf_async.cuh"
+#include "lsdf_tc.cuh"
 #include "lsdf_common.cuh"
 
 using namespace lsdf;
@@ -35,47 +36,8 @@ constexpr int TM = 128;   // output coordinates per tile (tcgen05 M)
 constexpr int TN = 256;   // rotations per tile (tcgen05 N)
 constexpr int KB_BYTES_A = TM * 128;  // one 32-wide k-block of A (W2^T): 128 rows x 128 B
 constexpr int KB_BYTES_B = TN * 128;  // one 32-wide k-block of B (h): 256 rows x 128 B
+constexpr uint32_t IDESC = idesc_tf32(TM, TN);
 
-
-// byte offset of element (row, k) inside a K-major, 128B-swizzled k-block
-__host__ __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t k) {
-    return row * 128u + ((((k >> 2) ^ (row & 7u)) & 7u) << 4) + ((k & 3u) << 2);
-}
-
-__device__ __forceinline__ float tf32_rna(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
-
-// tcgen05 shared-memory matrix descriptor: K-major, 128-byte swizzle,
-// 8-row groups 1024 B apart (SBO), version 1 (sm_100).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-
-// instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 256
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
-
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
 
 // W2 (H, N) row-major -> per output tile, per k-block: 128 rows (outputs) x
 // 128 B (32 hidden units), swizzled; hi and lo TF32 halves.
@@ -230,7 +192,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(const __grid_cons
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
                                 mma_tf32(d, sdesc(smem_u32(As[term] + b * KB_BYTES_A + kk * 32)),
-                                         sdesc(smem_u32(Bs[term] + b * KB_BYTES_B + kk * 32)), accumulate);
+                                         sdesc(smem_u32(Bs[term] + b * KB_BYTES_B + kk * 32)), IDESC, accumulate);
                                 accumulate = 1;
                             }
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(

@@ -19,8 +19,11 @@
 // the reference's quaternion formula approx.py:32-47) so nothing crosses PCIe
 // per step.
 #include <curand_kernel.h>
+#include <cstdlib>
 
+#include "lsdf_async.cuh"
 #include "lsdf_common.cuh"
+#include "lsdf_tc.cuh"
 
 using namespace lsdf;
 
@@ -92,6 +95,7 @@ __global__ void __launch_bounds__(THREADS) layer2_step_kernel(const __grid_const
     for (int i = threadIdx.x; i < B * 9; i += blockDim.x) s_x[i] = p.x[i];
     __syncthreads();
     const int64_t n_out = p.s.n_out;
+    const int64_t ldw = p.s.ld_w2 > 0 ? p.s.ld_w2 : n_out;  // row pitch of W2 and its moments
     // dy = sign / float32(dy.size) (approx.py:255-256): +-RN(1 / n) exactly, as a multiply
     const float inv_n = __fdiv_rn(1.0f, (float)(B * n_out));
     float bc1, bc2;
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(THREADS) layer2_step_kernel(const __grid_const
         const bool live = j < n_out;
         float w[MAXH];
 #pragma unroll
-        for (int k = 0; k < MAXH; ++k) w[k] = (live && k < H) ? p.s.w2[(int64_t)k * n_out + j] : 0.0f;
+        for (int k = 0; k < MAXH; ++k) w[k] = (live && k < H) ? p.s.w2[(int64_t)k * ldw + j] : 0.0f;
 #pragma unroll
         for (int k = 0; k < MAXH; ++k)
             if (k < H) s_w[k * LD + threadIdx.x] = w[k];
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(THREADS) layer2_step_kernel(const __grid_const
 #pragma unroll
             for (int k = 0; k < MAXH; ++k) {
                 if (k < H) {
-                    const int64_t o = (int64_t)k * n_out + j;
+                    const int64_t o = (int64_t)k * ldw + j;
                     float pw = w[k], m = p.s.m_w2[o], vv = p.s.v_w2[o];
                     adam(pw, m, vv, gw[k], lr, omb1, omb2, bc1, bc2, eps);
                     p.s.w2[o] = pw;
@@ -192,6 +196,265 @@ __global__ void __launch_bounds__(THREADS) layer2_step_kernel(const __grid_const
         __syncthreads();
     }
     for (int i = threadIdx.x; i < B * H; i += blockDim.x) atomicAdd(p.dh + i, s_dh[i]);
+}
+
+// ---------------------------------------------------------------- tcgen05 step
+// The same layer-2 step for B = 64 and H = 32 with the forward and the W2
+// gradient on the tensor cores (kind::tf32, 3xTF32 split: hi*hi + hi*lo +
+// lo*hi, ~fp32 accuracy), per 128-column tile of W2:
+//   GEMM1  y^T (128 x 64)   = W2^T tile (128 x 32) . h^T        -> TMEM cols [0, 64)
+//   epilogue: thread t owns column j (TMEM lane t): y + b2, targets, dy, db2;
+//             dy^T written as the next A operand (row t, K = batch)
+//   GEMM2  dW2^T (128 x 32) = dy^T (128 x 64) . h                -> TMEM cols [64, 96)
+//   epilogue: the column's Adam update (W2, m, v read and written once)
+//   dh += dy . W2_old^T for the tile on the CUDA cores (register tiles from
+//   shared memory), one atomic pass per CTA at the end.
+// All operands are K-major, 128-byte swizzled (the layout of lsdf_mlp_tc.cu).
+constexpr int TC_B = 64, TC_H = 32, TC_T = 128;
+constexpr uint32_t IDESC_FWD = idesc_tf32(TC_T, TC_B);
+constexpr uint32_t IDESC_GRAD = idesc_tf32(TC_T, TC_H);
+constexpr int SDY_LD = TC_B + 2;       // fp32 dy rows (8-B aligned pairs)
+constexpr int SW_LD = TC_T + 4;        // fp32 W2 tile rows
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+size_t tc_step_smem() {
+    return 1024 + 2 * (TC_T * 128) + 2 * (TC_B * 128) + 2 * (2 * TC_T * 128) + 2 * (2 * TC_H * 128) +
+           (size_t)TC_T * SDY_LD * 4 + 3 * (size_t)TC_H * SW_LD * 4 + (size_t)TC_B * 9 * 4 + TC_T * 4 + 64;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// 256 threads: thread (half, c) with c = threadIdx % 128 owns column j (TMEM
+// lane c; warps w and w + 4 read the same lane quarter) and half = threadIdx /
+// 128 the batch rows [32 half, +32) of the epilogue, the hidden units
+// [16 half, +16) of the Adam update and half of the dh register tiles.
+constexpr int TC_THREADS = 2 * TC_T;
+__global__ void __launch_bounds__(TC_THREADS, 1) layer2_tc_step_kernel(const __grid_constant__ TrainParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* A1 = sm;                         // [hi | lo] 128 rows x 128 B: W2^T tile (row c, k)
+    uint8_t* B1 = A1 + 2 * TC_T * 128;        // [hi | lo] 64 rows x 128 B: h (row b, k)
+    uint8_t* A2 = B1 + 2 * TC_B * 128;        // [hi | lo][2 k-blocks] 128 rows x 128 B: dy^T (row c, b)
+    uint8_t* B2 = A2 + 2 * 2 * TC_T * 128;    // [hi | lo][2 k-blocks] 32 rows x 128 B: h^T (row k, b)
+    float* sDY = (float*)(B2 + 2 * 2 * TC_H * 128);   // [c][SDY_LD] fp32 dy
+    float* sW = sDY + TC_T * SDY_LD;                  // [k][SW_LD] fp32 W2 tile (old values)
+    float* sM = sW + TC_H * SW_LD;                    // the tile's Adam moments, same layout
+    float* sV = sM + TC_H * SW_LD;
+    float* sX = sV + TC_H * SW_LD;                    // [b][9] f32 rotations
+    float* sGB = sX + TC_B * 9;                       // [128] db2 of the upper batch half
+    uint64_t* bar = (uint64_t*)(((uintptr_t)(sGB + TC_T) + 7) & ~(uintptr_t)7);
+    uint32_t* tmem_slot = (uint32_t*)(bar + 1);
+    const int tid = threadIdx.x, warp = tid >> 5, c = tid & (TC_T - 1), half = tid >> 7;
+    const int64_t N = p.s.n_out;
+    const int64_t ldw = p.s.ld_w2 > 0 ? p.s.ld_w2 : N;  // row pitch of W2 and its moments
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "r"(128));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    // h (B x H) into both operand layouts, x for the targets
+    for (int i = tid; i < TC_B * TC_H; i += blockDim.x) {
+        const int b = i / TC_H, k = i - b * TC_H;
+        const float h = p.h[i];
+        const float hh = tf32_rna(h), hl = tf32_rna(h - hh);
+        const uint32_t o1 = sw128_offset((uint32_t)b, (uint32_t)k);
+        *(float*)(B1 + o1) = hh;
+        *(float*)(B1 + TC_B * 128 + o1) = hl;
+        const uint32_t o2 = (uint32_t)(b >> 5) * (TC_H * 128) + sw128_offset((uint32_t)k, (uint32_t)(b & 31));
+        *(float*)(B2 + o2) = hh;
+        *(float*)(B2 + 2 * TC_H * 128 + o2) = hl;
+    }
+    for (int i = tid; i < TC_B * 9; i += blockDim.x) sX[i] = p.x[i];
+    fence_async_smem();
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    float bc1, bc2;
+    bias_corrections(p.s, bc1, bc2);
+    const float lr = p.s.lr, omb1 = __fsub_rn(1.0f, p.s.beta1), omb2 = __fsub_rn(1.0f, p.s.beta2), eps = p.s.eps;
+    const float inv_n = __fdiv_rn(1.0f, (float)(TC_B * N));
+    // dh register tile: b pair (lane), k quad (warp)
+    const int b0 = 2 * (tid & 31), k0 = 4 * warp;
+    float dh[2][4] = {};
+    uint32_t phase = 0;
+    const int kh = 16 * half;  // this thread's hidden units in the A1 build and the Adam update
+    const int bh = 32 * half;  // this thread's batch rows in the epilogue
+    const int64_t n_tiles = (N + TC_T - 1) / TC_T;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t j = tile * TC_T + c;
+        const bool live = j < N;
+        // the tile's W2, m and v rows (k, 128 columns) land in shared memory
+        // with asynchronous copies, all in flight at once: one memory round
+        // trip per tile, the moments' latency hidden behind the products
+        {
+            const int64_t j0 = tile * TC_T;
+            const int ncols = (int)(N - j0 < TC_T ? N - j0 : TC_T);
+            const bool vec = ncols == TC_T && ((ldw & 3) == 0);
+            for (int i = tid; i < TC_H * (TC_T / 4); i += blockDim.x) {
+                const int k = i / (TC_T / 4), c4 = (i - k * (TC_T / 4)) * 4;
+                const int64_t g = (int64_t)k * ldw + j0 + c4;
+                if (vec) {
+                    cp_async16(sW + k * SW_LD + c4, p.s.w2 + g);
+                    cp_async16(sM + k * SW_LD + c4, p.s.m_w2 + g);
+                    cp_async16(sV + k * SW_LD + c4, p.s.v_w2 + g);
+                } else {
+                    for (int e = 0; e < 4; ++e) {
+                        if (c4 + e < ncols) {
+                            cp_async4(sW + k * SW_LD + c4 + e, p.s.w2 + g + e);
+                            cp_async4(sM + k * SW_LD + c4 + e, p.s.m_w2 + g + e);
+                            cp_async4(sV + k * SW_LD + c4 + e, p.s.v_w2 + g + e);
+                        } else {
+                            sW[k * SW_LD + c4 + e] = 0.0f;
+                        }
+                    }
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            __syncthreads();
+        }
+        // A1 = W2^T tile split into TF32 halves (this thread: 16 hidden units of column c)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int k = kh + q;
+            const float wv = sW[k * SW_LD + c];
+            const float hi = tf32_rna(wv), lo = tf32_rna(wv - hi);
+            const uint32_t o = sw128_offset((uint32_t)c, (uint32_t)k);
+            *(float*)(A1 + o) = hi;
+            *(float*)(A1 + TC_T * 128 + o) = lo;
+        }
+        const float bj = live ? p.s.b2[j] : 0.0f;
+        fence_async_smem();
+        tc_before();
+        __syncthreads();
+        if (tid == 0) {  // GEMM1: y^T = W2^T h^T, 3xTF32
+            tc_after();
+            const uint8_t* As[3] = {A1, A1, A1 + TC_T * 128};
+            const uint8_t* Bs[3] = {B1, B1 + TC_B * 128, B1};
+            uint32_t acc = 0;
+#pragma unroll
+            for (int term = 0; term < 3; ++term)
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    mma_tf32(tmem, sdesc(smem_u32(As[term] + kk * 32)), sdesc(smem_u32(Bs[term] + kk * 32)), IDESC_FWD,
+                             acc);
+                    acc = 1;
+                }
+            tc_commit(bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        tc_after();
+        float y[32];
+        tmem_ld16(tmem + lane_base + (uint32_t)bh, y);
+        tmem_ld16(tmem + lane_base + (uint32_t)(bh + 16), y + 16);
+        // targets, dy, db2 for this thread's 32 batch rows; dy^T into the GEMM2
+        // operand (k-block = half) and the fp32 copy
+        const int64_t v = live ? j / 3 : 0;
+        const int kk3 = live ? (int)(j - v * 3) : 0;
+        const float P0 = live ? p.s.points[3 * v] : 0.f, P1 = live ? p.s.points[3 * v + 1] : 0.f,
+                    P2 = live ? p.s.points[3 * v + 2] : 0.f;
+        float gb = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            const int b = bh + q;
+            const float yb = __fadd_rn(y[q], bj);
+            const float* xb = sX + b * 9;
+            const float tg = __fmaf_rn(P2, xb[6 + kk3], __fmaf_rn(P1, xb[3 + kk3], __fmul_rn(P0, xb[kk3])));
+            const float sg = yb > tg ? 1.0f : (yb < tg ? -1.0f : 0.0f);
+            const float dy = live ? sg * inv_n : 0.0f;
+            gb = __fadd_rn(gb, dy);
+            const float hi = tf32_rna(dy), lo = tf32_rna(dy - hi);
+            const uint32_t o = (uint32_t)half * (TC_T * 128) + sw128_offset((uint32_t)c, (uint32_t)q);
+            *(float*)(A2 + o) = hi;
+            *(float*)(A2 + 2 * TC_T * 128 + o) = lo;
+            sDY[c * SDY_LD + b] = dy;
+        }
+        if (half) sGB[c] = gb;
+        fence_async_smem();
+        tc_before();
+        __syncthreads();
+        if (tid == 0) {  // GEMM2: dW2^T = dy^T h, 3xTF32, K = 64 in two k-blocks
+            tc_after();
+            const uint8_t* As[3] = {A2, A2, A2 + 2 * TC_T * 128};
+            const uint8_t* Bs[3] = {B2, B2 + 2 * TC_H * 128, B2};
+            uint32_t acc = 0;
+#pragma unroll
+            for (int term = 0; term < 3; ++term)
+#pragma unroll
+                for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        mma_tf32(tmem + TC_B, sdesc(smem_u32(As[term] + kb * TC_T * 128 + kk * 32)),
+                                 sdesc(smem_u32(Bs[term] + kb * TC_H * 128 + kk * 32)), IDESC_GRAD, acc);
+                        acc = 1;
+                    }
+            tc_commit(bar);
+        }
+        // dh += dy . W2_old^T over the tile (CUDA cores) while GEMM2 runs
+#pragma unroll 4
+        for (int tt = 0; tt < TC_T; ++tt) {
+            const float2 d2 = *(const float2*)(sDY + tt * SDY_LD + b0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float wv = sW[(k0 + q) * SW_LD + tt];
+                dh[0][q] = __fmaf_rn(d2.x, wv, dh[0][q]);
+                dh[1][q] = __fmaf_rn(d2.y, wv, dh[1][q]);
+            }
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        tc_after();
+        float g[16];
+        tmem_ld16(tmem + lane_base + (uint32_t)(TC_B + kh), g);
+        if (live) {  // Adam on this thread's 16 entries of column j (approx.py:262-268)
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int k = kh + q;
+                const int64_t o = (int64_t)k * ldw + j;
+                float pw = sW[k * SW_LD + c], m = sM[k * SW_LD + c], vv = sV[k * SW_LD + c];
+                adam(pw, m, vv, g[q], lr, omb1, omb2, bc1, bc2, eps);
+                p.s.w2[o] = pw;
+                p.s.m_w2[o] = m;
+                p.s.v_w2[o] = vv;
+            }
+            if (!half) {  // b2 with db2 summed over both batch halves (rows 0-31, then 32-63)
+                float pb = bj, m = p.s.m_b2[j], vv = p.s.v_b2[j];
+                adam(pb, m, vv, __fadd_rn(gb, sGB[c]), lr, omb1, omb2, bc1, bc2, eps);
+                p.s.b2[j] = pb;
+                p.s.m_b2[j] = m;
+                p.s.v_b2[j] = vv;
+            }
+        }
+        tc_before();
+        __syncthreads();  // the next tile rewrites the operands and the staged rows
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        atomicAdd(p.dh + b0 * TC_H + k0 + q, dh[0][q]);
+        atomicAdd(p.dh + (b0 + 1) * TC_H + k0 + q, dh[1][q]);
+    }
+    tc_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(128));
 }
 
 __global__ void layer1_update_kernel(const __grid_constant__ TrainParams p) {
@@ -270,6 +533,19 @@ extern "C" int lsdf_tmlp_train_step(const lsdf_tmlp_train* state, const double* 
     cudaStream_t s = (cudaStream_t)stream;
     layer1_kernel<<<1, 256, 0, s>>>(p);
     LSDF_TRY(check_launch("layer1_kernel"));
+    static const int t_tc = [] { const char* v = getenv("LSDF_TUNE_TRAINTC"); return v && *v ? atoi(v) : 1; }();
+    if (t_tc && B == TC_B && state->hidden == TC_H) {  // forward and dW2 on the tensor cores
+        const size_t smem_tc = tc_step_smem();
+        LSDF_TRY(ensure_smem((const void*)layer2_tc_step_kernel, smem_tc, "layer2_tc_step_kernel"));
+        int dev = 0, n_sm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t n_tiles = (state->n_out + TC_T - 1) / TC_T;
+        layer2_tc_step_kernel<<<(unsigned)(n_tiles < n_sm ? n_tiles : n_sm), TC_THREADS, smem_tc, s>>>(p);
+        LSDF_TRY(check_launch("layer2_tc_step_kernel"));
+        layer1_update_kernel<<<1, 256, 0, s>>>(p);
+        return check_launch("layer1_update_kernel");
+    }
     const size_t smem = step_smem(B, state->hidden);
     LSDF_TRY(ensure_smem((const void*)layer2_step_kernel, smem, "layer2_step_kernel"));
     int dev = 0, n_sm = 148, per_sm = 1;
