@@ -9,6 +9,8 @@
 // earlier link.  For the geometry links the thread also splits T into the
 // window anchor and residual.  Outputs are written link-major per config,
 // matching LinkPoseBatch (C, L, 3, 3).
+#include <cstdlib>
+
 #include "lsdf_device.cuh"
 
 using namespace lsdf;
@@ -51,7 +53,7 @@ __device__ __forceinline__ void fk_epilogue(const FkParams& p, bool counted) {
 }
 
 constexpr int FK_THREADS = 128;
-constexpr int64_t FK_SERIAL_MIN = 6144;  // measured crossover (tools/_fk_sweep.py): 12.5 vs 13.9 us at 4096, 16.7 vs 14.6 at 8192
+constexpr int64_t FK_SERIAL_MIN = 6144;  // measured crossover (round 1): 12.5 vs 13.9 us at 4096, 16.7 vs 14.6 at 8192
 #ifndef FK_STAGE_OUTPUTS
 #define FK_STAGE_OUTPUTS 1
 #endif  // configurations from which one thread per configuration wins
@@ -452,11 +454,12 @@ int fk_align_impl(const lsdf_link* links, int32_t n_links, int32_t n_geo, const 
     if (flags_self_reset && flags_dev == nullptr) return fail(LSDF_ERR_VALIDATION, "fk: self-resetting flags need a buffer");
     if (flags_dev != nullptr && !flags_self_reset)
         LSDF_TRY(check_cuda(cudaMemsetAsync(flags_dev, 0, 2 * sizeof(int32_t), (cudaStream_t)stream), "fk flags memset"));
-    if (C >= FK_SERIAL_MIN && link_major) {
+    static const int64_t serial_min = [] { const char* v = getenv("LSDF_TUNE_FKSERIAL"); return v && *v ? atoll(v) : FK_SERIAL_MIN; }();
+    if (C >= serial_min && link_major) {
         fk_align_serial_kernel<true, true><<<grid_for(C, FKS_THREADS), FKS_THREADS, 0, (cudaStream_t)stream>>>(p);
         return check_launch("fk_align_serial_kernel");
     }
-    if (C >= FK_SERIAL_MIN) {
+    if (C >= serial_min) {
         if (FK_STAGE_OUTPUTS) {
             const size_t smem_s = (size_t)FKS_THREADS * n_geo * (12 * sizeof(double) + 3 * sizeof(int32_t));
             LSDF_TRY(ensure_smem((const void*)fk_align_serial_kernel<true, false>, smem_s, "fk_align_serial_kernel"));
