@@ -484,13 +484,13 @@ def live_counters(workload: str, timeout: float = 240.0):
                       f"{workload} cycle (replayed under the profiler, caches flushed; counted, not timed)"}
 
 
-def run_realtime(args, L):
-    """Config 2: p50/p99 per 500-waypoint query (device graph and host-to-host)."""
+def run_realtime(args, L, workload: str = "config2"):
+    """Config 2 (or 1): p50/p99 per 500-waypoint query (device graph and host-to-host)."""
     import torch
 
     from paper_2309_12543_b200 import scenarios as S
 
-    shape = _shape("config2")
+    shape = _shape(workload)
     robot, chk = _checker(shape, shape.n_waypoints, L)
     inputs = [(S.random_configs(shape.robot, shape.n_waypoints, seed=s), _cloud(shape, s)) for s in (21, 22, 23, 24)]
     dev = [(torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda()) for q, p in inputs]
@@ -520,13 +520,15 @@ def run_realtime(args, L):
     torch.cuda.synchronize()
     n_occ = int(chk.ws[:4].view(torch.int32).item())
     pct = lambda a, p: float(np.percentile(np.asarray(a) * 1e3, p))  # noqa: E731  ms -> µs
-    sphere = sphere_comparison(torch, L, shape, inputs[0], flush)
-    return {"workload": f"{shape.name}: arm6g 500 waypoints vs 100k pts, 64^3, W=16", "occupied_voxels": n_occ,
+    sphere = sphere_comparison(torch, L, shape, inputs[0], flush) if workload == "config2" else None
+    grid_n = int(round(2 * shape.link_extent / shape.link_res))
+    return {"workload": f"{shape.name}: arm6g 500 waypoints vs {shape.n_points // 1000}k pts, {grid_n}^3, W=16",
+            "occupied_voxels": n_occ,
             "device_p50_us": pct(devt, 50), "device_p99_us": pct(devt, 99),
             "e2e_p50_us": pct(e2e, 50), "e2e_p99_us": pct(e2e, 99), "samples": n,
             "waypoint_queries_per_s_device": 500 / (statistics.mean(devt) / 1e3),
             "paper_gpu_ms_per_trajectory": 0.391,
-            "sphere_baseline": sphere}
+            **({"sphere_baseline": sphere} if sphere is not None else {})}
 
 
 # covering spheres of the arm6g links (tests/golden/make_golden_r2.py ARM6G_SPHERES)
@@ -851,6 +853,7 @@ def main():
         out = run_ours(args, rank, world, dist, sampler)
         if world == 1:
             out["realtime"] = run_realtime(args, L)
+            out["config1"] = run_realtime(args, L, "config1")
             out["dynamic"] = run_dynamic(L)
     finally:
         sampler.stop()
