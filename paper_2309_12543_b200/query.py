@@ -616,8 +616,18 @@ def query_trajectory(robot, configs, sdfs, grid: EnvGrid, provider_or_window, po
     ``link`` indexes the geometry links (``robot.geometry_links``); ``voxel``
     is the position in the sorted occupied-voxel list.
     """
+    from .placement import ExactTransformProvider, WindowGeometry
+
     window = getattr(provider_or_window, "window", provider_or_window)
-    traj = TrajectorySdf.from_configs(robot, configs, sdfs, grid, window, d_far_global)
+    if isinstance(provider_or_window, (WindowGeometry, ExactTransformProvider)):
+        traj = TrajectorySdf.from_configs(robot, configs, sdfs, grid, window, d_far_global)
+    else:  # another provider (neural): its placement, never silently the exact transform
+        from .robot import ConfigBatch, LinkPoseBatch, forward_kinematics_batch
+
+        poses = forward_kinematics_batch(robot, configs if isinstance(configs, ConfigBatch) else ConfigBatch(configs))
+        gl = robot.geometry_links
+        geo = LinkPoseBatch(rotations=poses.rotations[:, gl], translations=poses.translations[:, gl])
+        traj = PlacedTrajectorySdf.from_poses(sdfs, geo, grid, provider_or_window, d_far_global)
     obs = obstacles if obstacles is not None else voxelize_pointcloud(points, grid)
     return query_min_distances(traj, obs, return_argmin=True)
 

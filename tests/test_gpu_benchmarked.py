@@ -345,3 +345,6 @@ def test_neural_provider_honoured(L):
     assert np.array_equal(dm, dn) and np.array_equal(lm, ln) and np.array_equal(vm, vn)
     with pytest.raises(L.ValidationError):
         L.DistanceChecker(robot, sdfs, grid, prov)
+    # query_trajectory with the provider: the same placed-window path
+    d3, l3, v3 = L.query_trajectory(robot, q, sdfs, grid, prov, pts)
+    assert np.array_equal(d3, d) and np.array_equal(l3, link) and np.array_equal(v3, voxel)

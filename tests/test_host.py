@@ -205,3 +205,42 @@ def test_link_major_threshold_matches_fk_crossover():
 
     assert f"#define LSDF_QUERY_BY_POSITION {N.QUERY_BY_POSITION}" in header
     assert f"#define LSDF_QUERY_POSES_LINK_MAJOR {N.QUERY_POSES_LINK_MAJOR}" in header
+
+
+def test_exact_only_checker_refuses_other_providers():
+    """DistanceChecker runs the exact transform in its fused cycle: a neural (or any
+    other) provider is refused before any GPU work, never silently replaced."""
+    import paper_2309_12543_b200 as L
+    from paper_2309_12543_b200 import scenarios as S
+
+    robot = L.RobotModel.from_dict(S.ARM6G)
+    grid = L.EnvGrid(1.0, 0.04)
+    window = L.WindowGeometry.build(0.32, grid)
+    model = L.TinyMlp.initial(window.n_masked, hidden=32)
+    prov = L.NeuralTransformProvider(model, window)
+    ax = -0.32 + (np.arange(16) + 0.5) * 0.04
+    X, Y, Z = np.meshgrid(ax, ax, ax, indexing="ij")
+    sdfs = [L.LinkSdf(0.32, 0.04, np.sqrt(X * X + Y * Y + Z * Z) - 0.05, link_id=i) for i in robot.geometry_links]
+    with pytest.raises(L.ValidationError, match="exact transform"):
+        L.DistanceChecker(robot, sdfs, grid, prov)
+    L.checker._require_exact(window, "x")
+    L.checker._require_exact(L.ExactTransformProvider(window), "x")
+
+
+def test_replay_frame_reader(tmp_path):
+    """run_replay's reader: a frame's f32 points straight into a (cap, 3) buffer, NaN past them."""
+    from paper_2309_12543_b200 import query as Q
+    from paper_2309_12543_b200 import replay as R
+    from paper_2309_12543_b200.errors import ValidationError
+
+    pts = np.float64([[0.1, -0.2, 0.3], [1.5, 2.5, -3.5], [0.0, 0.0, 1e-3]])
+    f = tmp_path / "f.bin"
+    Q.write_pointcloud_frame(f, pts)
+    buf = np.zeros((5, 3), np.float32)
+    assert R.frame_point_count(f) == 3 and R.read_frame_into(f, buf) == 3
+    assert np.array_equal(buf[:3], pts.astype(np.float32)) and np.all(np.isnan(buf[3:]))
+    with pytest.raises(ValidationError):
+        R.read_frame_into(f, np.zeros((2, 3), np.float32))
+    f.write_bytes(f.read_bytes()[:-4])
+    with pytest.raises(ValidationError):
+        R.read_frame_into(f, buf)
