@@ -466,6 +466,21 @@ int lsdf_tmlp_train_step(const lsdf_tmlp_train* state, const double* R_dev, int3
 int lsdf_sample_rotations(uint64_t seed, uint64_t offset, int64_t n, double* R_dev, void* stream);
 
 /* The tensor-core operand layout of W2 (H, n_out): bytes and fill. */
+/* place_links_batch with the NeuralTransformProvider fused into one kernel
+ * (placement.py:300-313 fed by approx.py:292-306): TinyMlp layer 2 runs on
+ * the tensor cores (3xTF32, as lsdf_mlp_predict with use_tensor_cores) per
+ * block of 128 kept cells x 128 rotations and its epilogue samples the link
+ * grids directly, so the (C*n_geo, 3*n_points) coordinate matrix never
+ * reaches HBM.  Same arguments and output as lsdf_mlp_predict followed by
+ * lsdf_place_windows_g; grids must carry packed_dev; hidden <= 32.
+ * w2_place_packed_dev = lsdf_mlp_place_pack(W2) (lsdf_mlp_place_packed_bytes). */
+int64_t lsdf_mlp_place_packed_bytes(int32_t H, int64_t n_points);
+int lsdf_mlp_place_pack(const float* w2_dev, int32_t H, int64_t n_points, float* packed_dev, void* stream);
+int lsdf_mlp_place(const float* w1_dev, const float* b1_dev, const float* w2_place_packed_dev,
+                   const float* b2_dev, int32_t H, int64_t n_points, const int32_t* kept_cells_dev,
+                   const double* R_geo_dev, const double* dt_geo_dev, int64_t C, int32_t n_geo,
+                   const lsdf_link_grid* grids, const lsdf_window* window, float* windows_dev,
+                   void* stream);
 int64_t lsdf_mlp_packed_bytes(int32_t H, int64_t n_out);
 int lsdf_mlp_pack(const float* w2_dev, int32_t H, int64_t n_out, float* packed_dev, void* stream);
 

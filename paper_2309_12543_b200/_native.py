@@ -111,6 +111,10 @@ _SIGS = {
     "lsdf_mlp_predict": [_P, _P, _P, _P, _P, _I32, _I64, _P, _I64, _P, _I64, _I32, _P],
     "lsdf_mlp_packed_bytes": [_I32, _I64],
     "lsdf_mlp_pack": [_P, _I32, _I64, _P, _P],
+    "lsdf_mlp_place_packed_bytes": [_I32, _I64],
+    "lsdf_mlp_place_pack": [_P, _I32, _I64, _P, _P],
+    "lsdf_mlp_place": [_P, _P, _P, _P, _I32, _I64, _P, _P, _P, _I64, _I32, C.POINTER(LinkGridT), C.POINTER(WindowT),
+                       _P, _P],
     "lsdf_host_device_pointer": [_P, C.POINTER(C.c_void_p)],
     "lsdf_tmlp_train_workspace_bytes": [_I32, _I32],
     "lsdf_tmlp_train_step": [C.POINTER(TmlpTrainT), _P, _I32, _P, _P],

@@ -88,8 +88,7 @@ __global__ void place_windows_g_kernel(const __grid_constant__ PlaceParams p, co
     float* dst = p.out + f * (int64_t)n;
     const int stride = gridDim.x * blockDim.x;
     const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
-    for (int cell = i0; cell < n; cell += stride)  // masked cells: the link sentinel
-        if (!((__ldg(p.mask_bits + (cell >> 5)) >> (cell & 31)) & 1u)) dst[cell] = gv.d_far;
+    fill_masked_cells(p.mask_bits, n, dst, gv.d_far, i0, stride);  // masked cells: the link sentinel
     const float* yf = y + f * ldy;
     for (int k = i0; k < n_kept; k += stride) {
         const double gx = DADD((double)__ldg(yf + 3 * k), dtinv[0]);

@@ -128,7 +128,7 @@ struct PackedGrid {
     float d_far;
 };
 
-__device__ __forceinline__ PackedGrid packed_of(const lsdf_link_grid& g) {
+__host__ __device__ __forceinline__ PackedGrid packed_of(const lsdf_link_grid& g) {
     PackedGrid q;
     q.cells = (const float4*)g.packed_dev;
     for (int a = 0; a < 3; ++a) {
@@ -230,6 +230,64 @@ __device__ __forceinline__ float trilinear_packed(const PackedGrid& g, double px
     const int64_t cell = ix + (int64_t)g.cx * (iy + (int64_t)g.cy * iz);
     const float4 a = __ldg(g.cells + 2 * cell);      // v000 v100 v010 v110
     const float4 b = __ldg(g.cells + 2 * cell + 1);  // v001 v101 v011 v111
+    const float c00 = __fadd_rn(__fmul_rn(a.x, gx), __fmul_rn(a.y, fx));
+    const float c10 = __fadd_rn(__fmul_rn(a.z, gx), __fmul_rn(a.w, fx));
+    const float c01 = __fadd_rn(__fmul_rn(b.x, gx), __fmul_rn(b.y, fx));
+    const float c11 = __fadd_rn(__fmul_rn(b.z, gx), __fmul_rn(b.w, fx));
+    const float c0 = __fadd_rn(__fmul_rn(c00, gy), __fmul_rn(c10, fy));
+    const float c1 = __fadd_rn(__fmul_rn(c01, gy), __fmul_rn(c11, fy));
+    return __fadd_rn(__fmul_rn(c0, gz), __fmul_rn(c1, fz));
+}
+
+// dst[cell] = v for every cell of an n-cell window whose keep bit is clear
+// (the masked cells carry the link sentinel, placement.py:305-308).  Threads
+// take 4 cells each (one nibble of the mask) and write a float4 when all four
+// are masked; i0 / stride enumerate the calling threads.
+__device__ __forceinline__ void fill_masked_cells(const uint32_t* __restrict__ mask_bits, int64_t n, float* dst,
+                                                  float v, int64_t i0, int64_t stride) {
+    if ((n & 3) == 0 && ((uintptr_t)dst & 15) == 0) {
+        const float4 v4 = make_float4(v, v, v, v);
+        for (int64_t g = i0; g < (n >> 2); g += stride) {
+            const int64_t cell = g << 2;
+            const uint32_t nib = (__ldg(mask_bits + (cell >> 5)) >> (cell & 31)) & 0xFu;
+            if (nib == 0u) {
+                __stcs((float4*)(dst + cell), v4);
+            } else if (nib != 0xFu) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (!((nib >> k) & 1u)) __stcs(dst + cell + k, v);
+            }
+        }
+        return;
+    }
+    for (int64_t cell = i0; cell < n; cell += stride)
+        if (!((__ldg(mask_bits + (cell >> 5)) >> (cell & 31)) & 1u)) dst[cell] = v;
+}
+
+// trilinear_packed in two stages, so a caller can issue several lookups'
+// loads back to back (the same operations, bit-identical): packed_prep
+// returns the cell (-1 outside the grid) and the f32 fractions.
+__device__ __forceinline__ int64_t packed_prep(const PackedGrid& g, double px, double py, double pz, float& fx,
+                                               float& fy, float& fz) {
+    const double ux = cell_coord(px, g.ext[0], g.res[0], g.rinv[0]);
+    const double uy = cell_coord(py, g.ext[1], g.res[1], g.rinv[1]);
+    const double uz = cell_coord(pz, g.ext[2], g.res[2], g.rinv[2]);
+    const bool inside = (ux >= 0.0) && (ux <= g.hi[0]) && (uy >= 0.0) && (uy <= g.hi[1]) && (uz >= 0.0) &&
+                        (uz <= g.hi[2]);
+    if (!inside) return -1;
+    double fx0, fy0, fz0;
+    int ix = floor_small(ux, fx0), iy = floor_small(uy, fy0), iz = floor_small(uz, fz0);
+    if (ix > g.top[0]) { ix = g.top[0]; fx0 = (double)g.top[0]; }
+    if (iy > g.top[1]) { iy = g.top[1]; fy0 = (double)g.top[1]; }
+    if (iz > g.top[2]) { iz = g.top[2]; fz0 = (double)g.top[2]; }
+    fx = __double2float_rn(__dsub_rn(ux, fx0));
+    fy = __double2float_rn(__dsub_rn(uy, fy0));
+    fz = __double2float_rn(__dsub_rn(uz, fz0));
+    return ix + (int64_t)g.cx * (iy + (int64_t)g.cy * iz);
+}
+
+__device__ __forceinline__ float packed_finish(float4 a, float4 b, float fx, float fy, float fz) {
+    const float gx = __fsub_rn(1.0f, fx), gy = __fsub_rn(1.0f, fy), gz = __fsub_rn(1.0f, fz);
     const float c00 = __fadd_rn(__fmul_rn(a.x, gx), __fmul_rn(a.y, fx));
     const float c10 = __fadd_rn(__fmul_rn(a.z, gx), __fmul_rn(a.w, fx));
     const float c01 = __fadd_rn(__fmul_rn(b.x, gx), __fmul_rn(b.y, fx));

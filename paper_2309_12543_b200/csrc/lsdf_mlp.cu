@@ -56,6 +56,35 @@ int lsdf_mlp_predict_tc(const float* w1, const float* b1, const float* w2, const
 int64_t lsdf_mlp_packed_bytes_tc(int32_t H, int64_t n_out);
 int lsdf_mlp_pack_tc(const float* w2, int32_t H, int64_t n_out, float* packed, cudaStream_t s);
 
+int64_t lsdf_mlp_cells_packed_bytes(int32_t H, int64_t V);
+int lsdf_mlp_pack_cells(const float* w2, int32_t H, int64_t V, float* packed, cudaStream_t s);
+int lsdf_mlp_place_tc(const float* w1, const float* b1, const float* w2_cells_packed, const float* b2, int32_t H,
+                      int64_t V, const int32_t* kept_cells, const double* R, const double* dt, int64_t C, int32_t L,
+                      const lsdf_link_grid* grids, const lsdf_window* window, float* out, cudaStream_t s);
+
+extern "C" int64_t lsdf_mlp_place_packed_bytes(int32_t H, int64_t n_points) {
+    return lsdf_mlp_cells_packed_bytes(H, n_points);
+}
+
+extern "C" int lsdf_mlp_place_pack(const float* w2_dev, int32_t H, int64_t n_points, float* packed_dev, void* stream) {
+    if (H < 1 || H > 32) return fail(LSDF_ERR_UNSUPPORTED, "fused TinyMlp placement: hidden width %d outside 1..32", H);
+    if (n_points <= 0) return LSDF_OK;
+    return lsdf_mlp_pack_cells(w2_dev, H, n_points, packed_dev, (cudaStream_t)stream);
+}
+
+extern "C" int lsdf_mlp_place(const float* w1_dev, const float* b1_dev, const float* w2_place_packed_dev,
+                              const float* b2_dev, int32_t H, int64_t n_points, const int32_t* kept_cells_dev,
+                              const double* R_geo_dev, const double* dt_geo_dev, int64_t C, int32_t n_geo,
+                              const lsdf_link_grid* grids, const lsdf_window* window, float* windows_dev,
+                              void* stream) {
+    if (H < 1 || H > 32) return fail(LSDF_ERR_UNSUPPORTED, "fused TinyMlp placement: hidden width %d outside 1..32", H);
+    if (w2_place_packed_dev == nullptr) return fail(LSDF_ERR_VALIDATION, "fused placement: W2 not packed");
+    if (C <= 0) return LSDF_OK;
+    if (C * n_geo > 65535) return fail(LSDF_ERR_UNSUPPORTED, "fused placement: more than 65535 windows per call");
+    return lsdf_mlp_place_tc(w1_dev, b1_dev, w2_place_packed_dev, b2_dev, H, n_points, kept_cells_dev, R_geo_dev,
+                             dt_geo_dev, C, n_geo, grids, window, windows_dev, (cudaStream_t)stream);
+}
+
 extern "C" int64_t lsdf_mlp_packed_bytes(int32_t H, int64_t n_out) { return lsdf_mlp_packed_bytes_tc(H, n_out); }
 
 extern "C" int lsdf_mlp_pack(const float* w2_dev, int32_t H, int64_t n_out, float* packed_dev, void* stream) {

@@ -301,6 +301,13 @@ def place_windows_device(sdfs, R_dev, dt_dev, window: WindowGeometry, provider=N
     if isinstance(provider, NeuralTransformProvider):
         # the neural provider stays on the device: TinyMlp on the tensor cores
         # (or the CUDA-core sgemm replica), then the provider-coordinate sampler
+        if provider.fused:
+            m = provider.model
+            w1, b1, _, b2 = m.device_weights()
+            N.call("lsdf_mlp_place", w1, b1, m.packed_w2_cells(), b2, m.hidden, m.n_points, dev["kept_cells"],
+                   N.ptr(R_dev), N.ptr(dt_dev), C_, L, link_grid_table(sdfs, packed=True), ctypes.byref(ws), out,
+                   N.stream())
+            return out
         R_flat = R_dev.reshape(C_ * L, 9)
         y = provider.model.predict_device(R_flat, use_tensor_cores=provider.use_tensor_cores)
         N.call("lsdf_place_windows_g", y, int(y.stride(0)), dev["kept_cells"], window.n_masked, N.ptr(R_dev),

@@ -348,3 +348,40 @@ def test_neural_provider_honoured(L):
     # query_trajectory with the provider: the same placed-window path
     d3, l3, v3 = L.query_trajectory(robot, q, sdfs, grid, prov, pts)
     assert np.array_equal(d3, d) and np.array_equal(l3, link) and np.array_equal(v3, voxel)
+
+
+@pytest.mark.parametrize("n_cfg", [1, 37, 300])
+def test_fused_neural_placement_matches_two_kernels(L, n_cfg):
+    """lsdf_mlp_place (TinyMlp layer 2 on tcgen05 + trilinear epilogue, no G
+    in HBM) == lsdf_mlp_predict(use_tensor_cores) -> lsdf_place_windows_g on
+    the config-2 window (4.8k kept cells = 38 cell blocks), bit for bit: the
+    same 3xTF32 MMA chain per output, the same f32 bias add and fp64 sampler.
+    Rotation counts cover a partial tile, a tile spanning links and several tiles."""
+    from paper_2309_12543_b200 import placement as P
+    from paper_2309_12543_b200 import scenarios as S
+    import paper_2309_12543_b200._native as N
+
+    shape = S.CONFIG2
+    robot, grid, sdfs, window = _setup(L, shape)
+    rng = np.random.default_rng(n_cfg)
+    H = 32
+    model = L.TinyMlp(rng.normal(0, 0.5, (9, H)).astype(np.float32), rng.normal(0, 0.1, H).astype(np.float32),
+                      rng.normal(0, 0.05, (H, 3 * window.n_masked)).astype(np.float32),
+                      rng.normal(0, 0.2, 3 * window.n_masked).astype(np.float32))
+    q = S.random_configs(shape.robot, n_cfg, seed=n_cfg)
+    poses_all = L.forward_kinematics_batch(robot, L.ConfigBatch(q))
+    gl = robot.geometry_links
+    R = poses_all.rotations[:, gl]
+    T = poses_all.translations[:, gl]
+    from oracle import linksdf_oracle as O
+    env = O.Env(shape.grid_extent, shape.grid_res)
+    _, dt, _ = O.align(T.reshape(-1, 3), env, window.extent)
+    t = N.torch()
+    R_dev = N.to_device(np.ascontiguousarray(R.reshape(n_cfg, len(gl), 9)), t.float64)
+    dt_dev = N.to_device(np.ascontiguousarray(dt.reshape(n_cfg, len(gl), 3)), t.float64)
+    fused = P.place_windows_device(sdfs, R_dev, dt_dev, window, L.NeuralTransformProvider(model, window, fused=True))
+    two = P.place_windows_device(sdfs, R_dev, dt_dev, window,
+                                 L.NeuralTransformProvider(model, window, fused=False))
+    a, b = fused.cpu().numpy(), two.cpu().numpy()
+    assert a.shape == (n_cfg, len(gl), window.n_cells)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), np.abs(a - b).max()

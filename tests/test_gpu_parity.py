@@ -386,10 +386,11 @@ def test_mlp_predict(L):
     assert np.array_equal(ex, m["exact"])
 
 
-@pytest.mark.parametrize("tc", [False, True])
-def test_neural_placement(L, tc):
+@pytest.mark.parametrize("tc,fused", [(False, False), (True, False), (True, True)])
+def test_neural_placement(L, tc, fused):
     """place_links_batch with NeuralTransformProvider, fully on the device
-    (TinyMlp on tensor cores or CUDA cores -> provider-coordinate sampler), vs
+    (TinyMlp on tensor cores or CUDA cores -> provider-coordinate sampler, or
+    the fused MLP + sampler kernel), vs
     the oracle's numpy MLP transform + trilinear (approx.py:292-306,
     placement.py:300-313): window values within 1e-5 m."""
     from oracle import linksdf_oracle as O
@@ -397,7 +398,8 @@ def test_neural_placement(L, tc):
     g, m = golden("scene_small"), golden("mlp")
     robot, grid, sdfs, window = _scene(L, g)
     model = L.TinyMlp(m["w1"], m["b1"], m["w2"], m["b2"])
-    prov = L.NeuralTransformProvider(model, window, use_tensor_cores=tc)
+    prov = L.NeuralTransformProvider(model, window, use_tensor_cores=tc, fused=fused)
+    assert prov.fused == fused
     gl = [int(i) for i in g["geometry_links"]]
     R, T = g["R"][:, gl], g["T"][:, gl]
     fields = list(L.place_links_batch(sdfs, L.LinkPoseBatch(rotations=R, translations=T), grid, prov))

@@ -187,16 +187,29 @@ def main():
 
         _, dtg, _ = _align_device(Tg, grid, window.dims)
         dtg = dtg.reshape(500, len(gl), 3)
-        prov_n = L.NeuralTransformProvider(model, window)
+        prov_n = L.NeuralTransformProvider(model, window, fused=True)
         ms_place_exact = _time(torch, lambda: place_windows_device(sdfs, Rg, dtg, window), reps=3, warm=1)
         torch.cuda.empty_cache()
         ms_place_neural = _time(torch, lambda: place_windows_device(sdfs, Rg, dtg, window, prov_n), reps=3, warm=1)
+        torch.cuda.empty_cache()
+        prov_2k = L.NeuralTransformProvider(model, window, fused=False)
+        ms_place_2k = _time(torch, lambda: place_windows_device(sdfs, Rg, dtg, window, prov_2k), reps=3, warm=1)
+        torch.cuda.empty_cache()
+        wa = place_windows_device(sdfs, Rg, dtg, window, prov_n)
+        wb = place_windows_device(sdfs, Rg, dtg, window, prov_2k)
+        same = bool(torch.equal(wa.view(torch.int32), wb.view(torch.int32)))
+        del wa, wb
+        torch.cuda.empty_cache()
         out["placement"] = {"waypoints": 500, "links": len(gl), "windows": 500 * len(gl),
                             "cells_per_window": int(window.n_cells), "kept_per_window": V,
-                            "exact_ms": ms_place_exact, "neural_ms": ms_place_neural,
+                            "exact_ms": ms_place_exact, "neural_fused_ms": ms_place_neural,
+                            "neural_two_kernel_ms": ms_place_2k,
+                            "fused_equals_two_kernel": same,
                             "window_bytes_written": 500 * len(gl) * int(window.n_cells) * 4,
-                            "note": "neural = TinyMlp on tcgen05 writing G (f32) + provider-coordinate sampler reading "
-                                    "it back; exact = fused fp64 transform + sampler"}
+                            "note": "neural_fused = lsdf_mlp_place (TinyMlp layer 2 on tcgen05 with the sampler in "
+                                    "its epilogue, G never in HBM; opt-in); neural_two_kernel (the provider's default) "
+                                    "= TinyMlp on tcgen05 writing G (f32) + provider-coordinate sampler reading it "
+                                    "back; exact = fused fp64 transform + sampler"}
     if args.cpu:
         from oracle import linksdf_oracle as O
 
