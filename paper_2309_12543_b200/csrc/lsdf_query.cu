@@ -271,7 +271,41 @@ struct ShellView {
     const uint32_t* bits;    // occupancy bitmap (shared or global)
     const uint32_t* bricks;  // brick columns (shared), or null
     const double* P;         // window offsets (shared)
+    uint32_t cells_s, radius_s, bits_s;  // shared-window addresses of the staged tables
+    uint32_t P_s;                        // shared-window address of P
 };
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Table reads of the scan: with STAGED, explicit ld.shared on the shared-window
+// address (a generic load of a shared address costs the generic-to-shared
+// resolution on every chunk's dependent chain); otherwise through the pointer.
+template <bool STAGED>
+__device__ __forceinline__ uint32_t sv_u32(const uint32_t* ptr, uint32_t saddr, int i) {
+    if (!STAGED) return ptr[i];
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr + 4u * (uint32_t)i));
+    return v;
+}
+template <bool STAGED>
+__device__ __forceinline__ float sv_f32(const float* ptr, uint32_t saddr, int i) {
+    if (!STAGED) return ptr[i];
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr + 4u * (uint32_t)i));
+    return v;
+}
 
 // Per-task constants, computed by one lane per task (up to GRAB_MAX tasks at a
 // time) and read back from shared memory by the warp that scans the task.
@@ -442,7 +476,8 @@ __device__ __forceinline__ uint32_t lookup_round(const QueryParams& p, const She
         const int Wm = p.Wmax, ny = p.dims[1], nz = p.dims[2];
         const int mx = entry & 0xff, my = (entry >> 8) & 0xff, mz = (entry >> 16) & 0xff;
         double pt[3];
-        window_point(sv.P[mx], sv.P[Wm + my], sv.P[2 * Wm + mz], st.R, st.dtinv, p.e_r, pt);
+        window_point(lds_f64(sv.P_s + 8u * mx), lds_f64(sv.P_s + 8u * (Wm + my)), lds_f64(sv.P_s + 8u * (2 * Wm + mz)),
+                     st.R, st.dtinv, p.e_r, pt);
         const float v = trilinear_geom(p.geom, p.cells[l], p.dfar[l], pt[0], pt[1], pt[2]);
         const int lin = ((st.ax + mx) * ny + (st.ay + my)) * nz + (st.az + mz);
         const uint32_t pos = BY_POS ? (uint32_t)__ldg(p.posgrid + lin) : (uint32_t)lin;
@@ -463,8 +498,8 @@ __device__ __forceinline__ uint32_t lookup_round(const QueryParams& p, const She
 // `j` of the warp's grab.  Occupied candidate cells go to the warp's queue;
 // full rounds of 32 are looked up at once, a remainder stays queued for the
 // next task (the kernel flushes it after the grab).
-template <bool BY_POS, bool BRICKS>
-__device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView& sv, uint32_t* queue,
+template <bool BY_POS, bool BRICKS, bool STAGED>
+__device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView& sv, uint32_t queue,
                                            const ShellSetup* setups, uint32_t j, int& qlen, int lane) {
     const ShellSetup& st = setups[j];
     const int l = st.l;
@@ -511,14 +546,14 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
     unsigned long long sc[8] = {1, 0, 0, 0, 0, 0, 0, 0};
 #endif
     for (int k0 = sidx * 32; k0 < p.n_shell; k0 += 32 * p.split) {
-        if (sv.radius[k0] - slack > thresh) {  // every later cell is farther
+        if (sv_f32<STAGED>(sv.radius, sv.radius_s, k0) - slack > thresh) {  // every later cell is farther
             STAT(6, 1);
             STAT(7, k0 == sidx * 32);
             break;
         }
         STAT(1, 1);
         // the shell list is padded to whole chunks with copies of its last cell
-        const uint32_t cell = sv.cells[k0 + lane];
+        const uint32_t cell = sv_u32<STAGED>(sv.cells, sv.cells_s, k0 + lane);
         bool occ = false;
         {
             const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
@@ -527,7 +562,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
             // branch-free: cells outside the grid read word 0 and are masked out
             const bool inb = (x < (unsigned)nx) & (y < (unsigned)ny) & (z < (unsigned)nz);
             const int lin = inb ? lin0 + (mx * ny + my) * nz + mz : 0;
-            occ = inb & ((sv.bits[lin >> 5] >> (lin & 31)) & 1u);
+            occ = inb & ((sv_u32<STAGED>(sv.bits, sv.bits_s, lin >> 5) >> (lin & 31)) & 1u);
         }
 #ifdef LSDF_STATS
         {
@@ -553,21 +588,21 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
             const uint32_t m = __reduce_min_sync(FULL_MASK, __float_as_uint(d2q));
             // the upper bound d + k_hi holds only for samples inside the grid's
             // cell-centre hull: chunks past the inscribed ball leave thresh alone
-            if (m < 0x7f800000u && sv.radius[k0 + 31] <= hull_lim) {
+            if (m < 0x7f800000u && sv_f32<STAGED>(sv.radius, sv.radius_s, k0 + 31) <= hull_lim) {
                 const float dm = __uint_as_float(m);
                 const float r = dm > 0.0f ? dm * rsqrtf(dm) : 0.0f;  // ~2^-22 relative: rounded up below
                 thresh = fminf(thresh, fmaf(r, 1.0f + 0x1p-18f, k_hi));
             }
         }
         const unsigned ballot = __ballot_sync(FULL_MASK, occ);
-        if (occ) queue[qlen + __popc(ballot & ((1u << lane) - 1u))] = cell | (j << 24);
+        if (occ) sts_u32(queue + 4u * (uint32_t)(qlen + __popc(ballot & ((1u << lane) - 1u))), cell | (j << 24));
         qlen += __popc(ballot);
         STAT(4, __popc(ballot));
         __syncwarp();
         if (qlen >= p.round_min) {
             STAT(5, 1);
             const int n = qlen < 32 ? qlen : 32;
-            const uint32_t m = lookup_round<BY_POS>(p, sv, setups, lane < n ? queue[qlen - n + lane] : 0u, lane < n,
+            const uint32_t m = lookup_round<BY_POS>(p, sv, setups, lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u, lane < n,
                                                     j, lane);
             if (m != 0xffffffffu) thresh = fminf(thresh, from_orderable(m));
             if (share_cfg && (++rounds & 3) == 0) {
@@ -588,7 +623,9 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
 // offsets, the shell-ordered cell list and the occupancy bitmap are staged in
 // shared memory once per CTA when they fit, so the per-chunk loads of the
 // scan are shared-memory loads.
-template <bool BY_POS, bool BRICKS>
+// STAGED: the shell list and the bitmap are both in shared memory (a
+// compile-time fact, so the scan's table loads are LDS, not generic loads).
+template <bool BY_POS, bool BRICKS, bool STAGED>
 __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __grid_constant__ QueryParams p,
                                                                   int n_group, int launch, int grab,
                                                                   int stage_shell, int stage_bits, int64_t n_words,
@@ -683,12 +720,16 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
     }
 #endif
     ShellView sv;
-    sv.cells = stage_shell ? s_cells : p.shell_cells;
-    sv.radius = stage_shell ? s_radius : p.shell_radius;
-    sv.bits = stage_bits ? s_bits : p.bitmap;
+    sv.cells = (STAGED || stage_shell) ? s_cells : p.shell_cells;
+    sv.radius = (STAGED || stage_shell) ? s_radius : p.shell_radius;
+    sv.bits = (STAGED || stage_bits) ? s_bits : p.bitmap;
+    sv.cells_s = smem_u32(s_cells);
+    sv.radius_s = smem_u32(s_radius);
+    sv.bits_s = smem_u32(s_bits);
+    sv.P_s = smem_u32(sP);
     sv.bricks = n_cols ? s_bricks : p.bricks;
     sv.P = sP;
-    uint32_t* queue = s_queue + warp * QCAP_SHELL;
+    const uint32_t queue = smem_u32(s_queue + warp * QCAP_SHELL);
     // guided grab sizes: the grab shrinks as the remaining work does, so the
     // last warps to finish carry at most a small grab (shorter tail)
     const uint32_t warps_total = gridDim.x * WARPS;
@@ -722,13 +763,13 @@ __global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __gri
             g = max(1u, min((uint32_t)grab, left / (2 * warps_total)));
         }
         int qlen = 0;
-        for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS, BRICKS>(p, sv, queue, s_setup[warp], j, qlen, lane);
+        for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
 #ifdef LSDF_TIMING
         const unsigned long long t_g2 = gtime();
         if (lane == 0) TIM(6, t_g2 - t_g1);  // scans of the grab's tasks
 #endif
         if (qlen > 0)  // the grab's remaining lookups, before its setups are overwritten
-            lookup_round<BY_POS>(p, sv, s_setup[warp], lane < qlen ? queue[lane] : 0u, lane < qlen, 0xffu, lane);
+            lookup_round<BY_POS>(p, sv, s_setup[warp], lane < qlen ? lds_u32(queue + 4u * (uint32_t)lane) : 0u, lane < qlen, 0xffu, lane);
         __syncwarp();
 #ifdef LSDF_TIMING
         if (lane == 0) TIM(7, gtime() - t_g2);  // flush rounds
@@ -968,9 +1009,14 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
                                   (p.dilate ? (size_t)o.nbx * o.nby * 8 : 0) +
                                   96;  // 16-B alignment and 16-B rounding of the staged tables
             using ShellsKernel = void (*)(QueryParams, int, int, int, int, int, int64_t, int);
-            static const ShellsKernel kernels[4] = {query_shells_kernel<false, false>, query_shells_kernel<false, true>,
-                                                    query_shells_kernel<true, false>, query_shells_kernel<true, true>};
-            const int variant = (p.by_position ? 2 : 0) + (p.bricks != nullptr ? 1 : 0);
+            static const ShellsKernel kernels[8] = {
+                query_shells_kernel<false, false, false>, query_shells_kernel<false, true, false>,
+                query_shells_kernel<true, false, false>,  query_shells_kernel<true, true, false>,
+                query_shells_kernel<false, false, true>,  query_shells_kernel<false, true, true>,
+                query_shells_kernel<true, false, true>,   query_shells_kernel<true, true, true>};
+            static const int t_lds = tune("LSDF_TUNE_LDS", 1);
+            const int variant = (p.by_position ? 2 : 0) + (p.bricks != nullptr ? 1 : 0) +
+                                (t_lds && stage_shell && stage_bits ? 4 : 0);
             const ShellsKernel kern = kernels[variant];
             LSDF_TRY(ensure_smem((const void*)kern, smem_s, "query_shells_kernel"));
             // residency cache: (device, variant, smem bytes) -> CTAs per SM
