@@ -311,6 +311,9 @@ __device__ __forceinline__ float sv_f32(const float* ptr, uint32_t saddr, int i)
 // time) and read back from shared memory by the warp that scans the task.
 constexpr int GRAB_MAX = 16;
 constexpr int64_t SEG_FILTER_MIN_TASKS = 148LL * 32 * 8;  // ~8 tasks per resident warp
+#ifndef LSDF_SHELL_MINB
+#define LSDF_SHELL_MINB 3
+#endif
 struct __align__(16) ShellSetup {
     double R[9];
     double dtinv[3];
@@ -626,7 +629,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
 // STAGED: the shell list and the bitmap are both in shared memory (a
 // compile-time fact, so the scan's table loads are LDS, not generic loads).
 template <bool BY_POS, bool BRICKS, bool STAGED>
-__global__ void __launch_bounds__(32 * WARPS, 3) query_shells_kernel(const __grid_constant__ QueryParams p,
+__global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kernel(const __grid_constant__ QueryParams p,
                                                                   int n_group, int launch, int grab,
                                                                   int stage_shell, int stage_bits, int64_t n_words,
                                                                   int last_launch) {
