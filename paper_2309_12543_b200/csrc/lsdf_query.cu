@@ -46,6 +46,7 @@ struct QueryParams {
     const uint32_t* bricks;                 // occupancy brick columns (4^3 voxels), or null: no box test
     int32_t stage_bricks;                   // brick columns copied to shared memory (else read from global)
     int32_t dilate;                         // > 0: empty-neighbourhood test at setup, dilation radius in bricks
+    int32_t pair_scan;                      // throughput scan walks two tasks per chunk loop (shell_task_pair)
     const uint32_t* brick_cols;             // the occupancy brick columns (input of the dilation)
     int32_t nbx_brick, nbz_brick;           // brick grid (x columns, z bits)
     int32_t nby_brick;                      // brick columns per x row
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_c
 // the key slot), no remaining cell can reach or tie the minimum and the scan
 // stops.  Occupied cells are compacted with a ballot and evaluated 32 at a
 // time with the exact fp64 recipe, so the results are those of the full scan.
-constexpr int QCAP_SHELL = 64;
+constexpr int QCAP_SHELL = 96;  // < round_min + 64: a paired chunk queues up to 64 entries
 __host__ __device__ __forceinline__ int shell_padded(int n) { return (n + 31) & ~31; }
 constexpr int SHELL_STAGE_MAX = 4096;   // kept cells staged in shared memory (W <= 20)
 constexpr int BITMAP_STAGE_MAX = 8192;  // occupancy words staged in shared memory (<= 262k voxels)
@@ -467,7 +468,7 @@ __device__ unsigned long long g_stats[8];
 template <bool BY_POS>
 __device__ __forceinline__ uint32_t lookup_round(const QueryParams& p, const ShellView& sv,
                                                  const ShellSetup* setups, uint32_t entry, bool valid, uint32_t cur,
-                                                 int lane) {
+                                                 int lane, uint32_t* m_next = nullptr) {
     const uint32_t slot = valid ? entry >> 24 : 0xffu;
     uint32_t ov = 0xffffffffu, pk = 0xffffffffu;
     int64_t c = 0;
@@ -494,7 +495,119 @@ __device__ __forceinline__ uint32_t lookup_round(const QueryParams& p, const She
         atomicMax(p.keys + c, ~(((unsigned long long)h << 32) | lo));
         if (p.per_link != nullptr) atomicMax(p.perlink + c * p.n_geo + l, ~h);
     }
+    if (m_next != nullptr) *m_next = __reduce_min_sync(FULL_MASK, slot == cur + 1 ? ov : 0xffffffffu);
     return __reduce_min_sync(FULL_MASK, slot == cur ? ov : 0xffffffffu);
+}
+
+// Per-task scan state of the paired scan (shell_task_pair).
+struct PairTask {
+    float thresh, slack, hull_lim, k_lo, k_hi;
+    float4 su;
+    int ax, ay, az, lin0;
+    bool active, use_seg;
+};
+
+__device__ __forceinline__ PairTask pair_task(const QueryParams& p, const ShellSetup& st) {
+    PairTask t;
+    t.thresh = st.thresh0;
+    t.slack = st.slack;
+    t.hull_lim = st.hull_lim;
+    const float4 sa = p.seg_a[st.l];
+    t.su = p.seg_u[st.l];
+    t.k_lo = sa.w;
+    t.k_hi = p.seg_hi[st.l];
+    t.use_seg = p.seg_filter && t.k_lo >= 0.0f;
+    t.ax = st.ax;
+    t.ay = st.ay;
+    t.az = st.az;
+    t.lin0 = (st.ax * p.dims[1] + st.ay) * p.dims[2] + st.az;
+    t.active = true;
+    return t;
+}
+
+// One task's part of a chunk in the paired scan: occupancy and segment bound
+// of the lane's cell (decoded once for both tasks), and the threshold update
+// from the chunk's queued cells' upper bounds -- shell_task's chunk body.
+template <bool STAGED>
+__device__ __forceinline__ bool pair_chunk(const QueryParams& p, const ShellView& sv, const ShellSetup& st,
+                                           PairTask& t, int mx, int my, int mz, float px, float py, float pz,
+                                           int k0) {
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    const unsigned x = (unsigned)(t.ax + mx), y = (unsigned)(t.ay + my), z = (unsigned)(t.az + mz);
+    const bool inb = (x < (unsigned)nx) & (y < (unsigned)ny) & (z < (unsigned)nz);
+    const int lin = inb ? t.lin0 + (mx * ny + my) * nz + mz : 0;
+    bool occ = inb & ((sv_u32<STAGED>(sv.bits, sv.bits_s, lin >> 5) >> (lin & 31)) & 1u);
+    if (t.use_seg) {
+        float q[3];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) q[e] = fmaf(pz, st.A[6 + e], fmaf(py, st.A[3 + e], fmaf(px, st.A[e], st.b[e])));
+        const float4 su = t.su;
+        const float tt = fminf(fmaxf(fmaf(q[2], su.z, fmaf(q[1], su.y, q[0] * su.x)), 0.0f), su.w);
+        const float ex = fmaf(-tt, su.x, q[0]), ey = fmaf(-tt, su.y, q[1]), ez = fmaf(-tt, su.z, q[2]);
+        const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+        const float lim = t.thresh + t.k_lo;
+        occ = occ && lim >= 0.0f && d2 <= lim * lim;
+        const float d2q = occ ? d2 : INFINITY;
+        const uint32_t m = __reduce_min_sync(FULL_MASK, __float_as_uint(d2q));
+        if (m < 0x7f800000u && sv_f32<STAGED>(sv.radius, sv.radius_s, k0 + 31) <= t.hull_lim) {
+            const float dm = __uint_as_float(m);
+            const float r = dm > 0.0f ? dm * rsqrtf(dm) : 0.0f;
+            t.thresh = fminf(t.thresh, fmaf(r, 1.0f + 0x1p-18f, t.k_hi));
+        }
+    }
+    return occ;
+}
+
+// Two tasks of a grab (slots j, j + 1; split == 1, so both walk the same
+// chunk sequence) scanned together: the chunk's radius and cell are loaded
+// and decoded once, and the two tasks' occupancy / bound chains are
+// independent, so the warp has two dependency chains in flight.  Each task
+// stops at its own first chunk whose bound exceeds its own threshold, as in
+// shell_task; queue entries carry their slot, so lookups and reductions are
+// unchanged.
+template <bool BY_POS, bool STAGED>
+__device__ __forceinline__ void shell_task_pair(const QueryParams& p, const ShellView& sv, uint32_t queue,
+                                                const ShellSetup* setups, uint32_t j, int& qlen, int lane) {
+    const ShellSetup& sta = setups[j];
+    const ShellSetup& stb = setups[j + 1];
+    PairTask a = pair_task(p, sta), b = pair_task(p, stb);
+    const int64_t ca = sta.c, cb = stb.c;
+    const bool share_cfg = p.per_link == nullptr;
+    int rounds = 0;
+    for (int k0 = 0; k0 < p.n_shell; k0 += 32) {
+        const float rad = sv_f32<STAGED>(sv.radius, sv.radius_s, k0);
+        a.active = a.active && !(rad - a.slack > a.thresh);  // every later cell is farther
+        b.active = b.active && !(rad - b.slack > b.thresh);
+        if (!a.active && !b.active) break;
+        const uint32_t cell = sv_u32<STAGED>(sv.cells, sv.cells_s, k0 + lane);
+        const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
+        const float px = (float)mx, py = (float)my, pz = (float)mz;
+        const bool oa = a.active && pair_chunk<STAGED>(p, sv, sta, a, mx, my, mz, px, py, pz, k0);
+        const bool ob = b.active && pair_chunk<STAGED>(p, sv, stb, b, mx, my, mz, px, py, pz, k0);
+        const unsigned ba = __ballot_sync(FULL_MASK, oa), bb = __ballot_sync(FULL_MASK, ob);
+        const unsigned below = (1u << lane) - 1u;
+        if (oa) sts_u32(queue + 4u * (uint32_t)(qlen + __popc(ba & below)), cell | (j << 24));
+        qlen += __popc(ba);
+        if (ob) sts_u32(queue + 4u * (uint32_t)(qlen + __popc(bb & below)), cell | ((j + 1) << 24));
+        qlen += __popc(bb);
+        __syncwarp();
+        while (qlen >= p.round_min) {  // (two tasks can queue up to 64 entries in one chunk)
+            const int n = qlen < 32 ? qlen : 32;
+            uint32_t mb;
+            const uint32_t ma = lookup_round<BY_POS>(
+                p, sv, setups, lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u, lane < n, j, lane,
+                &mb);
+            if (ma != 0xffffffffu) a.thresh = fminf(a.thresh, from_orderable(ma));
+            if (mb != 0xffffffffu) b.thresh = fminf(b.thresh, from_orderable(mb));
+            if (share_cfg && (++rounds & 3) == 0) {
+                const uint64_t ka = ~(uint64_t)__ldcg(p.keys + ca), kb = ~(uint64_t)__ldcg(p.keys + cb);
+                if (ka != ~0ull) a.thresh = fminf(a.thresh, from_orderable((uint32_t)(ka >> 32)));
+                if (kb != ~0ull) b.thresh = fminf(b.thresh, from_orderable((uint32_t)(kb >> 32)));
+            }
+            qlen -= n;
+            __syncwarp();
+        }
+    }
 }
 
 // One warp, one (configuration c, link l, slice sidx) task: the task in slot
@@ -733,6 +846,8 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
     sv.bricks = n_cols ? s_bricks : p.bricks;
     sv.P = sP;
     const uint32_t queue = smem_u32(s_queue + warp * QCAP_SHELL);
+    // paired scan (two tasks per chunk walk) for throughput batches of one slice per task
+    const bool pair = p.pair_scan && p.split == 1;
     // guided grab sizes: the grab shrinks as the remaining work does, so the
     // last warps to finish carry at most a small grab (shorter tail)
     const uint32_t warps_total = gridDim.x * WARPS;
@@ -766,7 +881,10 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
             g = max(1u, min((uint32_t)grab, left / (2 * warps_total)));
         }
         int qlen = 0;
-        for (uint32_t j = 0; j < cnt; ++j) shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
+        uint32_t j = 0;
+        if (!BRICKS && pair)
+            for (; j + 1 < cnt; j += 2) shell_task_pair<BY_POS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
+        for (; j < cnt; ++j) shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
 #ifdef LSDF_TIMING
         const unsigned long long t_g2 = gtime();
         if (lane == 0) TIM(6, t_g2 - t_g1);  // scans of the grab's tasks
@@ -1018,6 +1136,8 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
                 query_shells_kernel<false, false, true>,  query_shells_kernel<false, true, true>,
                 query_shells_kernel<true, false, true>,   query_shells_kernel<true, true, true>};
             static const int t_lds = tune("LSDF_TUNE_LDS", 1);
+            static const int t_pair = tune("LSDF_TUNE_PAIR", 1);
+            p.pair_scan = t_pair;
             const int variant = (p.by_position ? 2 : 0) + (p.bricks != nullptr ? 1 : 0) +
                                 (t_lds && stage_shell && stage_bits ? 4 : 0);
             const ShellsKernel kern = kernels[variant];
