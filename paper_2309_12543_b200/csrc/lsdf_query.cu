@@ -257,7 +257,10 @@ __global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_c
 // the key slot), no remaining cell can reach or tie the minimum and the scan
 // stops.  Occupied cells are compacted with a ballot and evaluated 32 at a
 // time with the exact fp64 recipe, so the results are those of the full scan.
-constexpr int QCAP_SHELL = 96;  // < round_min + 64: a paired chunk queues up to 64 entries
+#ifndef LSDF_PAIR_N
+#define LSDF_PAIR_N 2
+#endif
+constexpr int QCAP_SHELL = 32 + 32 * LSDF_PAIR_N;  // > round_min - 1 + 32 PAIR_N: a chunk of the paired scan queues up to 32 PAIR_N entries
 __host__ __device__ __forceinline__ int shell_padded(int n) { return (n + 31) & ~31; }
 constexpr int SHELL_STAGE_MAX = 4096;   // kept cells staged in shared memory (W <= 20)
 constexpr int BITMAP_STAGE_MAX = 8192;  // occupancy words staged in shared memory (<= 262k voxels)
@@ -468,7 +471,7 @@ __device__ unsigned long long g_stats[8];
 template <bool BY_POS>
 __device__ __forceinline__ uint32_t lookup_round(const QueryParams& p, const ShellView& sv,
                                                  const ShellSetup* setups, uint32_t entry, bool valid, uint32_t cur,
-                                                 int lane, uint32_t* m_next = nullptr) {
+                                                 int lane, uint32_t* ov_out = nullptr) {
     const uint32_t slot = valid ? entry >> 24 : 0xffu;
     uint32_t ov = 0xffffffffu, pk = 0xffffffffu;
     int64_t c = 0;
@@ -495,7 +498,10 @@ __device__ __forceinline__ uint32_t lookup_round(const QueryParams& p, const She
         atomicMax(p.keys + c, ~(((unsigned long long)h << 32) | lo));
         if (p.per_link != nullptr) atomicMax(p.perlink + c * p.n_geo + l, ~h);
     }
-    if (m_next != nullptr) *m_next = __reduce_min_sync(FULL_MASK, slot == cur + 1 ? ov : 0xffffffffu);
+    if (ov_out != nullptr) {  // the caller reduces per slot itself
+        *ov_out = ov;
+        return 0xffffffffu;
+    }
     return __reduce_min_sync(FULL_MASK, slot == cur ? ov : 0xffffffffu);
 }
 
@@ -558,51 +564,63 @@ __device__ __forceinline__ bool pair_chunk(const QueryParams& p, const ShellView
     return occ;
 }
 
-// Two tasks of a grab (slots j, j + 1; split == 1, so both walk the same
-// chunk sequence) scanned together: the chunk's radius and cell are loaded
-// and decoded once, and the two tasks' occupancy / bound chains are
-// independent, so the warp has two dependency chains in flight.  Each task
+// NT tasks of a grab (slots j .. j + NT - 1; split == 1, so all walk the
+// same chunk sequence) scanned together: the chunk's radius and cell are
+// loaded and decoded once, and the tasks' occupancy / bound chains are
+// independent, so the warp has NT dependency chains in flight.  Each task
 // stops at its own first chunk whose bound exceeds its own threshold, as in
 // shell_task; queue entries carry their slot, so lookups and reductions are
 // unchanged.
+constexpr int PAIR_N = LSDF_PAIR_N;
 template <bool BY_POS, bool STAGED>
 __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const ShellView& sv, uint32_t queue,
                                                 const ShellSetup* setups, uint32_t j, int& qlen, int lane) {
-    const ShellSetup& sta = setups[j];
-    const ShellSetup& stb = setups[j + 1];
-    PairTask a = pair_task(p, sta), b = pair_task(p, stb);
-    const int64_t ca = sta.c, cb = stb.c;
+    PairTask t[PAIR_N];
+#pragma unroll
+    for (int i = 0; i < PAIR_N; ++i) t[i] = pair_task(p, setups[j + i]);
     const bool share_cfg = p.per_link == nullptr;
     int rounds = 0;
     for (int k0 = 0; k0 < p.n_shell; k0 += 32) {
         const float rad = sv_f32<STAGED>(sv.radius, sv.radius_s, k0);
-        a.active = a.active && !(rad - a.slack > a.thresh);  // every later cell is farther
-        b.active = b.active && !(rad - b.slack > b.thresh);
-        if (!a.active && !b.active) break;
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < PAIR_N; ++i) {
+            t[i].active = t[i].active && !(rad - t[i].slack > t[i].thresh);  // every later cell is farther
+            any |= t[i].active;
+        }
+        if (!any) break;
         const uint32_t cell = sv_u32<STAGED>(sv.cells, sv.cells_s, k0 + lane);
         const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
         const float px = (float)mx, py = (float)my, pz = (float)mz;
-        const bool oa = a.active && pair_chunk<STAGED>(p, sv, sta, a, mx, my, mz, px, py, pz, k0);
-        const bool ob = b.active && pair_chunk<STAGED>(p, sv, stb, b, mx, my, mz, px, py, pz, k0);
-        const unsigned ba = __ballot_sync(FULL_MASK, oa), bb = __ballot_sync(FULL_MASK, ob);
+        bool o[PAIR_N];
+#pragma unroll
+        for (int i = 0; i < PAIR_N; ++i)
+            o[i] = t[i].active && pair_chunk<STAGED>(p, sv, setups[j + i], t[i], mx, my, mz, px, py, pz, k0);
         const unsigned below = (1u << lane) - 1u;
-        if (oa) sts_u32(queue + 4u * (uint32_t)(qlen + __popc(ba & below)), cell | (j << 24));
-        qlen += __popc(ba);
-        if (ob) sts_u32(queue + 4u * (uint32_t)(qlen + __popc(bb & below)), cell | ((j + 1) << 24));
-        qlen += __popc(bb);
+#pragma unroll
+        for (int i = 0; i < PAIR_N; ++i) {
+            const unsigned bl = __ballot_sync(FULL_MASK, o[i]);
+            if (o[i]) sts_u32(queue + 4u * (uint32_t)(qlen + __popc(bl & below)), cell | ((j + i) << 24));
+            qlen += __popc(bl);
+        }
         __syncwarp();
-        while (qlen >= p.round_min) {  // (two tasks can queue up to 64 entries in one chunk)
+        while (qlen >= p.round_min) {  // (NT tasks can queue up to 32 NT entries in one chunk)
             const int n = qlen < 32 ? qlen : 32;
-            uint32_t mb;
-            const uint32_t ma = lookup_round<BY_POS>(
-                p, sv, setups, lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u, lane < n, j, lane,
-                &mb);
-            if (ma != 0xffffffffu) a.thresh = fminf(a.thresh, from_orderable(ma));
-            if (mb != 0xffffffffu) b.thresh = fminf(b.thresh, from_orderable(mb));
+            const uint32_t entry = lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u;
+            uint32_t ov;
+            lookup_round<BY_POS>(p, sv, setups, entry, lane < n, j, lane, &ov);
+            const uint32_t slot = entry >> 24;  // (ov is 0xffffffff on lanes without an entry)
+#pragma unroll
+            for (int i = 0; i < PAIR_N; ++i) {
+                const uint32_t m = __reduce_min_sync(FULL_MASK, slot == j + i ? ov : 0xffffffffu);
+                if (m != 0xffffffffu) t[i].thresh = fminf(t[i].thresh, from_orderable(m));
+            }
             if (share_cfg && (++rounds & 3) == 0) {
-                const uint64_t ka = ~(uint64_t)__ldcg(p.keys + ca), kb = ~(uint64_t)__ldcg(p.keys + cb);
-                if (ka != ~0ull) a.thresh = fminf(a.thresh, from_orderable((uint32_t)(ka >> 32)));
-                if (kb != ~0ull) b.thresh = fminf(b.thresh, from_orderable((uint32_t)(kb >> 32)));
+#pragma unroll
+                for (int i = 0; i < PAIR_N; ++i) {
+                    const uint64_t k = ~(uint64_t)__ldcg(p.keys + setups[j + i].c);
+                    if (k != ~0ull) t[i].thresh = fminf(t[i].thresh, from_orderable((uint32_t)(k >> 32)));
+                }
             }
             qlen -= n;
             __syncwarp();
@@ -883,7 +901,8 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
         int qlen = 0;
         uint32_t j = 0;
         if (!BRICKS && pair)
-            for (; j + 1 < cnt; j += 2) shell_task_pair<BY_POS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
+            for (; j + PAIR_N <= cnt; j += PAIR_N)
+                shell_task_pair<BY_POS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
         for (; j < cnt; ++j) shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
 #ifdef LSDF_TIMING
         const unsigned long long t_g2 = gtime();
