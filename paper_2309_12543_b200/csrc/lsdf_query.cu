@@ -313,7 +313,10 @@ __device__ __forceinline__ float sv_f32(const float* ptr, uint32_t saddr, int i)
 
 // Per-task constants, computed by one lane per task (up to GRAB_MAX tasks at a
 // time) and read back from shared memory by the warp that scans the task.
-constexpr int GRAB_MAX = 16;
+#ifndef LSDF_GRAB_MAX
+#define LSDF_GRAB_MAX 16
+#endif
+constexpr int GRAB_MAX = LSDF_GRAB_MAX;
 constexpr int64_t SEG_FILTER_MIN_TASKS = 148LL * 32 * 8;  // ~8 tasks per resident warp
 #ifndef LSDF_SHELL_MINB
 #define LSDF_SHELL_MINB 3
