@@ -42,6 +42,18 @@ inline int check_cuda(cudaError_t e, const char* what) {
 
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
+// SM count of the current device (cached per thread and device)
+inline int sm_count() {
+    thread_local int dev_cached = -1, n_sm = 148;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != dev_cached) {
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        dev_cached = dev;
+    }
+    return n_sm;
+}
+
 #define LSDF_TRY(expr)                 \
     do {                               \
         int _rc = (expr);              \

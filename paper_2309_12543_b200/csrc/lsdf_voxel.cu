@@ -76,8 +76,10 @@ voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, do
                      int32_t n_cols, int32_t use_vec) {
     extern __shared__ uint32_t s_bits[];
     uint32_t* s_bricks = s_bits + n_words;  // brick columns (PRIVATE)
-    if (PRIVATE) {
-        for (int64_t w = threadIdx.x; w < n_words + n_cols; w += blockDim.x) s_bits[w] = 0u;
+    if (PRIVATE) {  // (the allocation is rounded up to whole 16-B groups)
+        uint4* s4 = (uint4*)s_bits;
+        const int n4 = (int)((n_words + n_cols + 3) >> 2);
+        for (int w = threadIdx.x; w < n4; w += blockDim.x) s4[w] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
     }
     // grid-stride: a persistent grid of a few CTAs per SM amortises the
@@ -149,7 +151,17 @@ voxel_scatter_kernel(const T* __restrict__ pts, int64_t N, lsdf_env_grid env, do
     if ((threadIdx.x & 31) == 0 && dropped_count) atomicAdd(&counters[1], dropped_count);
     if (PRIVATE) {
         __syncthreads();
-        for (int64_t w = threadIdx.x; w < n_words; w += blockDim.x) {
+        const uint4* s4 = (const uint4*)s_bits;
+        const int n4 = (int)(n_words >> 2);
+        for (int w4 = threadIdx.x; w4 < n4; w4 += blockDim.x) {
+            const uint4 v = s4[w4];
+            uint32_t* g = bitmap + 4 * w4;
+            if (v.x) atomicOr(g, v.x);
+            if (v.y) atomicOr(g + 1, v.y);
+            if (v.z) atomicOr(g + 2, v.z);
+            if (v.w) atomicOr(g + 3, v.w);
+        }
+        for (int w = 4 * n4 + threadIdx.x; w < (int)n_words; w += blockDim.x) {
             const uint32_t v = s_bits[w];
             if (v) atomicOr(bitmap + w, v);
         }
@@ -264,21 +276,22 @@ int scatter_bitmap(const void* points_dev, int32_t points_f32, int64_t N, const 
     // come over PCIe: more SMs with reads in flight, config 2 host to host
     // 56.6 -> 50.8 us); large clouds: 1024-thread CTAs amortise the private
     // bitmap's clear and merge
+    const int n_sm = sm_count();
     static const int t_threads = [] { const char* v = getenv("LSDF_TUNE_VOXTHREADS"); return v && *v ? atoi(v) : 0; }();
     const unsigned threads = t_threads > 0 ? (unsigned)t_threads
-                                           : (N >= 148LL * 2 * SCATTER_THREADS ? SCATTER_THREADS : 256u);
+                                           : (N >= n_sm * 2LL * SCATTER_THREADS ? SCATTER_THREADS : 256u);
     // 4 points per thread (float4 loads) only when that still fills the GPU:
     // small clouds keep one point per thread (more CTAs in flight)
     static const int t_vec = [] { const char* v = getenv("LSDF_TUNE_VOXVEC"); return v && *v ? atoi(v) : -1; }();
-    const bool want_vec = t_vec >= 0 ? t_vec != 0 : N >= 148LL * 2 * SCATTER_THREADS * 2;
+    const bool want_vec = t_vec >= 0 ? t_vec != 0 : N >= n_sm * 2LL * SCATTER_THREADS * 2;
     const int64_t per_thread = (want_vec && points_f32 && (((uintptr_t)points_dev) & 15) == 0) ? 4 : 1;
     const unsigned want = grid_for((N + per_thread - 1) / per_thread, threads);
     static const int t_blocks = [] { const char* v = getenv("LSDF_TUNE_VOXBLOCKS"); return v && *v ? atoi(v) : 0; }();
-    // 1,024-thread CTAs fit once per SM (registers): one wave of 148, each
-    // striding over more points, instead of 1.7 waves (config 4: +1.2 %)
-    const unsigned cap = t_blocks > 0 ? (unsigned)t_blocks : (threads == SCATTER_THREADS ? 148u : 148u * 2u);
+    // 1,024-thread CTAs fit once per SM (registers): one wave, each striding
+    // over more points, instead of 1.7 waves (config 4: +1.2 %)
+    const unsigned cap = t_blocks > 0 ? (unsigned)t_blocks : (unsigned)(threads == SCATTER_THREADS ? n_sm : 2 * n_sm);
     const unsigned blocks = want < cap ? want : cap;  // (more CTAs: more private-bitmap merges)
-    const size_t smem = priv ? (size_t)(o.n_words + n_cols) * 4 : 0;
+    const size_t smem = priv ? (size_t)((o.n_words + n_cols + 3) & ~3LL) * 4 : 0;
     if (points_f32) {
         if (priv)
             voxel_scatter_kernel<float, true><<<blocks, threads, smem, s>>>(

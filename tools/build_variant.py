@@ -3,6 +3,7 @@ nvcc defines, linked with the other objects of the current build.
 
     python tools/build_variant.py OUT.so -DLSDF_SHELL_MINB=4
     python tools/build_variant.py OUT.so --src old_query.cu   (e.g. from `git show HEAD~1:...`)
+    python tools/build_variant.py OUT.so --unit lsdf_voxel.cu --src old_voxel.cu
 
 Select it at run time with LINKSDF_B200_LIB=OUT.so (paper_2309_12543_b200/_native.py).
 """
@@ -17,6 +18,10 @@ from paper_2309_12543_b200 import build as B  # noqa: E402
 def main(out, args, source="lsdf_query.cu"):
     B.build()
     nvcc = B._nvcc()
+    if "--unit" in args:  # which translation unit the variant replaces (default lsdf_query.cu)
+        k = args.index("--unit")
+        source = args[k + 1]
+        args = args[:k] + args[k + 2:]
     src = B.CSRC / source
     if "--src" in args:  # another version of lsdf_query.cu (compiled from the csrc directory for its includes)
         k = args.index("--src")
