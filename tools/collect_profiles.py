@@ -31,7 +31,7 @@ def main():
         (dst / b).write_text(line + "\n")
     for f in ("launches_bench.csv", "scan_stats.txt", "scan_timing.txt", "cycle_parts_config2.txt",
               "e2e_breakdown_config2.txt", "vmajor_config2.json", "vmajor_config5.json", "config3_precompute.json",
-              "pytest_gpu.log"):
+              "pytest_gpu.log", "placement_launches.csv"):
         if (src / f).exists():
             shutil.copy(src / f, dst / f)
     lines = [f"# ncu summaries, round {args.round[1:]} (tools/refresh_profiles.sh; B200, --clock-control none)", ""]
@@ -42,6 +42,10 @@ def main():
         lines += [f"## query_shells_kernel, {w} (ncu --set full, the 4th cycle of bench.py --probe-counters)",
                   _run([str(REPO / "tools" / "ncu_summary.py"), str(rep)]),
                   "### hottest source lines", _run([str(REPO / "tools" / "ncu_lines.py"), str(rep), "30"])]
+    if (src / "placement_launches.csv").exists():
+        lines += ["## neural placement at config-3 scale (500 x 6 windows, W = 128): fused lsdf_mlp_place vs "
+                  "TinyMlp + place_windows_g, and the exact place_windows (ncu, serialised)",
+                  _run([str(REPO / "tools" / "ncu_launches.py"), str(src / "placement_launches.csv")])]
     rep = src / "cycle_config2.ncu-rep"
     lines += ["## every kernel of one config-2 cycle (ncu --set full)", _run([str(REPO / "tools" / "ncu_summary.py"),
                                                                             str(rep)])]

@@ -22,6 +22,10 @@ python tools/cycle_parts.py --workload config2 --flush > $O/cycle_parts_config2.
 python tools/e2e_breakdown.py > $O/e2e_breakdown_config2.txt 2>&1
 python tools/bench_vmajor.py --workload config2 > $O/vmajor_config2.json 2> $O/vmajor.err
 python tools/bench_vmajor.py --workload config5 > $O/vmajor_config5.json 2>> $O/vmajor.err
-python tools/bench_precompute.py --train > $O/config3_precompute.json 2> $O/config3_precompute.err
+python tools/bench_precompute.py --train --placement > $O/config3_precompute.json 2> $O/config3_precompute.err
+# neural placement at config-3 scale: the fused MLP + sampler kernel vs the two-kernel path
+ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,l1tex__throughput.avg.pct_of_peak_sustained_active \
+    -k regex:"mlp_place_tc|place_windows|fill_masked|layer1_pack|mlp_tc_kernel" --clock-control none --csv \
+    --log-file $O/placement_launches.csv python tools/bench_precompute.py --placement > $O/ncu_placement.log 2>&1
 python tools/reference_tests.py run > $O/reference_tests.log 2>&1; cp gpurun_out/reference_tests.txt $O/ 2>/dev/null
 echo done
