@@ -1159,7 +1159,11 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
                 query_shells_kernel<true, false, true>,   query_shells_kernel<true, true, true>};
             static const int t_lds = tune("LSDF_TUNE_LDS", 1);
             static const int t_pair = tune("LSDF_TUNE_PAIR", 1);
+#ifdef LSDF_STATS
+            p.pair_scan = 0;  // the per-task counters live in shell_task: count the same decisions one task at a time
+#else
             p.pair_scan = t_pair;
+#endif
             const int variant = (p.by_position ? 2 : 0) + (p.bricks != nullptr ? 1 : 0) +
                                 (t_lds && stage_shell && stage_bits ? 4 : 0);
             const ShellsKernel kern = kernels[variant];
