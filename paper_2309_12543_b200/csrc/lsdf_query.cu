@@ -508,6 +508,131 @@ __device__ __forceinline__ uint32_t lookup_round(const QueryParams& p, const She
     return __reduce_min_sync(FULL_MASK, slot == cur ? ov : 0xffffffffu);
 }
 
+#ifndef LSDF_PAIR_V2
+#define LSDF_PAIR_V2 1
+#endif
+#if LSDF_PAIR_V2
+// Per-task scan state of the paired scan (shell_task_pair).  A disabled
+// segment bound is encoded in the constants (k_lo = +inf passes every cell,
+// hull_lim = -inf never lowers the threshold), so the chunk body is the same
+// branch-free code for every task.
+struct PairTask {
+    float thresh, slack, hull_lim, k_lo, k_hi;
+    int ax, ay, az, lin0;
+    bool active;
+};
+
+__device__ __forceinline__ PairTask pair_task(const QueryParams& p, const ShellSetup& st) {
+    PairTask t;
+    t.thresh = st.thresh0;
+    t.slack = st.slack;
+    const float k_lo = p.seg_a[st.l].w;
+    const bool use_seg = p.seg_filter && k_lo >= 0.0f;
+    t.k_lo = use_seg ? k_lo : INFINITY;
+    t.k_hi = p.seg_hi[st.l];
+    t.hull_lim = use_seg ? st.hull_lim : -INFINITY;
+    t.ax = st.ax;
+    t.ay = st.ay;
+    t.az = st.az;
+    t.lin0 = (st.ax * p.dims[1] + st.ay) * p.dims[2] + st.az;
+    t.active = true;
+    return t;
+}
+
+// NT tasks of a grab (slots j .. j + NT - 1; split == 1, so all walk the
+// same chunk sequence) scanned together: per chunk, the cell's indices, its
+// float coordinates and its C-order offset in the environment grid are
+// computed once for all tasks, and every task then runs the same
+// branch-free occupancy test and segment bound (a stopped task's lanes are
+// masked, not skipped: both tasks are live in ~96 % of the chunks at config 4).
+// The tasks' chains are independent, so the warp has NT of them in flight.
+// Each task stops at its own first chunk whose bound exceeds its own
+// threshold, as in shell_task; queue entries carry their slot, so lookups and
+// reductions are unchanged.
+constexpr int PAIR_N = LSDF_PAIR_N;
+template <bool BY_POS, bool STAGED>
+__device__ __forceinline__ void shell_task_pair(const QueryParams& p, const ShellView& sv, uint32_t queue,
+                                                const ShellSetup* setups, uint32_t j, int& qlen, int lane) {
+    PairTask t[PAIR_N];
+#pragma unroll
+    for (int i = 0; i < PAIR_N; ++i) t[i] = pair_task(p, setups[j + i]);
+    const float4 su0 = p.seg_u[setups[j].l];  // consecutive tasks of a grab share the link (link-major order)
+    const bool share_cfg = p.per_link == nullptr;
+    const unsigned nx = (unsigned)p.dims[0], ny = (unsigned)p.dims[1], nz = (unsigned)p.dims[2];
+    const unsigned below = (1u << lane) - 1u;
+    int rounds = 0;
+    for (int k0 = 0; k0 < p.n_shell; k0 += 32) {
+        const float rad = sv_f32<STAGED>(sv.radius, sv.radius_s, k0);
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < PAIR_N; ++i) {
+            t[i].active = t[i].active && !(rad - t[i].slack > t[i].thresh);  // every later cell is farther
+            any |= t[i].active;
+        }
+        if (!any) break;
+        const uint32_t cell = sv_u32<STAGED>(sv.cells, sv.cells_s, k0 + lane);
+        const float rad_hi = sv_f32<STAGED>(sv.radius, sv.radius_s, k0 + 31);  // the chunk's largest radius
+        const unsigned mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
+        const int off = (int)((mx * ny + my) * nz + mz);  // C-order offset from the window's corner voxel
+        const float px = (float)mx, py = (float)my, pz = (float)mz;  // offsets folded into A, b
+        bool o[PAIR_N];
+#pragma unroll
+        for (int i = 0; i < PAIR_N; ++i) {
+            const ShellSetup& st = setups[j + i];
+            const bool inb = ((unsigned)t[i].ax + mx < nx) & ((unsigned)t[i].ay + my < ny) & ((unsigned)t[i].az + mz < nz);
+            const int lin = inb ? t[i].lin0 + off : 0;  // cells outside the grid read word 0, masked below
+            bool occ = t[i].active & inb & ((sv_u32<STAGED>(sv.bits, sv.bits_s, lin >> 5) >> (lin & 31)) & 1u);
+            // segment bound (f32, conservative): d(p) - k_lo <= value(p) <= d(p) + k_hi
+            float q[3];
+#pragma unroll
+            for (int e = 0; e < 3; ++e) q[e] = fmaf(pz, st.A[6 + e], fmaf(py, st.A[3 + e], fmaf(px, st.A[e], st.b[e])));
+            const float tt = fminf(fmaxf(fmaf(q[2], su0.z, fmaf(q[1], su0.y, q[0] * su0.x)), 0.0f), su0.w);
+            const float ex = fmaf(-tt, su0.x, q[0]), ey = fmaf(-tt, su0.y, q[1]), ez = fmaf(-tt, su0.z, q[2]);
+            const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+            const float lim = t[i].thresh + t[i].k_lo;
+            occ = occ & (lim >= 0.0f) & (d2 <= lim * lim);
+            // a queued cell WILL be looked up, so its upper bound lowers the
+            // threshold at once -- only inside the hull of the grid's cell
+            // centres, where the upper bound holds
+            const uint32_t m = __reduce_min_sync(FULL_MASK, occ ? __float_as_uint(d2) : 0x7f800000u);
+            if (m < 0x7f800000u && rad_hi <= t[i].hull_lim) {
+                const float dm = __uint_as_float(m);
+                const float r = dm > 0.0f ? dm * rsqrtf(dm) : 0.0f;  // ~2^-22 relative: rounded up below
+                t[i].thresh = fminf(t[i].thresh, fmaf(r, 1.0f + 0x1p-18f, t[i].k_hi));
+            }
+            o[i] = occ;
+        }
+#pragma unroll
+        for (int i = 0; i < PAIR_N; ++i) {
+            const unsigned bl = __ballot_sync(FULL_MASK, o[i]);
+            if (o[i]) sts_u32(queue + 4u * (uint32_t)(qlen + __popc(bl & below)), cell | ((j + i) << 24));
+            qlen += __popc(bl);
+        }
+        __syncwarp();
+        while (qlen >= p.round_min) {  // (NT tasks can queue up to 32 NT entries in one chunk)
+            const int n = qlen < 32 ? qlen : 32;
+            const uint32_t entry = lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u;
+            uint32_t ov;
+            lookup_round<BY_POS>(p, sv, setups, entry, lane < n, j, lane, &ov);
+            const uint32_t slot = entry >> 24;  // (ov is 0xffffffff on lanes without an entry)
+#pragma unroll
+            for (int i = 0; i < PAIR_N; ++i) {
+                const uint32_t m = __reduce_min_sync(FULL_MASK, slot == j + i ? ov : 0xffffffffu);
+                if (m != 0xffffffffu) t[i].thresh = fminf(t[i].thresh, from_orderable(m));
+            }
+            if (share_cfg && (++rounds & 3) == 0) {
+#pragma unroll
+                for (int i = 0; i < PAIR_N; ++i) {
+                    const uint64_t k = ~(uint64_t)__ldcg(p.keys + setups[j + i].c);
+                    if (k != ~0ull) t[i].thresh = fminf(t[i].thresh, from_orderable((uint32_t)(k >> 32)));
+                }
+            }
+            qlen -= n;
+            __syncwarp();
+        }
+    }
+}
+#else
 // Per-task scan state of the paired scan (shell_task_pair).
 struct PairTask {
     float thresh, slack, hull_lim, k_lo, k_hi;
@@ -630,6 +755,8 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
         }
     }
 }
+
+#endif  // LSDF_PAIR_V2
 
 // One warp, one (configuration c, link l, slice sidx) task: the task in slot
 // `j` of the warp's grab.  Occupied candidate cells go to the warp's queue;
@@ -904,8 +1031,16 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
         int qlen = 0;
         uint32_t j = 0;
         if (!BRICKS && pair)
-            for (; j + PAIR_N <= cnt; j += PAIR_N)
-                shell_task_pair<BY_POS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
+            while (j + PAIR_N <= cnt) {
+                // the paired tasks share one link (a grab straddles a link boundary at most once)
+                if (s_setup[warp][j].l == s_setup[warp][j + PAIR_N - 1].l) {
+                    shell_task_pair<BY_POS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
+                    j += PAIR_N;
+                } else {
+                    shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
+                    ++j;
+                }
+            }
         for (; j < cnt; ++j) shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
 #ifdef LSDF_TIMING
         const unsigned long long t_g2 = gtime();
