@@ -292,6 +292,25 @@ __device__ __forceinline__ double lds_f64(uint32_t a) {
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+// predicated store (no branch around it)
+__device__ __forceinline__ void sts_u32_if(bool pred, uint32_t a, uint32_t v) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.shared.u32 [%0], %1;\n}" ::"r"(a), "r"(v),
+                 "r"((uint32_t)pred)
+                 : "memory");
+}
+// warp collectives of the scan's convergent loop as plain PTX
+__device__ __forceinline__ uint32_t warp_redux_min(uint32_t v) {
+    uint32_t r;
+    asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
+}
+__device__ __forceinline__ uint32_t warp_ballot(bool pred) {
+    uint32_t r;
+    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n vote.sync.ballot.b32 %0, p, 0xffffffff;\n}"
+                 : "=r"(r)
+                 : "r"((uint32_t)pred));
+    return r;
+}
 
 // Table reads of the scan: with STAGED, explicit ld.shared on the shared-window
 // address (a generic load of a shared address costs the generic-to-shared
@@ -324,8 +343,12 @@ constexpr int64_t SEG_FILTER_MIN_TASKS = 148LL * 32 * 8;  // ~8 tasks per reside
 struct __align__(16) ShellSetup {
     double R[9];
     double dtinv[3];
-    float A[9];  // f32 link-frame point of window offset P minus the segment origin:
-    float b[3];  //   p_k - a_k = Px A[k] + Py A[3+k] + Pz A[6+k] + b[k]
+    // Segment bound in quadratic form (see seg_d2): with m' the cell index
+    // relative to the window centre c, q = p - a = A m' + b (A = e_r s_a R,
+    // rows orthogonal, |row a|^2 = sigma_a^2), |q|^2 = sum_a sigma_a^2 m'_a^2 +
+    // m'.(2 A b) + |b|^2 and q.u = m'.(A u) + b.u
+    float4 sw;   // (2 A b, |b|^2)
+    float4 sv;   // (A u, b.u)
     float slack;     // |dt| (rounded up) + core radius of the link
     float hull_lim;  // cells with shell radius <= hull_lim map inside the link grid's cell-centre hull
     int32_t l;       // geometry link
@@ -400,22 +423,32 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, const int* ord
 #pragma unroll
     for (int e = 0; e < 3; ++e) s.dtinv[e] = dtinv[e];
     if (p.seg_filter) {  // segment-bound constants (throughput batches only)
-        const float4 sa = p.seg_a[l];
-        const float a3[3] = {sa.x, sa.y, sa.z};
-        // the window offsets are affine in the cell index, P_a[m] = P_a[0] + m s_a:
-        // fold them in, so the scan evaluates A' m + b' straight from the cell
-        // indices (no offset-table loads)
+        const float4 sa = p.seg_a[l], su = p.seg_u[l];
+        const double a3[3] = {sa.x, sa.y, sa.z}, u3[3] = {su.x, su.y, su.z};
+        // the window offsets are affine in the cell index, P_a[m] = P_a[c] + (m - c) s_a
+        // (c = W/2): fold them in, so the scan evaluates the bound straight from
+        // the centred cell indices (no offset-table loads)
         const int Wm = p.Wmax;
-        const double p0[3] = {__ldg(p.P), __ldg(p.P + Wm), __ldg(p.P + 2 * Wm)};
-        const double sc[3] = {__ldg(p.P + 1) - p0[0], __ldg(p.P + Wm + 1) - p0[1], __ldg(p.P + 2 * Wm + 1) - p0[2]};
+        const int c0 = p.W[0] / 2, c1 = p.W[1] / 2, c2 = p.W[2] / 2;
+        const double pc[3] = {__ldg(p.P + c0), __ldg(p.P + Wm + c1), __ldg(p.P + 2 * Wm + c2)};
+        const double sc[3] = {__ldg(p.P + 1) - __ldg(p.P), __ldg(p.P + Wm + 1) - __ldg(p.P + Wm),
+                              __ldg(p.P + 2 * Wm + 1) - __ldg(p.P + 2 * Wm)};
+        double b[3], bb = 0.0, bu = 0.0;
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
+        for (int k = 0; k < 3; ++k) {
+            b[k] = dtinv[k] * p.e_r - a3[k] + p.e_r * (R[k] * pc[0] + R[3 + k] * pc[1] + R[6 + k] * pc[2]);
+            bb += b[k] * b[k];
+            bu += b[k] * u3[k];
+        }
+        float w2[3], v[3];
 #pragma unroll
-            for (int k = 0; k < 3; ++k) s.A[3 * a + k] = (float)(R[3 * a + k] * p.e_r * sc[a]);
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-            s.b[k] = (float)(dtinv[k] * p.e_r - (double)a3[k] +
-                             p.e_r * (R[k] * p0[0] + R[3 + k] * p0[1] + R[6 + k] * p0[2]));
+        for (int a = 0; a < 3; ++a) {
+            const double f = p.e_r * sc[a];
+            w2[a] = (float)(2.0 * f * (R[3 * a] * b[0] + R[3 * a + 1] * b[1] + R[3 * a + 2] * b[2]));
+            v[a] = (float)(f * (R[3 * a] * u3[0] + R[3 * a + 1] * u3[1] + R[3 * a + 2] * u3[2]));
+        }
+        s.sw = make_float4(w2[0], w2[1], w2[2], (float)bb);
+        s.sv = make_float4(v[0], v[1], v[2], (float)bu);
         // |link-frame point| <= rho + |dt|: a cell with rho <= hull - |dt| samples
         // inside the hull of the grid's cell centres, where the segment's upper
         // bound holds (outside it the sample is the link's far value)
@@ -508,10 +541,48 @@ __device__ __forceinline__ uint32_t lookup_round(const QueryParams& p, const She
     return __reduce_min_sync(FULL_MASK, slot == cur ? ov : 0xffffffffu);
 }
 
-#ifndef LSDF_PAIR_V2
-#define LSDF_PAIR_V2 1
-#endif
-#if LSDF_PAIR_V2
+// Centred cell coordinates m' = m - W/2 of a shell cell and sum_a sigma_a^2 m'_a^2.
+struct SegCell {
+    float px, py, pz, mm;
+};
+struct SegAxes {  // per launch: the window centre and sigma_a^2 = (e_r s_a)^2
+    float cx, cy, cz, s2x, s2y, s2z;
+};
+__device__ __forceinline__ SegAxes seg_axes(const QueryParams& p) {
+    const int Wm = p.Wmax;
+    SegAxes g;
+    g.cx = (float)(p.W[0] / 2);
+    g.cy = (float)(p.W[1] / 2);
+    g.cz = (float)(p.W[2] / 2);
+    const double fx = p.e_r * (__ldg(p.P + 1) - __ldg(p.P));
+    const double fy = p.e_r * (__ldg(p.P + Wm + 1) - __ldg(p.P + Wm));
+    const double fz = p.e_r * (__ldg(p.P + 2 * Wm + 1) - __ldg(p.P + 2 * Wm));
+    g.s2x = (float)(fx * fx);
+    g.s2y = (float)(fy * fy);
+    g.s2z = (float)(fz * fz);
+    return g;
+}
+__device__ __forceinline__ SegCell seg_cell(const SegAxes& g, unsigned mx, unsigned my, unsigned mz) {
+    SegCell m;
+    m.px = (float)mx - g.cx;
+    m.py = (float)my - g.cy;
+    m.pz = (float)mz - g.cz;
+    m.mm = fmaf(m.px, m.px * g.s2x, fmaf(m.py, m.py * g.s2y, m.pz * m.pz * g.s2z));
+    return m;
+}
+// Squared distance from the cell's link-frame point to the link's axis segment,
+// f32: |q|^2 - s^2 + (s - t)^2 with s = q.u and t = clamp(s, 0, L).  The
+// evaluation error stays below 2^-23 m^2 on the window's range (sampled with
+// fma emulation in tests/test_host.py::test_segment_bound_quadratic_form);
+// callers widen by SEG_D2_ERR on both sides.
+constexpr float SEG_D2_ERR = 0x1p-21f;
+__device__ __forceinline__ float seg_d2(const float4 sw, const float4 sv, const SegCell& m, float len) {
+    const float qq = fmaf(m.pz, sw.z, fmaf(m.py, sw.y, fmaf(m.px, sw.x, m.mm + sw.w)));
+    const float sp = fmaf(m.pz, sv.z, fmaf(m.py, sv.y, fmaf(m.px, sv.x, sv.w)));
+    const float dd = sp - fminf(fmaxf(sp, 0.0f), len);
+    return fmaxf(fmaf(dd, dd, fmaf(-sp, sp, qq)), 0.0f);
+}
+
 // Per-task scan state of the paired scan (shell_task_pair).  A disabled
 // segment bound is encoded in the constants (k_lo = +inf passes every cell,
 // hull_lim = -inf never lowers the threshold), so the chunk body is the same
@@ -552,11 +623,12 @@ __device__ __forceinline__ PairTask pair_task(const QueryParams& p, const ShellS
 constexpr int PAIR_N = LSDF_PAIR_N;
 template <bool BY_POS, bool STAGED>
 __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const ShellView& sv, uint32_t queue,
-                                                const ShellSetup* setups, uint32_t j, int& qlen, int lane) {
+                                                const ShellSetup* setups, uint32_t j, int& qlen, int lane,
+                                                const SegAxes& ga) {
     PairTask t[PAIR_N];
 #pragma unroll
     for (int i = 0; i < PAIR_N; ++i) t[i] = pair_task(p, setups[j + i]);
-    const float4 su0 = p.seg_u[setups[j].l];  // consecutive tasks of a grab share the link (link-major order)
+    const float len = p.seg_u[setups[j].l].w;  // the paired tasks share the link
     const bool share_cfg = p.per_link == nullptr;
     const unsigned nx = (unsigned)p.dims[0], ny = (unsigned)p.dims[1], nz = (unsigned)p.dims[2];
     const unsigned below = (1u << lane) - 1u;
@@ -574,7 +646,7 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
         const float rad_hi = sv_f32<STAGED>(sv.radius, sv.radius_s, k0 + 31);  // the chunk's largest radius
         const unsigned mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
         const int off = (int)((mx * ny + my) * nz + mz);  // C-order offset from the window's corner voxel
-        const float px = (float)mx, py = (float)my, pz = (float)mz;  // offsets folded into A, b
+        const SegCell sc = seg_cell(ga, mx, my, mz);
         bool o[PAIR_N];
 #pragma unroll
         for (int i = 0; i < PAIR_N; ++i) {
@@ -583,29 +655,24 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
             const int lin = inb ? t[i].lin0 + off : 0;  // cells outside the grid read word 0, masked below
             bool occ = t[i].active & inb & ((sv_u32<STAGED>(sv.bits, sv.bits_s, lin >> 5) >> (lin & 31)) & 1u);
             // segment bound (f32, conservative): d(p) - k_lo <= value(p) <= d(p) + k_hi
-            float q[3];
-#pragma unroll
-            for (int e = 0; e < 3; ++e) q[e] = fmaf(pz, st.A[6 + e], fmaf(py, st.A[3 + e], fmaf(px, st.A[e], st.b[e])));
-            const float tt = fminf(fmaxf(fmaf(q[2], su0.z, fmaf(q[1], su0.y, q[0] * su0.x)), 0.0f), su0.w);
-            const float ex = fmaf(-tt, su0.x, q[0]), ey = fmaf(-tt, su0.y, q[1]), ez = fmaf(-tt, su0.z, q[2]);
-            const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+            const float d2 = seg_d2(st.sw, st.sv, sc, len);
             const float lim = t[i].thresh + t[i].k_lo;
-            occ = occ & (lim >= 0.0f) & (d2 <= lim * lim);
+            occ = occ & (lim >= 0.0f) & (d2 <= fmaf(lim, lim, SEG_D2_ERR));
             // a queued cell WILL be looked up, so its upper bound lowers the
             // threshold at once -- only inside the hull of the grid's cell
             // centres, where the upper bound holds
-            const uint32_t m = __reduce_min_sync(FULL_MASK, occ ? __float_as_uint(d2) : 0x7f800000u);
+            const uint32_t m = warp_redux_min(occ ? __float_as_uint(d2) : 0x7f800000u);
             if (m < 0x7f800000u && rad_hi <= t[i].hull_lim) {
-                const float dm = __uint_as_float(m);
-                const float r = dm > 0.0f ? dm * rsqrtf(dm) : 0.0f;  // ~2^-22 relative: rounded up below
+                const float dm = __uint_as_float(m) + SEG_D2_ERR;
+                const float r = dm * rsqrtf(dm);  // ~2^-22 relative: rounded up below
                 t[i].thresh = fminf(t[i].thresh, fmaf(r, 1.0f + 0x1p-18f, t[i].k_hi));
             }
             o[i] = occ;
         }
 #pragma unroll
         for (int i = 0; i < PAIR_N; ++i) {
-            const unsigned bl = __ballot_sync(FULL_MASK, o[i]);
-            if (o[i]) sts_u32(queue + 4u * (uint32_t)(qlen + __popc(bl & below)), cell | ((j + i) << 24));
+            const unsigned bl = warp_ballot(o[i]);
+            sts_u32_if(o[i], queue + 4u * (uint32_t)(qlen + __popc(bl & below)), cell | ((j + i) << 24));
             qlen += __popc(bl);
         }
         __syncwarp();
@@ -632,131 +699,6 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
         }
     }
 }
-#else
-// Per-task scan state of the paired scan (shell_task_pair).
-struct PairTask {
-    float thresh, slack, hull_lim, k_lo, k_hi;
-    float4 su;
-    int ax, ay, az, lin0;
-    bool active, use_seg;
-};
-
-__device__ __forceinline__ PairTask pair_task(const QueryParams& p, const ShellSetup& st) {
-    PairTask t;
-    t.thresh = st.thresh0;
-    t.slack = st.slack;
-    t.hull_lim = st.hull_lim;
-    const float4 sa = p.seg_a[st.l];
-    t.su = p.seg_u[st.l];
-    t.k_lo = sa.w;
-    t.k_hi = p.seg_hi[st.l];
-    t.use_seg = p.seg_filter && t.k_lo >= 0.0f;
-    t.ax = st.ax;
-    t.ay = st.ay;
-    t.az = st.az;
-    t.lin0 = (st.ax * p.dims[1] + st.ay) * p.dims[2] + st.az;
-    t.active = true;
-    return t;
-}
-
-// One task's part of a chunk in the paired scan: occupancy and segment bound
-// of the lane's cell (decoded once for both tasks), and the threshold update
-// from the chunk's queued cells' upper bounds -- shell_task's chunk body.
-template <bool STAGED>
-__device__ __forceinline__ bool pair_chunk(const QueryParams& p, const ShellView& sv, const ShellSetup& st,
-                                           PairTask& t, int mx, int my, int mz, float px, float py, float pz,
-                                           int k0) {
-    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
-    const unsigned x = (unsigned)(t.ax + mx), y = (unsigned)(t.ay + my), z = (unsigned)(t.az + mz);
-    const bool inb = (x < (unsigned)nx) & (y < (unsigned)ny) & (z < (unsigned)nz);
-    const int lin = inb ? t.lin0 + (mx * ny + my) * nz + mz : 0;
-    bool occ = inb & ((sv_u32<STAGED>(sv.bits, sv.bits_s, lin >> 5) >> (lin & 31)) & 1u);
-    if (t.use_seg) {
-        float q[3];
-#pragma unroll
-        for (int e = 0; e < 3; ++e) q[e] = fmaf(pz, st.A[6 + e], fmaf(py, st.A[3 + e], fmaf(px, st.A[e], st.b[e])));
-        const float4 su = t.su;
-        const float tt = fminf(fmaxf(fmaf(q[2], su.z, fmaf(q[1], su.y, q[0] * su.x)), 0.0f), su.w);
-        const float ex = fmaf(-tt, su.x, q[0]), ey = fmaf(-tt, su.y, q[1]), ez = fmaf(-tt, su.z, q[2]);
-        const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
-        const float lim = t.thresh + t.k_lo;
-        occ = occ && lim >= 0.0f && d2 <= lim * lim;
-        const float d2q = occ ? d2 : INFINITY;
-        const uint32_t m = __reduce_min_sync(FULL_MASK, __float_as_uint(d2q));
-        if (m < 0x7f800000u && sv_f32<STAGED>(sv.radius, sv.radius_s, k0 + 31) <= t.hull_lim) {
-            const float dm = __uint_as_float(m);
-            const float r = dm > 0.0f ? dm * rsqrtf(dm) : 0.0f;
-            t.thresh = fminf(t.thresh, fmaf(r, 1.0f + 0x1p-18f, t.k_hi));
-        }
-    }
-    return occ;
-}
-
-// NT tasks of a grab (slots j .. j + NT - 1; split == 1, so all walk the
-// same chunk sequence) scanned together: the chunk's radius and cell are
-// loaded and decoded once, and the tasks' occupancy / bound chains are
-// independent, so the warp has NT dependency chains in flight.  Each task
-// stops at its own first chunk whose bound exceeds its own threshold, as in
-// shell_task; queue entries carry their slot, so lookups and reductions are
-// unchanged.
-constexpr int PAIR_N = LSDF_PAIR_N;
-template <bool BY_POS, bool STAGED>
-__device__ __forceinline__ void shell_task_pair(const QueryParams& p, const ShellView& sv, uint32_t queue,
-                                                const ShellSetup* setups, uint32_t j, int& qlen, int lane) {
-    PairTask t[PAIR_N];
-#pragma unroll
-    for (int i = 0; i < PAIR_N; ++i) t[i] = pair_task(p, setups[j + i]);
-    const bool share_cfg = p.per_link == nullptr;
-    int rounds = 0;
-    for (int k0 = 0; k0 < p.n_shell; k0 += 32) {
-        const float rad = sv_f32<STAGED>(sv.radius, sv.radius_s, k0);
-        bool any = false;
-#pragma unroll
-        for (int i = 0; i < PAIR_N; ++i) {
-            t[i].active = t[i].active && !(rad - t[i].slack > t[i].thresh);  // every later cell is farther
-            any |= t[i].active;
-        }
-        if (!any) break;
-        const uint32_t cell = sv_u32<STAGED>(sv.cells, sv.cells_s, k0 + lane);
-        const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
-        const float px = (float)mx, py = (float)my, pz = (float)mz;
-        bool o[PAIR_N];
-#pragma unroll
-        for (int i = 0; i < PAIR_N; ++i)
-            o[i] = t[i].active && pair_chunk<STAGED>(p, sv, setups[j + i], t[i], mx, my, mz, px, py, pz, k0);
-        const unsigned below = (1u << lane) - 1u;
-#pragma unroll
-        for (int i = 0; i < PAIR_N; ++i) {
-            const unsigned bl = __ballot_sync(FULL_MASK, o[i]);
-            if (o[i]) sts_u32(queue + 4u * (uint32_t)(qlen + __popc(bl & below)), cell | ((j + i) << 24));
-            qlen += __popc(bl);
-        }
-        __syncwarp();
-        while (qlen >= p.round_min) {  // (NT tasks can queue up to 32 NT entries in one chunk)
-            const int n = qlen < 32 ? qlen : 32;
-            const uint32_t entry = lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u;
-            uint32_t ov;
-            lookup_round<BY_POS>(p, sv, setups, entry, lane < n, j, lane, &ov);
-            const uint32_t slot = entry >> 24;  // (ov is 0xffffffff on lanes without an entry)
-#pragma unroll
-            for (int i = 0; i < PAIR_N; ++i) {
-                const uint32_t m = __reduce_min_sync(FULL_MASK, slot == j + i ? ov : 0xffffffffu);
-                if (m != 0xffffffffu) t[i].thresh = fminf(t[i].thresh, from_orderable(m));
-            }
-            if (share_cfg && (++rounds & 3) == 0) {
-#pragma unroll
-                for (int i = 0; i < PAIR_N; ++i) {
-                    const uint64_t k = ~(uint64_t)__ldcg(p.keys + setups[j + i].c);
-                    if (k != ~0ull) t[i].thresh = fminf(t[i].thresh, from_orderable((uint32_t)(k >> 32)));
-                }
-            }
-            qlen -= n;
-            __syncwarp();
-        }
-    }
-}
-
-#endif  // LSDF_PAIR_V2
 
 // One warp, one (configuration c, link l, slice sidx) task: the task in slot
 // `j` of the warp's grab.  Occupied candidate cells go to the warp's queue;
@@ -764,7 +706,8 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
 // next task (the kernel flushes it after the grab).
 template <bool BY_POS, bool BRICKS, bool STAGED>
 __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView& sv, uint32_t queue,
-                                           const ShellSetup* setups, uint32_t j, int& qlen, int lane) {
+                                           const ShellSetup* setups, uint32_t j, int& qlen, int lane,
+                                           const SegAxes& ga) {
     const ShellSetup& st = setups[j];
     const int l = st.l;
     const int64_t c = st.c;
@@ -802,8 +745,8 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
     // lower bound exceeds the threshold can neither undercut nor tie the
     // minimum and skips the exact lookup; every cell that is queued WILL be
     // looked up, so its upper bound may lower the threshold at once.
-    const float4 sa = p.seg_a[l], su = p.seg_u[l];
-    const float k_lo = sa.w, k_hi = p.seg_hi[l];
+    const float4 su = p.seg_u[l];
+    const float k_lo = p.seg_a[l].w, k_hi = p.seg_hi[l];
     const bool use_seg = p.seg_filter && k_lo >= 0.0f;
     const float hull_lim = st.hull_lim;
 #ifdef LSDF_STATS
@@ -837,24 +780,18 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
 #endif
         if (use_seg) {  // (dense clouds: some lane of a chunk is nearly always occupied)
             // every lane evaluates the bound (no divergent branch; most lanes are occupied)
-            const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
-            const float px = (float)mx, py = (float)my, pz = (float)mz;  // offsets folded into A, b
-            float q[3];
-#pragma unroll
-            for (int e = 0; e < 3; ++e) q[e] = fmaf(pz, st.A[6 + e], fmaf(py, st.A[3 + e], fmaf(px, st.A[e], st.b[e])));
-            const float t = fminf(fmaxf(fmaf(q[2], su.z, fmaf(q[1], su.y, q[0] * su.x)), 0.0f), su.w);
-            const float ex = fmaf(-t, su.x, q[0]), ey = fmaf(-t, su.y, q[1]), ez = fmaf(-t, su.z, q[2]);
-            const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+            const SegCell sc = seg_cell(ga, cell & 0xff, (cell >> 8) & 0xff, cell >> 16);
+            const float d2 = seg_d2(st.sw, st.sv, sc, su.w);
             const float lim = thresh + k_lo;
-            occ = occ && lim >= 0.0f && d2 <= lim * lim;
+            occ = occ && lim >= 0.0f && d2 <= fmaf(lim, lim, SEG_D2_ERR);
             const float d2q = occ ? d2 : INFINITY;  // squared segment distance of a cell that stays queued
             // non-negative floats order like their bits: one integer min over the warp
             const uint32_t m = __reduce_min_sync(FULL_MASK, __float_as_uint(d2q));
             // the upper bound d + k_hi holds only for samples inside the grid's
             // cell-centre hull: chunks past the inscribed ball leave thresh alone
             if (m < 0x7f800000u && sv_f32<STAGED>(sv.radius, sv.radius_s, k0 + 31) <= hull_lim) {
-                const float dm = __uint_as_float(m);
-                const float r = dm > 0.0f ? dm * rsqrtf(dm) : 0.0f;  // ~2^-22 relative: rounded up below
+                const float dm = __uint_as_float(m) + SEG_D2_ERR;
+                const float r = dm * rsqrtf(dm);  // ~2^-22 relative: rounded up below
                 thresh = fminf(thresh, fmaf(r, 1.0f + 0x1p-18f, k_hi));
             }
         }
@@ -996,6 +933,7 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
     const uint32_t queue = smem_u32(s_queue + warp * QCAP_SHELL);
     // paired scan (two tasks per chunk walk) for throughput batches of one slice per task
     const bool pair = p.pair_scan && p.split == 1;
+    const SegAxes ga = seg_axes(p);  // (segment-bound cell constants, once per warp)
     // guided grab sizes: the grab shrinks as the remaining work does, so the
     // last warps to finish carry at most a small grab (shorter tail)
     const uint32_t warps_total = gridDim.x * WARPS;
@@ -1034,14 +972,14 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
             while (j + PAIR_N <= cnt) {
                 // the paired tasks share one link (a grab straddles a link boundary at most once)
                 if (s_setup[warp][j].l == s_setup[warp][j + PAIR_N - 1].l) {
-                    shell_task_pair<BY_POS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
+                    shell_task_pair<BY_POS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane, ga);
                     j += PAIR_N;
                 } else {
-                    shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
+                    shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane, ga);
                     ++j;
                 }
             }
-        for (; j < cnt; ++j) shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane);
+        for (; j < cnt; ++j) shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane, ga);
 #ifdef LSDF_TIMING
         const unsigned long long t_g2 = gtime();
         if (lane == 0) TIM(6, t_g2 - t_g1);  // scans of the grab's tasks

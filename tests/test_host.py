@@ -192,6 +192,53 @@ def test_scan_bounds_hold_on_random_grids():
         assert np.any(v[outside] > d[outside] + k_hi)  # why the guard exists (not vacuous)
 
 
+def test_segment_bound_quadratic_form():
+    """The scan's f32 segment distance (lsdf_query.cu seg_d2: |q|^2 - s^2 + (s - t)^2
+    from per-task constants 2 A b, |b|^2, A u, b.u and per-cell sigma^2 |m'|^2, with
+    fma emulated as one rounding of the exact fp64 product-sum) stays within
+    SEG_D2_ERR / 4 = 2^-23 m^2 of the exact squared distance, over random rotations,
+    window residuals, segments and every window cell."""
+    f32 = np.float32
+    rng = np.random.default_rng(11)
+
+    def fma(a, b, c):
+        return f32(np.float64(a) * np.float64(b) + np.float64(c))
+
+    n, W, e_r, r_e = 300_000, 16, 0.32, 0.04
+    P = (np.arange(W) - W // 2) * r_e / e_r
+    qn = rng.normal(size=(n, 4))
+    qn /= np.linalg.norm(qn, axis=1, keepdims=True)
+    w, x, y, z = qn.T
+    R = np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w),
+                  2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w),
+                  2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)], 1).reshape(n, 3, 3)
+    dtinv = rng.uniform(-0.1, 0.1, (n, 3))
+    a3 = rng.uniform(-0.12, 0.12, (n, 3)).astype(f32).astype(np.float64)
+    u = rng.normal(size=(n, 3))
+    u = (u / np.linalg.norm(u, axis=1, keepdims=True)).astype(f32).astype(np.float64)
+    L = rng.uniform(0, 0.25, n).astype(f32)
+    m = rng.integers(0, W, (n, 3))
+    c = W // 2
+    # exact: the fp64 link-frame point (placement.py:164-167) minus the segment origin
+    q = e_r * (np.einsum("na,nak->nk", P[m], R) + dtinv) - a3
+    s_ex = np.einsum("nk,nk->n", q, u)
+    t_ex = np.clip(s_ex, 0, L.astype(np.float64))
+    d2_ex = np.sum((q - t_ex[:, None] * u) ** 2, axis=1)
+    # the kernel's constants (shell_setup) and evaluation (seg_cell, seg_d2)
+    f = e_r * (P[1] - P[0])
+    b = e_r * dtinv - a3 + e_r * np.einsum("a,nak->nk", np.full(3, P[c]), R)
+    sw = np.concatenate([2 * f * np.einsum("nak,nk->na", R, b), np.sum(b * b, 1)[:, None]], 1).astype(f32)
+    sv = np.concatenate([f * np.einsum("nak,nk->na", R, u), np.sum(b * u, 1)[:, None]], 1).astype(f32)
+    s2 = f32(f * f)
+    px, py, pz = [(m[:, i] - c).astype(f32) for i in range(3)]
+    mm = fma(px, f32(px * s2), fma(py, f32(py * s2), f32(f32(pz * pz) * s2)))
+    qq = fma(pz, sw[:, 2], fma(py, sw[:, 1], fma(px, sw[:, 0], f32(mm + sw[:, 3]))))
+    sp = fma(pz, sv[:, 2], fma(py, sv[:, 1], fma(px, sv[:, 0], sv[:, 3])))
+    dd = f32(sp - np.minimum(np.maximum(sp, f32(0)), L))
+    d2 = np.maximum(fma(dd, dd, fma(-sp, sp, qq)), f32(0))
+    assert np.abs(d2.astype(np.float64) - d2_ex).max() <= 2.0 ** -23
+
+
 def test_link_major_threshold_matches_fk_crossover():
     """The checker keeps poses link-major from the batch size at which FK runs one
     thread per configuration (the kernel whose writes the layout serves)."""
