@@ -23,6 +23,7 @@
 // query_direct_kernel (fallback when a link's far value is below the clamp or
 // the mask has no column intervals): walks the window's (x, y) columns over
 // the kept z-interval of each, with `split` column slices per (c, l).
+#include <cstddef>
 #include <cstdlib>
 
 #include "lsdf_async.cuh"
@@ -349,14 +350,24 @@ struct __align__(16) ShellSetup {
     // m'.(2 A b) + |b|^2 and q.u = m'.(A u) + b.u
     float4 sw;   // (2 A b, |b|^2)
     float4 sv;   // (A u, b.u)
+    // the paired scan's per-task state, read as two 16-B records:
+    float thresh0;   // starting threshold: min(clamp, the configuration's best key at setup time)
     float slack;     // |dt| (rounded up) + core radius of the link
     float hull_lim;  // cells with shell radius <= hull_lim map inside the link grid's cell-centre hull
+                     // (-inf: the segment bound is off)
+    float k_lo;      // segment bound kappa_lo (+inf: off, every cell passes)
+    int32_t ax, ay, az;
+    int32_t lin0;    // C-order index of window cell (0, 0, 0)
+    float k_hi;      // segment bound kappa_hi
     int32_t l;       // geometry link
     int32_t c;       // configuration
     int32_t sidx;    // slice of the shell list
-    int32_t ax, ay, az;
-    float thresh0;   // starting threshold: min(clamp, the configuration's best key at setup time)
 };
+
+static_assert(offsetof(ShellSetup, thresh0) % 16 == 0 && offsetof(ShellSetup, ax) % 16 == 0 &&
+                  offsetof(ShellSetup, k_lo) == offsetof(ShellSetup, thresh0) + 12 &&
+                  offsetof(ShellSetup, lin0) == offsetof(ShellSetup, ax) + 12,
+              "pair_task reads (thresh0, slack, hull_lim, k_lo) and (ax, ay, az, lin0) as 16-B records");
 
 // Dilated brick occupancy (throughput batches): a (bx, by) column word whose
 // bit bz is set when some occupied brick lies within `dilate` bricks of
@@ -422,6 +433,12 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, const int* ord
     for (int e = 0; e < 9; ++e) s.R[e] = R[e];
 #pragma unroll
     for (int e = 0; e < 3; ++e) s.dtinv[e] = dtinv[e];
+    // segment bound off unless set below: every cell passes, the threshold is never lowered by it
+    s.sw = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    s.sv = s.sw;
+    s.k_lo = INFINITY;
+    s.hull_lim = -INFINITY;
+    s.k_hi = 0.0f;
     if (p.seg_filter) {  // segment-bound constants (throughput batches only)
         const float4 sa = p.seg_a[l], su = p.seg_u[l];
         const double a3[3] = {sa.x, sa.y, sa.z}, u3[3] = {su.x, su.y, su.z};
@@ -453,6 +470,10 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, const int* ord
         // inside the hull of the grid's cell centres, where the segment's upper
         // bound holds (outside it the sample is the link's far value)
         s.hull_lim = (float)(p.hull - (double)dtn) * (1.0f - 0x1p-20f) - 1e-6f;
+        const bool use_seg = sa.w >= 0.0f;  // (kappa_lo < 0: disabled for this link)
+        s.k_lo = use_seg ? sa.w : INFINITY;
+        if (!use_seg) s.hull_lim = -INFINITY;
+        s.k_hi = p.seg_hi[l];
     }
     s.slack = dtn + p.core[l];
     float t0 = p.clamp;  // values >= clamp never change the answer
@@ -467,6 +488,7 @@ __device__ __forceinline__ void shell_setup(const QueryParams& p, const int* ord
     s.ax = __ldg(p.anchor + o * 3);
     s.ay = __ldg(p.anchor + o * 3 + 1);
     s.az = __ldg(p.anchor + o * 3 + 2);
+    s.lin0 = (s.ax * p.dims[1] + s.ay) * p.dims[2] + s.az;
     if (dil != nullptr) {  // nothing occupied near the window: the task stops at its first chunk
         const unsigned bx = (unsigned)(s.ax + p.W[0] / 2) >> BRICK_LOG2, by = (unsigned)(s.ay + p.W[1] / 2) >> BRICK_LOG2;
         const unsigned bz = (unsigned)(s.az + p.W[2] / 2) >> BRICK_LOG2;
@@ -593,19 +615,19 @@ struct PairTask {
     bool active;
 };
 
-__device__ __forceinline__ PairTask pair_task(const QueryParams& p, const ShellSetup& st) {
+__device__ __forceinline__ PairTask pair_task(const ShellSetup& st) {  // (seg_filter is on)
+    const float4 f = *reinterpret_cast<const float4*>(&st.thresh0);
+    const int4 a = *reinterpret_cast<const int4*>(&st.ax);
     PairTask t;
-    t.thresh = st.thresh0;
-    t.slack = st.slack;
-    const float k_lo = p.seg_a[st.l].w;
-    const bool use_seg = p.seg_filter && k_lo >= 0.0f;
-    t.k_lo = use_seg ? k_lo : INFINITY;
-    t.k_hi = p.seg_hi[st.l];
-    t.hull_lim = use_seg ? st.hull_lim : -INFINITY;
-    t.ax = st.ax;
-    t.ay = st.ay;
-    t.az = st.az;
-    t.lin0 = (st.ax * p.dims[1] + st.ay) * p.dims[2] + st.az;
+    t.thresh = f.x;
+    t.slack = f.y;
+    t.hull_lim = f.z;
+    t.k_lo = f.w;
+    t.k_hi = st.k_hi;
+    t.ax = a.x;
+    t.ay = a.y;
+    t.az = a.z;
+    t.lin0 = a.w;
     t.active = true;
     return t;
 }
@@ -627,7 +649,7 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
                                                 const SegAxes& ga) {
     PairTask t[PAIR_N];
 #pragma unroll
-    for (int i = 0; i < PAIR_N; ++i) t[i] = pair_task(p, setups[j + i]);
+    for (int i = 0; i < PAIR_N; ++i) t[i] = pair_task(setups[j + i]);
     const float len = p.seg_u[setups[j].l].w;  // the paired tasks share the link
     const bool share_cfg = p.per_link == nullptr;
     const unsigned nx = (unsigned)p.dims[0], ny = (unsigned)p.dims[1], nz = (unsigned)p.dims[2];
