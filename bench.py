@@ -220,6 +220,31 @@ def _e2e_entry(C_total, pipe_ms, single_ms, h2d, d2h, world=1):
             "pipelined_ms_per_step": pipe_ms, "single_cycle_ms": single_ms}
 
 
+def _h2d_peak_gbs(torch, nbytes=64 << 20, reps=5):
+    """Measured host->device copy bandwidth from page-locked memory (best of `reps`, CUDA events):
+    the denominator of the e2e path's PCIe bound."""
+    src = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    best = float("inf")
+    for _ in range(reps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return nbytes / (best / 1e3) / 1e9
+
+
+def _pcie_bound(e2e, peak_gbs):
+    """The e2e path's bound: every cycle's inputs cross PCIe (H2D), overlapped with the compute of
+    the cycles in flight, so the pipelined step can be no shorter than h2d_bytes / H2D bandwidth."""
+    ms = e2e["ms_per_step"]
+    ach = e2e["h2d_bytes_per_step"] / (ms / 1e3) / 1e9
+    return {"bound": "pcie_h2d", "achieved": ach, "peak": peak_gbs, "unit": "GB/s", "frac": ach / peak_gbs,
+            "peak_kind": "measured in this run: 64 MiB page-locked -> device copy, best of 5"}
+
+
 def run_ours(args, rank, world, dist, sampler):
     import torch
 
@@ -374,6 +399,8 @@ def run_ours(args, rank, world, dist, sampler):
                          "peak_gbs": peak, "peak_kind": peak_kind},
         "clocks": clocks,
     }
+    if world == 1:  # (N > 1: each rank moves 1/N of the cloud, see ShardedCloudPipeline)
+        out["e2e"]["roofline"] = _pcie_bound(out["e2e"], _h2d_peak_gbs(torch))
     if variants is not None:
         out["cloud_variants"] = variants
     # the bound the kernel meets: its warp-instruction stream
