@@ -201,7 +201,10 @@ __device__ __forceinline__ bool fk_align_body(const FkParams& p, int lp_log2) {
 // kernel keeps small batches latency-short.
 constexpr int FKS_THREADS = 64;
 
-template <bool STAGE, bool LM>
+// FAR: some link's parent is not the link before it; those parents' poses go
+// through a per-thread array (local memory).  Serial chains (every arm here)
+// compile without it.
+template <bool STAGE, bool LM, bool FAR = true>
 __device__ __forceinline__ bool fk_serial_body(const FkParams& p) {
     bool counted = false;
     // every thread walks the same link at the same time: the chain table is
@@ -209,7 +212,7 @@ __device__ __forceinline__ bool fk_serial_body(const FkParams& p) {
     const lsdf_link* s_links = p.links;
     __shared__ bool s_far_child[LSDF_MAX_LINKS];  // link k is the parent of a link other than k + 1
     extern __shared__ double s_out[];  // [FKS_THREADS * n_geo * 9] R, [.. * 3] dt, then i32 anchors
-    {
+    if (FAR) {
         if (threadIdx.x < LSDF_MAX_LINKS) {
             bool f = false;
             for (int j = 0; j < p.n_links; ++j)
@@ -249,7 +252,7 @@ __device__ __forceinline__ bool fk_serial_body(const FkParams& p) {
         // world pose of the previous link in registers (serial chains); poses
         // a later non-adjacent child needs go to a per-thread local array
         double prev[12];
-        double world[LSDF_MAX_LINKS][12];
+        double world[FAR ? LSDF_MAX_LINKS : 1][12];
         // the joints' sines and cosines first: independent of the chain, so
         // they overlap instead of sitting on its dependent path
         double sn[LSDF_MAX_LINKS], cs[LSDF_MAX_LINKS];
@@ -283,13 +286,13 @@ __device__ __forceinline__ bool fk_serial_body(const FkParams& p) {
                 tj[0] = tj[1] = tj[2] = 0.0;
             } else {
                 double rp[9], tp[3], tmp[3];
-                if (L.parent == k2 - 1) {
+                if (!FAR || L.parent == k2 - 1) {
 #pragma unroll
                     for (int e = 0; e < 9; ++e) rp[e] = prev[e];
 #pragma unroll
                     for (int k = 0; k < 3; ++k) tp[k] = prev[9 + k];
                 } else {
-                    const double* wp = world[L.parent];
+                    const double* wp = world[FAR ? L.parent : 0];
 #pragma unroll
                     for (int e = 0; e < 9; ++e) rp[e] = wp[e];
 #pragma unroll
@@ -309,8 +312,8 @@ __device__ __forceinline__ bool fk_serial_body(const FkParams& p) {
             for (int e = 0; e < 9; ++e) prev[e] = R[e];
 #pragma unroll
             for (int k = 0; k < 3; ++k) prev[9 + k] = T[k];
-            if (s_far_child[k2]) {
-                double* w = world[k2];
+            if (FAR && s_far_child[k2]) {
+                double* w = world[FAR ? k2 : 0];
 #pragma unroll
                 for (int e = 0; e < 12; ++e) w[e] = prev[e];
             }
@@ -390,9 +393,9 @@ __global__ void __launch_bounds__(FK_THREADS) fk_align_kernel(const __grid_const
     fk_epilogue(p, counted);
 }
 
-template <bool STAGE, bool LM>
+template <bool STAGE, bool LM, bool FAR = true>
 __global__ void __launch_bounds__(FKS_THREADS) fk_align_serial_kernel(const __grid_constant__ FkParams p) {
-    const bool counted = fk_serial_body<STAGE, LM>(p);
+    const bool counted = fk_serial_body<STAGE, LM, FAR>(p);
     fk_epilogue(p, counted);
 }
 
@@ -455,8 +458,13 @@ int fk_align_impl(const lsdf_link* links, int32_t n_links, int32_t n_geo, const 
     if (flags_dev != nullptr && !flags_self_reset)
         LSDF_TRY(check_cuda(cudaMemsetAsync(flags_dev, 0, 2 * sizeof(int32_t), (cudaStream_t)stream), "fk flags memset"));
     static const int64_t serial_min = [] { const char* v = getenv("LSDF_TUNE_FKSERIAL"); return v && *v ? atoll(v) : FK_SERIAL_MIN; }();
+    bool far = false;  // a link whose parent is not the link before it
+    for (int j = 0; j < n_links; ++j) far |= links[j].kind != 0 && links[j].parent != j - 1;
     if (C >= serial_min && link_major) {
-        fk_align_serial_kernel<true, true><<<grid_for(C, FKS_THREADS), FKS_THREADS, 0, (cudaStream_t)stream>>>(p);
+        if (far)
+            fk_align_serial_kernel<true, true, true><<<grid_for(C, FKS_THREADS), FKS_THREADS, 0, (cudaStream_t)stream>>>(p);
+        else
+            fk_align_serial_kernel<true, true, false><<<grid_for(C, FKS_THREADS), FKS_THREADS, 0, (cudaStream_t)stream>>>(p);
         return check_launch("fk_align_serial_kernel");
     }
     if (C >= serial_min) {
