@@ -48,6 +48,7 @@ struct QueryParams {
     int32_t stage_bricks;                   // brick columns copied to shared memory (else read from global)
     int32_t dilate;                         // > 0: empty-neighbourhood test at setup, dilation radius in bricks
     int32_t pair_scan;                      // throughput scan walks two tasks per chunk loop (shell_task_pair)
+    int32_t skip_empty;                     // paired scan skips chunks without occupied cells: 0 never, 1 sparse clouds, 2 always
     const uint32_t* brick_cols;             // the occupancy brick columns (input of the dilation)
     int32_t nbx_brick, nbz_brick;           // brick grid (x columns, z bits)
     int32_t nby_brick;                      // brick columns per x row
@@ -643,7 +644,12 @@ __device__ __forceinline__ PairTask pair_task(const ShellSetup& st) {  // (seg_f
 // threshold, as in shell_task; queue entries carry their slot, so lookups and
 // reductions are unchanged.
 constexpr int PAIR_N = LSDF_PAIR_N;
-template <bool BY_POS, bool STAGED>
+constexpr int64_t SPARSE_FRACTION = 20;  // "sparse": under 5 % of the voxels occupied (config 4's crowd: 40 %)
+// SKIP (sparse clouds, chosen per CTA from the occupied fraction): a chunk in
+// which neither task has an occupied cell goes straight to the next chunk
+// (no bound, no ballots).  Dense clouds almost never have such a chunk and do
+// without the vote.
+template <bool BY_POS, bool STAGED, bool SKIP>
 __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const ShellView& sv, uint32_t queue,
                                                 const ShellSetup* setups, uint32_t j, int& qlen, int lane,
                                                 const SegAxes& ga) {
@@ -670,12 +676,19 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
         const int off = (int)((mx * ny + my) * nz + mz);  // C-order offset from the window's corner voxel
         const SegCell sc = seg_cell(ga, mx, my, mz);
         bool o[PAIR_N];
+        bool any_occ = false;
+#pragma unroll
+        for (int i = 0; i < PAIR_N; ++i) {
+            const bool inb = ((unsigned)t[i].ax + mx < nx) & ((unsigned)t[i].ay + my < ny) & ((unsigned)t[i].az + mz < nz);
+            const int lin = inb ? t[i].lin0 + off : 0;  // cells outside the grid read word 0, masked below
+            o[i] = t[i].active & inb & ((sv_u32<STAGED>(sv.bits, sv.bits_s, lin >> 5) >> (lin & 31)) & 1u);
+            any_occ |= o[i];
+        }
+        if (SKIP && warp_ballot(any_occ) == 0u) continue;
 #pragma unroll
         for (int i = 0; i < PAIR_N; ++i) {
             const ShellSetup& st = setups[j + i];
-            const bool inb = ((unsigned)t[i].ax + mx < nx) & ((unsigned)t[i].ay + my < ny) & ((unsigned)t[i].az + mz < nz);
-            const int lin = inb ? t[i].lin0 + off : 0;  // cells outside the grid read word 0, masked below
-            bool occ = t[i].active & inb & ((sv_u32<STAGED>(sv.bits, sv.bits_s, lin >> 5) >> (lin & 31)) & 1u);
+            bool occ = o[i];
             // segment bound (f32, conservative): d(p) - k_lo <= value(p) <= d(p) + k_hi
             const float d2 = seg_d2(st.sw, st.sv, sc, len);
             const float lim = t[i].thresh + t[i].k_lo;
@@ -956,6 +969,26 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
     // paired scan (two tasks per chunk walk) for throughput batches of one slice per task
     const bool pair = p.pair_scan && p.split == 1;
     const SegAxes ga = seg_axes(p);  // (segment-bound cell constants, once per warp)
+    // sparse clouds (throughput batches): the paired scan skips chunks with no
+    // occupied cell when under 1/SPARSE_FRACTION of the voxels are occupied;
+    // each warp estimates the fraction from 128 bitmap words spread over the
+    // grid (no CTA barrier on the prologue)
+    bool skip_empty = false;
+    if (!BRICKS && pair && p.skip_empty) {
+        const int64_t step = n_words / 128 > 1 ? n_words / 128 : 1;
+        uint32_t cnt = 0, words = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t w = (int64_t)(lane + 32 * k) * step;
+            if (w < n_words) {
+                cnt += __popc(sv_u32<STAGED>(sv.bits, sv.bits_s, (int)w));
+                ++words;
+            }
+        }
+        cnt = __reduce_add_sync(FULL_MASK, cnt);
+        words = __reduce_add_sync(FULL_MASK, words);
+        skip_empty = p.skip_empty == 2 || (int64_t)cnt * SPARSE_FRACTION < (int64_t)words * 32;
+    }
     // guided grab sizes: the grab shrinks as the remaining work does, so the
     // last warps to finish carry at most a small grab (shorter tail)
     const uint32_t warps_total = gridDim.x * WARPS;
@@ -994,7 +1027,10 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
             while (j + PAIR_N <= cnt) {
                 // the paired tasks share one link (a grab straddles a link boundary at most once)
                 if (s_setup[warp][j].l == s_setup[warp][j + PAIR_N - 1].l) {
-                    shell_task_pair<BY_POS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane, ga);
+                    if (skip_empty)
+                        shell_task_pair<BY_POS, STAGED, true>(p, sv, queue, s_setup[warp], j, qlen, lane, ga);
+                    else
+                        shell_task_pair<BY_POS, STAGED, false>(p, sv, queue, s_setup[warp], j, qlen, lane, ga);
                     j += PAIR_N;
                 } else {
                     shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane, ga);
@@ -1259,6 +1295,8 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
 #else
             p.pair_scan = t_pair;
 #endif
+            static const int t_skip = tune("LSDF_TUNE_SKIPEMPTY", 1);
+            p.skip_empty = t_skip;
             const int variant = (p.by_position ? 2 : 0) + (p.bricks != nullptr ? 1 : 0) +
                                 (t_lds && stage_shell && stage_bits ? 4 : 0);
             const ShellsKernel kern = kernels[variant];
