@@ -281,6 +281,11 @@ struct ShellView {
     uint32_t P_s;                        // shared-window address of P
 };
 
+// the value of x, hidden from the optimizer (no rematerialization from its inputs)
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(x));
+    return x;
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -867,7 +872,7 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
                                                                   int stage_shell, int stage_bits, int64_t n_words,
                                                                   int last_launch) {
     extern __shared__ double s_dyn[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, lane = (int)opaque_u32(threadIdx.x & 31);
 #ifdef LSDF_TIMING
     const unsigned long long t_entry = gtime();
     if (lane == 0) atomicMin(g_tim + 0, t_entry);
@@ -959,13 +964,15 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
     sv.cells = (STAGED || stage_shell) ? s_cells : p.shell_cells;
     sv.radius = (STAGED || stage_shell) ? s_radius : p.shell_radius;
     sv.bits = (STAGED || stage_bits) ? s_bits : p.bitmap;
-    sv.cells_s = smem_u32(s_cells);
-    sv.radius_s = smem_u32(s_radius);
-    sv.bits_s = smem_u32(s_bits);
-    sv.P_s = smem_u32(sP);
+    // (opaque to the compiler: it would otherwise rematerialize these
+    // shared-window addresses from the dynamic-smem base in every chunk)
+    sv.cells_s = opaque_u32(smem_u32(s_cells));
+    sv.radius_s = opaque_u32(smem_u32(s_radius));
+    sv.bits_s = opaque_u32(smem_u32(s_bits));
+    sv.P_s = opaque_u32(smem_u32(sP));
     sv.bricks = n_cols ? s_bricks : p.bricks;
     sv.P = sP;
-    const uint32_t queue = smem_u32(s_queue + warp * QCAP_SHELL);
+    const uint32_t queue = opaque_u32(smem_u32(s_queue + warp * QCAP_SHELL));
     // paired scan (two tasks per chunk walk) for throughput batches of one slice per task
     const bool pair = p.pair_scan && p.split == 1;
     const SegAxes ga = seg_axes(p);  // (segment-bound cell constants, once per warp)
