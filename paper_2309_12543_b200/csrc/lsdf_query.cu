@@ -286,6 +286,11 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
     asm volatile("mov.b32 %0, %0;" : "+r"(x));
     return x;
 }
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -662,6 +667,9 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
 #pragma unroll
     for (int i = 0; i < PAIR_N; ++i) t[i] = pair_task(setups[j + i]);
     const float len = p.seg_u[setups[j].l].w;  // the paired tasks share the link
+    // the tasks' segment constants, read per chunk through an opaque shared
+    // address (not rematerialized from the array base every chunk)
+    const uint32_t st_s = opaque_u32(smem_u32(&setups[j]));
     const bool share_cfg = p.per_link == nullptr;
     const unsigned nx = (unsigned)p.dims[0], ny = (unsigned)p.dims[1], nz = (unsigned)p.dims[2];
     const unsigned below = (1u << lane) - 1u;
@@ -692,10 +700,11 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
         if (SKIP && warp_ballot(any_occ) == 0u) continue;
 #pragma unroll
         for (int i = 0; i < PAIR_N; ++i) {
-            const ShellSetup& st = setups[j + i];
             bool occ = o[i];
             // segment bound (f32, conservative): d(p) - k_lo <= value(p) <= d(p) + k_hi
-            const float d2 = seg_d2(st.sw, st.sv, sc, len);
+            const uint32_t sa = st_s + (uint32_t)(i * sizeof(ShellSetup));
+            const float d2 = seg_d2(lds_f4(sa + (uint32_t)offsetof(ShellSetup, sw)),
+                                    lds_f4(sa + (uint32_t)offsetof(ShellSetup, sv)), sc, len);
             const float lim = t[i].thresh + t[i].k_lo;
             occ = occ & (lim >= 0.0f) & (d2 <= fmaf(lim, lim, SEG_D2_ERR));
             // a queued cell WILL be looked up, so its upper bound lowers the
