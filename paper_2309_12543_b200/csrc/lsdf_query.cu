@@ -281,6 +281,12 @@ struct ShellView {
     uint32_t P_s;                        // shared-window address of P
 };
 
+// MUFU.RSQ alone (rsqrtf adds a subnormal-input fix-up; callers pass normal values)
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 // the value of x, hidden from the optimizer (no rematerialization from its inputs)
 __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
     asm volatile("mov.b32 %0, %0;" : "+r"(x));
@@ -671,7 +677,10 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
     // address (not rematerialized from the array base every chunk)
     const uint32_t st_s = opaque_u32(smem_u32(&setups[j]));
     const bool share_cfg = p.per_link == nullptr;
-    const unsigned nx = (unsigned)p.dims[0], ny = (unsigned)p.dims[1], nz = (unsigned)p.dims[2];
+    // grid dimensions in registers for the whole walk (not reloaded from the
+    // constant bank every chunk)
+    const unsigned nx = opaque_u32((unsigned)p.dims[0]), ny = opaque_u32((unsigned)p.dims[1]),
+                   nz = opaque_u32((unsigned)p.dims[2]);
     const unsigned below = (1u << lane) - 1u;
     int rounds = 0;
     for (int k0 = 0; k0 < p.n_shell; k0 += 32) {
@@ -712,8 +721,8 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
             // centres, where the upper bound holds
             const uint32_t m = warp_redux_min(occ ? __float_as_uint(d2) : 0x7f800000u);
             if (m < 0x7f800000u && rad_hi <= t[i].hull_lim) {
-                const float dm = __uint_as_float(m) + SEG_D2_ERR;
-                const float r = dm * rsqrtf(dm);  // ~2^-22 relative: rounded up below
+                const float dm = __uint_as_float(m) + SEG_D2_ERR;  // (>= 2^-21: never subnormal)
+                const float r = dm * rsqrt_approx(dm);  // ~2^-22 relative: rounded up below
                 t[i].thresh = fminf(t[i].thresh, fmaf(r, 1.0f + 0x1p-18f, t[i].k_hi));
             }
             o[i] = occ;
