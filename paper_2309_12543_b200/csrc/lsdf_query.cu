@@ -682,8 +682,9 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
     const unsigned nx = opaque_u32((unsigned)p.dims[0]), ny = opaque_u32((unsigned)p.dims[1]),
                    nz = opaque_u32((unsigned)p.dims[2]);
     const unsigned below = (1u << lane) - 1u;
+    const int n_shell = (int)opaque_u32((uint32_t)p.n_shell), round_min = (int)opaque_u32((uint32_t)p.round_min);
     int rounds = 0;
-    for (int k0 = 0; k0 < p.n_shell; k0 += 32) {
+    for (int k0 = 0; k0 < n_shell; k0 += 32) {
         const float rad = sv_f32<STAGED>(sv.radius, sv.radius_s, k0);
         bool any = false;
 #pragma unroll
@@ -707,6 +708,7 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
             any_occ |= o[i];
         }
         if (SKIP && warp_ballot(any_occ) == 0u) continue;
+        uint32_t mins[PAIR_N];
 #pragma unroll
         for (int i = 0; i < PAIR_N; ++i) {
             bool occ = o[i];
@@ -714,18 +716,28 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
             const uint32_t sa = st_s + (uint32_t)(i * sizeof(ShellSetup));
             const float d2 = seg_d2(lds_f4(sa + (uint32_t)offsetof(ShellSetup, sw)),
                                     lds_f4(sa + (uint32_t)offsetof(ShellSetup, sv)), sc, len);
-            const float lim = t[i].thresh + t[i].k_lo;
-            occ = occ & (lim >= 0.0f) & (d2 <= fmaf(lim, lim, SEG_D2_ERR));
-            // a queued cell WILL be looked up, so its upper bound lowers the
-            // threshold at once -- only inside the hull of the grid's cell
-            // centres, where the upper bound holds
-            const uint32_t m = warp_redux_min(occ ? __float_as_uint(d2) : 0x7f800000u);
-            if (m < 0x7f800000u && rad_hi <= t[i].hull_lim) {
-                const float dm = __uint_as_float(m) + SEG_D2_ERR;  // (>= 2^-21: never subnormal)
-                const float r = dm * rsqrt_approx(dm);  // ~2^-22 relative: rounded up below
-                t[i].thresh = fminf(t[i].thresh, fmaf(r, 1.0f + 0x1p-18f, t[i].k_hi));
-            }
+            // (lim < 0: only cells with d2 <= SEG_D2_ERR pass -- extra lookups, never a missed cell)
+            const float lim = fmaxf(t[i].thresh + t[i].k_lo, 0.0f);
+            occ = occ & (d2 <= fmaf(lim, lim, SEG_D2_ERR));
             o[i] = occ;
+            mins[i] = warp_redux_min(occ ? __float_as_uint(d2) : 0x7f800000u);
+        }
+        // a queued cell WILL be looked up, so its upper bound lowers the
+        // threshold at once -- only inside the hull of the grid's cell
+        // centres, where the upper bound holds (one branch for the tasks)
+        bool upd[PAIR_N], any_upd = false;
+#pragma unroll
+        for (int i = 0; i < PAIR_N; ++i) {
+            upd[i] = (mins[i] < 0x7f800000u) & (rad_hi <= t[i].hull_lim);
+            any_upd |= upd[i];
+        }
+        if (any_upd) {
+#pragma unroll
+            for (int i = 0; i < PAIR_N; ++i) {
+                const float dm = __uint_as_float(mins[i]) + SEG_D2_ERR;  // (>= 2^-21: never subnormal)
+                const float r = dm * rsqrt_approx(dm);  // ~2^-22 relative: rounded up below
+                if (upd[i]) t[i].thresh = fminf(t[i].thresh, fmaf(r, 1.0f + 0x1p-18f, t[i].k_hi));
+            }
         }
 #pragma unroll
         for (int i = 0; i < PAIR_N; ++i) {
@@ -734,7 +746,7 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
             qlen += __popc(bl);
         }
         __syncwarp();
-        while (qlen >= p.round_min) {  // (NT tasks can queue up to 32 NT entries in one chunk)
+        while (qlen >= round_min) {  // (NT tasks can queue up to 32 NT entries in one chunk)
             const int n = qlen < 32 ? qlen : 32;
             const uint32_t entry = lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u;
             uint32_t ov;
