@@ -785,7 +785,11 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
     const float slack = st.slack;
     const int ax = st.ax, ay = st.ay, az = st.az;
     const int Wm = p.Wmax;
-    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    // loop-invariant launch constants in registers (opaque: not reloaded per chunk)
+    const int nx = (int)opaque_u32((uint32_t)p.dims[0]), ny = (int)opaque_u32((uint32_t)p.dims[1]),
+              nz = (int)opaque_u32((uint32_t)p.dims[2]);
+    const int n_shell = (int)opaque_u32((uint32_t)p.n_shell), stride = (int)opaque_u32(32u * (uint32_t)p.split);
+    const int round_min = (int)opaque_u32((uint32_t)p.round_min);
     const int lin0 = (ax * ny + ay) * nz + az;
     const bool share_cfg = p.per_link == nullptr;
 
@@ -822,7 +826,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
 #ifdef LSDF_STATS
     unsigned long long sc[8] = {1, 0, 0, 0, 0, 0, 0, 0};
 #endif
-    for (int k0 = sidx * 32; k0 < p.n_shell; k0 += 32 * p.split) {
+    for (int k0 = sidx * 32; k0 < n_shell; k0 += stride) {
         if (sv_f32<STAGED>(sv.radius, sv.radius_s, k0) - slack > thresh) {  // every later cell is farther
             STAT(6, 1);
             STAT(7, k0 == sidx * 32);
@@ -870,7 +874,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
         qlen += __popc(ballot);
         STAT(4, __popc(ballot));
         __syncwarp();
-        if (qlen >= p.round_min) {
+        if (qlen >= round_min) {
             STAT(5, 1);
             const int n = qlen < 32 ? qlen : 32;
             const uint32_t m = lookup_round<BY_POS>(p, sv, setups, lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u, lane < n,
