@@ -292,6 +292,21 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
     asm volatile("mov.b32 %0, %0;" : "+r"(x));
     return x;
 }
+__device__ __forceinline__ int32_t lds_s32(uint32_t a) {
+    int32_t v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int4 lds_i4(uint32_t a) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double2 lds_d2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -381,6 +396,8 @@ struct __align__(16) ShellSetup {
     int32_t sidx;    // slice of the shell list
 };
 
+static_assert(offsetof(ShellSetup, R) == 0 && offsetof(ShellSetup, dtinv) == 72 && sizeof(ShellSetup) % 16 == 0,
+              "lookup_round reads R and dtinv at fixed offsets");
 static_assert(offsetof(ShellSetup, thresh0) % 16 == 0 && offsetof(ShellSetup, ax) % 16 == 0 &&
                   offsetof(ShellSetup, k_lo) == offsetof(ShellSetup, thresh0) + 12 &&
                   offsetof(ShellSetup, lin0) == offsetof(ShellSetup, ax) + 12,
@@ -543,25 +560,40 @@ __device__ unsigned long long g_stats[8];
 // warp's grab can share a round, so a task's leftover lookups ride with the
 // next task's instead of costing a partial round each.  Returns the
 // orderable minimum over the entries of task slot `cur`.
+// setups_s: the shared-window address of the warp's ShellSetup array (opaque,
+// so its base is not rebuilt from the shared-memory window every round)
 template <bool BY_POS>
 __device__ __forceinline__ uint32_t lookup_round(const QueryParams& p, const ShellView& sv,
-                                                 const ShellSetup* setups, uint32_t entry, bool valid, uint32_t cur,
+                                                 uint32_t setups_s, uint32_t entry, bool valid, uint32_t cur,
                                                  int lane, uint32_t* ov_out = nullptr) {
     const uint32_t slot = valid ? entry >> 24 : 0xffu;
     uint32_t ov = 0xffffffffu, pk = 0xffffffffu;
     int64_t c = 0;
     int l = 0;
     if (valid) {
-        const ShellSetup& st = setups[slot];
-        l = st.l;
-        c = st.c;
+        const uint32_t sa = setups_s + slot * (uint32_t)sizeof(ShellSetup);
+        l = lds_s32(sa + (uint32_t)offsetof(ShellSetup, l));
+        c = lds_s32(sa + (uint32_t)offsetof(ShellSetup, c));
+        double R[9], dtinv[3];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const double2 r2 = lds_d2(sa + 16u * e);
+            R[2 * e] = r2.x;
+            R[2 * e + 1] = r2.y;
+        }
+        R[8] = lds_f64(sa + 64u);
+        dtinv[0] = lds_f64(sa + 72u);
+        const double2 d2 = lds_d2(sa + 80u);
+        dtinv[1] = d2.x;
+        dtinv[2] = d2.y;
+        const int4 an = lds_i4(sa + (uint32_t)offsetof(ShellSetup, ax));
         const int Wm = p.Wmax, ny = p.dims[1], nz = p.dims[2];
         const int mx = entry & 0xff, my = (entry >> 8) & 0xff, mz = (entry >> 16) & 0xff;
         double pt[3];
         window_point(lds_f64(sv.P_s + 8u * mx), lds_f64(sv.P_s + 8u * (Wm + my)), lds_f64(sv.P_s + 8u * (2 * Wm + mz)),
-                     st.R, st.dtinv, p.e_r, pt);
+                     R, dtinv, p.e_r, pt);
         const float v = trilinear_geom(p.geom, p.cells[l], p.dfar[l], pt[0], pt[1], pt[2]);
-        const int lin = ((st.ax + mx) * ny + (st.ay + my)) * nz + (st.az + mz);
+        const int lin = ((an.x + mx) * ny + (an.y + my)) * nz + (an.z + mz);
         const uint32_t pos = BY_POS ? (uint32_t)__ldg(p.posgrid + lin) : (uint32_t)lin;
         ov = orderable(v);
         pk = pos * (uint32_t)p.n_geo + (uint32_t)l;
@@ -632,15 +664,15 @@ struct PairTask {
     bool active;
 };
 
-__device__ __forceinline__ PairTask pair_task(const ShellSetup& st) {  // (seg_filter is on)
-    const float4 f = *reinterpret_cast<const float4*>(&st.thresh0);
-    const int4 a = *reinterpret_cast<const int4*>(&st.ax);
+__device__ __forceinline__ PairTask pair_task(uint32_t sa) {  // sa: shared address of the ShellSetup
+    const float4 f = lds_f4(sa + (uint32_t)offsetof(ShellSetup, thresh0));
+    const int4 a = lds_i4(sa + (uint32_t)offsetof(ShellSetup, ax));
     PairTask t;
     t.thresh = f.x;
     t.slack = f.y;
     t.hull_lim = f.z;
     t.k_lo = f.w;
-    t.k_hi = st.k_hi;
+    t.k_hi = __int_as_float(lds_s32(sa + (uint32_t)offsetof(ShellSetup, k_hi)));
     t.ax = a.x;
     t.ay = a.y;
     t.az = a.z;
@@ -667,15 +699,15 @@ constexpr int64_t SPARSE_FRACTION = 20;  // "sparse": under 5 % of the voxels oc
 // without the vote.
 template <bool BY_POS, bool STAGED, bool SKIP>
 __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const ShellView& sv, uint32_t queue,
-                                                const ShellSetup* setups, uint32_t j, int& qlen, int lane,
+                                                uint32_t setups_s, uint32_t j, int& qlen, int lane,
                                                 const SegAxes& ga) {
+    // the tasks' setup records, read through the warp's opaque shared address
+    // (not rebuilt from the shared-memory window for every access)
+    const uint32_t st_s = setups_s + j * (uint32_t)sizeof(ShellSetup);
     PairTask t[PAIR_N];
 #pragma unroll
-    for (int i = 0; i < PAIR_N; ++i) t[i] = pair_task(setups[j + i]);
-    const float len = p.seg_u[setups[j].l].w;  // the paired tasks share the link
-    // the tasks' segment constants, read per chunk through an opaque shared
-    // address (not rematerialized from the array base every chunk)
-    const uint32_t st_s = opaque_u32(smem_u32(&setups[j]));
+    for (int i = 0; i < PAIR_N; ++i) t[i] = pair_task(st_s + (uint32_t)(i * sizeof(ShellSetup)));
+    const float len = p.seg_u[lds_s32(st_s + (uint32_t)offsetof(ShellSetup, l))].w;  // the paired tasks share the link
     const bool share_cfg = p.per_link == nullptr;
     // grid dimensions in registers for the whole walk (not reloaded from the
     // constant bank every chunk)
@@ -750,7 +782,7 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
             const int n = qlen < 32 ? qlen : 32;
             const uint32_t entry = lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u;
             uint32_t ov;
-            lookup_round<BY_POS>(p, sv, setups, entry, lane < n, j, lane, &ov);
+            lookup_round<BY_POS>(p, sv, setups_s, entry, lane < n, j, lane, &ov);
             const uint32_t slot = entry >> 24;  // (ov is 0xffffffff on lanes without an entry)
 #pragma unroll
             for (int i = 0; i < PAIR_N; ++i) {
@@ -760,7 +792,8 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
             if (share_cfg && (++rounds & 3) == 0) {
 #pragma unroll
                 for (int i = 0; i < PAIR_N; ++i) {
-                    const uint64_t k = ~(uint64_t)__ldcg(p.keys + setups[j + i].c);
+                    const int32_t ci = lds_s32(st_s + (uint32_t)(i * sizeof(ShellSetup) + offsetof(ShellSetup, c)));
+                    const uint64_t k = ~(uint64_t)__ldcg(p.keys + ci);
                     if (k != ~0ull) t[i].thresh = fminf(t[i].thresh, from_orderable((uint32_t)(k >> 32)));
                 }
             }
@@ -776,8 +809,8 @@ __device__ __forceinline__ void shell_task_pair(const QueryParams& p, const Shel
 // next task (the kernel flushes it after the grab).
 template <bool BY_POS, bool BRICKS, bool STAGED>
 __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView& sv, uint32_t queue,
-                                           const ShellSetup* setups, uint32_t j, int& qlen, int lane,
-                                           const SegAxes& ga) {
+                                           const ShellSetup* setups, uint32_t setups_s, uint32_t j, int& qlen,
+                                           int lane, const SegAxes& ga) {
     const ShellSetup& st = setups[j];
     const int l = st.l;
     const int64_t c = st.c;
@@ -877,7 +910,7 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
         if (qlen >= round_min) {
             STAT(5, 1);
             const int n = qlen < 32 ? qlen : 32;
-            const uint32_t m = lookup_round<BY_POS>(p, sv, setups, lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u, lane < n,
+            const uint32_t m = lookup_round<BY_POS>(p, sv, setups_s, lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u, lane < n,
                                                     j, lane);
             if (m != 0xffffffffu) thresh = fminf(thresh, from_orderable(m));
             if (share_cfg && (++rounds & 3) == 0) {
@@ -1007,6 +1040,7 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
     sv.bricks = n_cols ? s_bricks : p.bricks;
     sv.P = sP;
     const uint32_t queue = opaque_u32(smem_u32(s_queue + warp * QCAP_SHELL));
+    const uint32_t setups_s = opaque_u32(smem_u32(&s_setup[warp][0]));
     // paired scan (two tasks per chunk walk) for throughput batches of one slice per task
     const bool pair = p.pair_scan && p.split == 1;
     const SegAxes ga = seg_axes(p);  // (segment-bound cell constants, once per warp)
@@ -1067,24 +1101,25 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
         if (!BRICKS && pair)
             while (j + PAIR_N <= cnt) {
                 // the paired tasks share one link (a grab straddles a link boundary at most once)
-                if (s_setup[warp][j].l == s_setup[warp][j + PAIR_N - 1].l) {
+                if (lds_s32(setups_s + j * (uint32_t)sizeof(ShellSetup) + (uint32_t)offsetof(ShellSetup, l)) ==
+                    lds_s32(setups_s + (j + PAIR_N - 1) * (uint32_t)sizeof(ShellSetup) + (uint32_t)offsetof(ShellSetup, l))) {
                     if (skip_empty)
-                        shell_task_pair<BY_POS, STAGED, true>(p, sv, queue, s_setup[warp], j, qlen, lane, ga);
+                        shell_task_pair<BY_POS, STAGED, true>(p, sv, queue, setups_s, j, qlen, lane, ga);
                     else
-                        shell_task_pair<BY_POS, STAGED, false>(p, sv, queue, s_setup[warp], j, qlen, lane, ga);
+                        shell_task_pair<BY_POS, STAGED, false>(p, sv, queue, setups_s, j, qlen, lane, ga);
                     j += PAIR_N;
                 } else {
-                    shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane, ga);
+                    shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], setups_s, j, qlen, lane, ga);
                     ++j;
                 }
             }
-        for (; j < cnt; ++j) shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], j, qlen, lane, ga);
+        for (; j < cnt; ++j) shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], setups_s, j, qlen, lane, ga);
 #ifdef LSDF_TIMING
         const unsigned long long t_g2 = gtime();
         if (lane == 0) TIM(6, t_g2 - t_g1);  // scans of the grab's tasks
 #endif
         if (qlen > 0)  // the grab's remaining lookups, before its setups are overwritten
-            lookup_round<BY_POS>(p, sv, s_setup[warp], lane < qlen ? lds_u32(queue + 4u * (uint32_t)lane) : 0u, lane < qlen, 0xffu, lane);
+            lookup_round<BY_POS>(p, sv, setups_s, lane < qlen ? lds_u32(queue + 4u * (uint32_t)lane) : 0u, lane < qlen, 0xffu, lane);
         __syncwarp();
 #ifdef LSDF_TIMING
         if (lane == 0) TIM(7, gtime() - t_g2);  // flush rounds
