@@ -49,6 +49,7 @@ struct QueryParams {
     int32_t dilate;                         // > 0: empty-neighbourhood test at setup, dilation radius in bricks
     int32_t pair_scan;                      // throughput scan walks two tasks per chunk loop (shell_task_pair)
     int32_t skip_empty;                     // paired scan skips chunks without occupied cells: 0 never, 1 sparse clouds, 2 always
+    int32_t dual;                           // latency batches: one task per (c, l) walking two chunks per step
     const uint32_t* brick_cols;             // the occupancy brick columns (input of the dilation)
     int32_t nbx_brick, nbz_brick;           // brick grid (x columns, z bits)
     int32_t nby_brick;                      // brick columns per x row
@@ -927,6 +928,83 @@ __device__ __forceinline__ void shell_task(const QueryParams& p, const ShellView
 #endif
 }
 
+// Latency batches (split 1, no segment bound): one warp walks its task's
+// shells two chunks per step -- the two chunks' loads, occupancy tests and
+// ballots are independent, so each step costs one chunk's dependent latency,
+// and one task per (configuration, link) fits the resident warps in one wave
+// (split 2 gave 6,000 tasks for 3,552 warps at config 2: a second wave).  The
+// second chunk of a step is tested against the threshold at the step's start.
+template <bool BY_POS, bool STAGED>
+__device__ __forceinline__ void shell_task_dual(const QueryParams& p, const ShellView& sv, uint32_t queue,
+                                                const ShellSetup* setups, uint32_t setups_s, uint32_t j, int& qlen,
+                                                int lane) {
+    const ShellSetup& st = setups[j];
+    const int64_t c = st.c;
+    const float slack = st.slack;
+    const int ax = st.ax, ay = st.ay, az = st.az;
+    const int nx = p.dims[0], ny = p.dims[1], nz = p.dims[2];
+    const int lin0 = st.lin0;
+    const bool share_cfg = p.per_link == nullptr;
+    {  // nothing occupied in the window's box: the task has nothing to look up (as shell_task)
+        const int x0 = max(ax, 0), x1 = min(ax + p.W[0], nx) - 1;
+        const int y0 = max(ay, 0), y1 = min(ay + p.W[1], ny) - 1;
+        const int z0 = max(az, 0), z1 = min(az + p.W[2], nz) - 1;
+        bool hit = false;
+        if (x0 <= x1 && y0 <= y1 && z0 <= z1) {
+            const int bx0 = x0 >> BRICK_LOG2, by0 = y0 >> BRICK_LOG2, nbyr = (y1 >> BRICK_LOG2) - by0 + 1;
+            const int ncol = ((x1 >> BRICK_LOG2) - bx0 + 1) * nbyr;
+            const uint32_t zmask = (2u << (z1 >> BRICK_LOG2)) - (1u << (z0 >> BRICK_LOG2));
+            const float rinv_y = 1.0f / (float)nbyr;
+            for (int i = lane; i < ncol; i += 32) {
+                const int qx = __float2int_rz(((float)i + 0.5f) * rinv_y);  // i / nbyr (small integers: exact)
+                const int bx = bx0 + qx, by = by0 + (i - qx * nbyr);
+                hit |= (sv.bricks[bx * p.nby_brick + by] & zmask) != 0u;
+            }
+        }
+        if (!__any_sync(FULL_MASK, hit)) return;
+    }
+    float thresh = st.thresh0;
+    int rounds = 0;
+    const int n_shell = p.n_shell, round_min = p.round_min;
+    const unsigned below = (1u << lane) - 1u;
+    auto occupied = [&](uint32_t cell) {
+        const int mx = cell & 0xff, my = (cell >> 8) & 0xff, mz = cell >> 16;
+        const unsigned x = (unsigned)(ax + mx), y = (unsigned)(ay + my), z = (unsigned)(az + mz);
+        const bool inb = (x < (unsigned)nx) & (y < (unsigned)ny) & (z < (unsigned)nz);
+        const int lin = inb ? lin0 + (mx * ny + my) * nz + mz : 0;
+        return inb & ((sv_u32<STAGED>(sv.bits, sv.bits_s, lin >> 5) >> (lin & 31)) & 1u);
+    };
+    for (int k0 = 0; k0 < n_shell; k0 += 64) {
+        const float ra = sv_f32<STAGED>(sv.radius, sv.radius_s, k0);
+        if (ra - slack > thresh) break;  // every later cell is farther
+        const bool has_b = k0 + 32 < n_shell;
+        const int kb = has_b ? k0 + 32 : k0;
+        const bool act_b = has_b && !(sv_f32<STAGED>(sv.radius, sv.radius_s, kb) - slack > thresh);
+        const uint32_t cell_a = sv_u32<STAGED>(sv.cells, sv.cells_s, k0 + lane);
+        const uint32_t cell_b = sv_u32<STAGED>(sv.cells, sv.cells_s, kb + lane);
+        const bool oa = occupied(cell_a);
+        const bool ob = act_b && occupied(cell_b);
+        const unsigned ba = warp_ballot(oa), bb = warp_ballot(ob);
+        sts_u32_if(oa, queue + 4u * (uint32_t)(qlen + __popc(ba & below)), cell_a | (j << 24));
+        qlen += __popc(ba);
+        sts_u32_if(ob, queue + 4u * (uint32_t)(qlen + __popc(bb & below)), cell_b | (j << 24));
+        qlen += __popc(bb);
+        __syncwarp();
+        while (qlen >= round_min) {
+            const int n = qlen < 32 ? qlen : 32;
+            const uint32_t m = lookup_round<BY_POS>(p, sv, setups_s, lane < n ? lds_u32(queue + 4u * (uint32_t)(qlen - n + lane)) : 0u,
+                                                    lane < n, j, lane);
+            if (m != 0xffffffffu) thresh = fminf(thresh, from_orderable(m));
+            if (share_cfg && (++rounds & 3) == 0) {
+                const uint64_t kk = ~(uint64_t)__ldcg(p.keys + c);
+                if (kk != ~0ull) thresh = fminf(thresh, from_orderable((uint32_t)(kk >> 32)));
+            }
+            qlen -= n;
+            __syncwarp();
+        }
+    }
+}
+
 // Persistent over groups of 8 tasks (a group never mixes links).  The window
 // offsets, the shell-ordered cell list and the occupancy bitmap are staged in
 // shared memory once per CTA when they fit, so the per-chunk loads of the
@@ -1113,6 +1191,8 @@ __global__ void __launch_bounds__(32 * WARPS, LSDF_SHELL_MINB) query_shells_kern
                     ++j;
                 }
             }
+        if (BRICKS && p.dual && p.split == 1)
+            for (; j < cnt; ++j) shell_task_dual<BY_POS, STAGED>(p, sv, queue, s_setup[warp], setups_s, j, qlen, lane);
         for (; j < cnt; ++j) shell_task<BY_POS, BRICKS, STAGED>(p, sv, queue, s_setup[warp], setups_s, j, qlen, lane, ga);
 #ifdef LSDF_TIMING
         const unsigned long long t_g2 = gtime();
@@ -1230,6 +1310,11 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     static const int t_split = tune("LSDF_TUNE_SPLIT", 0);
     if (t_split > 0 && shells) split = t_split;
     if (shells) split = split >= 4 ? 4 : (split >= 2 ? 2 : 1);  // a power of two: shifts in the task decode
+    // latency batches walk two chunks per step with one task per (c, l) instead
+    // (shell_task_dual: every task resident in one wave)
+    static const int t_dual = tune("LSDF_TUNE_DUAL", 1);
+    p.dual = t_dual && shells && C * n_geo < SEG_FILTER_MIN_TASKS && t_split == 0;
+    if (p.dual) split = 1;
     p.split_log2 = split == 4 ? 2 : (split == 2 ? 1 : 0);
     p.split = (int32_t)split;
     p.n_tasks = C * n_geo * split;
