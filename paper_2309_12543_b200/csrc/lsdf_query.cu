@@ -263,7 +263,13 @@ __global__ void __launch_bounds__(32 * WARPS) query_direct_kernel(const __grid_c
 #ifndef LSDF_PAIR_N
 #define LSDF_PAIR_N 2
 #endif
-constexpr int QCAP_SHELL = 32 + 32 * LSDF_PAIR_N;  // > round_min - 1 + 32 PAIR_N: a chunk of the paired scan queues up to 32 PAIR_N entries
+#ifndef LSDF_DUAL_CHUNKS
+#define LSDF_DUAL_CHUNKS 2
+#endif
+constexpr int DUAL_CHUNKS = LSDF_DUAL_CHUNKS;  // chunks per step of shell_task_dual (latency batches)
+// > round_min - 1 + 32 PAIR_N (a chunk of the paired scan queues up to 32
+// PAIR_N entries) and > 15 + 32 DUAL_CHUNKS (a step of the latency walk)
+constexpr int QCAP_SHELL = 32 + 32 * (LSDF_PAIR_N > LSDF_DUAL_CHUNKS ? LSDF_PAIR_N : LSDF_DUAL_CHUNKS);
 __host__ __device__ __forceinline__ int shell_padded(int n) { return (n + 31) & ~31; }
 constexpr int SHELL_STAGE_MAX = 4096;   // kept cells staged in shared memory (W <= 20)
 constexpr int BITMAP_STAGE_MAX = 8192;  // occupancy words staged in shared memory (<= 262k voxels)
@@ -974,21 +980,24 @@ __device__ __forceinline__ void shell_task_dual(const QueryParams& p, const Shel
         const int lin = inb ? lin0 + (mx * ny + my) * nz + mz : 0;
         return inb & ((sv_u32<STAGED>(sv.bits, sv.bits_s, lin >> 5) >> (lin & 31)) & 1u);
     };
-    for (int k0 = 0; k0 < n_shell; k0 += 64) {
-        const float ra = sv_f32<STAGED>(sv.radius, sv.radius_s, k0);
-        if (ra - slack > thresh) break;  // every later cell is farther
-        const bool has_b = k0 + 32 < n_shell;
-        const int kb = has_b ? k0 + 32 : k0;
-        const bool act_b = has_b && !(sv_f32<STAGED>(sv.radius, sv.radius_s, kb) - slack > thresh);
-        const uint32_t cell_a = sv_u32<STAGED>(sv.cells, sv.cells_s, k0 + lane);
-        const uint32_t cell_b = sv_u32<STAGED>(sv.cells, sv.cells_s, kb + lane);
-        const bool oa = occupied(cell_a);
-        const bool ob = act_b && occupied(cell_b);
-        const unsigned ba = warp_ballot(oa), bb = warp_ballot(ob);
-        sts_u32_if(oa, queue + 4u * (uint32_t)(qlen + __popc(ba & below)), cell_a | (j << 24));
-        qlen += __popc(ba);
-        sts_u32_if(ob, queue + 4u * (uint32_t)(qlen + __popc(bb & below)), cell_b | (j << 24));
-        qlen += __popc(bb);
+    for (int k0 = 0; k0 < n_shell; k0 += 32 * DUAL_CHUNKS) {
+        if (sv_f32<STAGED>(sv.radius, sv.radius_s, k0) - slack > thresh) break;  // every later cell is farther
+        uint32_t cell[DUAL_CHUNKS];
+        bool occ[DUAL_CHUNKS];
+#pragma unroll
+        for (int q = 0; q < DUAL_CHUNKS; ++q) {
+            const bool has = k0 + 32 * q < n_shell;
+            const int kq = has ? k0 + 32 * q : k0;
+            const bool act = has && !(sv_f32<STAGED>(sv.radius, sv.radius_s, kq) - slack > thresh);
+            cell[q] = sv_u32<STAGED>(sv.cells, sv.cells_s, kq + lane);
+            occ[q] = act && occupied(cell[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < DUAL_CHUNKS; ++q) {
+            const unsigned b = warp_ballot(occ[q]);
+            sts_u32_if(occ[q], queue + 4u * (uint32_t)(qlen + __popc(b & below)), cell[q] | (j << 24));
+            qlen += __popc(b);
+        }
         __syncwarp();
         while (qlen >= round_min) {
             const int n = qlen < 32 ? qlen : 32;
