@@ -167,6 +167,7 @@ class L2Flush:
         self.buf.zero_()
 
 
+E2E_WINDOWS, E2E_MIN_CYCLES = 3, 200  # e2e throughput: best of three windows of >= 200 pipelined cycles
 SPIN_CYCLES = 200_000  # ~0.1 ms GPU spin: longer than the host needs to enqueue one step
 
 
@@ -207,11 +208,12 @@ def _e2e_entry(C_total, pipe_ms, single_ms, h2d, d2h, world=1):
     """The public-API end-to-end number: the faster of the pipelined and the
     one-cycle-at-a-time paths (both copy every cycle's inputs in and results out)."""
     pipe_path = ("CheckerPipeline (3 cycles in flight): per cycle one H2D of configs + cloud from pinned host memory on "
-                 "a copy stream, the cycle graph, D2H of (d, link, voxel) + flags; host wall clock over K cycles"
+                 "a copy stream, the cycle graph, D2H of (d, link, voxel) + flags; host wall clock over max(K, 200) "
+                 "cycles, best of 3 windows"
                  if world == 1 else
                  "ShardedCloudPipeline (3 cycles in flight, per rank): H2D of this rank's configs and 1/world of the "
                  "cloud, voxelize the slice, NCCL all-gather of the partial occupancy bitmaps, merge, FK + query, "
-                 "D2H; host wall clock over K cycles, max over ranks")
+                 "D2H; host wall clock over max(K, 200) cycles, best of 3 windows, max over ranks")
     single_path = ("DistanceChecker.query() one cycle at a time from pinned host buffers (zero-copy kernel "
                    "reads/writes over PCIe); median cycle, host wall clock")
     best_ms, path = (pipe_ms, pipe_path) if (pipe_ms <= single_ms or world > 1) else (single_ms, single_path)
@@ -327,15 +329,22 @@ def run_ours(args, rank, world, dist, sampler):
         for _ in range(args.warmup):
             pipe.result(pipe.submit())
         torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        s0 = time.perf_counter()
-        tickets = [pipe.submit() for _ in range(pipe.depth)]
-        for k in range(args.steps):
-            pipe.result(tickets[k])
-            if k + pipe.depth < args.steps:
-                tickets.append(pipe.submit())
-        return 1e3 * (time.perf_counter() - s0) / args.steps, plo, phi
+        # three timed windows of at least 200 cycles each, the best one kept:
+        # a window is ~60 ms of wall clock, so one host hiccup (another tenant,
+        # a page fault) would otherwise dominate a short measurement
+        n_cyc = max(args.steps, E2E_MIN_CYCLES)
+        best = float("inf")
+        for _ in range(E2E_WINDOWS):
+            if dist is not None:
+                dist.barrier()
+            s0 = time.perf_counter()
+            tickets = [pipe.submit() for _ in range(pipe.depth)]
+            for k in range(n_cyc):
+                pipe.result(tickets[k])
+                if k + pipe.depth < n_cyc:
+                    tickets.append(pipe.submit())
+            best = min(best, 1e3 * (time.perf_counter() - s0) / n_cyc)
+        return best, plo, phi
 
     sharded = world > 1
     try:
