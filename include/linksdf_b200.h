@@ -259,12 +259,17 @@ int lsdf_voxel_index(const double* points_dev, int64_t N, const lsdf_env_grid* e
  * (query.py:153-176).  by_position is a flags word: LSDF_QUERY_BY_POSITION
  * selects the general (unsorted list) tie rule (set it when the occupancy came
  * from an unsorted index list); LSDF_QUERY_POSES_LINK_MAJOR reads the poses
- * in the (n_geo, C, .) layout of lsdf_fk_align_link_major.
+ * in the (n_geo, C, .) layout of lsdf_fk_align_link_major;
+ * LSDF_QUERY_DENSE_HINT tells a latency-sized batch (below ~38k configuration x
+ * link tasks) that the obstacles are dense (e.g. a cloud of >= 64k points):
+ * one task per (configuration, link) then walks its shells two chunks per
+ * step, all tasks resident in one wave (same results either way).
  * workspace_dev: lsdf_query_workspace_bytes(C, n_geo) bytes, zeroed once at
  * allocation; every launch leaves it zeroed again (the finalize pass of each
  * configuration resets its slots), so graph replays need no memset. */
 #define LSDF_QUERY_BY_POSITION 1
 #define LSDF_QUERY_POSES_LINK_MAJOR 2
+#define LSDF_QUERY_DENSE_HINT 4
 int lsdf_query_direct(const double* R_geo_dev, const double* dt_geo_dev,
                       const int32_t* anchor_geo_dev, int64_t C, int32_t n_geo,
                       const lsdf_link_grid* grids, const lsdf_window* window,

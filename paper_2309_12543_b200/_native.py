@@ -124,6 +124,7 @@ _SIGS = {
 
 QUERY_BY_POSITION = 1        # lsdf_query_* flags word (include/linksdf_b200.h)
 QUERY_POSES_LINK_MAJOR = 2
+QUERY_DENSE_HINT = 4
 FK_LINK_MAJOR = 1            # lsdf_fk_align_ex options
 FK_FLAGS_SELF_RESET = 2
 

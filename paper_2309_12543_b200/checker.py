@@ -33,6 +33,7 @@ from .query import TrajectorySdf, occupancy_workspace
 # batch size from which FK runs one thread per configuration (lsdf_fk.cu
 # FK_SERIAL_MIN) and the checker keeps its poses link-major
 LINK_MAJOR_MIN = 6144
+DENSE_HINT_POINTS = 65536  # clouds from this capacity set LSDF_QUERY_DENSE_HINT (config 2: 100k; config 5: 30k)
 
 
 def _require_exact(window_or_provider, who: str):
@@ -128,6 +129,8 @@ class DistanceChecker:
         # self-resetting FK flags: no reset node ahead of FK on the cycle's critical branch
         self._fk_opts = (N.FK_LINK_MAJOR if self.link_major else 0) | N.FK_FLAGS_SELF_RESET
         self._qflags = N.QUERY_POSES_LINK_MAJOR if self.link_major else 0
+        if n_points >= DENSE_HINT_POINTS:  # dense obstacles: the one-wave latency walk (lsdf_query.cu)
+            self._qflags |= N.QUERY_DENSE_HINT
         # FK flags: [0..1] published per cycle, [2..4] the kernel's self-resetting counters
         self.flags = t.zeros((8,), dtype=t.int32, device=dev)
         self.limits = N.to_device(np.ascontiguousarray(self._limits), t.float64)

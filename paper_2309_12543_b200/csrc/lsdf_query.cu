@@ -1321,8 +1321,12 @@ int query_impl(const double* R_geo_dev, const double* dt_geo_dev, const int32_t*
     if (shells) split = split >= 4 ? 4 : (split >= 2 ? 2 : 1);  // a power of two: shifts in the task decode
     // latency batches walk two chunks per step with one task per (c, l) instead
     // (shell_task_dual: every task resident in one wave)
-    static const int t_dual = tune("LSDF_TUNE_DUAL", 1);
-    p.dual = t_dual && shells && C * n_geo < SEG_FILTER_MIN_TASKS && t_split == 0;
+    // (dense obstacles, LSDF_QUERY_DENSE_HINT: tasks stop early, and the second
+    // wave of split 2 was the latency; sparse ones keep split 2, whose two warps
+    // per (c, l) share the lookups of long walks)
+    static const int t_dual = tune("LSDF_TUNE_DUAL", 1);  // 0 never, 1 with the hint, 2 always
+    p.dual = shells && C * n_geo < SEG_FILTER_MIN_TASKS && t_split == 0 &&
+             (t_dual == 2 || (t_dual == 1 && (by_position & LSDF_QUERY_DENSE_HINT) != 0));
     if (p.dual) split = 1;
     p.split_log2 = split == 4 ? 2 : (split == 2 ? 1 : 0);
     p.split = (int32_t)split;
